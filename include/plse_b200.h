@@ -1,0 +1,187 @@
+/*
+ * plse_b200.h -- C ABI of the B200-native Partial-MPMA hot path.
+ *
+ * The reference (/root/reference/proj, header-only C++20) has no plugin or FFI
+ * layer: its seam is five C++ calls inside run().  Each entry
+ * point below replaces one of them with a batched, device-resident version:
+ *
+ *   plse_init_population  <- initialize_population      engine.hpp:88-106
+ *   plse_improve          <- partial_mpma_improve x p    partial.hpp:156-169,
+ *                            driven by the improve phase engine.hpp:184-209
+ *                            (+ best tracking engine.hpp:211-217)
+ *   plse_distances        <- compute_cross_distances    population.hpp:41-61
+ *   plse_update           <- update_population          population.hpp:103-183
+ *   plse_offspring        <- build_offspring            crossover.hpp:54-104
+ *   plse_solve            <- run (Partial-MPMA)         engine.hpp:114-262
+ *
+ * plus the reference's host helpers kept on the host side of the boundary:
+ *   plse_generate_instance <- generate_instance         instance.hpp:204-262
+ *   plse_parse_instance    <- parse_instance            instance.hpp:107-170
+ *   plse_preprocess        <- preprocess(build_graph()) lsgraph.hpp:115-211
+ *
+ * Conventions (mirroring the reference's C++ contract):
+ *   - every entry point returns PLSE_OK (0) or a plse_status; the message of
+ *     the last failure is available from plse_last_error().  Status codes map
+ *     onto the reference's exception types (std::invalid_argument ->
+ *     PLSE_ERR_INVALID, std::runtime_error / GenerationError / ParseError ->
+ *     PLSE_ERR_RUNTIME).
+ *   - colours are uint16_t on the host side of the ABI (Color = Symbol =
+ *     uint16_t, instance.hpp:15 / lsgraph.hpp:14); distances are int32_t
+ *     (DistanceMatrix, population.hpp:19-32).
+ *   - a plse_ctx owns one device and is not thread-safe (one host thread or
+ *     process per GPU).  The population stays device-resident between calls.
+ *   - there is NO CPU fallback: without a usable sm_100 device plse_create
+ *     fails with PLSE_ERR_CUDA.
+ */
+#ifndef PLSE_B200_H
+#define PLSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLSE_ABI_VERSION 1
+
+typedef enum {
+    PLSE_OK = 0,
+    PLSE_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
+    PLSE_ERR_CUDA = 2,        /* device / driver failure, or no sm_100 device */
+    PLSE_ERR_UNSUPPORTED = 3, /* outside the device path's envelope (e.g. n > 127) */
+    PLSE_ERR_RUNTIME = 4      /* std::runtime_error, GenerationError, ParseError */
+} plse_status;
+
+/* population buffers addressed by plse_set_colors / plse_get_colors */
+enum { PLSE_MEMBERS = 0, PLSE_OFFSPRING = 1, PLSE_IMPROVED = 2 };
+/* distance matrices addressed by plse_get_dist / plse_set_dist */
+enum { PLSE_DIST = 0, PLSE_CROSS = 1, PLSE_FRESH = 2 };
+/* SolverConfig enums (crossover.hpp:17-19, engine.hpp:18) */
+enum { PLSE_X_AUX = 0, PLSE_X_UX = 1, PLSE_X_NONE = 2 };
+enum { PLSE_M_NEAREST = 0, PLSE_M_RANDOM = 1 };
+enum { PLSE_E_RUN = 0, PLSE_E_GENERATION = 1, PLSE_E_OFF = 2 };
+enum { PLSE_V_MPMA = 0, PLSE_V_PARTIAL = 1 };
+enum { PLSE_TIE_CANON = 0 };
+enum { PLSE_STOP_OPTIMAL = 0, PLSE_STOP_TIME = 1, PLSE_STOP_ITERS = 2, PLSE_STOP_GENS = 3, PLSE_STOP_TRIVIAL = 4,
+       PLSE_STOP_TARGET = 5 /* harness: target_score reached */ };
+
+typedef struct plse_ctx plse_ctx;
+typedef struct plse_graph_h plse_graph_h; /* host-side ReducedGraph handle */
+
+/* ReducedGraph (lsgraph.hpp:67-109) as plain arrays. */
+typedef struct {
+    int32_t order;              /* n */
+    int32_t vertex_count;       /* |V| */
+    int32_t l;                  /* cells impossible to fill */
+    const int32_t* cell_row;    /* [|V|] */
+    const int32_t* cell_col;    /* [|V|] */
+    const int32_t* dom_offsets; /* [|V|+1] CSR domains, ascending, starting with 0 */
+    const uint16_t* dom;        /* [dom_offsets[|V|]] */
+    int32_t n_prefilled;        /* ReducedGraph::prefilled (lsgraph.hpp:85) */
+    const int32_t* prefilled;   /* [3*n_prefilled]: row, col, symbol */
+} plse_graph;
+
+/* SolverConfig (engine.hpp:26-47) + the island coordinates of this shard. */
+typedef struct {
+    int32_t p;              /* population (of this shard) */
+    double alpha;           /* tenure factor (partial.hpp:136-137) */
+    double gamma;           /* spacing divisor (population.hpp:74) */
+    double beta;            /* AUX divisor (crossover.hpp:26-30) */
+    int64_t phase1_iters;   /* 0 -> 100|V| (engine.hpp:173-174) */
+    int32_t crossover;      /* PLSE_X_* */
+    int32_t matching;       /* PLSE_M_* */
+    int32_t exclusion;      /* PLSE_E_* */
+    int32_t tie_mode;       /* PLSE_TIE_CANON */
+    uint64_t master_seed;
+    int64_t p_total;        /* stream index space: gen*p_total + offset + i; 0 -> p */
+    int64_t offset;         /* first global individual of this shard */
+} plse_params;
+
+/* One PartialCol step, for the per-step parity probe (partial.hpp:92-143). */
+typedef struct {
+    int64_t step;
+    int32_t v, k, e, ev0, ev1;
+    int32_t f_before, f_after, best_f;
+    int32_t tenure, n_adm, level;
+} plse_step;
+
+/* Timings / counters of the last plse_improve (device-side CUDA events). */
+typedef struct {
+    double improve_ms;          /* improve kernel */
+    double alg_bytes;           /* sum of SURVEY 8(d) algorithmic bytes over the launch */
+    int64_t moves;              /* iterations (tabu moves) of the launch */
+    int32_t grid, threads, warps_per_sm, slots;
+    int64_t smem_bytes;
+    int64_t kernel_launches;    /* this context's kernel launches so far */
+} plse_counters;
+
+/* RunResult (engine.hpp:59-71) */
+typedef struct {
+    int32_t best_f, best_score, proven_optimal, stop_reason, l, upper_bound, vertex_count;
+    int64_t generations, total_iterations;
+    double elapsed_seconds;
+    double time_to_best_seconds; /* elapsed when best_f first reached its final value */
+} plse_run_result;
+
+/* SolverConfig + RunLimits for plse_solve */
+typedef struct {
+    plse_params params;
+    int32_t variant;            /* PLSE_V_PARTIAL (MPMA/PLITS -> PLSE_ERR_UNSUPPORTED) */
+    double time_limit;          /* seconds, 0 = unlimited */
+    int64_t iteration_limit;    /* 0 = unlimited */
+    int64_t generation_limit;   /* 0 = unlimited */
+    int32_t device;
+    int32_t disable_optimal_stop; /* harness flag */
+    double target_score;        /* >0: stop as soon as best_score >= target (time-to-target) */
+} plse_solver_config;
+
+/* per-generation callback (GenerationCallback, engine.hpp:108) */
+typedef void (*plse_generation_cb)(int64_t generation, int32_t best_f, int64_t iterations,
+                                   double elapsed_seconds, int32_t shortfall, void* user);
+
+int plse_abi_version(void);
+const char* plse_last_error(const plse_ctx* ctx); /* ctx may be NULL: last global error */
+
+/* ---- host helpers (C++ host library, instance.hpp / lsgraph.hpp semantics) */
+int plse_generate_instance(int32_t n, double r, uint64_t seed, uint16_t* grid /* n*n */);
+int plse_parse_instance(const char* text, int32_t* n, uint16_t* grid /* cap n*n */, int32_t grid_cap);
+int plse_preprocess(int32_t n, const uint16_t* grid, plse_graph_h** out);
+void plse_graph_free(plse_graph_h* g);
+int plse_graph_view(const plse_graph_h* g, plse_graph* view); /* borrowed arrays, valid until free */
+
+/* ---- device context */
+int plse_create(const plse_graph* graph, const plse_params* params, int32_t device, plse_ctx** out);
+void plse_destroy(plse_ctx* ctx);
+int plse_set_colors(plse_ctx* ctx, int32_t which, const uint16_t* host, int64_t count /* p*|V| */);
+int plse_get_colors(plse_ctx* ctx, int32_t which, uint16_t* host);
+int plse_get_dist(plse_ctx* ctx, int32_t which, int32_t* host /* p*p */);
+int plse_set_dist(plse_ctx* ctx, int32_t which, const int32_t* host);
+/* f, c (conflicting edges) and the last improve's iterations per individual; any may be NULL */
+int plse_get_stats(plse_ctx* ctx, int32_t which, int32_t* f, int32_t* c, int64_t* iters);
+int plse_get_partners(plse_ctx* ctx, int32_t* host /* p */);
+int plse_get_counters(plse_ctx* ctx, plse_counters* out);
+
+int plse_init_population(plse_ctx* ctx);
+int plse_full_distances(plse_ctx* ctx); /* dist <- D(members, members) */
+int plse_improve(plse_ctx* ctx, uint64_t generation, int64_t* iters_total, int32_t* best_f, int32_t* best_idx);
+int plse_distances(plse_ctx* ctx);
+int plse_update(plse_ctx* ctx, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* shortfall_slots /* cap p */);
+int plse_reset_exclusion(plse_ctx* ctx);
+int plse_offspring(plse_ctx* ctx, uint64_t generation);
+/* run individual idx of OFFSPRING through improve with a per-step trace (parity probe) */
+int plse_trace(plse_ctx* ctx, int32_t idx, uint64_t generation, int64_t max_steps, plse_step* out, int64_t* n_out);
+
+/* ---- island exchange (multi-GPU): the driver moves the bytes (NCCL all-gather) */
+/* copy the n_elite best members (ascending f, lowest index) as u8 rows [n_elite*|V|] into dev_out */
+int plse_export_elites(plse_ctx* ctx, int32_t n_elite, void* dev_out, int32_t* f_out);
+/* replace the n_in worst members by the given u8 rows [n_in*|V|] (device pointer) and refresh dist */
+int plse_import_migrants(plse_ctx* ctx, int32_t n_in, const void* dev_in);
+
+/* ---- the whole run() (engine.hpp:114-262) on one device */
+int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, plse_run_result* res,
+               uint16_t* best_colors /* |V| */, plse_generation_cb cb, void* user);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

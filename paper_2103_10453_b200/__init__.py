@@ -1,0 +1,447 @@
+"""B200-native Partial-MPMA (arXiv 2103.10453) behind the reference's operator API.
+
+Python mirror of the reference's host interface for the hot path
+(/root/reference/proj/include/plse), bound through the C ABI in
+``include/plse_b200.h`` (ctypes; no torch types cross the boundary):
+
+================================  =======================================
+this module                       reference
+================================  =======================================
+``generate_instance``             instance.hpp:204  generate_instance
+``parse_instance``                instance.hpp:107  parse_instance
+``serialize_instance``            instance.hpp:172  serialize_instance
+``preprocess``                    lsgraph.hpp:115   preprocess(build_graph)
+``DevicePopulation``              Population + the five run() phases:
+  ``.initialize_population()``    engine.hpp:88     initialize_population
+  ``.improve(gen)``               engine.hpp:184    parallel partial_mpma_improve
+  ``.compute_cross_distances()``  population.hpp:41 compute_cross_distances
+  ``.update_population()``        population.hpp:103 update_population
+  ``.build_offspring(gen)``       crossover.hpp:54  build_offspring
+``run``                           engine.hpp:114    run (variant=partial)
+================================  =======================================
+
+Errors map like the reference's exceptions: ``std::invalid_argument`` ->
+``ValueError``, ``std::runtime_error`` -> ``RuntimeError``; device failures
+raise ``PlseCudaError``; requests outside the device envelope raise
+``NotImplementedError``.  There is no CPU fallback: importing this package on
+a machine without the built library raises ``ImportError``, and creating a
+device context without an sm_100 GPU raises ``PlseCudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Callable, List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libplse_b200.so")
+
+__all__ = [
+    "generate_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
+    "SolverConfig", "RunResult", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
+    "lib_path", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
+]
+
+AUX, UX, NONE = 0, 1, 2
+NEAREST, RANDOM = 0, 1
+RUN, GENERATION, OFF = 0, 1, 2
+MPMA, PARTIAL = 0, 1
+MEMBERS, OFFSPRING, IMPROVED = 0, 1, 2
+DIST, CROSS, FRESH = 0, 1, 2
+STOP_NAMES = ["optimal", "time_limit", "iteration_limit", "generation_limit", "trivial", "target"]
+
+
+class PlseCudaError(RuntimeError):
+    """A CUDA / device failure (PLSE_ERR_CUDA)."""
+
+
+# ----------------------------------------------------------------- ctypes
+class _Graph(C.Structure):
+    _fields_ = [("order", C.c_int32), ("vertex_count", C.c_int32), ("l", C.c_int32),
+                ("cell_row", C.POINTER(C.c_int32)), ("cell_col", C.POINTER(C.c_int32)),
+                ("dom_offsets", C.POINTER(C.c_int32)), ("dom", C.POINTER(C.c_uint16)),
+                ("n_prefilled", C.c_int32), ("prefilled", C.POINTER(C.c_int32))]
+
+
+class _Params(C.Structure):
+    _fields_ = [("p", C.c_int32), ("alpha", C.c_double), ("gamma", C.c_double), ("beta", C.c_double),
+                ("phase1_iters", C.c_int64), ("crossover", C.c_int32), ("matching", C.c_int32),
+                ("exclusion", C.c_int32), ("tie_mode", C.c_int32), ("master_seed", C.c_uint64),
+                ("p_total", C.c_int64), ("offset", C.c_int64)]
+
+
+class Step(C.Structure):
+    """plse_step: one PartialCol step of the parity probe (partial.hpp:92-143)."""
+    _fields_ = [("step", C.c_int64), ("v", C.c_int32), ("k", C.c_int32), ("e", C.c_int32),
+                ("ev0", C.c_int32), ("ev1", C.c_int32), ("f_before", C.c_int32), ("f_after", C.c_int32),
+                ("best_f", C.c_int32), ("tenure", C.c_int32), ("n_adm", C.c_int32), ("level", C.c_int32)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("improve_ms", C.c_double), ("alg_bytes", C.c_double), ("moves", C.c_int64),
+                ("grid", C.c_int32), ("threads", C.c_int32), ("warps_per_sm", C.c_int32), ("slots", C.c_int32),
+                ("smem_bytes", C.c_int64), ("kernel_launches", C.c_int64)]
+
+
+class _RunResult(C.Structure):
+    _fields_ = [("best_f", C.c_int32), ("best_score", C.c_int32), ("proven_optimal", C.c_int32),
+                ("stop_reason", C.c_int32), ("l", C.c_int32), ("upper_bound", C.c_int32),
+                ("vertex_count", C.c_int32), ("generations", C.c_int64), ("total_iterations", C.c_int64),
+                ("elapsed_seconds", C.c_double), ("time_to_best_seconds", C.c_double)]
+
+
+class _SolverConfig(C.Structure):
+    _fields_ = [("params", _Params), ("variant", C.c_int32), ("time_limit", C.c_double),
+                ("iteration_limit", C.c_int64), ("generation_limit", C.c_int64), ("device", C.c_int32),
+                ("disable_optimal_stop", C.c_int32), ("target_score", C.c_double)]
+
+
+_GEN_CB = C.CFUNCTYPE(None, C.c_int64, C.c_int32, C.c_int64, C.c_double, C.c_int32, C.c_void_p)
+
+
+def lib_path() -> str:
+    return LIB_PATH
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2103_10453_b200.build` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+    i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+    i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+    vp, ctx = C.c_void_p, C.c_void_p
+    sig = {
+        "plse_abi_version": ([], C.c_int),
+        "plse_last_error": ([vp], C.c_char_p),
+        "plse_generate_instance": ([C.c_int32, C.c_double, C.c_uint64, u16p], C.c_int),
+        "plse_parse_instance": ([C.c_char_p, C.POINTER(C.c_int32), vp, C.c_int32], C.c_int),
+        "plse_preprocess": ([C.c_int32, u16p, C.POINTER(vp)], C.c_int),
+        "plse_graph_free": ([vp], None),
+        "plse_graph_view": ([vp, C.POINTER(_Graph)], C.c_int),
+        "plse_create": ([C.POINTER(_Graph), C.POINTER(_Params), C.c_int32, C.POINTER(vp)], C.c_int),
+        "plse_destroy": ([ctx], None),
+        "plse_set_colors": ([ctx, C.c_int32, u16p, C.c_int64], C.c_int),
+        "plse_get_colors": ([ctx, C.c_int32, u16p], C.c_int),
+        "plse_get_dist": ([ctx, C.c_int32, i32p], C.c_int),
+        "plse_set_dist": ([ctx, C.c_int32, i32p], C.c_int),
+        "plse_get_stats": ([ctx, C.c_int32, vp, vp, vp], C.c_int),
+        "plse_get_partners": ([ctx, i32p], C.c_int),
+        "plse_get_counters": ([ctx, C.POINTER(Counters)], C.c_int),
+        "plse_init_population": ([ctx], C.c_int),
+        "plse_full_distances": ([ctx], C.c_int),
+        "plse_improve": ([ctx, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
+                         C.c_int),
+        "plse_distances": ([ctx], C.c_int),
+        "plse_update": ([ctx, C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32p], C.c_int),
+        "plse_reset_exclusion": ([ctx], C.c_int),
+        "plse_offspring": ([ctx, C.c_uint64], C.c_int),
+        "plse_trace": ([ctx, C.c_int32, C.c_uint64, C.c_int64, vp, C.POINTER(C.c_int64)], C.c_int),
+        "plse_export_elites": ([ctx, C.c_int32, vp, vp], C.c_int),
+        "plse_import_migrants": ([ctx, C.c_int32, vp], C.c_int),
+        "plse_solve": ([C.c_int32, u16p, C.POINTER(_SolverConfig), C.POINTER(_RunResult), u16p, _GEN_CB, vp],
+                       C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.plse_abi_version() != 1:
+        raise ImportError("libplse_b200.so ABI mismatch")
+    return L
+
+
+_lib = _load()
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc == 0:
+        return
+    msg = (_lib.plse_last_error(ctx) or b"").decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise PlseCudaError(msg)
+    if rc == 3:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+# --------------------------------------------------------------- instances
+def generate_instance(n: int, r: float, seed: int) -> np.ndarray:
+    """instance.hpp:204 -- random partial Latin square (n x n uint16 grid)."""
+    g = np.zeros(n * n, np.uint16)
+    _check(_lib.plse_generate_instance(n, r, seed & (2**64 - 1), g))
+    return g.reshape(n, n)
+
+
+def parse_instance(text: str) -> np.ndarray:
+    """instance.hpp:107 -- 'n' then n rows of n symbols (0 = empty)."""
+    n = C.c_int32()
+    _check(_lib.plse_parse_instance(text.encode(), C.byref(n), None, 0))
+    g = np.zeros(n.value * n.value, np.uint16)
+    _check(_lib.plse_parse_instance(text.encode(), C.byref(n), g.ctypes.data_as(C.c_void_p), g.size))
+    return g.reshape(n.value, n.value)
+
+
+def serialize_instance(grid: np.ndarray) -> str:
+    """instance.hpp:172"""
+    n = grid.shape[0]
+    return f"{n}\n" + "".join(" ".join(str(int(x)) for x in row) + "\n" for row in grid)
+
+
+@dataclasses.dataclass
+class ReducedGraph:
+    """lsgraph.hpp:67 (cells row-major, CSR domains starting with 0, prefilled triples)."""
+    order: int
+    vertex_count: int
+    l: int
+    cell_row: np.ndarray
+    cell_col: np.ndarray
+    dom_offsets: np.ndarray
+    dom: np.ndarray
+    prefilled: np.ndarray  # (k, 3): row, col, symbol
+
+    def _struct(self) -> _Graph:
+        self._keep = [np.ascontiguousarray(a, dt) for a, dt in (
+            (self.cell_row, np.int32), (self.cell_col, np.int32), (self.dom_offsets, np.int32),
+            (self.dom, np.uint16), (self.prefilled.reshape(-1), np.int32))]
+        cr, cc, do, dm, pf = self._keep
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        return _Graph(self.order, self.vertex_count, self.l, P(cr, C.c_int32), P(cc, C.c_int32),
+                      P(do, C.c_int32), P(dm, C.c_uint16), len(pf) // 3, P(pf, C.c_int32))
+
+
+def preprocess(grid: np.ndarray) -> ReducedGraph:
+    """lsgraph.hpp:115 -- Alg. 1 reduction of an instance grid."""
+    grid = np.ascontiguousarray(grid, np.uint16)
+    n = grid.shape[0]
+    h = C.c_void_p()
+    _check(_lib.plse_preprocess(n, grid.reshape(-1), C.byref(h)))
+    try:
+        v = _Graph()
+        _check(_lib.plse_graph_view(h, C.byref(v)))
+        nv = v.vertex_count
+        arr = lambda ptr, cnt: np.ctypeslib.as_array(ptr, shape=(cnt,)).copy() if cnt else np.zeros(0, ptr._type_)
+        dom_off = arr(v.dom_offsets, nv + 1)
+        return ReducedGraph(v.order, nv, v.l, arr(v.cell_row, nv), arr(v.cell_col, nv), dom_off,
+                            arr(v.dom, int(dom_off[-1])), arr(v.prefilled, 3 * v.n_prefilled).reshape(-1, 3))
+    finally:
+        _lib.plse_graph_free(h)
+
+
+# ------------------------------------------------------------------ config
+@dataclasses.dataclass
+class SolverConfig:
+    """engine.hpp:26-47 (+ RunLimits engine.hpp:20-24)."""
+    p: int = 12288
+    alpha: float = 0.6
+    phase1_iters: int = 0
+    gamma: float = 10.0
+    beta: float = 20.0
+    crossover: int = AUX
+    matching: int = NEAREST
+    exclusion: int = RUN
+    master_seed: int = 0
+    time_limit: float = 0.0
+    iteration_limit: int = 0
+    generation_limit: int = 0
+    variant: int = PARTIAL
+    device: int = 0
+    p_total: int = 0
+    offset: int = 0
+    disable_optimal_stop: bool = False
+    target_score: float = 0.0
+
+    def _params(self) -> _Params:
+        return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,
+                       self.exclusion, 0, self.master_seed & (2**64 - 1), self.p_total, self.offset)
+
+
+@dataclasses.dataclass
+class RunResult:
+    """engine.hpp:59-71"""
+    best_f: int
+    best_score: int
+    proven_optimal: bool
+    stop_reason: str
+    l: int
+    upper_bound: int
+    vertex_count: int
+    generations: int
+    total_iterations: int
+    elapsed_seconds: float
+    time_to_best_seconds: float
+    best_solution: np.ndarray
+
+
+def run(grid: np.ndarray, config: SolverConfig,
+        on_generation: Optional[Callable[[int, int, int, float, int], None]] = None) -> RunResult:
+    """engine.hpp:114 -- the whole Partial-MPMA run on one B200."""
+    grid = np.ascontiguousarray(grid, np.uint16)
+    n = grid.shape[0]
+    cfg = _SolverConfig(config._params(), config.variant, config.time_limit, config.iteration_limit,
+                        config.generation_limit, config.device, int(config.disable_optimal_stop),
+                        config.target_score)
+    res = _RunResult()
+    best = np.zeros(n * n + 1, np.uint16)
+    errors: List[BaseException] = []
+
+    def cb(gen, best_f, iters, elapsed, shortfall, _user):
+        if on_generation is None:
+            return
+        try:
+            on_generation(gen, best_f, iters, elapsed, shortfall)
+        except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
+            errors.append(e)
+
+    cfun = _GEN_CB(cb)
+    _check(_lib.plse_solve(n, grid.reshape(-1), C.byref(cfg), C.byref(res), best, cfun, None))
+    if errors:
+        raise errors[0]
+    return RunResult(res.best_f, res.best_score, bool(res.proven_optimal), STOP_NAMES[res.stop_reason], res.l,
+                     res.upper_bound, res.vertex_count, res.generations, res.total_iterations,
+                     res.elapsed_seconds, res.time_to_best_seconds, best[:res.vertex_count].copy())
+
+
+@dataclasses.dataclass
+class UpdateInfo:
+    """population.hpp:90-95"""
+    pool_best_f: int
+    shortfall_slots: List[int]
+
+
+class DevicePopulation:
+    """A device-resident population (one B200) with the reference's five phases.
+
+    Buffers: ``members`` (Population::members), ``offspring`` (input of the
+    improve phase), ``improved`` (its output); distance matrices ``dist``
+    (members x members), ``cross`` (members x improved), ``fresh`` (improved x
+    improved).  Colours cross the boundary as uint16 (Color), distances as int32.
+    """
+
+    def __init__(self, graph: ReducedGraph, config: SolverConfig):
+        self.graph = graph
+        self.config = config
+        self.p = config.p
+        self.nv = graph.vertex_count
+        self._ctx = C.c_void_p()
+        gs = graph._struct()
+        prm = config._params()
+        _check(_lib.plse_create(C.byref(gs), C.byref(prm), config.device, C.byref(self._ctx)))
+
+    def close(self) -> None:
+        if self._ctx:
+            _lib.plse_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- buffers
+    def _set(self, which, colors):
+        a = np.ascontiguousarray(colors, np.uint16).reshape(-1)
+        _check(_lib.plse_set_colors(self._ctx, which, a, a.size), self._ctx)
+
+    def _get(self, which):
+        a = np.zeros(self.p * self.nv, np.uint16)
+        _check(_lib.plse_get_colors(self._ctx, which, a), self._ctx)
+        return a.reshape(self.p, self.nv)
+
+    members = property(lambda s: s._get(MEMBERS), lambda s, v: s._set(MEMBERS, v))
+    offspring = property(lambda s: s._get(OFFSPRING), lambda s, v: s._set(OFFSPRING, v))
+    improved = property(lambda s: s._get(IMPROVED), lambda s, v: s._set(IMPROVED, v))
+
+    def get_dist(self, which=DIST) -> np.ndarray:
+        a = np.zeros(self.p * self.p, np.int32)
+        _check(_lib.plse_get_dist(self._ctx, which, a), self._ctx)
+        return a.reshape(self.p, self.p)
+
+    def set_dist(self, d: np.ndarray, which=DIST) -> None:
+        a = np.ascontiguousarray(d, np.int32).reshape(-1)
+        _check(_lib.plse_set_dist(self._ctx, which, a), self._ctx)
+
+    dist = property(lambda s: s.get_dist(DIST), lambda s, v: s.set_dist(v, DIST))
+
+    def stats(self, which=MEMBERS):
+        f = np.zeros(self.p, np.int32)
+        c = np.zeros(self.p, np.int32)
+        it = np.zeros(self.p, np.int64)
+        _check(_lib.plse_get_stats(self._ctx, which, f.ctypes.data_as(C.c_void_p), c.ctypes.data_as(C.c_void_p),
+                                   it.ctypes.data_as(C.c_void_p)), self._ctx)
+        return f, c, it
+
+    def partners(self) -> np.ndarray:
+        a = np.zeros(self.p, np.int32)
+        _check(_lib.plse_get_partners(self._ctx, a), self._ctx)
+        return a
+
+    def counters(self) -> Counters:
+        c = Counters()
+        _check(_lib.plse_get_counters(self._ctx, C.byref(c)), self._ctx)
+        return c
+
+    # -- phases
+    def initialize_population(self) -> None:
+        _check(_lib.plse_init_population(self._ctx), self._ctx)
+
+    def compute_full_distances(self) -> None:
+        _check(_lib.plse_full_distances(self._ctx), self._ctx)
+
+    def improve(self, generation: int):
+        """Improve every offspring -> improved; returns (iterations, best_f, best_idx)."""
+        it, bf, bi = C.c_int64(), C.c_int32(), C.c_int32()
+        _check(_lib.plse_improve(self._ctx, generation, C.byref(it), C.byref(bf), C.byref(bi)), self._ctx)
+        return it.value, bf.value, bi.value
+
+    def compute_cross_distances(self) -> None:
+        _check(_lib.plse_distances(self._ctx), self._ctx)
+
+    def update_population(self) -> UpdateInfo:
+        pbf, nsf = C.c_int32(), C.c_int32()
+        slots = np.zeros(self.p, np.int32)
+        _check(_lib.plse_update(self._ctx, C.byref(pbf), C.byref(nsf), slots), self._ctx)
+        return UpdateInfo(pbf.value, slots[:nsf.value].tolist())
+
+    def reset_exclusion(self) -> None:
+        _check(_lib.plse_reset_exclusion(self._ctx), self._ctx)
+
+    def build_offspring(self, generation: int) -> None:
+        _check(_lib.plse_offspring(self._ctx, generation), self._ctx)
+
+    def trace(self, idx: int, generation: int, max_steps: int):
+        """Per-step parity probe: runs OFFSPRING[idx] through improve (clobbers IMPROVED[idx])."""
+        buf = (Step * max(max_steps, 1))()
+        n = C.c_int64()
+        _check(_lib.plse_trace(self._ctx, idx, generation, max_steps, C.cast(buf, C.c_void_p), C.byref(n)),
+               self._ctx)
+        m = min(n.value, max_steps)
+        return [{k: getattr(buf[i], k) for k, _ in Step._fields_} for i in range(m)], n.value
+
+    def export_elites(self, n_elite: int, dev_ptr: int):
+        f = np.zeros(max(n_elite, 1), np.int32)
+        _check(_lib.plse_export_elites(self._ctx, n_elite, C.c_void_p(dev_ptr), f.ctypes.data_as(C.c_void_p)),
+               self._ctx)
+        return f[:n_elite]
+
+    def import_migrants(self, n_in: int, dev_ptr: int) -> None:
+        _check(_lib.plse_import_migrants(self._ctx, n_in, C.c_void_p(dev_ptr)), self._ctx)
+
+    @property
+    def row_bytes(self) -> int:
+        """bytes per exported/imported u8 colour row (|V| rounded up to 16)."""
+        return (self.nv + 15) // 16 * 16

@@ -1,0 +1,951 @@
+// capi.cu -- the C ABI (include/plse_b200.h): device context, buffer
+// management, the host halves of the population phases, and plse_solve, the
+// generational driver that mirrors engine.hpp:114-262 on top of the kernels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "device_api.h"
+#include "host_internal.h"
+#include "plse_b200.h"
+
+using namespace plse_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e__ = (x);                                                                  \
+        if (e__ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e__)); \
+    } while (0)
+
+template <class T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct plse_ctx {
+    int device = 0, nsm = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int n = 0, nv = 0, nvpad = 0, W = 1, lane_words = 1, l = 0;
+    plse_params prm{};
+    int64_t budget = 0;
+    int stop_f = 0;
+    // graph
+    uint16_t *d_cell = nullptr, *d_rs = nullptr, *d_cs = nullptr, *d_cl = nullptr;
+    uint64_t *d_pr = nullptr, *d_pc = nullptr, *d_below = nullptr;
+    int32_t* d_dom_off = nullptr;
+    uint8_t* d_dom = nullptr;
+    std::vector<uint64_t> h_dommask;  // nv * W, bit k set iff k in D(v) (incl. 0)
+    // population
+    uint8_t *d_members = nullptr, *d_offspring = nullptr, *d_improved = nullptr, *d_next = nullptr;
+    uint16_t *d_dist = nullptr, *d_cross = nullptr, *d_fresh = nullptr, *d_dnext = nullptr;
+    int32_t *d_best_f = nullptr, *d_rep_f = nullptr, *d_mf = nullptr, *d_mc = nullptr, *d_tmpf = nullptr,
+            *d_tmpc = nullptr;
+    int64_t* d_iters = nullptr;
+    unsigned long long* d_bytes = nullptr;
+    std::vector<int32_t> h_mf, h_mc, h_if, h_ic;
+    std::vector<int64_t> h_iters;
+    uint32_t* d_excl = nullptr;
+    int excl_words = 0;
+    int32_t* d_partner = nullptr;
+    // improve launch
+    void* d_rec = nullptr;
+    uint32_t* d_until = nullptr;
+    size_t rec_stride = 0, until_stride = 0;
+    int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
+    size_t smem = 0;
+    int* d_work = nullptr;
+    // pool update scratch
+    int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
+    uint32_t* d_conf = nullptr;
+    uint8_t *d_legal = nullptr, *d_admitted = nullptr;
+    // host staging
+    std::vector<uint8_t> stage;
+    plse_counters ctr{};
+    std::string err;
+
+    ~plse_ctx() {
+        if (device >= 0) cudaSetDevice(device);
+        void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
+                        d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_work, d_order,
+                        d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
+        for (void* b : bufs)
+            if (b) cudaFree(b);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    PopGraph pop_graph() const {
+        PopGraph g;
+        g.n = n;
+        g.nv = nv;
+        g.nvpad = nvpad;
+        g.cell = d_cell;
+        g.row_start = d_rs;
+        g.col_start = d_cs;
+        g.col_list = d_cl;
+        g.dom_off = d_dom_off;
+        g.dom = d_dom;
+        g.below_thr = d_below;
+        return g;
+    }
+    uint8_t* colors(int which) {
+        if (which == PLSE_MEMBERS) return d_members;
+        if (which == PLSE_OFFSPRING) return d_offspring;
+        if (which == PLSE_IMPROVED) return d_improved;
+        throw std::invalid_argument("unknown population buffer");
+    }
+    uint16_t* distbuf(int which) {
+        if (which == PLSE_DIST) return d_dist;
+        if (which == PLSE_CROSS) return d_cross;
+        if (which == PLSE_FRESH) return d_fresh;
+        throw std::invalid_argument("unknown distance matrix");
+    }
+    void launched(cudaError_t e, int count = 1) {
+        CK(e);
+        ctr.kernel_launches += count;
+    }
+    uint64_t stream_base(uint64_t gen) const { return gen * (uint64_t)prm.p_total + (uint64_t)prm.offset; }
+};
+
+namespace {
+
+int finish(plse_ctx* ctx, int code, const char* what) {
+    g_last_error = what;
+    if (ctx) ctx->err = what;
+    return code;
+}
+
+template <class F>
+int guard(plse_ctx* ctx, F&& f) {
+    try {
+        f();
+        return PLSE_OK;
+    } catch (const std::invalid_argument& e) {
+        return finish(ctx, PLSE_ERR_INVALID, e.what());
+    } catch (const CudaError& e) {
+        return finish(ctx, PLSE_ERR_CUDA, e.what());
+    } catch (const Unsupported& e) {
+        return finish(ctx, PLSE_ERR_UNSUPPORTED, e.what());
+    } catch (const std::exception& e) {
+        return finish(ctx, PLSE_ERR_RUNTIME, e.what());
+    } catch (...) {
+        return finish(ctx, PLSE_ERR_RUNTIME, "unknown error");
+    }
+}
+
+// engine.hpp:38-46
+void validate_params(const plse_params& p) {
+    if (p.p < 2) throw std::invalid_argument("population size must be at least 2");
+    if (!(p.gamma > 1.0)) throw std::invalid_argument("gamma must exceed 1");
+    if (p.crossover == PLSE_X_AUX && !(p.beta > p.gamma)) throw std::invalid_argument("beta must exceed gamma");
+    if (!(p.alpha >= 0.0)) throw std::invalid_argument("alpha must be non-negative");
+    if (p.phase1_iters < 0) throw std::invalid_argument("phase budgets must be positive");
+    if (p.crossover < 0 || p.crossover > 2) throw std::invalid_argument("unknown crossover mode");
+    if (p.matching < 0 || p.matching > 1) throw std::invalid_argument("unknown matching strategy");
+    if (p.exclusion < 0 || p.exclusion > 2) throw std::invalid_argument("unknown exclusion scope");
+    if (p.tie_mode != PLSE_TIE_CANON) throw Unsupported("only the canonical tie-break runs on the device");
+    if (p.p_total < 0 || p.offset < 0) throw std::invalid_argument("negative island coordinates");
+}
+
+void eval_into(plse_ctx* c, const uint8_t* colors, std::vector<int32_t>& f, std::vector<int32_t>& cc, int32_t* df,
+               int32_t* dc) {
+    c->launched(launch_eval_fc(c->pop_graph(), c->prm.p, colors, df, dc, c->st));
+    f.resize(c->prm.p);
+    cc.resize(c->prm.p);
+    CK(cudaMemcpyAsync(f.data(), df, sizeof(int32_t) * c->prm.p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(cc.data(), dc, sizeof(int32_t) * c->prm.p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+
+void hamming(plse_ctx* c, const uint8_t* A, const uint8_t* B, uint16_t* D) {
+    c->launched(launch_hamming(A, c->prm.p, B, c->prm.p, c->nv, c->nvpad, D, c->prm.p, c->st));
+}
+
+void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_ctx** out) {
+    if (!gr || !pp || !out) throw std::invalid_argument("null argument");
+    validate_params(*pp);
+    const int n = gr->order, nv = gr->vertex_count;
+    if (n <= 0) throw std::invalid_argument("order must be positive");
+    if (n > 127) throw Unsupported("device path supports n <= 127 (u8 colours, <= 2 mask words)");
+    if (nv <= 0) throw Unsupported("empty reduced graph: nothing to search (trivial instance)");
+    if (nv > 65535) throw Unsupported("device path supports |V| <= 65535");
+    auto ctx = std::make_unique<plse_ctx>();
+    plse_ctx* c = ctx.get();
+    c->device = -1;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw CudaError("no CUDA device " + std::to_string(device));
+    CK(cudaSetDevice(device));
+    c->device = device;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError(std::string("device is not sm_100 (B200): ") + prop.name);
+    c->nsm = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    c->n = n;
+    c->nv = nv;
+    c->l = gr->l;
+    c->prm = *pp;
+    if (c->prm.p_total == 0) c->prm.p_total = c->prm.p;
+    c->budget = pp->phase1_iters > 0 ? pp->phase1_iters : 100LL * nv;
+    if (c->budget >= (1LL << 31)) throw Unsupported("budget must be < 2^31 iterations");
+    c->stop_f = gr->l == 1 ? 1 : 0;
+    c->W = n < 64 ? 1 : 2;
+    c->nvpad = (int)up((size_t)nv, 16);
+    const int nwords = (nv + 31) / 32;
+    c->lane_words = (nwords + 31) / 32;
+    const int W = c->W;
+
+    // ---- graph: cells must be row-major (lsgraph.hpp:149-165)
+    std::vector<uint16_t> cell(nv), rs(n + 1, 0), cs(n + 1, 0), cl(nv);
+    std::vector<int> ccount(n, 0);
+    for (int v = 0; v < nv; ++v) {
+        const int r = gr->cell_row[v], col = gr->cell_col[v];
+        if (r < 0 || r >= n || col < 0 || col >= n) throw std::invalid_argument("cell out of range");
+        if (v && (r < gr->cell_row[v - 1] || (r == gr->cell_row[v - 1] && col <= gr->cell_col[v - 1])))
+            throw std::invalid_argument("vertices must be in row-major cell order");
+        cell[v] = (uint16_t)(r << 8 | col);
+        ccount[col]++;
+    }
+    for (int r = 0, v = 0; r <= n; ++r) {
+        while (v < nv && gr->cell_row[v] < r) ++v;
+        rs[r] = (uint16_t)v;
+    }
+    for (int col = 0; col < n; ++col) cs[col + 1] = (uint16_t)(cs[col] + ccount[col]);
+    {
+        std::vector<int> fill(cs.begin(), cs.end() - 1);
+        for (int v = 0; v < nv; ++v) cl[fill[gr->cell_col[v]]++] = (uint16_t)v;
+    }
+    std::vector<uint64_t> pr((size_t)n * W, 0), pc((size_t)n * W, 0);
+    for (int q = 0; q < gr->n_prefilled; ++q) {
+        const int r = gr->prefilled[3 * q], col = gr->prefilled[3 * q + 1], s = gr->prefilled[3 * q + 2];
+        if (r < 0 || r >= n || col < 0 || col >= n || s < 1 || s > n) throw std::invalid_argument("bad prefilled cell");
+        pr[(size_t)r * W + s / 64] |= 1ULL << (s % 64);
+        pc[(size_t)col * W + s / 64] |= 1ULL << (s % 64);
+    }
+    // domains must be exactly {0} u {k : k not prefilled in row or column} (lsgraph.hpp:152-156)
+    c->h_dommask.assign((size_t)nv * W, 0);
+    std::vector<uint8_t> dom8(gr->dom_offsets[nv]);
+    for (int v = 0; v < nv; ++v) {
+        const int r = gr->cell_row[v], col = gr->cell_col[v];
+        int expect = 1;
+        for (int k = 1; k <= n; ++k) expect += !(((pr[(size_t)r * W + k / 64] | pc[(size_t)col * W + k / 64]) >> (k % 64)) & 1);
+        const int b = gr->dom_offsets[v], e = gr->dom_offsets[v + 1];
+        if (e - b != expect || gr->dom[b] != 0) throw std::invalid_argument("domain does not match the prefilled cells");
+        for (int a = b; a < e; ++a) {
+            const int k = gr->dom[a];
+            if (a > b && (k <= gr->dom[a - 1] ||
+                          (((pr[(size_t)r * W + k / 64] | pc[(size_t)col * W + k / 64]) >> (k % 64)) & 1)))
+                throw std::invalid_argument("domain does not match the prefilled cells");
+            c->h_dommask[(size_t)v * W + k / 64] |= 1ULL << (k % 64);
+            dom8[a] = (uint8_t)k;
+        }
+    }
+    std::vector<uint64_t> below(n + 1, 0);
+    for (int b = 1; b <= n; ++b) below[b] = (0 - (uint64_t)b) % (uint64_t)b;
+
+    c->d_cell = dalloc<uint16_t>(nv);
+    c->d_rs = dalloc<uint16_t>(n + 1);
+    c->d_cs = dalloc<uint16_t>(n + 1);
+    c->d_cl = dalloc<uint16_t>(nv);
+    c->d_pr = dalloc<uint64_t>((size_t)n * W);
+    c->d_pc = dalloc<uint64_t>((size_t)n * W);
+    c->d_below = dalloc<uint64_t>(n + 1);
+    c->d_dom_off = dalloc<int32_t>(nv + 1);
+    c->d_dom = dalloc<uint8_t>(dom8.size());
+    CK(cudaMemcpy(c->d_cell, cell.data(), 2 * nv, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_rs, rs.data(), 2 * (n + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_cs, cs.data(), 2 * (n + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_cl, cl.data(), 2 * nv, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_pr, pr.data(), 8 * pr.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_pc, pc.data(), 8 * pc.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_below, below.data(), 8 * below.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_dom_off, gr->dom_offsets, 4 * (nv + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_dom, dom8.data(), dom8.size(), cudaMemcpyHostToDevice));
+
+    // ---- population buffers
+    const size_t p = (size_t)c->prm.p;
+    const size_t rows = p * c->nvpad;
+    c->d_members = dalloc<uint8_t>(rows);
+    c->d_offspring = dalloc<uint8_t>(rows);
+    c->d_improved = dalloc<uint8_t>(rows);
+    c->d_next = dalloc<uint8_t>(rows);
+    CK(cudaMemset(c->d_members, 0, rows));
+    CK(cudaMemset(c->d_offspring, 0, rows));
+    CK(cudaMemset(c->d_improved, 0, rows));
+    CK(cudaMemset(c->d_next, 0, rows));
+    c->d_dist = dalloc<uint16_t>(p * p);
+    c->d_cross = dalloc<uint16_t>(p * p);
+    c->d_fresh = dalloc<uint16_t>(p * p);
+    c->d_dnext = dalloc<uint16_t>(p * p);
+    CK(cudaMemset(c->d_dist, 0, 2 * p * p));
+    c->d_best_f = dalloc<int32_t>(p);
+    c->d_rep_f = dalloc<int32_t>(p);
+    c->d_mf = dalloc<int32_t>(p);
+    c->d_mc = dalloc<int32_t>(p);
+    c->d_tmpf = dalloc<int32_t>(p);
+    c->d_tmpc = dalloc<int32_t>(p);
+    c->d_iters = dalloc<int64_t>(p);
+    c->d_bytes = dalloc<unsigned long long>(p);
+    c->h_mf.assign(p, nv);
+    c->h_mc.assign(p, 0);
+    c->h_if.assign(p, nv);
+    c->h_ic.assign(p, 0);
+    c->h_iters.assign(p, 0);
+    c->excl_words = (int)((p + 31) / 32);
+    c->d_excl = dalloc<uint32_t>(p * c->excl_words);
+    CK(cudaMemset(c->d_excl, 0, 4 * p * c->excl_words));
+    c->d_partner = dalloc<int32_t>(p);
+    c->d_order = dalloc<int32_t>(2 * p);
+    c->d_sel = dalloc<int32_t>(p);
+    c->d_nsel = dalloc<int32_t>(1);
+    c->d_mts = dalloc<int32_t>(1024);
+    c->d_conf = dalloc<uint32_t>(1024 * 32);
+    c->d_legal = dalloc<uint8_t>(2 * p);
+    c->d_admitted = dalloc<uint8_t>(2 * p);
+    c->d_work = dalloc<int>(1);
+
+    // ---- improve launch shape: maximise resident warps per SM (one individual per warp)
+    const void* kern = improve_kernel_ptr(W);
+    const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+    int best_warps = 0;
+    int force_wpc = 0;
+    if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
+    int max_optin = 0;
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    for (int wpc : {16, 8, 4, 2, 1}) {
+        if (force_wpc && wpc != force_wpc) continue;
+        const size_t smem = L.graph_bytes + (size_t)wpc * L.warp_bytes;
+        if (smem > (size_t)max_optin) continue;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * wpc, smem));
+        if (bps * wpc > best_warps) {
+            best_warps = bps * wpc;
+            c->wpc = wpc;
+            c->smem = smem;
+            c->grid = bps * c->nsm;
+        }
+    }
+    if (best_warps == 0) throw Unsupported("instance too large for the shared-memory resident search");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    c->threads = 32 * c->wpc;
+    c->warps_per_sm = best_warps;
+    c->slots = c->grid * c->wpc;
+    c->rec_stride = up((size_t)nv * tabu_rec_bytes(W), 256);
+    c->until_stride = up((size_t)nv * (n + 1), 64);
+    c->d_rec = dalloc<uint8_t>((size_t)c->slots * c->rec_stride);
+    c->d_until = dalloc<uint32_t>((size_t)c->slots * c->until_stride);
+    c->ctr.grid = c->grid;
+    c->ctr.threads = c->threads;
+    c->ctr.warps_per_sm = c->warps_per_sm;
+    c->ctr.slots = c->slots;
+    c->ctr.smem_bytes = (int64_t)c->smem;
+    *out = ctx.release();
+}
+
+void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) {
+    const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad, W = c->W;
+    if (!host) throw std::invalid_argument("null colours");
+    if (count != (int64_t)p * nv) throw std::invalid_argument("assignment size mismatch");
+    c->stage.assign((size_t)p * nvpad, 0);
+    for (int i = 0; i < p; ++i)
+        for (int v = 0; v < nv; ++v) {
+            const uint16_t k = host[(size_t)i * nv + v];
+            if (k > c->n || !((c->h_dommask[(size_t)v * W + k / 64] >> (k % 64)) & 1))
+                throw std::invalid_argument("assignment leaves vertex domain");
+            c->stage[(size_t)i * nvpad + v] = (uint8_t)k;
+        }
+    uint8_t* dst = c->colors(which);
+    CK(cudaMemcpyAsync(dst, c->stage.data(), c->stage.size(), cudaMemcpyHostToDevice, c->st));
+    if (which == PLSE_MEMBERS) eval_into(c, dst, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
+    if (which == PLSE_IMPROVED) eval_into(c, dst, c->h_if, c->h_ic, c->d_tmpf, c->d_tmpc);
+    CK(cudaStreamSynchronize(c->st));
+}
+
+void download_colors(plse_ctx* c, int which, uint16_t* host) {
+    const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad;
+    if (!host) throw std::invalid_argument("null output");
+    c->stage.resize((size_t)p * nvpad);
+    CK(cudaMemcpyAsync(c->stage.data(), c->colors(which), c->stage.size(), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (int i = 0; i < p; ++i)
+        for (int v = 0; v < nv; ++v) host[(size_t)i * nv + v] = c->stage[(size_t)i * nvpad + v];
+}
+
+void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, plse_step* d_trace, int p_eff,
+                  int first) {
+    ImproveArgs a{};
+    a.n = c->n;
+    a.nv = c->nv;
+    a.nvpad = c->nvpad;
+    a.lane_words = c->lane_words;
+    a.cell = c->d_cell;
+    a.row_start = c->d_rs;
+    a.col_start = c->d_cs;
+    a.col_list = c->d_cl;
+    a.pre_row = c->d_pr;
+    a.pre_col = c->d_pc;
+    a.p = p_eff;
+    a.offspring = c->d_offspring;
+    a.improved = c->d_improved;
+    a.best_f = c->d_best_f;
+    a.repaired_f = c->d_rep_f;
+    a.iters = c->d_iters;
+    a.bytes = c->d_bytes;
+    a.tabu_rec = c->d_rec;
+    a.rec_stride = c->rec_stride;
+    a.until = c->d_until;
+    a.until_stride = c->until_stride;
+    a.work_counter = c->d_work;
+    a.master = c->prm.master_seed;
+    a.generation = gen;
+    a.p_total = (uint64_t)c->prm.p_total;
+    a.offset = (uint64_t)c->prm.offset;
+    a.budget = c->budget;
+    a.stop_f = c->stop_f;
+    a.alpha = c->prm.alpha;
+    a.trace_idx = trace_idx;
+    a.trace_cap = trace_cap;
+    a.trace = d_trace;
+    CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    CK(cudaEventRecord(c->ev0, c->st));
+    c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
+    CK(cudaEventRecord(c->ev1, c->st));
+}
+
+void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t* best_idx) {
+    const int p = c->prm.p;
+    std::vector<unsigned long long> bytes(p);
+    c->h_if.resize(p);
+    c->h_iters.resize(p);
+    CK(cudaMemcpyAsync(c->h_if.data(), c->d_best_f, 4 * p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->h_iters.data(), c->d_iters, 8 * p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(bytes.data(), c->d_bytes, 8 * p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->h_ic.assign(p, 0);
+    int64_t tot = 0;
+    double by = 0;
+    int bf = c->nv + 1, bi = -1;
+    for (int i = 0; i < p; ++i) {
+        tot += c->h_iters[i];
+        by += (double)bytes[i];
+        if (c->h_if[i] < bf) {  // engine.hpp:212-217: strict <, lowest index wins
+            bf = c->h_if[i];
+            bi = i;
+        }
+    }
+    c->ctr.improve_ms = ms;
+    c->ctr.alg_bytes = by;
+    c->ctr.moves = tot;
+    if (iters_total) *iters_total = tot;
+    if (best_f) *best_f = bf;
+    if (best_idx) *best_idx = bi;
+}
+
+// population.hpp:103-183 on the device: host sorts the 2p pool keys, the
+// admission chain runs in blocks of 1024 candidates (k_pool_check/resolve),
+// then next_dist and the next members are gathered on the device.
+void update_impl(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* slots_out) {
+    const int p = c->prm.p, P2 = 2 * p;
+    const double thr = c->nv / c->prm.gamma;
+    std::vector<int> f(P2), legal(P2);
+    for (int i = 0; i < p; ++i) {
+        f[i] = c->h_mf[i];
+        legal[i] = c->h_mc[i] == 0;
+        f[p + i] = c->h_if[i];
+        legal[p + i] = c->h_ic[i] == 0;
+    }
+    std::vector<int32_t> order(P2);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        return std::make_tuple(legal[a] ? 0 : 1, f[a], a) < std::make_tuple(legal[b] ? 0 : 1, f[b], b);
+    });
+    std::vector<uint8_t> leg8(P2);
+    for (int i = 0; i < P2; ++i) leg8[i] = (uint8_t)legal[i];
+    CK(cudaMemcpyAsync(c->d_order, order.data(), 4 * P2, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_legal, leg8.data(), P2, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->d_admitted, 0, P2, c->st));
+    const int one = 1;
+    const uint8_t yes = 1;
+    CK(cudaMemcpyAsync(c->d_sel, &order[0], 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_nsel, &one, 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_admitted, &yes, 1, cudaMemcpyHostToDevice, c->st));
+    PoolView pv{p, c->d_dist, c->d_cross, c->d_fresh};
+    int ns = 1;
+    const int BLK = 1024;
+    for (int lo = 1; lo < P2 && ns < p; lo += BLK) {
+        const int bn = std::min(BLK, P2 - lo);
+        const int cw = (bn + 31) / 32;
+        c->launched(launch_pool_block_check(pv, c->d_order, lo, bn, c->d_sel, ns, thr, c->d_legal, c->d_mts,
+                                            c->d_conf, cw, c->st));
+        c->launched(launch_pool_block_resolve(c->d_order, lo, bn, c->d_mts, c->d_conf, cw, thr, c->d_legal, c->d_sel,
+                                              c->d_nsel, p, c->d_admitted, c->st));
+        CK(cudaMemcpyAsync(&ns, c->d_nsel, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+    std::vector<int32_t> sel(p);
+    CK(cudaMemcpyAsync(sel.data(), c->d_sel, 4 * ns, cudaMemcpyDeviceToHost, c->st));
+    std::vector<uint8_t> adm(P2);
+    CK(cudaMemcpyAsync(adm.data(), c->d_admitted, P2, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int nsf = 0;
+    if (ns < p) {
+        // shortfall rule (population.hpp:157-160): skipped candidates in pool order
+        for (int pos = 1; pos < P2 && ns < p; ++pos) {
+            if (adm[pos]) continue;
+            if (slots_out) slots_out[nsf] = ns;
+            ++nsf;
+            sel[ns++] = order[pos];
+        }
+        CK(cudaMemcpyAsync(c->d_sel, sel.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
+    }
+    c->launched(launch_pool_gather(pv, c->d_sel, c->d_dnext, c->d_members, c->d_improved, c->d_next, c->nvpad, c->st),
+                2);
+    std::swap(c->d_members, c->d_next);
+    std::swap(c->d_dist, c->d_dnext);
+    std::vector<int32_t> nf(p), nc(p);
+    for (int i = 0; i < p; ++i) {
+        const int id = sel[i];
+        nf[i] = f[id];
+        nc[i] = id < p ? c->h_mc[id] : c->h_ic[id - p];
+    }
+    c->h_mf = nf;
+    c->h_mc = nc;
+    CK(cudaMemcpyAsync(c->d_mf, c->h_mf.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_mc, c->h_mc.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (pool_best_f) *pool_best_f = f[order[0]];
+    if (n_shortfall) *n_shortfall = nsf;
+}
+
+void offspring_impl(plse_ctx* c, uint64_t gen) {
+    const int p = c->prm.p;
+    if (c->prm.crossover == PLSE_X_NONE) {
+        CK(cudaMemcpyAsync(c->d_offspring, c->d_members, (size_t)p * c->nvpad, cudaMemcpyDeviceToDevice, c->st));
+    } else {
+        c->launched(launch_match(c->d_dist, p, c->prm.matching, c->prm.exclusion, c->d_excl, c->excl_words,
+                                 c->prm.master_seed, c->stream_base(gen), c->d_partner, c->st));
+        c->launched(launch_crossover(c->d_members, c->d_dist, c->d_partner, p, c->nv, c->nvpad, c->prm.crossover,
+                                     c->prm.beta, c->prm.master_seed, c->stream_base(gen), c->d_offspring, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+}
+
+void init_impl(plse_ctx* c) {
+    c->launched(launch_init_population(c->pop_graph(), c->prm.p, c->prm.master_seed, (uint64_t)c->prm.offset,
+                                       c->d_members, c->st));
+    eval_into(c, c->d_members, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
+    hamming(c, c->d_members, c->d_members, c->d_dist);
+    CK(cudaStreamSynchronize(c->st));
+}
+
+}  // namespace
+
+extern "C" {
+
+int plse_abi_version(void) { return PLSE_ABI_VERSION; }
+
+const char* plse_last_error(const plse_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int plse_generate_instance(int32_t n, double r, uint64_t seed, uint16_t* grid) {
+    return guard(nullptr, [&] {
+        if (!grid) throw std::invalid_argument("null grid");
+        auto g = plse_host::generate_instance(n, r, seed);
+        std::memcpy(grid, g.data(), 2 * g.size());
+    });
+}
+
+int plse_parse_instance(const char* text, int32_t* n, uint16_t* grid, int32_t grid_cap) {
+    return guard(nullptr, [&] {
+        if (!text || !n) throw std::invalid_argument("null argument");
+        int nn = 0;
+        auto g = plse_host::parse_instance(text, nn);
+        *n = nn;
+        if (grid) {
+            if ((int64_t)g.size() > grid_cap) throw std::invalid_argument("grid buffer too small");
+            std::memcpy(grid, g.data(), 2 * g.size());
+        }
+    });
+}
+
+int plse_preprocess(int32_t n, const uint16_t* grid, plse_graph_h** out) {
+    return guard(nullptr, [&] {
+        if (!grid || !out || n <= 0) throw std::invalid_argument("bad arguments");
+        for (int q = 0; q < n * n; ++q)
+            if (grid[q] > n) throw std::invalid_argument("symbol out of range");
+        auto* h = new plse_graph_h;
+        h->g = plse_host::preprocess(n, grid);
+        *out = h;
+    });
+}
+
+void plse_graph_free(plse_graph_h* g) { delete g; }
+
+int plse_graph_view(const plse_graph_h* h, plse_graph* v) {
+    return guard(nullptr, [&] {
+        if (!h || !v) throw std::invalid_argument("null argument");
+        const auto& g = h->g;
+        v->order = g.n;
+        v->vertex_count = g.nv;
+        v->l = g.l;
+        v->cell_row = g.cell_row.data();
+        v->cell_col = g.cell_col.data();
+        v->dom_offsets = g.dom_off.data();
+        v->dom = g.dom.data();
+        v->n_prefilled = (int32_t)(g.prefilled.size() / 3);
+        v->prefilled = g.prefilled.data();
+    });
+}
+
+int plse_create(const plse_graph* graph, const plse_params* params, int32_t device, plse_ctx** out) {
+    return guard(nullptr, [&] { create_impl(graph, params, device, out); });
+}
+
+void plse_destroy(plse_ctx* ctx) { delete ctx; }
+
+int plse_set_colors(plse_ctx* c, int32_t which, const uint16_t* host, int64_t count) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        upload_colors(c, which, host, count);
+    });
+}
+
+int plse_get_colors(plse_ctx* c, int32_t which, uint16_t* host) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        download_colors(c, which, host);
+    });
+}
+
+int plse_get_dist(plse_ctx* c, int32_t which, int32_t* host) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!host) throw std::invalid_argument("null output");
+        const size_t pp = (size_t)c->prm.p * c->prm.p;
+        std::vector<uint16_t> tmp(pp);
+        CK(cudaMemcpyAsync(tmp.data(), c->distbuf(which), 2 * pp, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (size_t q = 0; q < pp; ++q) host[q] = tmp[q];
+    });
+}
+
+int plse_set_dist(plse_ctx* c, int32_t which, const int32_t* host) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!host) throw std::invalid_argument("null input");
+        const size_t pp = (size_t)c->prm.p * c->prm.p;
+        std::vector<uint16_t> tmp(pp);
+        for (size_t q = 0; q < pp; ++q) {
+            if (host[q] < 0 || host[q] > c->nv) throw std::invalid_argument("distance out of range");
+            tmp[q] = (uint16_t)host[q];
+        }
+        CK(cudaMemcpyAsync(c->distbuf(which), tmp.data(), 2 * pp, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_get_stats(plse_ctx* c, int32_t which, int32_t* f, int32_t* cc, int64_t* iters) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        const int p = c->prm.p;
+        std::vector<int32_t> ff, cv;
+        if (which == PLSE_MEMBERS) {
+            ff = c->h_mf;
+            cv = c->h_mc;
+        } else if (which == PLSE_IMPROVED) {
+            ff = c->h_if;
+            cv = c->h_ic;
+        } else {
+            eval_into(c, c->colors(which), ff, cv, c->d_tmpf, c->d_tmpc);
+        }
+        if (f) std::memcpy(f, ff.data(), 4 * p);
+        if (cc) std::memcpy(cc, cv.data(), 4 * p);
+        if (iters) std::memcpy(iters, c->h_iters.data(), 8 * p);
+    });
+}
+
+int plse_get_partners(plse_ctx* c, int32_t* host) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(host, c->d_partner, 4 * c->prm.p, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_get_counters(plse_ctx* c, plse_counters* out) {
+    if (!c || !out) return finish(c, PLSE_ERR_INVALID, "null argument");
+    *out = c->ctr;
+    return PLSE_OK;
+}
+
+int plse_init_population(plse_ctx* c) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        init_impl(c);
+    });
+}
+
+int plse_full_distances(plse_ctx* c) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        hamming(c, c->d_members, c->d_members, c->d_dist);
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_improve(plse_ctx* c, uint64_t generation, int64_t* iters_total, int32_t* best_f, int32_t* best_idx) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        improve_impl(c, generation, -1, 0, nullptr, c->prm.p, 0);
+        collect_improve(c, iters_total, best_f, best_idx);
+    });
+}
+
+int plse_distances(plse_ctx* c) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        hamming(c, c->d_members, c->d_improved, c->d_cross);
+        hamming(c, c->d_improved, c->d_improved, c->d_fresh);
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_update(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* shortfall_slots) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        update_impl(c, pool_best_f, n_shortfall, shortfall_slots);
+    });
+}
+
+int plse_reset_exclusion(plse_ctx* c) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemsetAsync(c->d_excl, 0, 4ull * c->prm.p * c->excl_words, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_offspring(plse_ctx* c, uint64_t generation) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        offspring_impl(c, generation);
+    });
+}
+
+int plse_trace(plse_ctx* c, int32_t idx, uint64_t generation, int64_t max_steps, plse_step* out, int64_t* n_out) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (idx < 0 || idx >= c->prm.p) throw std::invalid_argument("individual out of range");
+        if (max_steps < 0 || (max_steps && !out)) throw std::invalid_argument("bad trace buffer");
+        plse_step* d_tr = nullptr;
+        if (max_steps) d_tr = dalloc<plse_step>((size_t)max_steps);
+        try {
+            improve_impl(c, generation, idx, max_steps, d_tr, idx + 1, idx);
+            CK(cudaStreamSynchronize(c->st));
+            int64_t it = 0;
+            CK(cudaMemcpy(&it, c->d_iters + idx, 8, cudaMemcpyDeviceToHost));
+            const int64_t m = std::min(it, max_steps);
+            if (m) CK(cudaMemcpy(out, d_tr, sizeof(plse_step) * m, cudaMemcpyDeviceToHost));
+            if (n_out) *n_out = it;
+        } catch (...) {
+            if (d_tr) cudaFree(d_tr);
+            throw;
+        }
+        if (d_tr) cudaFree(d_tr);
+    });
+}
+
+int plse_export_elites(plse_ctx* c, int32_t n_elite, void* dev_out, int32_t* f_out) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        const int p = c->prm.p;
+        if (n_elite < 0 || n_elite > p || (n_elite && !dev_out)) throw std::invalid_argument("bad elite count");
+        std::vector<int> idx(p);
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+            return std::make_tuple(c->h_mc[a] ? 1 : 0, c->h_mf[a]) < std::make_tuple(c->h_mc[b] ? 1 : 0, c->h_mf[b]);
+        });
+        for (int e = 0; e < n_elite; ++e) {
+            CK(cudaMemcpyAsync(static_cast<uint8_t*>(dev_out) + (size_t)e * c->nvpad,
+                               c->d_members + (size_t)idx[e] * c->nvpad, c->nvpad, cudaMemcpyDeviceToDevice, c->st));
+            if (f_out) f_out[e] = c->h_mf[idx[e]];
+        }
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+int plse_import_migrants(plse_ctx* c, int32_t n_in, const void* dev_in) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        const int p = c->prm.p;
+        if (n_in < 0 || n_in > p || (n_in && !dev_in)) throw std::invalid_argument("bad migrant count");
+        std::vector<int> idx(p);
+        std::iota(idx.begin(), idx.end(), 0);
+        // worst first: illegal, then highest f, then highest index
+        std::sort(idx.begin(), idx.end(), [&](int a, int b) {
+            return std::make_tuple(c->h_mc[a] ? 1 : 0, c->h_mf[a], a) > std::make_tuple(c->h_mc[b] ? 1 : 0, c->h_mf[b], b);
+        });
+        for (int e = 0; e < n_in; ++e)
+            CK(cudaMemcpyAsync(c->d_members + (size_t)idx[e] * c->nvpad,
+                               static_cast<const uint8_t*>(dev_in) + (size_t)e * c->nvpad, c->nvpad,
+                               cudaMemcpyDeviceToDevice, c->st));
+        eval_into(c, c->d_members, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
+        hamming(c, c->d_members, c->d_members, c->d_dist);
+        CK(cudaStreamSynchronize(c->st));
+    });
+}
+
+// engine.hpp:114-262 (Partial-MPMA) on one device.
+int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, plse_run_result* res,
+               uint16_t* best_colors, plse_generation_cb cb, void* user) {
+    plse_ctx* ctx = nullptr;
+    const int rc = guard(nullptr, [&] {
+        if (!grid || !cfg || !res) throw std::invalid_argument("null argument");
+        validate_params(cfg->params);
+        if (cfg->variant != PLSE_V_PARTIAL)
+            throw Unsupported("only the Partial-MPMA variant runs on the device (PLITS/MPMA is out of scope)");
+        const auto t0 = std::chrono::steady_clock::now();
+        auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+        const plse_host::GraphH g = plse_host::preprocess(n, grid);
+        std::memset(res, 0, sizeof(*res));
+        res->l = g.l;
+        res->upper_bound = g.l == 1 ? n * n - 2 : n * n - g.l;
+        res->vertex_count = g.nv;
+        res->best_f = g.nv;
+        std::vector<uint16_t> best(g.nv, 0);
+        double ttb = 0;
+        auto finalize = [&](int reason) {
+            res->best_score = n * n - g.l - res->best_f;
+            res->proven_optimal = (res->best_f == 0 && g.l != 1) || (res->best_f == 1 && g.l == 1);
+            res->stop_reason = res->proven_optimal ? PLSE_STOP_OPTIMAL : reason;
+            res->elapsed_seconds = elapsed();
+            res->time_to_best_seconds = ttb;
+            if (best_colors) std::memcpy(best_colors, best.data(), 2 * best.size());
+        };
+        if (g.nv == 0) {
+            res->best_f = 0;
+            finalize(PLSE_STOP_TRIVIAL);
+            return;
+        }
+        plse_graph view;
+        view.order = g.n;
+        view.vertex_count = g.nv;
+        view.l = g.l;
+        view.cell_row = g.cell_row.data();
+        view.cell_col = g.cell_col.data();
+        view.dom_offsets = g.dom_off.data();
+        view.dom = g.dom.data();
+        view.n_prefilled = (int32_t)(g.prefilled.size() / 3);
+        view.prefilled = g.prefilled.data();
+        create_impl(&view, &cfg->params, cfg->device, &ctx);
+        plse_ctx* c = ctx;
+        const int p = c->prm.p;
+        const bool opt_stop = !cfg->disable_optimal_stop;
+        auto is_opt = [&](int f) { return (f == 0 && g.l != 1) || (f == 1 && g.l == 1); };
+        auto fetch_row = [&](uint8_t* buf, int i) {
+            std::vector<uint8_t> row(c->nvpad);
+            CK(cudaMemcpy(row.data(), buf + (size_t)i * c->nvpad, c->nvpad, cudaMemcpyDeviceToHost));
+            for (int v = 0; v < g.nv; ++v) best[v] = row[v];
+        };
+        init_impl(c);
+        for (int i = 0; i < p; ++i)
+            if (c->h_mc[i] == 0 && c->h_mf[i] < res->best_f) {
+                res->best_f = c->h_mf[i];
+                fetch_row(c->d_members, i);
+                ttb = elapsed();
+            }
+        if (opt_stop && is_opt(res->best_f)) {
+            finalize(PLSE_STOP_OPTIMAL);
+            return;
+        }
+        CK(cudaMemcpy(c->d_offspring, c->d_members, (size_t)p * c->nvpad, cudaMemcpyDeviceToDevice));
+        CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
+        for (int64_t gen = 1;; ++gen) {
+            int64_t it = 0;
+            int32_t bf = 0, bi = -1;
+            improve_impl(c, (uint64_t)gen, -1, 0, nullptr, p, 0);
+            collect_improve(c, &it, &bf, &bi);
+            res->total_iterations += it;
+            res->generations = gen;
+            if (bi >= 0 && bf < res->best_f) {
+                res->best_f = bf;
+                fetch_row(c->d_improved, bi);
+                ttb = elapsed();
+            }
+            const bool optimal = opt_stop && is_opt(res->best_f);
+            const bool time_up = cfg->time_limit > 0 && elapsed() >= cfg->time_limit;
+            const bool iters_up = cfg->iteration_limit > 0 && res->total_iterations >= cfg->iteration_limit;
+            const bool gens_up = cfg->generation_limit > 0 && gen >= cfg->generation_limit;
+            const bool target = cfg->target_score > 0 && (n * n - g.l - res->best_f) >= cfg->target_score;
+            if (optimal || time_up || iters_up || gens_up || target) {
+                if (cb) cb(gen, res->best_f, res->total_iterations, elapsed(), 0, user);
+                finalize(optimal ? PLSE_STOP_OPTIMAL
+                         : time_up ? PLSE_STOP_TIME
+                         : iters_up ? PLSE_STOP_ITERS
+                         : gens_up ? PLSE_STOP_GENS
+                                   : PLSE_STOP_TARGET);
+                return;
+            }
+            hamming(c, c->d_members, c->d_improved, c->d_cross);
+            hamming(c, c->d_improved, c->d_improved, c->d_fresh);
+            int32_t pbf = 0, nsf = 0;
+            update_impl(c, &pbf, &nsf, nullptr);
+            if (c->prm.exclusion == PLSE_E_GENERATION) CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
+            offspring_impl(c, (uint64_t)gen);
+            if (cb) cb(gen, res->best_f, res->total_iterations, elapsed(), nsf, user);
+        }
+    });
+    delete ctx;
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// device_api.h -- internal interface between the host context (capi.cu) and
+// the sm_100a kernels.  Not part of the public C ABI (include/plse_b200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plse_b200.h"
+
+namespace plse_dev {
+
+constexpr int kImproveMaxThreads = 512;
+
+struct ImproveArgs {
+    // graph (global copies; the kernel stages them in shared memory)
+    int n, nv, nvpad, lane_words;
+    const uint16_t* cell;       // [nv] row << 8 | col
+    const uint16_t* row_start;  // [n+1] survivors of row r are ids [row_start[r], row_start[r+1])
+    const uint16_t* col_start;  // [n+1]
+    const uint16_t* col_list;   // [nv] survivors grouped by column, ascending
+    const uint64_t* pre_row;    // [n*W] prefilled symbols per row
+    const uint64_t* pre_col;    // [n*W]
+    // population
+    int p;
+    const uint8_t* offspring;   // [p*nvpad]
+    uint8_t* improved;          // [p*nvpad]
+    int32_t* best_f;
+    int32_t* repaired_f;
+    int64_t* iters;
+    unsigned long long* bytes;
+    // per-warp-slot tabu scratch
+    void* tabu_rec;
+    size_t rec_stride;          // bytes per slot
+    uint32_t* until;
+    size_t until_stride;        // u32 per slot
+    int* work_counter;
+    // streams (engine.hpp:189-191): seed = derive(master, 2, gen*p_total + offset + i)
+    uint64_t master, generation, p_total, offset;
+    int64_t budget;
+    int stop_f;
+    double alpha;
+    // parity probe
+    int trace_idx;
+    int64_t trace_cap;
+    void* trace;
+};
+
+struct ImproveSmemLayout {
+    size_t cell, rs, cs, cl, pr, pc, graph_bytes;
+    size_t warp0, warp_bytes, w_col, w_conf, w_R, w_C, w_U;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, int nvpad, int lane_words, int W) {
+    ImproveSmemLayout L;
+    size_t o = 0;
+    L.cell = o;
+    o += (size_t)nv * 2;
+    L.rs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cl = o;
+    o += (size_t)nv * 2;
+    o = align_up(o, 16);
+    L.pr = o;
+    o += (size_t)n * W * 8;
+    L.pc = o;
+    o += (size_t)n * W * 8;
+    o = align_up(o, 16);
+    L.graph_bytes = o;
+    L.warp0 = o;
+    size_t w = 0;
+    L.w_col = w;
+    w += (size_t)nvpad;
+    L.w_conf = w;
+    w += (size_t)nvpad;
+    w = align_up(w, 16);
+    L.w_R = w;
+    w += (size_t)n * W * 8;
+    L.w_C = w;
+    w += (size_t)n * W * 8;
+    L.w_U = w;
+    w += (size_t)32 * lane_words * 4;
+    L.warp_bytes = align_up(w, 16);
+    return L;
+}
+
+size_t tabu_rec_bytes(int W);
+const void* improve_kernel_ptr(int W);
+cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
+
+// ---- distances (K3)
+// D[i][j] = #{v : A_i[v] != B_j[v]} for u8 rows with stride nvpad (pad bytes equal)
+cudaError_t launch_hamming(const uint8_t* A, int na, const uint8_t* B, int nb, int nv, int nvpad, uint16_t* D,
+                           int ldd, cudaStream_t st);
+
+// ---- population kernels (population.cu)
+struct PopGraph {
+    int n, nv, nvpad;
+    const uint16_t* cell;
+    const uint16_t* row_start;
+    const uint16_t* col_start;
+    const uint16_t* col_list;
+    const int32_t* dom_off;
+    const uint8_t* dom;
+    const uint64_t* below_thr;  // [n+1] (2^64 - b) % b for b = 1..n
+};
+cudaError_t launch_init_population(const PopGraph& g, int p, uint64_t master, uint64_t offset, uint8_t* members,
+                                   cudaStream_t st);
+cudaError_t launch_eval_fc(const PopGraph& g, int p, const uint8_t* colors, int32_t* f, int32_t* c,
+                           cudaStream_t st);
+cudaError_t launch_match(const uint16_t* dist, int p, int matching, int exclusion, uint32_t* excl, int excl_words,
+                         uint64_t master, uint64_t stream_base, int32_t* partner, cudaStream_t st);
+cudaError_t launch_crossover(const uint8_t* members, const uint16_t* dist, const int32_t* partner, int p, int nv,
+                             int nvpad, int mode, double beta, uint64_t master, uint64_t stream_base,
+                             uint8_t* offspring, cudaStream_t st);
+// pool update helpers
+struct PoolView {
+    int p;
+    const uint16_t* dist;   // members x members
+    const uint16_t* cross;  // members x improved
+    const uint16_t* fresh;  // improved x improved
+};
+cudaError_t launch_pool_block_check(const PoolView& pv, const int32_t* order, int blk_lo, int blk_n,
+                                    const int32_t* selected, int n_selected, double thr, const uint8_t* legal,
+                                    int32_t* min_to_sel, uint32_t* conflict, int cwords, cudaStream_t st);
+cudaError_t launch_pool_block_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
+                                      const uint32_t* conflict, int cwords, double thr, const uint8_t* legal,
+                                      int32_t* selected, int32_t* n_selected, int p, uint8_t* admitted,
+                                      cudaStream_t st);
+cudaError_t launch_pool_gather(const PoolView& pv, const int32_t* sel, uint16_t* next_dist,
+                               const uint8_t* members, const uint8_t* improved, uint8_t* next_members, int nvpad,
+                               cudaStream_t st);
+cudaError_t launch_u16_to_i32(const uint16_t* in, int32_t* out, size_t count, cudaStream_t st);
+cudaError_t launch_i32_to_u16(const int32_t* in, uint16_t* out, size_t count, cudaStream_t st);
+cudaError_t launch_colors_u16_to_u8(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, cudaStream_t st);
+cudaError_t launch_colors_u8_to_u16(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad, cudaStream_t st);
+
+}  // namespace plse_dev

@@ -1,0 +1,156 @@
+// host_graph.cpp -- host side of the boundary that the north star keeps on the
+// CPU: instance generation / parsing and the PLSE -> partial-colouring
+// reduction.  Same semantics as the reference (cited per function), written
+// for this library; exported through include/plse_b200.h.
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host_internal.h"
+
+namespace plse_host {
+
+using plse_dev::Xoshiro;
+using plse_dev::derive_seed;
+
+// instance.hpp:204-262 -- random partial Latin square: uniform empty cell,
+// uniform admissible symbol, resample on dead cells, restart with stream
+// (seed, 4, restart) after 50 n^2 consecutive failures, at most 100 restarts.
+std::vector<uint16_t> generate_instance(int n, double r, uint64_t seed) {
+    if (n <= 0) throw std::invalid_argument("order must be positive");
+    if (!(r > 0.0 && r < 1.0)) throw std::invalid_argument("fill ratio must be in (0,1)");
+    const int cells = n * n;
+    const int want = static_cast<int>(r * cells);
+    const int fail_cap = 50 * cells;
+    std::vector<uint16_t> grid(static_cast<size_t>(cells));
+    std::vector<uint8_t> row_has(static_cast<size_t>(n) * (n + 1)), col_has(static_cast<size_t>(n) * (n + 1));
+    std::vector<int> open(static_cast<size_t>(cells));
+    std::vector<uint16_t> cand;
+    for (int attempt = 0; attempt < 100; ++attempt) {
+        Xoshiro rng(derive_seed(seed, 4, static_cast<uint64_t>(attempt)));
+        std::fill(grid.begin(), grid.end(), 0);
+        std::fill(row_has.begin(), row_has.end(), 0);
+        std::fill(col_has.begin(), col_has.end(), 0);
+        for (int q = 0; q < cells; ++q) open[q] = q;
+        int n_open = cells, placed = 0, misses = 0;
+        while (placed < want && misses < fail_cap) {
+            const int slot = static_cast<int>(rng.below(static_cast<uint64_t>(n_open)));
+            const int cell = open[slot];
+            const int rr = cell / n, cc = cell % n;
+            cand.clear();
+            for (int s = 1; s <= n; ++s)
+                if (!row_has[rr * (n + 1) + s] && !col_has[cc * (n + 1) + s]) cand.push_back(static_cast<uint16_t>(s));
+            if (cand.empty()) {
+                ++misses;
+                continue;
+            }
+            const uint16_t s = cand[rng.below(cand.size())];
+            grid[cell] = s;
+            row_has[rr * (n + 1) + s] = 1;
+            col_has[cc * (n + 1) + s] = 1;
+            open[slot] = open[--n_open];
+            ++placed;
+            misses = 0;
+        }
+        if (placed == want) return grid;
+    }
+    throw std::runtime_error("instance generation failed: (n=" + std::to_string(n) + ", r=" + std::to_string(r) +
+                             ") exhausted the retry budget");
+}
+
+// instance.hpp:107-170 -- "n" header line, then n rows of n integers; blank
+// lines skipped; errors carry the 1-based line number.
+std::vector<uint16_t> parse_instance(const std::string& text, int& n_out) {
+    std::istringstream in(text);
+    std::string line;
+    int lineno = 0;
+    auto fail = [&](int at, const std::string& msg) -> void {
+        throw std::runtime_error("line " + std::to_string(at) + ": " + msg);
+    };
+    auto next = [&](const char* what) {
+        while (std::getline(in, line)) {
+            ++lineno;
+            if (line.find_first_not_of(" \t\r") != std::string::npos) return;
+        }
+        fail(lineno + 1, std::string("unexpected end of input, expected ") + what);
+    };
+    next("grid order");
+    long n = 0;
+    {
+        std::istringstream ls(line);
+        if (!(ls >> n) || n <= 0) fail(lineno, "malformed header: expected positive grid order");
+        std::string rest;
+        if (ls >> rest) fail(lineno, "malformed header: trailing tokens");
+    }
+    if (n > 0xFFFF) fail(lineno, "grid order too large");
+    std::vector<uint16_t> grid(static_cast<size_t>(n) * n);
+    for (long rr = 0; rr < n; ++rr) {
+        next("grid row");
+        std::istringstream ls(line);
+        for (long cc = 0; cc < n; ++cc) {
+            long v = 0;
+            if (!(ls >> v)) fail(lineno, "malformed row: expected " + std::to_string(n) + " entries");
+            if (v < 0 || v > n) fail(lineno, "symbol out of range: " + std::to_string(v));
+            grid[rr * n + cc] = static_cast<uint16_t>(v);
+        }
+        std::string rest;
+        if (ls >> rest) fail(lineno, "malformed row: trailing tokens");
+    }
+    for (long rr = 0; rr < n; ++rr) {
+        std::vector<int> seen(static_cast<size_t>(n) + 1, 0);
+        for (long cc = 0; cc < n; ++cc) {
+            const int s = grid[rr * n + cc];
+            if (s && seen[s]++) fail(static_cast<int>(2 + rr), "duplicate symbol " + std::to_string(s) + " in row " + std::to_string(rr));
+        }
+    }
+    for (long cc = 0; cc < n; ++cc) {
+        std::vector<int> seen(static_cast<size_t>(n) + 1, 0);
+        for (long rr = 0; rr < n; ++rr) {
+            const int s = grid[rr * n + cc];
+            if (s && seen[s]++) fail(static_cast<int>(2 + rr), "duplicate symbol " + std::to_string(s) + " in column " + std::to_string(cc));
+        }
+    }
+    n_out = static_cast<int>(n);
+    return grid;
+}
+
+// lsgraph.hpp:115-211 -- drop prefilled cells (removing their symbol from the
+// row/column domains), drop cells left with domain {0} (counted in l), keep
+// the rest row-major with domains {0} u free symbols.
+GraphH preprocess(int n, const uint16_t* grid) {
+    GraphH g;
+    g.n = n;
+    std::vector<uint8_t> used(static_cast<size_t>(2) * n * (n + 1), 0);
+    for (int cell = 0; cell < n * n; ++cell) {
+        const int s = grid[cell];
+        if (!s) continue;
+        used[(cell / n) * (n + 1) + s] = 1;
+        used[(n + cell % n) * (n + 1) + s] = 1;
+        g.prefilled.push_back(cell / n);
+        g.prefilled.push_back(cell % n);
+        g.prefilled.push_back(s);
+    }
+    g.dom_off.push_back(0);
+    for (int cell = 0; cell < n * n; ++cell) {
+        if (grid[cell]) continue;
+        const int rr = cell / n, cc = cell % n;
+        const size_t mark = g.dom.size();
+        g.dom.push_back(0);
+        for (int s = 1; s <= n; ++s)
+            if (!used[rr * (n + 1) + s] && !used[(n + cc) * (n + 1) + s]) g.dom.push_back(static_cast<uint16_t>(s));
+        if (g.dom.size() == mark + 1) {
+            g.dom.resize(mark);
+            ++g.l;
+            continue;
+        }
+        g.cell_row.push_back(rr);
+        g.cell_col.push_back(cc);
+        g.dom_off.push_back(static_cast<int32_t>(g.dom.size()));
+    }
+    g.nv = static_cast<int>(g.cell_row.size());
+    return g;
+}
+
+}  // namespace plse_host

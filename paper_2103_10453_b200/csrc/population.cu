@@ -1,0 +1,354 @@
+// population.cu -- K0 init, f/c evaluation, K4a pool update, K4b matching,
+// K4c crossover on sm_100a.  All integer / byte work (HBM-bound); the
+// sequential xoshiro streams of the reference are replayed exactly, one
+// thread per individual, so these phases are bit-exact with the reference.
+#include "common.cuh"
+#include "device_api.h"
+
+namespace plse_dev {
+
+// ---------------------------------------------------------------- K0 init
+// engine.hpp:88-106: colour = D(v)[1 + next_index(|D(v)|-1)] from stream (seed, 1, i)
+__global__ void k_init_population(const PopGraph g, int p, uint64_t master, uint64_t offset, uint8_t* members) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    Xoshiro rng(derive_seed(master, 1, offset + (uint64_t)i));
+    uint8_t* row = members + (size_t)i * g.nvpad;
+    uint32_t word[4] = {0, 0, 0, 0};
+    for (int v = 0; v < g.nvpad; ++v) {
+        uint32_t c = 0;
+        if (v < g.nv) {
+            const int begin = g.dom_off[v] + 1;
+            const int b = g.dom_off[v + 1] - begin;
+            const uint64_t x = rng.below((uint64_t)b, g.below_thr[b]);
+            c = g.dom[begin + (int)x];
+        }
+        word[(v >> 2) & 3] |= c << (8 * (v & 3));
+        if ((v & 15) == 15) {
+            *reinterpret_cast<uint4*>(row + v - 15) = make_uint4(word[0], word[1], word[2], word[3]);
+            word[0] = word[1] = word[2] = word[3] = 0;
+        }
+    }
+}
+
+cudaError_t launch_init_population(const PopGraph& g, int p, uint64_t master, uint64_t offset, uint8_t* members,
+                                   cudaStream_t st) {
+    k_init_population<<<(p + 127) / 128, 128, 0, st>>>(g, p, master, offset, members);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- f / c
+// coloring.hpp:59-73: f = #zeros, c = #edges with equal non-zero colours.
+// One warp per individual; c = sum over coloured v of same-coloured neighbours / 2.
+__global__ void k_eval_fc(const PopGraph g, int p, const uint8_t* colors, int32_t* fo, int32_t* co) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= p) return;
+    const uint8_t* row = colors + (size_t)i * g.nvpad;
+    int zf = 0, cc = 0;
+    for (int v = lane; v < g.nv; v += 32) {
+        const int k = row[v];
+        if (!k) {
+            ++zf;
+            continue;
+        }
+        const uint16_t rc = g.cell[v];
+        const int r = rc >> 8, c = rc & 0xFF;
+        for (int u = g.row_start[r]; u < g.row_start[r + 1]; ++u) cc += (row[u] == k);
+        for (int t = g.col_start[c]; t < g.col_start[c + 1]; ++t) cc += (row[g.col_list[t]] == k);
+        cc -= 2;
+    }
+    zf = __reduce_add_sync(kFull, zf);
+    cc = __reduce_add_sync(kFull, cc);
+    if (lane == 0) {
+        if (fo) fo[i] = zf;
+        if (co) co[i] = cc / 2;
+    }
+}
+
+cudaError_t launch_eval_fc(const PopGraph& g, int p, const uint8_t* colors, int32_t* f, int32_t* c, cudaStream_t st) {
+    k_eval_fc<<<(p + 7) / 8, 256, 0, st>>>(g, p, colors, f, c);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K4b matching
+// crossover.hpp:67-83 + nearest_neighbor population.hpp:209-228.  The partner
+// loop is sequential in the reference but every row reads and writes only its
+// own (slot-keyed) exclusion row, so rows are independent: one warp per row.
+__global__ void k_match(const uint16_t* dist, int p, int matching, int exclusion, uint32_t* excl, int ew,
+                        uint64_t master, uint64_t stream_base, int32_t* partner) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= p) return;
+    int j;
+    if (matching == PLSE_M_RANDOM) {
+        if (lane == 0) {
+            Xoshiro m(derive_seed(master, 6, stream_base + (uint64_t)i));
+            j = (int)m.below((uint64_t)(p - 1));
+            if (j >= i) ++j;
+        }
+        j = __shfl_sync(kFull, j, 0);
+    } else {
+        const uint16_t* row = dist + (size_t)i * p;
+        const uint32_t* ex = excl + (size_t)i * ew;
+        const bool use_ex = exclusion != PLSE_E_OFF;
+        uint32_t bu = 0xFFFFFFFFu, br = 0xFFFFFFFFu;  // (d << 16 | j) would overflow for p > 65535: keep two keys
+        int bju = -1, bjr = -1;
+        for (int jj = lane; jj < p; jj += 32) {
+            if (jj == i) continue;
+            const uint32_t d = row[jj];
+            if (d < bu) {
+                bu = d;
+                bju = jj;
+            }
+            if (use_ex && ((ex[jj >> 5] >> (jj & 31)) & 1)) continue;
+            if (d < br) {
+                br = d;
+                bjr = jj;
+            }
+        }
+        // warp argmin, lowest index on ties
+        const uint32_t mu = __reduce_min_sync(kFull, bu);
+        const uint32_t ju = __reduce_min_sync(kFull, bu == mu && bju >= 0 ? (uint32_t)bju : 0xFFFFFFFFu);
+        const uint32_t mr = __reduce_min_sync(kFull, br);
+        const uint32_t jr = __reduce_min_sync(kFull, br == mr && bjr >= 0 ? (uint32_t)bjr : 0xFFFFFFFFu);
+        if (jr == 0xFFFFFFFFu) {
+            // every partner excluded: clear the row, return the unrestricted nearest neighbour
+            for (int w = lane; w < ew; w += 32) excl[(size_t)i * ew + w] = 0;
+            __syncwarp();
+            j = (int)ju;
+        } else {
+            j = (int)jr;
+        }
+    }
+    if (lane == 0) {
+        if (exclusion != PLSE_E_OFF) excl[(size_t)i * ew + (j >> 5)] |= 1u << (j & 31);
+        partner[i] = j;
+    }
+}
+
+cudaError_t launch_match(const uint16_t* dist, int p, int matching, int exclusion, uint32_t* excl, int excl_words,
+                         uint64_t master, uint64_t stream_base, int32_t* partner, cudaStream_t st) {
+    k_match<<<(p + 7) / 8, 256, 0, st>>>(dist, p, matching, exclusion, excl, excl_words, master, stream_base,
+                                         partner);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K4c crossover
+// crossover.hpp:26-46, 85-102.  keep first parent's colour iff
+// next_double() < p_ij  <=>  (x >> 11) < ceil(p_ij * 2^53)  (exact: both sides scaled by 2^53).
+__global__ void k_crossover(const uint8_t* members, const uint16_t* dist, const int32_t* partner, int p, int nv,
+                            int nvpad, int mode, double beta, uint64_t master, uint64_t stream_base,
+                            uint8_t* offspring) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const uint8_t* first = members + (size_t)i * nvpad;
+    uint8_t* child = offspring + (size_t)i * nvpad;
+    if (mode == PLSE_X_NONE) {
+        for (int t = 0; t < nvpad / 16; ++t)
+            reinterpret_cast<uint4*>(child)[t] = reinterpret_cast<const uint4*>(first)[t];
+        return;
+    }
+    const int j = partner[i];
+    const uint8_t* second = members + (size_t)j * nvpad;
+    double pij = 0.5;
+    if (mode == PLSE_X_AUX) {
+        const int32_t d = dist[(size_t)i * p + j];
+        if ((double)d * beta <= (double)nv) {
+            for (int t = 0; t < nvpad / 16; ++t)
+                reinterpret_cast<uint4*>(child)[t] = reinterpret_cast<const uint4*>(first)[t];
+            return;
+        }
+        pij = 1.0 - (double)nv / (beta * (double)d);
+    }
+    const uint64_t thr = (uint64_t)ceil(pij * 9007199254740992.0);
+    Xoshiro rng(derive_seed(master, 3, stream_base + (uint64_t)i));
+    for (int t = 0; t < nvpad / 16; ++t) {
+        const uint4 a4 = reinterpret_cast<const uint4*>(first)[t];
+        const uint4 b4 = reinterpret_cast<const uint4*>(second)[t];
+        uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w}, b[4] = {b4.x, b4.y, b4.z, b4.w}, o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t sel = 0;
+#pragma unroll
+            for (int by = 0; by < 4; ++by) {
+                const int v = t * 16 + q * 4 + by;
+                if (v < nv && (rng.next() >> 11) < thr) sel |= 0xFFu << (8 * by);
+            }
+            o[q] = (a[q] & sel) | (b[q] & ~sel);
+        }
+        // pad bytes (v >= nv) take the second parent's pad byte, which is 0 like the first's
+        reinterpret_cast<uint4*>(child)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+cudaError_t launch_crossover(const uint8_t* members, const uint16_t* dist, const int32_t* partner, int p, int nv,
+                             int nvpad, int mode, double beta, uint64_t master, uint64_t stream_base,
+                             uint8_t* offspring, cudaStream_t st) {
+    k_crossover<<<(p + 63) / 64, 64, 0, st>>>(members, dist, partner, p, nv, nvpad, mode, beta, master, stream_base,
+                                             offspring);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K4a pool update
+// population.hpp:103-183.  Pool ids 0..p-1 are members, p..2p-1 improved.
+__device__ __forceinline__ uint32_t pool_dist(const PoolView& v, int a, int b) {
+    const int p = v.p;
+    if (a == b) return 0;
+    if (a < p && b < p) return v.dist[(size_t)a * p + b];
+    if (a >= p && b >= p) return v.fresh[(size_t)(a - p) * p + (b - p)];
+    return a < p ? v.cross[(size_t)a * p + (b - p)] : v.cross[(size_t)b * p + (a - p)];
+}
+
+// One CTA per block candidate: min distance to the already selected set, and the
+// candidate's conflict row (d <= |V|/gamma) against the later candidates of the block.
+__global__ void k_pool_check(const PoolView pv, const int32_t* order, int blk_lo, int blk_n, const int32_t* sel,
+                             int n_sel, double thr, const uint8_t* legal, int32_t* min_to_sel, uint32_t* conflict,
+                             int cwords) {
+    const int t = blockIdx.x;
+    const int c = order[blk_lo + t];
+    __shared__ uint32_t red[32];
+    if (!legal[c]) {
+        if (threadIdx.x == 0) min_to_sel[t] = 0;
+        for (int w = threadIdx.x; w < cwords; w += blockDim.x) conflict[(size_t)t * cwords + w] = 0;
+        return;
+    }
+    uint32_t md = 0xFFFFFFFFu;
+    for (int q = threadIdx.x; q < n_sel; q += blockDim.x) md = min(md, pool_dist(pv, c, sel[q]));
+    md = __reduce_min_sync(kFull, md);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = md;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0xFFFFFFFFu;
+        x = __reduce_min_sync(kFull, x);
+        if (threadIdx.x == 0) min_to_sel[t] = (int32_t)min(x, 0x7FFFFFFFu);
+    }
+    for (int base = 0; base < cwords * 32; base += blockDim.x) {
+        const int u = base + threadIdx.x;
+        bool hit = false;
+        if (u > t && u < blk_n) {
+            const int cu = order[blk_lo + u];
+            hit = legal[cu] && !((double)pool_dist(pv, c, cu) > thr);
+        }
+        const unsigned bal = __ballot_sync(kFull, hit);
+        if ((threadIdx.x & 31) == 0 && (u >> 5) < cwords) conflict[(size_t)t * cwords + (u >> 5)] = bal;
+    }
+}
+
+cudaError_t launch_pool_block_check(const PoolView& pv, const int32_t* order, int blk_lo, int blk_n,
+                                    const int32_t* selected, int n_selected, double thr, const uint8_t* legal,
+                                    int32_t* min_to_sel, uint32_t* conflict, int cwords, cudaStream_t st) {
+    if (blk_n <= 0) return cudaSuccess;
+    k_pool_check<<<blk_n, 256, 0, st>>>(pv, order, blk_lo, blk_n, selected, n_selected, thr, legal, min_to_sel,
+                                         conflict, cwords);
+    return cudaGetLastError();
+}
+
+// One warp walks the block in pool order (the reference's greedy, population.hpp:144-156).
+// Lane l keeps word l of the "blocked by an admitted in-block candidate" bitmask.
+__global__ void k_pool_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
+                               const uint32_t* conflict, int cwords, double thr, const uint8_t* legal, int32_t* sel,
+                               int32_t* n_sel_io, int p, uint8_t* admitted) {
+    const int lane = threadIdx.x;
+    int ns = *n_sel_io;
+    uint32_t blocked = 0;  // lane's word(s); cwords <= 32
+    for (int t = 0; t < blk_n && ns < p; ++t) {
+        const int c = order[blk_lo + t];
+        const uint32_t wbits = __shfl_sync(kFull, blocked, t >> 5);
+        const bool is_blocked = (wbits >> (t & 31)) & 1;
+        const bool ok = legal[c] && !is_blocked && ((double)min_to_sel[t] > thr);
+        if (ok) {
+            if (lane == 0) {
+                sel[ns] = c;
+                admitted[blk_lo + t] = 1;
+            }
+            ++ns;
+            if (lane < cwords) blocked |= conflict[(size_t)t * cwords + lane];
+        }
+    }
+    if (lane == 0) *n_sel_io = ns;
+}
+
+cudaError_t launch_pool_block_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
+                                      const uint32_t* conflict, int cwords, double thr, const uint8_t* legal,
+                                      int32_t* selected, int32_t* n_selected, int p, uint8_t* admitted,
+                                      cudaStream_t st) {
+    if (blk_n <= 0) return cudaSuccess;
+    k_pool_resolve<<<1, 32, 0, st>>>(order, blk_lo, blk_n, min_to_sel, conflict, cwords, thr, legal, selected,
+                                     n_selected, p, admitted);
+    return cudaGetLastError();
+}
+
+// next_dist[i][j] = pool_dist(sel[i], sel[j]); next_members[i] = pool row sel[i]
+__global__ void k_pool_gather_dist(const PoolView pv, const int32_t* sel, uint16_t* next_dist) {
+    const int p = pv.p;
+    const int i = blockIdx.y;
+    const int a = sel[i];
+    for (int jj = blockIdx.x * blockDim.x + threadIdx.x; jj < p; jj += gridDim.x * blockDim.x)
+        next_dist[(size_t)i * p + jj] = (uint16_t)pool_dist(pv, a, sel[jj]);
+}
+
+__global__ void k_pool_gather_rows(const int32_t* sel, int p, const uint8_t* members, const uint8_t* improved,
+                                   uint8_t* next_members, int nvpad) {
+    const int i = blockIdx.x;
+    const int a = sel[i];
+    const uint4* src = reinterpret_cast<const uint4*>(a < p ? members + (size_t)a * nvpad
+                                                            : improved + (size_t)(a - p) * nvpad);
+    uint4* dst = reinterpret_cast<uint4*>(next_members + (size_t)i * nvpad);
+    for (int t = threadIdx.x; t < nvpad / 16; t += blockDim.x) dst[t] = src[t];
+}
+
+cudaError_t launch_pool_gather(const PoolView& pv, const int32_t* sel, uint16_t* next_dist, const uint8_t* members,
+                               const uint8_t* improved, uint8_t* next_members, int nvpad, cudaStream_t st) {
+    dim3 grid((pv.p + 255) / 256 < 8 ? (pv.p + 255) / 256 : 8, pv.p);
+    k_pool_gather_dist<<<grid, 256, 0, st>>>(pv, sel, next_dist);
+    k_pool_gather_rows<<<pv.p, 128, 0, st>>>(sel, pv.p, members, improved, next_members, nvpad);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- conversions
+__global__ void k_u16_to_i32(const uint16_t* in, int32_t* out, size_t n) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
+        out[t] = in[t];
+}
+__global__ void k_i32_to_u16(const int32_t* in, uint16_t* out, size_t n) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
+        out[t] = (uint16_t)in[t];
+}
+__global__ void k_c16_to_8(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad) {
+    const size_t total = (size_t)p * nvpad;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = t / nvpad, v = t % nvpad;
+        out[t] = v < (size_t)nv ? (uint8_t)in[i * nv + v] : 0;
+    }
+}
+__global__ void k_c8_to_16(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad) {
+    const size_t total = (size_t)p * nv;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = t / nv, v = t % nv;
+        out[t] = in[i * nvpad + v];
+    }
+}
+
+static int grid_for(size_t n) {
+    size_t g = (n + 255) / 256;
+    return (int)(g > 148 * 16 ? 148 * 16 : (g ? g : 1));
+}
+cudaError_t launch_u16_to_i32(const uint16_t* in, int32_t* out, size_t count, cudaStream_t st) {
+    k_u16_to_i32<<<grid_for(count), 256, 0, st>>>(in, out, count);
+    return cudaGetLastError();
+}
+cudaError_t launch_i32_to_u16(const int32_t* in, uint16_t* out, size_t count, cudaStream_t st) {
+    k_i32_to_u16<<<grid_for(count), 256, 0, st>>>(in, out, count);
+    return cudaGetLastError();
+}
+cudaError_t launch_colors_u16_to_u8(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, cudaStream_t st) {
+    k_c16_to_8<<<grid_for((size_t)p * nvpad), 256, 0, st>>>(in, out, p, nv, nvpad);
+    return cudaGetLastError();
+}
+cudaError_t launch_colors_u8_to_u16(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad, cudaStream_t st) {
+    k_c8_to_16<<<grid_for((size_t)p * nv), 256, 0, st>>>(in, out, p, nv, nvpad);
+    return cudaGetLastError();
+}
+
+}  // namespace plse_dev

@@ -1,0 +1,155 @@
+"""GPU (canonical tie-break) vs the C oracle, bit-exact, through the C ABI.
+
+Parity bar (north star): gamma-derived moves, chosen moves, tabu tenures,
+offspring and distance matrices bit-exact per step; final colourings, best f
+and iteration counts identical for a fixed seed.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(5, 0.5, 61), (10, 0.3, 606), (20, 0.7, 505), (30, 0.5, 12345), (60, 0.5, 12345), (70, 0.6, 12345)]
+
+
+def _pop(P, grid, p, seed=7, **kw):
+    g = P.preprocess(grid)
+    cfg = P.SolverConfig(p=p, master_seed=seed, **kw)
+    return g, P.DevicePopulation(g, cfg)
+
+
+@pytest.mark.parametrize("n,r,s", CASES)
+def test_init_population_matches_reference_stream(plse, orc, n, r, s):
+    grid = orc.generate_instance(n, r, s)
+    g, dp = _pop(plse, grid, 16, seed=99)
+    dp.initialize_population()
+    mem = orc.init_population(grid, 16, 99)
+    assert np.array_equal(dp.members, mem)
+    assert np.array_equal(dp.dist, orc.full_distances(mem))
+    f, c, _ = dp.stats()
+    for i in range(16):
+        assert (f[i], c[i]) == orc.eval(grid, mem[i])
+
+
+@pytest.mark.parametrize("n,r,s", CASES)
+@pytest.mark.parametrize("budget", [1, 7, 300, 0])
+def test_improve_matches_oracle(plse, orc, n, r, s, budget):
+    grid = orc.generate_instance(n, r, s)
+    g = plse.preprocess(grid)
+    p = 24
+    cfg = plse.SolverConfig(p=p, master_seed=3, phase1_iters=budget)
+    dp = plse.DevicePopulation(g, cfg)
+    dp.initialize_population()
+    off = orc.init_population(grid, p, 3)
+    # mix fully random (heavy repair) and legal partial inputs
+    for i in range(0, p, 3):
+        off[i] = orc.repair(grid, off[i])
+    dp.offspring = off
+    gen = 1
+    it, bf, bi = dp.improve(gen)
+    imp = dp.improved
+    f, c, iters = dp.stats(plse.IMPROVED)
+    tot = 0
+    eff_budget = budget if budget > 0 else 100 * g.vertex_count
+    stop_f = 1 if g.l == 1 else 0
+    for i in range(p):
+        seed = orc.derive_seed(3, 2, gen * p + i)
+        o = orc.improve(grid, off[i], seed, eff_budget, stop_f=stop_f, tie=oracle.TIE_CANON)
+        assert iters[i] == o["iterations"], (i, iters[i], o["iterations"])
+        assert f[i] == o["best_f"]
+        assert np.array_equal(imp[i], o["best"]), i
+        tot += o["iterations"]
+    assert it == tot
+    assert bf == min(f)
+    assert bi == int(np.argmin(f))
+    ctr = dp.counters()
+    want = sum(orc.improve(grid, off[i], orc.derive_seed(3, 2, gen * p + i), eff_budget, stop_f=stop_f)["alg_bytes"]
+               for i in range(p))
+    assert ctr.alg_bytes == want
+
+
+@pytest.mark.parametrize("n,r,s", [(20, 0.7, 505), (30, 0.5, 12345), (60, 0.5, 12345), (70, 0.6, 12345)])
+def test_per_step_trace_matches_oracle(plse, orc, n, r, s):
+    grid = orc.generate_instance(n, r, s)
+    g = plse.preprocess(grid)
+    p = 4
+    dp = plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=11, phase1_iters=20000))
+    dp.initialize_population()
+    off = orc.init_population(grid, p, 11)
+    dp.offspring = off
+    for idx in range(p):
+        steps, n_it = dp.trace(idx, 2, 20000)
+        o = orc.improve(grid, off[idx], orc.derive_seed(11, 2, 2 * p + idx), 20000,
+                        stop_f=1 if g.l == 1 else 0, trace_cap=20000)
+        assert n_it == o["iterations"]
+        assert len(steps) == len(o["trace"])
+        for a, b in zip(steps, o["trace"]):
+            assert a == b, (idx, a, b)
+
+
+@pytest.mark.parametrize("n,r,s", [(10, 0.3, 606), (20, 0.7, 505), (30, 0.5, 12345)])
+def test_population_phases_match_reference(plse, orc, ref, n, r, s):
+    """distances, update (incl. shortfall), matching + AUX crossover over several generations."""
+    grid = orc.generate_instance(n, r, s)
+    g = plse.preprocess(grid)
+    p = 32
+    dp = plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=55, phase1_iters=2000))
+    dp.initialize_population()
+    mem, dist = ref.init_population(grid, p, 55)
+    off = mem.copy()
+    ex = ref.new_exclusion(p)
+    dp.offspring = off
+    for gen in range(1, 6):
+        dp.improve(gen)
+        imp = dp.improved
+        for i in range(p):
+            o = orc.improve(grid, off[i], orc.derive_seed(55, 2, gen * p + i), 2000, stop_f=1 if g.l == 1 else 0)
+            assert np.array_equal(imp[i], o["best"])
+        dp.compute_cross_distances()
+        cr, fr = ref.cross_distances(grid, mem, imp)
+        assert np.array_equal(dp.get_dist(plse.CROSS), cr)
+        assert np.array_equal(dp.get_dist(plse.FRESH), fr)
+        info = dp.update_population()
+        u = ref.update(grid, mem, dist, imp, cr, fr)
+        assert info.pool_best_f == u["pool_best_f"]
+        assert info.shortfall_slots == u["shortfall_slots"]
+        mem, dist = u["members"], u["dist"]
+        assert np.array_equal(dp.members, mem)
+        assert np.array_equal(dp.dist, dist)
+        dp.build_offspring(gen)
+        off = ref.offspring(grid, mem, dist, ex, 55, gen)
+        assert np.array_equal(dp.offspring, off), gen
+
+
+@pytest.mark.parametrize("mode", [(1, 1, 0), (2, 0, 0), (0, 0, 2), (0, 1, 1), (0, 0, 1)])
+def test_offspring_modes_match_reference(plse, orc, ref, mode):
+    x, m, e = mode
+    grid = orc.generate_instance(20, 0.7, 505)
+    g = plse.preprocess(grid)
+    p = 32
+    dp = plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=9, crossover=x, matching=m, exclusion=e))
+    mem = np.stack([orc.repair(grid, c) for c in orc.init_population(grid, p, 9)])
+    dist = orc.full_distances(mem)
+    dp.members = mem
+    dp.dist = dist
+    ex = ref.new_exclusion(p)
+    for gen in range(1, 5):
+        if e == 1:
+            dp.reset_exclusion()
+            ref.lib.ref_excl_reset(ex, p)
+        dp.build_offspring(gen)
+        want = ref.offspring(grid, mem, dist, ex, 9, gen, crossover=x, matching=m, exclusion=e)
+        assert np.array_equal(dp.offspring, want), (mode, gen)
+
+
+@pytest.mark.parametrize("n,r,s,p", [(10, 0.5, 3, 16), (20, 0.7, 505, 16), (30, 0.5, 12345, 16)])
+def test_run_matches_oracle(plse, orc, n, r, s, p):
+    grid = orc.generate_instance(n, r, s)
+    res = plse.run(grid, plse.SolverConfig(p=p, master_seed=7, generation_limit=4))
+    o = orc.run(grid, p=p, seed=7, generation_limit=4, tie=oracle.TIE_CANON)
+    for k in ("best_f", "best_score", "stop_reason", "generations", "total_iterations", "l", "upper_bound"):
+        assert getattr(res, k) == o[k], k
+    assert bool(res.proven_optimal) == bool(o["proven_optimal"])
+    assert np.array_equal(res.best_solution, o["best_colors"])
