@@ -160,6 +160,11 @@ int plse_set_dist(plse_ctx* ctx, int32_t which, const int32_t* host);
 int plse_get_stats(plse_ctx* ctx, int32_t which, int32_t* f, int32_t* c, int64_t* iters);
 int plse_get_partners(plse_ctx* ctx, int32_t* host /* p */);
 int plse_get_counters(plse_ctx* ctx, plse_counters* out);
+/* device-side timing on the context's stream (CUDA events): start, then stop -> elapsed ms */
+int plse_timer_start(plse_ctx* ctx);
+int plse_timer_stop(plse_ctx* ctx, double* ms);
+/* device pointer of a u8 population buffer (row stride = |V| rounded up to 16), for NCCL / torch interop */
+int plse_device_colors(plse_ctx* ctx, int32_t which, void** dev_ptr, int64_t* row_stride);
 
 int plse_init_population(plse_ctx* ctx);
 int plse_full_distances(plse_ctx* ctx); /* dist <- D(members, members) */

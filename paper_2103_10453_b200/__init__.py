@@ -133,6 +133,9 @@ def _load() -> C.CDLL:
         "plse_get_stats": ([ctx, C.c_int32, vp, vp, vp], C.c_int),
         "plse_get_partners": ([ctx, i32p], C.c_int),
         "plse_get_counters": ([ctx, C.POINTER(Counters)], C.c_int),
+        "plse_timer_start": ([ctx], C.c_int),
+        "plse_timer_stop": ([ctx, C.POINTER(C.c_double)], C.c_int),
+        "plse_device_colors": ([ctx, C.c_int32, C.POINTER(vp), C.POINTER(C.c_int64)], C.c_int),
         "plse_init_population": ([ctx], C.c_int),
         "plse_full_distances": ([ctx], C.c_int),
         "plse_improve": ([ctx, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
@@ -394,6 +397,22 @@ class DevicePopulation:
         c = Counters()
         _check(_lib.plse_get_counters(self._ctx, C.byref(c)), self._ctx)
         return c
+
+    def timer_start(self) -> None:
+        """Record a CUDA event on this population's stream."""
+        _check(_lib.plse_timer_start(self._ctx), self._ctx)
+
+    def timer_stop(self) -> float:
+        """Record a second event, synchronise, return the device-side elapsed ms."""
+        ms = C.c_double()
+        _check(_lib.plse_timer_stop(self._ctx, C.byref(ms)), self._ctx)
+        return ms.value
+
+    def device_colors(self, which=MEMBERS):
+        """(device pointer, row stride) of a u8 population buffer."""
+        ptr, stride = C.c_void_p(), C.c_int64()
+        _check(_lib.plse_device_colors(self._ctx, which, C.byref(ptr), C.byref(stride)), self._ctx)
+        return ptr.value, stride.value
 
     # -- phases
     def initialize_population(self) -> None:

@@ -84,8 +84,10 @@ struct plse_ctx {
     int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
     uint32_t* d_conf = nullptr;
     uint8_t *d_legal = nullptr, *d_admitted = nullptr;
-    // host staging
-    std::vector<uint8_t> stage;
+    // host staging (pinned, so host<->device copies run at full PCIe rate)
+    uint8_t* stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t tm0 = nullptr, tm1 = nullptr;
     plse_counters ctr{};
     std::string err;
 
@@ -97,6 +99,9 @@ struct plse_ctx {
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
+        if (stage) cudaFreeHost(stage);
+        if (tm0) cudaEventDestroy(tm0);
+        if (tm1) cudaEventDestroy(tm1);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st) cudaStreamDestroy(st);
@@ -133,6 +138,15 @@ struct plse_ctx {
         ctr.kernel_launches += count;
     }
     uint64_t stream_base(uint64_t gen) const { return gen * (uint64_t)prm.p_total + (uint64_t)prm.offset; }
+    uint8_t* staging(size_t bytes) {
+        if (bytes > stage_bytes) {
+            if (stage) cudaFreeHost(stage);
+            stage = nullptr;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&stage), bytes, cudaHostAllocDefault));
+            stage_bytes = bytes;
+        }
+        return stage;
+    }
 };
 
 namespace {
@@ -378,16 +392,19 @@ void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) 
     const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad, W = c->W;
     if (!host) throw std::invalid_argument("null colours");
     if (count != (int64_t)p * nv) throw std::invalid_argument("assignment size mismatch");
-    c->stage.assign((size_t)p * nvpad, 0);
-    for (int i = 0; i < p; ++i)
+    uint8_t* stage = c->staging((size_t)p * nvpad);
+    for (int i = 0; i < p; ++i) {
+        uint8_t* row = stage + (size_t)i * nvpad;
         for (int v = 0; v < nv; ++v) {
             const uint16_t k = host[(size_t)i * nv + v];
             if (k > c->n || !((c->h_dommask[(size_t)v * W + k / 64] >> (k % 64)) & 1))
                 throw std::invalid_argument("assignment leaves vertex domain");
-            c->stage[(size_t)i * nvpad + v] = (uint8_t)k;
+            row[v] = (uint8_t)k;
         }
+        std::memset(row + nv, 0, nvpad - nv);
+    }
     uint8_t* dst = c->colors(which);
-    CK(cudaMemcpyAsync(dst, c->stage.data(), c->stage.size(), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dst, stage, (size_t)p * nvpad, cudaMemcpyHostToDevice, c->st));
     if (which == PLSE_MEMBERS) eval_into(c, dst, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
     if (which == PLSE_IMPROVED) eval_into(c, dst, c->h_if, c->h_ic, c->d_tmpf, c->d_tmpc);
     CK(cudaStreamSynchronize(c->st));
@@ -396,11 +413,11 @@ void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) 
 void download_colors(plse_ctx* c, int which, uint16_t* host) {
     const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad;
     if (!host) throw std::invalid_argument("null output");
-    c->stage.resize((size_t)p * nvpad);
-    CK(cudaMemcpyAsync(c->stage.data(), c->colors(which), c->stage.size(), cudaMemcpyDeviceToHost, c->st));
+    uint8_t* stage = c->staging((size_t)p * nvpad);
+    CK(cudaMemcpyAsync(stage, c->colors(which), (size_t)p * nvpad, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     for (int i = 0; i < p; ++i)
-        for (int v = 0; v < nv; ++v) host[(size_t)i * nv + v] = c->stage[(size_t)i * nvpad + v];
+        for (int v = 0; v < nv; ++v) host[(size_t)i * nv + v] = stage[(size_t)i * nvpad + v];
 }
 
 void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, plse_step* d_trace, int p_eff,
@@ -715,6 +732,37 @@ int plse_get_counters(plse_ctx* c, plse_counters* out) {
     if (!c || !out) return finish(c, PLSE_ERR_INVALID, "null argument");
     *out = c->ctr;
     return PLSE_OK;
+}
+
+int plse_timer_start(plse_ctx* c) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!c->tm0) CK(cudaEventCreate(&c->tm0));
+        if (!c->tm1) CK(cudaEventCreate(&c->tm1));
+        CK(cudaEventRecord(c->tm0, c->st));
+    });
+}
+
+int plse_timer_stop(plse_ctx* c, double* ms) {
+    if (!c || !ms) return finish(c, PLSE_ERR_INVALID, "null argument");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!c->tm0) throw std::invalid_argument("timer not started");
+        CK(cudaEventRecord(c->tm1, c->st));
+        CK(cudaEventSynchronize(c->tm1));
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, c->tm0, c->tm1));
+        *ms = f;
+    });
+}
+
+int plse_device_colors(plse_ctx* c, int32_t which, void** dev_ptr, int64_t* row_stride) {
+    if (!c || !dev_ptr) return finish(c, PLSE_ERR_INVALID, "null argument");
+    return guard(c, [&] {
+        *dev_ptr = c->colors(which);
+        if (row_stride) *row_stride = c->nvpad;
+    });
 }
 
 int plse_init_population(plse_ctx* c) {
