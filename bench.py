@@ -59,7 +59,7 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--migrate-every", type=int, default=2)
     ap.add_argument("--elites", type=int, default=32)
-    ap.add_argument("--cpu-per-thread", type=int, default=12, help="individuals per host thread in the CPU sample")
+    ap.add_argument("--cpu-per-thread", type=int, default=72, help="individuals per host thread in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttb", action="store_true")
     ap.add_argument("--ttb-ref-pop", type=int, default=1024)
