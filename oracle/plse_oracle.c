@@ -645,7 +645,7 @@ int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members,
     const int pool = 2 * p;
     pool_key* keys = (pool_key*)malloc(sizeof(pool_key) * pool);
     int* legal = (int*)malloc(sizeof(int) * pool);
-    int* fval = (int*)malloc(sizeof(int) * pool);
+    int* fval = (int*)calloc(pool, sizeof(int));
     for (int id = 0; id < pool; ++id) {
         const uint16_t* c = id < p ? members + (size_t)id * nv : improved + (size_t)(id - p) * nv;
         int f, cc;
@@ -846,7 +846,7 @@ int or_run(int n, const uint16_t* grid, const or_config* cfg, or_result* res, ui
         {
             int f, c;
             or_eval(g, best, &f, &c);
-            if (is_optimal_fc(f, c, g->l)) {
+            if (!cfg->disable_optimal_stop && is_optimal_fc(f, c, g->l)) {
                 reason = OR_STOP_OPTIMAL;
                 goto done;
             }

@@ -1,0 +1,121 @@
+"""Generate tests/golden/ref_golden.npz from the REAL reference.
+
+Runs the unmodified reference headers compiled in place (oracle/_ref, built by
+oracle/Makefile from /root/reference) and records input/output vectors for the
+hot path, so that the C oracle stays pinned where /root/reference does not
+exist (the GPU box, the driver's CPU check).  Re-run with:
+
+    make -C oracle && python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import oracle  # noqa: E402
+
+
+def main():
+    R = oracle.Reference()
+    out = {}
+    # --- instances (instance.hpp:204) and the LSC builder (builders.hpp:46)
+    inst = [(5, 0.5, 61), (10, 0.3, 606), (20, 0.7, 505), (30, 0.5, 12345), (60, 0.5, 12345), (70, 0.6, 12345),
+            (50, 0.4, 12345), (4, 0.2, 7), (6, 0.8, 3)]
+    for n, r, s in inst:
+        g = R.generate_instance(n, r, s)
+        out[f"inst_{n}_{r}_{s}"] = g
+        gr = R.preprocess(g)
+        out[f"graph_{n}_{r}_{s}"] = np.concatenate([[gr.nv, gr.l], gr.cell_row, gr.cell_col, gr.adj_off, gr.adj,
+                                                    gr.dom_off, gr.dom.astype(np.int32)]).astype(np.int32)
+    out["lsc_20_0.4_7"] = R.lsc_instance(20, 0.4, 7)
+    out["lsc_70_0.4_7"] = R.lsc_instance(70, 0.4, 7)
+
+    # --- repair (partial.hpp:22) and gamma (coloring.hpp:105) on random colourings
+    rng = np.random.default_rng(404)
+    for n, r, s in [(10, 0.3, 606), (20, 0.7, 505), (30, 0.5, 12345)]:
+        g = out[f"inst_{n}_{r}_{s}"]
+        gr = R.preprocess(g)
+        cols = []
+        for t in range(8):
+            c = np.array([gr.dom[rng.integers(gr.dom_off[v], gr.dom_off[v + 1])] for v in range(gr.nv)], np.uint16)
+            cols.append(c)
+        cols = np.stack(cols)
+        out[f"repair_in_{n}"] = cols
+        out[f"repair_out_{n}"] = np.stack([R.repair(g, c) for c in cols])
+        out[f"gamma_{n}"] = R.gamma(g, cols[0])
+
+    # --- partial_mpma_improve trajectories (REF tie-break) and per-step states
+    for n, r, s in [(10, 0.3, 606), (20, 0.7, 505), (30, 0.5, 12345), (60, 0.5, 12345)]:
+        g = out[f"inst_{n}_{r}_{s}"]
+        mem, _ = R.init_population(g, 4, 77)
+        nv = mem.shape[1]
+        res = []
+        for i in range(4):
+            seed = 1000 + i
+            o = R.improve(g, mem[i], seed, 100 * nv if n <= 30 else 20000)
+            res.append(np.concatenate([[o["iterations"], o["best_f"]], o["best"]]).astype(np.int64))
+        out[f"improve_in_{n}"] = mem
+        out[f"improve_out_{n}"] = np.stack(res)
+        rep, states, bf = R.improve_states(g, mem[0], 4242, 300)
+        out[f"states_rep_{n}"] = rep
+        out[f"states_{n}"] = states
+        out[f"states_bf_{n}"] = bf
+
+    # --- one population generation chain (init -> improve -> distances -> update -> offspring)
+    g = out["inst_20_0.7_505"]
+    p = 16
+    mem, dist = R.init_population(g, p, 55)
+    out["chain_init_members"] = mem
+    out["chain_init_dist"] = dist
+    nv = mem.shape[1]
+    imp = np.stack([R.improve(g, mem[i], oracle.Oracle().derive_seed(55, 2, p + i), 100 * nv)["best"]
+                    for i in range(p)])
+    out["chain_improved"] = imp
+    cr, fr = R.cross_distances(g, mem, imp)
+    out["chain_cross"] = cr
+    out["chain_fresh"] = fr
+    u = R.update(g, mem, dist, imp, cr, fr)
+    out["chain_members1"] = u["members"]
+    out["chain_dist1"] = u["dist"]
+    out["chain_info1"] = np.array([u["pool_best_f"]] + u["shortfall_slots"], np.int32)
+    ex = R.new_exclusion(p)
+    out["chain_offspring1"] = R.offspring(g, u["members"], u["dist"], ex, 55, 1)
+
+    # --- full runs (engine.hpp:114), workers=1, Partial-MPMA
+    runs = []
+    for n, r, s, pp in [(10, 0.5, 3, 16), (20, 0.7, 505, 16), (30, 0.5, 12345, 16)]:
+        gg = R.generate_instance(n, r, s)
+        out[f"run_inst_{n}"] = gg
+        rr = R.run(gg, p=pp, seed=7, generation_limit=5, workers=1)
+        runs.append([n, pp, rr["best_f"], rr["best_score"], rr["proven_optimal"], ["optimal", "time_limit",
+                     "iteration_limit", "generation_limit", "trivial"].index(rr["stop_reason"]), rr["generations"],
+                     rr["total_iterations"]])
+        out[f"run_best_{n}"] = rr["best_colors"]
+    out["runs"] = np.array(runs, np.int64)
+
+    # --- acceptance c1/c9 small suite (acceptance.cpp:49-60) with exact optima (oracle.hpp:134)
+    O = oracle.Oracle()
+    suite = []
+    for i in range(200):
+        n = 4 + (i % 3)
+        r = 0.3 + 0.1 * ((i // 3) % 6)
+        seed = O.derive_seed(20240801, 1000, i)
+        gg = R.generate_instance(n, r, seed)
+        f, exact = R.solve_exact(gg)
+        assert exact
+        gr = R.preprocess(gg)
+        suite.append([n, seed & 0xFFFFFFFFFFFF, f, n * n - gr.l - f, gr.l])
+        out[f"suite_{i}"] = gg
+    out["suite"] = np.array(suite, np.int64)
+    path = os.path.join(HERE, "ref_golden.npz")
+    np.savez_compressed(path, **out)
+    print(path, os.path.getsize(path), "bytes,", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
