@@ -19,7 +19,7 @@
  *                   DESIGN.md "Canonical tie-break"): the r-th admissible
  *                   minimum-delta candidate in ascending (v, k) order with
  *                   r = floor(u32 * N / 2^32), u32 from a counter-based
- *                   splitmix64 draw keyed (stream seed, step).  Everything
+ *                   fmix32 hash keyed (stream seed, step).  Everything
  *                   else in the step (gamma, aspiration, tabu, eviction,
  *                   tenure formula, best snapshot) is shared code with
  *                   OR_TIE_REF, so pinning the REF policy pins it.
@@ -50,7 +50,7 @@ uint64_t or_rng_next(or_rng* r);
 uint64_t or_rng_below(or_rng* r, uint64_t bound);
 double or_rng_double(or_rng* r);
 uint64_t or_derive_seed(uint64_t master, uint64_t tag, uint64_t index);
-/* counter-based draw used by OR_TIE_CANON: splitmix64 output number j of seed s */
+/* counter-based draw used by OR_TIE_CANON for step j (hi: move rank, lo: tenure offset) */
 uint64_t or_canon_draw(uint64_t s, uint64_t j);
 
 /* ---- instance.hpp:204-262, builders.hpp:30-58 ------------------------- */

@@ -37,7 +37,7 @@ from typing import Callable, List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libplse_b200.so")
+LIB_PATH = os.environ.get("PLSE_LIB") or os.path.join(HERE, "libplse_b200.so")  # PLSE_LIB: A/B experiments
 
 __all__ = [
     "generate_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",

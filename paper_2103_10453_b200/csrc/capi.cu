@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -76,10 +77,13 @@ struct plse_ctx {
     // improve launch
     void* d_rec = nullptr;
     uint32_t* d_until = nullptr;
+    uint32_t* d_slot_clock = nullptr;
+    uint32_t tenure_cap = 0;
     size_t rec_stride = 0, until_stride = 0;
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
     size_t smem = 0;
     int* d_work = nullptr;
+    unsigned long long* d_prof = nullptr;  // PLSE_PROFILE instrumentation counters
     // pool update scratch
     int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
     uint32_t* d_conf = nullptr;
@@ -95,7 +99,7 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_work, d_order,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_order,
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -232,7 +236,9 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->prm = *pp;
     if (c->prm.p_total == 0) c->prm.p_total = c->prm.p;
     c->budget = pp->phase1_iters > 0 ? pp->phase1_iters : 100LL * nv;
-    if (c->budget >= (1LL << 31)) throw Unsupported("budget must be < 2^31 iterations");
+    if (c->budget >= (1LL << 30)) throw Unsupported("budget must be < 2^30 iterations");
+    if (pp->alpha * nv >= (double)(1 << 29)) throw Unsupported("alpha * |V| must be < 2^29 (tabu tenure range)");
+    c->tenure_cap = 10u + (uint32_t)(pp->alpha * (double)nv);
     c->stop_f = gr->l == 1 ? 1 : 0;
     c->W = n < 64 ? 1 : 2;
     c->nvpad = (int)up((size_t)nv, 16);
@@ -357,7 +363,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    for (int wpc : {16, 8, 4, 2, 1}) {
+    for (int wpc : {8, 4, 2, 1}) {
         if (force_wpc && wpc != force_wpc) continue;
         const size_t smem = L.graph_bytes + (size_t)wpc * L.warp_bytes;
         if (smem > (size_t)max_optin) continue;
@@ -380,6 +386,9 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->until_stride = up((size_t)nv * (n + 1), 64);
     c->d_rec = dalloc<uint8_t>((size_t)c->slots * c->rec_stride);
     c->d_until = dalloc<uint32_t>((size_t)c->slots * c->until_stride);
+    CK(cudaMemset(c->d_until, 0, sizeof(uint32_t) * (size_t)c->slots * c->until_stride));
+    c->d_slot_clock = dalloc<uint32_t>(c->slots);
+    CK(cudaMemset(c->d_slot_clock, 0, sizeof(uint32_t) * c->slots));
     c->ctr.grid = c->grid;
     c->ctr.threads = c->threads;
     c->ctr.warps_per_sm = c->warps_per_sm;
@@ -444,6 +453,8 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.rec_stride = c->rec_stride;
     a.until = c->d_until;
     a.until_stride = c->until_stride;
+    a.slot_clock = c->d_slot_clock;
+    a.tenure_cap = c->tenure_cap;
     a.work_counter = c->d_work;
     a.master = c->prm.master_seed;
     a.generation = gen;
@@ -455,6 +466,14 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.trace_idx = trace_idx;
     a.trace_cap = trace_cap;
     a.trace = d_trace;
+    a.prof = nullptr;
+    if (const char* env = std::getenv("PLSE_PROFILE")) {
+        if (env[0] == '1') {
+            if (!c->d_prof) c->d_prof = dalloc<unsigned long long>(16);
+            CK(cudaMemsetAsync(c->d_prof, 0, 16 * 8, c->st));
+            a.prof = c->d_prof;
+        }
+    }
     CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->ev0, c->st));
     c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
@@ -483,6 +502,16 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
             bf = c->h_if[i];
             bi = i;
         }
+    }
+    if (c->d_prof && std::getenv("PLSE_PROFILE")) {
+        unsigned long long pr[16];
+        CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr,
+                     "[plse-prof] indiv %llu prologue %.0f cyc/indiv | dense %llu steps %.0f cyc/step mean f %.1f | "
+                     "sparse %llu steps %.0f cyc/step | enter %llu | total %.3g cyc/indiv\n",
+                     pr[0], (double)pr[1] / pr[0], pr[2], pr[2] ? (double)pr[3] / pr[2] : 0.0,
+                     pr[2] ? (double)pr[6] / pr[2] : 0.0, pr[4], pr[4] ? (double)pr[5] / pr[4] : 0.0, pr[7],
+                     (double)pr[8] / pr[0]);
     }
     c->ctr.improve_ms = ms;
     c->ctr.alg_bytes = by;

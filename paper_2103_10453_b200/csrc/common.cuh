@@ -37,9 +37,16 @@ __host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t master, uint64
     return splitmix64(s);
 }
 
-// canonical tie-break draw j of stream seed s: mix(s + (j+1)*golden)
-__host__ __device__ __forceinline__ uint64_t canon_draw(uint64_t s, uint64_t j) {
-    return mix64(s + (j + 1) * kGolden);
+// murmur3 finaliser; the canonical tie-break draw of step j is
+//   h1 = fmix32(fold(s) + (j+1) * 0x9E3779B9), h2 = fmix32(h1 + 0x632BE5AB)
+// with fold(s) = lo32(s ^ (s >> 32)); h1 ranks the move, h2 the tenure offset.
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
 }
 
 // xoshiro256++ seeded by splitmix64 (rng.hpp:21-58)

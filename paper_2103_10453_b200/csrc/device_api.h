@@ -9,7 +9,8 @@
 
 namespace plse_dev {
 
-constexpr int kImproveMaxThreads = 512;
+constexpr int kImproveMaxThreads = 256;
+constexpr int kImproveMinBlocks = 4;  // 32 resident warps per SM -> <= 64 registers
 
 struct ImproveArgs {
     // graph (global copies; the kernel stages them in shared memory)
@@ -32,13 +33,17 @@ struct ImproveArgs {
     void* tabu_rec;
     size_t rec_stride;          // bytes per slot
     uint32_t* until;
-    size_t until_stride;        // u32 per slot
+    size_t until_stride;        // u32 per slot (multiple of 4)
+    uint32_t* slot_clock;       // per slot: tabu clock base of its next individual
+    uint32_t tenure_cap;        // 10 + floor(alpha*|V|) > any tenure
     int* work_counter;
     // streams (engine.hpp:189-191): seed = derive(master, 2, gen*p_total + offset + i)
     uint64_t master, generation, p_total, offset;
     int64_t budget;
     int stop_f;
     double alpha;
+    // optional clock64 instrumentation (PLSE_PROFILE=1): 16 counters, see capi.cu
+    unsigned long long* prof;
     // parity probe
     int trace_idx;
     int64_t trace_cap;
@@ -46,7 +51,7 @@ struct ImproveArgs {
 };
 
 struct ImproveSmemLayout {
-    size_t cell, rs, cs, cl, pr, pc, graph_bytes;
+    size_t cell, rs, cs, cl, deg, pr, pc, graph_bytes;
     size_t warp0, warp_bytes, w_col, w_conf, w_R, w_C, w_U;
 };
 
@@ -63,6 +68,8 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     o += (size_t)(n + 1) * 2;
     L.cl = o;
     o += (size_t)nv * 2;
+    L.deg = o;
+    o += (size_t)nv;
     o = align_up(o, 16);
     L.pr = o;
     o += (size_t)n * W * 8;
@@ -74,8 +81,8 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     size_t w = 0;
     L.w_col = w;
     w += (size_t)nvpad;
-    L.w_conf = w;
-    w += (size_t)nvpad;
+    L.w_conf = w;  // repair counters; afterwards the 32-entry u16 list that seeds sparse mode
+    w += nvpad > 64 ? (size_t)nvpad : 64;
     w = align_up(w, 16);
     L.w_R = w;
     w += (size_t)n * W * 8;

@@ -8,33 +8,39 @@
 //
 // Data layout:
 //   * The individual's colours (u8) live in shared memory for the whole
-//     search, together with per-row / per-column colour-occupancy bitmasks
-//     R[r], C[c] (W x u64 each) and the uncoloured set U as a bitmask.
-//     In a legal colouring gamma[v][k] = [k in R[row v]] + [k in C[col v]]
-//     for every uncoloured v, so the three move classes of an uncoloured
-//     vertex (delta -1 / 0 / +1) are three W-word mask expressions -- the
-//     int16 gamma rows of the north star are never materialised.
+//     search, with per-row / per-column colour-occupancy bitmasks R[r], C[c]
+//     (W x u64) and the uncoloured set U as a bitmask.  In a legal colouring
+//     gamma[v][k] = [k in R[row v]] + [k in C[col v]] for every uncoloured v,
+//     so the three move classes of an uncoloured vertex (delta -1 / 0 / +1)
+//     are three W-word mask expressions: the gamma rows the north star puts in
+//     HBM are never materialised.
 //   * The domain of v is ~(PR[row] | PC[col]) over the prefilled-symbol masks
 //     (lsgraph.hpp:152-156), shared by the CTA in shared memory.
-//   * Tabu state (search_util.hpp:54-81) is per warp slot in HBM/L2: a dense
-//     u32 `until[v][k]` table (the reference layout) plus a 16/32-byte record
-//     per vertex {tabu-bit mask, max until, exact flag} so that the common
-//     case costs one vector load per uncoloured vertex per step.
-//   * Selection is the canonical order-free rule: count the
-//     admissible candidates per delta level per lane, warp-scan the counts of
-//     the lowest non-empty level, draw r = floor(u32 * N / 2^32) from the
-//     counter-based stream, and let the lane holding the r-th candidate (in
-//     ascending (v, k) order) recover it with a popcount search.
+//   * Tabu state (search_util.hpp:54-81): the reference's dense until[v][k]
+//     table lives per warp slot in HBM, on a monotone per-slot clock so it is
+//     never cleared (the reference's skip_past, partial.hpp:60).  A 16-byte
+//     record per vertex caches its two most recent (colour, until) pairs plus
+//     an overflow flag; only a vertex with three or more live tabu colours
+//     reads the dense table.
+//   * Sparse mode (|V0| <= 32, i.e. everything after the first ~1% of the
+//     descent): lane l holds the l-th uncoloured vertex (ascending id) and its
+//     tabu pairs in registers, so scoring a step costs two shared loads per
+//     lane.  Dense mode scans the U bitmask (lane-owned 32*lane_words blocks).
+//   * Selection is the canonical order-free rule: the lowest
+//     admissible delta level, per-lane counts, a warp prefix sum, and
+//     r = floor(h1 * N / 2^32) from a counter hash of (stream seed, step); the
+//     lane holding the r-th candidate in ascending (v, k) order recovers it
+//     with a popcount search.
 #include "common.cuh"
 #include "device_api.h"
 
 namespace plse_dev {
 
-template <int W>
+// per-vertex tabu cache: (k1, u1), (k2, u2) exact until values of the two
+// most recently forbidden colours; kk = k1 | k2 << 8 | ovf << 16.  ovf: a
+// third colour was forbidden while both pairs were live -> consult until[][].
 struct alignas(16) TabuRec {
-    uint64_t tm[W];
-    uint32_t umax;
-    uint32_t exact;
+    uint32_t u1, u2, kk, pad;
 };
 
 struct WarpSmem {
@@ -49,6 +55,7 @@ template <int W>
 struct Graph {
     int n, nv, nvpad, lane_words;
     const uint16_t* cell;
+    const uint8_t* deg;  // |N(v)| = row-mates + column-mates (for the 8(d) byte counter)
     const uint16_t* rs;
     const uint16_t* cs;
     const uint16_t* cl;
@@ -58,75 +65,111 @@ struct Graph {
 };
 
 template <int W>
-__device__ __forceinline__ void tabu_mask(TabuRec<W>* rec, const uint32_t* until, int w1, int v, uint32_t j,
-                                          uint64_t (&T)[W]) {
-    TabuRec<W> r = rec[v];
-    if (r.umax <= j) {
-        bool any = false;
+__device__ __forceinline__ void dom_mask(const Graph<W>& g, int r, int c, uint64_t (&d)[W]) {
 #pragma unroll
-        for (int q = 0; q < W; ++q) {
-            any |= r.tm[q] != 0;
-            T[q] = 0;
-        }
-        if (any) {
-            TabuRec<W> z;
+    for (int q = 0; q < W; ++q) d[q] = ~(g.pr[r * W + q] | g.pc[c * W + q]) & g.full[q];
+}
+
+// exact tabu mask at clock t from a (u1, u2, kk) cache; the overflow case reads
+// the dense table for every colour of D(v) and rebuilds the cache when <= 2 remain
+template <int W>
+__device__ __forceinline__ void tabu_of(uint32_t& u1, uint32_t& u2, uint32_t& kk, const uint32_t* until_row,
+                                        const uint64_t (&dom)[W], uint32_t t, uint64_t (&T)[W]) {
 #pragma unroll
-            for (int q = 0; q < W; ++q) z.tm[q] = 0;
-            z.umax = 0;
-            z.exact = 1;
-            rec[v] = z;
-        }
+    for (int q = 0; q < W; ++q) T[q] = 0;
+    if (!(kk >> 16)) {
+        const int k1 = kk & 0xFF, k2 = (kk >> 8) & 0xFF;
+        if (u1 > t) T[k1 >> 6] |= 1ULL << (k1 & 63);
+        if (u2 > t) T[k2 >> 6] |= 1ULL << (k2 & 63);
         return;
     }
-    int pc = 0;
-#pragma unroll
-    for (int q = 0; q < W; ++q) pc += __popcll(r.tm[q]);
-    if (r.exact && pc == 1) {
-#pragma unroll
-        for (int q = 0; q < W; ++q) T[q] = r.tm[q];
-        return;
-    }
-    // slow path: verify every set bit against the dense until table, recompute umax
-    uint32_t um = 0;
+    int n_live = 0, ka = 0, kb = 0;
+    uint32_t ua = 0, ub = 0;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-        uint64_t m = r.tm[q];
-        uint64_t keep = 0;
+        uint64_t m = dom[q];
         while (m) {
             const int b = __ffsll((long long)m) - 1;
             m &= m - 1;
-            const uint32_t u = until[(size_t)v * w1 + q * 64 + b];
-            if (u > j) {
-                keep |= 1ULL << b;
-                um = max(um, u);
+            const int k = q * 64 + b;
+            const uint32_t u = until_row[k];
+            if (u > t) {
+                T[q] |= 1ULL << b;
+                if (n_live == 0) {
+                    ka = k;
+                    ua = u;
+                } else if (n_live == 1) {
+                    kb = k;
+                    ub = u;
+                }
+                ++n_live;
             }
         }
-        r.tm[q] = keep;
-        T[q] = keep;
     }
-    r.umax = um;
-    r.exact = 1;
-    rec[v] = r;
+    if (n_live <= 2) {
+        u1 = ua;
+        u2 = ub;
+        kk = (uint32_t)ka | ((uint32_t)kb << 8);
+    }
 }
 
-// Admissible candidate masks of an uncoloured vertex v at the three delta levels.
+// forbid (k, until = ut) in a vertex's cache (search_util.hpp:73-75 overwrite semantics)
+__device__ __forceinline__ void cache_forbid(TabuRec& r, int k, uint32_t ut, uint32_t t) {
+    const int k1 = r.kk & 0xFF, k2 = (r.kk >> 8) & 0xFF;
+    uint32_t ovf = r.kk & 0xFF0000u;
+    int n1 = k1, n2 = k2;
+    if (k1 == k && r.u1) {
+        r.u1 = ut;
+    } else if (k2 == k && r.u2) {
+        r.u2 = ut;
+    } else if (r.u1 <= t) {
+        n1 = k;
+        r.u1 = ut;
+    } else if (r.u2 <= t) {
+        n2 = k;
+        r.u2 = ut;
+    } else {
+        ovf = 1u << 16;  // both cached colours still tabu: the dense table is now authoritative
+        if (r.u1 <= r.u2) {
+            n1 = k;
+            r.u1 = ut;
+        } else {
+            n2 = k;
+            r.u2 = ut;
+        }
+    }
+    r.kk = (uint32_t)n1 | ((uint32_t)n2 << 8) | ovf;
+}
+
+// admissible candidate masks of an uncoloured vertex at the three delta levels
 template <int W>
-__device__ __forceinline__ void cand_masks(const Graph<W>& g, const WarpSmem& s, TabuRec<W>* rec,
-                                           const uint32_t* until, int v, uint32_t j, bool asp,
-                                           uint64_t (&m0)[W], uint64_t (&m1)[W], uint64_t (&m2)[W]) {
-    const uint16_t rc = g.cell[v];
-    const int r = rc >> 8, c = rc & 0xFF;
-    uint64_t T[W];
-    tabu_mask<W>(rec, until, g.n + 1, v, j, T);
+__device__ __forceinline__ void level_masks(const WarpSmem& s, int r, int c, const uint64_t (&dom)[W],
+                                            const uint64_t (&T)[W], bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
+                                            uint64_t (&m2)[W]) {
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-        const uint64_t dom = ~(g.pr[r * W + q] | g.pc[c * W + q]) & g.full[q];
         const uint64_t Rr = s.R[r * W + q], Cc = s.C[c * W + q];
-        const uint64_t fr = dom & ~Rr & ~Cc;
+        const uint64_t fr = dom[q] & ~Rr & ~Cc;
         m0[q] = asp ? fr : (fr & ~T[q]);
-        m1[q] = dom & (Rr ^ Cc) & ~T[q];
-        m2[q] = dom & Rr & Cc & ~T[q];
+        m1[q] = dom[q] & (Rr ^ Cc) & ~T[q];
+        m2[q] = dom[q] & Rr & Cc & ~T[q];
     }
+}
+
+// dense mode: masks of vertex v with its tabu cache read from (and written back to) HBM
+template <int W>
+__device__ __forceinline__ void dense_masks(const Graph<W>& g, const WarpSmem& s, TabuRec* rec, const uint32_t* until,
+                                            int v, uint32_t t, bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
+                                            uint64_t (&m2)[W]) {
+    const uint16_t rc = g.cell[v];
+    const int r = rc >> 8, c = rc & 0xFF;
+    uint64_t dom[W], T[W];
+    dom_mask<W>(g, r, c, dom);
+    TabuRec tr = rec[v];
+    const uint32_t kk0 = tr.kk;
+    tabu_of<W>(tr.u1, tr.u2, tr.kk, until + (size_t)v * (g.n + 1), dom, t, T);
+    if (tr.kk != kk0) rec[v] = tr;
+    level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
 }
 
 template <int W>
@@ -137,6 +180,19 @@ __device__ __forceinline__ int popc_w(const uint64_t (&m)[W]) {
     return c;
 }
 
+// 0-based rr-th set bit of a W-word mask (rr < popc)
+template <int W>
+__device__ __forceinline__ int nth_bit_w(const uint64_t (&m)[W], int rr) {
+    int k = 0;
+#pragma unroll
+    for (int z = 0; z < W; ++z) {
+        const int pz = __popcll(m[z]);
+        if (rr >= 0 && rr < pz) k = z * 64 + nth_bit64(m[z], rr);
+        rr -= pz;
+    }
+    return k;
+}
+
 __device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int nvpad, int lane) {
     const uint4* s4 = reinterpret_cast<const uint4*>(col);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -144,26 +200,33 @@ __device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int n
 }
 
 template <int W>
-__device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec<W>* rec,
-                            uint32_t* until, int i, int lane) {
+__device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
+                            uint32_t* until, uint32_t* slot_clock, int i, int lane) {
     const int n = g.n, nv = g.nv, w1 = n + 1;
     const int B = 32 * g.lane_words;
     const int v_lo = lane * B;
     const int v_hi = min(nv, v_lo + B);
     uint8_t* col = s.col;
     uint8_t* conf = s.conf;
+    unsigned long long* prof = a.prof;
+    long long t_start = prof ? clock64() : 0, t_step = 0;
+    unsigned long long pc_dense = 0, pc_sparse = 0, pn_dense = 0, pn_sparse = 0, pf_dense = 0, pn_enter = 0;
 
-    // ---- load the offspring (u8, row stride nvpad) and reset this slot's tabu records
+    // ---- tabu clock of this warp slot: every until[][] left by earlier individuals is <= base
+    uint32_t base = *slot_clock;
+    if ((uint64_t)base + (uint64_t)a.budget + a.tenure_cap + 2 >= 0xFFFFFFFFull) {
+        uint4* u4 = reinterpret_cast<uint4*>(until);
+        for (size_t x = lane; x < a.until_stride / 4; x += 32) u4[x] = make_uint4(0, 0, 0, 0);
+        base = 0;
+    }
+
+    // ---- load the offspring (u8, row stride nvpad) and reset this slot's tabu caches
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.offspring + (size_t)i * g.nvpad);
         uint4* d4 = reinterpret_cast<uint4*>(col);
-        for (int t = lane; t < g.nvpad / 16; t += 32) d4[t] = src[t];
-        TabuRec<W> z;
-#pragma unroll
-        for (int q = 0; q < W; ++q) z.tm[q] = 0;
-        z.umax = 0;
-        z.exact = 1;
-        for (int t = lane; t < nv; t += 32) rec[t] = z;
+        for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
+        const TabuRec z{0, 0, 0, 0};
+        for (int x = lane; x < nv; x += 32) rec[x] = z;
     }
     __syncwarp();
 
@@ -175,7 +238,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint16_t rc = g.cell[v];
             const int r = rc >> 8, c = rc & 0xFF;
             for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) cnt += col[u] == k;
-            for (int t = g.cs[c]; t < g.cs[c + 1]; ++t) cnt += col[g.cl[t]] == k;
+            for (int x = g.cs[c]; x < g.cs[c + 1]; ++x) cnt += col[g.cl[x]] == k;
             cnt -= 2;  // v itself in its row and its column
         }
         conf[v] = (uint8_t)cnt;
@@ -201,8 +264,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         const int r = rc >> 8, c = rc & 0xFF;
         for (int u = g.rs[r] + lane; u < g.rs[r + 1]; u += 32)
             if (u != w && col[u] == k) conf[u] -= 1;
-        for (int t = g.cs[c] + lane; t < g.cs[c + 1]; t += 32) {
-            const int u = g.cl[t];
+        for (int x = g.cs[c] + lane; x < g.cs[c + 1]; x += 32) {
+            const int u = g.cl[x];
             if (u != w && col[u] == k) conf[u] -= 1;
         }
         __syncwarp();
@@ -214,17 +277,17 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     }
 
     // ---- occupancy masks R/C and uncoloured bitmask U of the (now legal) colouring
-    for (int t = lane; t < n * W; t += 32) {
-        s.R[t] = 0;
-        s.C[t] = 0;
+    for (int x = lane; x < n * W; x += 32) {
+        s.R[x] = 0;
+        s.C[x] = 0;
     }
     __syncwarp();
     int fl = 0;
     for (int q = 0; q < g.lane_words; ++q) {
-        const int base = v_lo + 32 * q;
+        const int vb = v_lo + 32 * q;
         uint32_t bits = 0;
         for (int b = 0; b < 32; ++b) {
-            const int v = base + b;
+            const int v = vb + b;
             if (v >= nv) break;
             const int k = col[v];
             if (!k) {
@@ -241,47 +304,160 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     int f = (int)__reduce_add_sync(kFull, (unsigned)fl);
     __syncwarp();
 
+    const long long t_prologue = prof ? clock64() - t_start : 0;
     const int repaired_f = f;
     int bestf = f;
     bool pending = true;  // best_ == current (partial.hpp:84)
     uint32_t j = 0;
-    unsigned long long bytes = 0;
+    // SURVEY 8(d) algorithmic bytes: lane 0 accounts the scan, v*'s RMW and the
+    // snapshots, lanes 1/2 the evictees' RMW; summed over the warp at the end.
+    unsigned long long acc = 0;
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
+    const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
     const bool tracing = (i == a.trace_idx) && a.trace != nullptr;
+    bool sparse = false;
+    // sparse-mode slot (valid on lanes < f): vertex | row << 16 | col << 24, tabu cache
+    uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
 
     while ((int64_t)j < a.budget && bestf > a.stop_f && f > 0) {
+        if (prof) t_step = clock64();
+        const bool step_sparse = f <= 32;
         const bool asp = (f == bestf);
-        // ---- phase A: admissible counts per level over this lane's uncoloured vertices
-        int c0 = 0, c1 = 0, c2 = 0;
-        for (int q = 0; q < g.lane_words; ++q) {
-            uint32_t bits = s.U[lane * g.lane_words + q];
-            while (bits) {
-                const int v = v_lo + 32 * q + __ffs(bits) - 1;
-                bits &= bits - 1;
-                uint64_t m0[W], m1[W], m2[W];
-                cand_masks<W>(g, s, rec, until, v, j, asp, m0, m1, m2);
-                c0 += popc_w<W>(m0);
-                c1 += popc_w<W>(m1);
-                c2 += popc_w<W>(m2);
-            }
-        }
-        const unsigned b0 = __ballot_sync(kFull, c0 > 0);
-        const unsigned b1 = __ballot_sync(kFull, c1 > 0);
-        const unsigned b2 = __ballot_sync(kFull, c2 > 0);
-        const int lvl = b0 ? -1 : b1 ? 0 : b2 ? 1 : 2;
-        const int cnt = lvl == -1 ? c0 : lvl == 0 ? c1 : lvl == 1 ? c2 : 0;
-        int incl = cnt;
+        const uint32_t t = base + j;  // tabu clock of this step's scan
+        if (f <= 32 && !sparse) {
+            // enter sparse mode: lane l takes the l-th uncoloured vertex (ascending v)
+            if (prof) ++pn_enter;
+            int cnt = 0;
+            for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
+            int incl = cnt;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int t = __shfl_up_sync(kFull, incl, d);
-            if (lane >= d) incl += t;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += x;
+            }
+            uint16_t* list = reinterpret_cast<uint16_t*>(conf);
+            int at = incl - cnt;
+            for (int q = 0; q < g.lane_words; ++q) {
+                uint32_t bits = s.U[lane * g.lane_words + q];
+                while (bits) {
+                    list[at++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
+                    bits &= bits - 1;
+                }
+            }
+            __syncwarp();
+            if (lane < f) {
+                const int v = list[lane];
+                const TabuRec tr = rec[v];
+                const uint16_t rc = g.cell[v];
+                svc = (uint32_t)v | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24);
+                su1 = tr.u1;
+                su2 = tr.u2;
+                skk = tr.kk;
+            }
+            __syncwarp();
+            sparse = true;
         }
-        const int N = __shfl_sync(kFull, incl, 31);
-        const uint64_t x = canon_draw(seed, j);
+        const uint32_t h1 = fmix32(s32 + (j + 1) * 0x9E3779B9u);
+        const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
+        int lvl, N, vs, ks = 0, wl = 0;
+        if (sparse) {
+            // ---- sparse: each lane scores its own slot
+            uint64_t m[W];
+            int lv = 3;
+            uint64_t m0[W], m1[W], m2[W];
+            if (lane < f) {
+                const int r = (svc >> 16) & 0xFF, c = svc >> 24;
+                uint64_t dom[W], T[W];
+                dom_mask<W>(g, r, c, dom);
+                tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, t, T);
+                level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
+                uint64_t o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+                for (int z = 0; z < W; ++z) {
+                    o0 |= m0[z];
+                    o1 |= m1[z];
+                    o2 |= m2[z];
+                }
+                lv = o0 ? 0 : o1 ? 1 : o2 ? 2 : 3;
+            }
+            const int lc = (int)__reduce_min_sync(kFull, (unsigned)lv);
+            lvl = lc - 1;
+#pragma unroll
+            for (int z = 0; z < W; ++z) m[z] = (lane < f) ? (lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z]) : 0ULL;
+            const int cnt = lc == 3 ? 0 : popc_w<W>(m);
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += x;
+            }
+            N = __shfl_sync(kFull, incl, 31);
+            const uint32_t r = __umulhi(h1, (uint32_t)N);
+            wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
+            if (wl < 0) wl = 0;
+            if (lane == wl && N > 0) ks = nth_bit_w<W>(m, (int)r - (incl - cnt));
+            vs = (int)(__shfl_sync(kFull, svc, wl) & 0xFFFFu);
+            ks = __shfl_sync(kFull, ks, wl);
+        } else {
+            // ---- dense: each lane scans its bitmask words (start of the descent, |V0| > 32)
+            int c0 = 0, c1 = 0, c2 = 0;
+            for (int q = 0; q < g.lane_words; ++q) {
+                uint32_t bits = s.U[lane * g.lane_words + q];
+                while (bits) {
+                    const int v = v_lo + 32 * q + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    uint64_t x0[W], x1[W], x2[W];
+                    dense_masks<W>(g, s, rec, until, v, t, asp, x0, x1, x2);
+                    c0 += popc_w<W>(x0);
+                    c1 += popc_w<W>(x1);
+                    c2 += popc_w<W>(x2);
+                }
+            }
+            const unsigned b0 = __ballot_sync(kFull, c0 > 0);
+            const unsigned b1 = __ballot_sync(kFull, c1 > 0);
+            const unsigned b2 = __ballot_sync(kFull, c2 > 0);
+            lvl = b0 ? -1 : b1 ? 0 : b2 ? 1 : 2;
+            const int cnt = lvl == -1 ? c0 : lvl == 0 ? c1 : lvl == 1 ? c2 : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += x;
+            }
+            N = __shfl_sync(kFull, incl, 31);
+            vs = -1;
+            const uint32_t r = __umulhi(h1, (uint32_t)N);
+            wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
+            if (wl < 0) wl = 0;
+            if (lane == wl && N > 0) {
+                int rr = (int)r - (incl - cnt);
+                for (int q = 0; q < g.lane_words && vs < 0; ++q) {
+                    uint32_t bits = s.U[lane * g.lane_words + q];
+                    while (bits) {
+                        const int v = v_lo + 32 * q + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        uint64_t x0[W], x1[W], x2[W];
+                        dense_masks<W>(g, s, rec, until, v, t, asp, x0, x1, x2);
+                        uint64_t mm[W];
+#pragma unroll
+                        for (int z = 0; z < W; ++z) mm[z] = lvl == -1 ? x0[z] : lvl == 0 ? x1[z] : x2[z];
+                        const int pc = popc_w<W>(mm);
+                        if (rr < pc) {
+                            ks = nth_bit_w<W>(mm, rr);
+                            vs = v;
+                            break;
+                        }
+                        rr -= pc;
+                    }
+                }
+            }
+            vs = __shfl_sync(kFull, vs, wl);
+            ks = __shfl_sync(kFull, ks, wl);
+        }
         const int f_before = f;
-        unsigned long long bt = 2ULL * (unsigned)w1 * (unsigned)f_before;
         if (N == 0) {
             // every candidate tabu: no move, the clock still advances (partial.hpp:121-122)
+            if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
             if (tracing && lane == 0 && (int64_t)j < a.trace_cap) {
                 plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + j;
                 tr->step = j;
@@ -295,49 +471,9 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 tr->n_adm = 0;
                 tr->level = 2;
             }
-            bytes += bt;
             ++j;
             continue;
         }
-        const uint32_t r = (uint32_t)(((x >> 32) * (uint64_t)(uint32_t)N) >> 32);
-        const unsigned wb = __ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl);
-        const int wl = __ffs(wb) - 1;
-        // ---- phase B: the winner lane recovers its (r - prefix)-th candidate in (v, k) order
-        int vs = -1, ks = 0;
-        if (lane == wl) {
-            int rr = (int)r - (incl - cnt);
-            for (int q = 0; q < g.lane_words && vs < 0; ++q) {
-                uint32_t bits = s.U[lane * g.lane_words + q];
-                while (bits) {
-                    const int v = v_lo + 32 * q + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    uint64_t m0[W], m1[W], m2[W];
-                    cand_masks<W>(g, s, rec, until, v, j, asp, m0, m1, m2);
-                    uint64_t m[W];
-#pragma unroll
-                    for (int z = 0; z < W; ++z) m[z] = lvl == -1 ? m0[z] : lvl == 0 ? m1[z] : m2[z];
-                    const int pc = popc_w<W>(m);
-                    if (rr < pc) {
-#pragma unroll
-                        for (int z = 0; z < W; ++z) {
-                            const int pz = __popcll(m[z]);
-                            if (vs < 0) {
-                                if (rr < pz) {
-                                    ks = z * 64 + nth_bit64(m[z], rr);
-                                    vs = v;
-                                } else {
-                                    rr -= pz;
-                                }
-                            }
-                        }
-                        break;
-                    }
-                    rr -= pc;
-                }
-            }
-        }
-        vs = __shfl_sync(kFull, vs, wl);
-        ks = __shfl_sync(kFull, ks, wl);
 
         // ---- apply (partial.hpp:124-141)
         if (pending && lvl >= 0) {
@@ -349,78 +485,103 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
         const int kw = ks >> 6;
         const uint64_t bitk = 1ULL << (ks & 63);
-        const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
-        const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
         int ur = -1, uc = -1;
-        if (inR) {
-            for (int base = g.rs[rs_]; base < g.rs[rs_ + 1]; base += 32) {
-                const int u = base + lane;
-                const unsigned hit = __ballot_sync(kFull, u < g.rs[rs_ + 1] && col[u] == ks);
-                if (hit) {
-                    ur = base + __ffs(hit) - 1;
-                    break;
+        if (lvl >= 0) {
+            // the row / column holder of k* (at most one each: the colouring is legal)
+            const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
+            const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
+            if (inR) {
+                for (int b0 = g.rs[rs_]; b0 < g.rs[rs_ + 1]; b0 += 32) {
+                    const int u = b0 + lane;
+                    const unsigned hit = __ballot_sync(kFull, u < g.rs[rs_ + 1] && col[u] == ks);
+                    if (hit) {
+                        ur = b0 + __ffs(hit) - 1;
+                        break;
+                    }
                 }
             }
-        }
-        if (inC) {
-            for (int base = g.cs[cs_]; base < g.cs[cs_ + 1]; base += 32) {
-                const int t = base + lane;
-                const int u = t < g.cs[cs_ + 1] ? g.cl[t] : 0;
-                const unsigned hit = __ballot_sync(kFull, t < g.cs[cs_ + 1] && col[u] == ks);
-                if (hit) {
-                    uc = __shfl_sync(kFull, u, __ffs(hit) - 1);
-                    break;
+            if (inC) {
+                for (int b0 = g.cs[cs_]; b0 < g.cs[cs_ + 1]; b0 += 32) {
+                    const int x = b0 + lane;
+                    const int u = x < g.cs[cs_ + 1] ? g.cl[x] : 0;
+                    const unsigned hit = __ballot_sync(kFull, x < g.cs[cs_ + 1] && col[u] == ks);
+                    if (hit) {
+                        uc = __shfl_sync(kFull, u, __ffs(hit) - 1);
+                        break;
+                    }
                 }
             }
         }
         const int e = (ur >= 0) + (uc >= 0);
-        int deg_bytes = 0;
-        {
-            auto deg = [&](int v) {
-                const uint16_t rc = g.cell[v];
-                const int r_ = rc >> 8, c_ = rc & 0xFF;
-                return (g.rs[r_ + 1] - g.rs[r_] - 1) + (g.cs[c_ + 1] - g.cs[c_] - 1);
-            };
-            deg_bytes = deg(vs) + (ur >= 0 ? deg(ur) : 0) + (uc >= 0 ? deg(uc) : 0);
-        }
+        const int f_new = f - 1 + e;
+        const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(a.alpha * (double)f_new);
+        const uint32_t ut = t + 1 + tenure;
+        const bool improved = f_new < bestf;
         __syncwarp();
+        // distributed update: lane 0 colours v*, lanes 1 / 2 evict the row / column holder
+        TabuRec nr{0, 0, 0, 0};
         if (lane == 0) {
             col[vs] = (uint8_t)ks;
-            s.U[vs >> 5] &= ~(1u << (vs & 31));
-            if (ur >= 0) {
-                col[ur] = 0;
-                s.U[ur >> 5] |= 1u << (ur & 31);
-                s.C[(g.cell[ur] & 0xFF) * W + kw] &= ~bitk;
-            }
-            if (uc >= 0) {
-                col[uc] = 0;
-                s.U[uc >> 5] |= 1u << (uc & 31);
-                s.R[(g.cell[uc] >> 8) * W + kw] &= ~bitk;
-            }
+            atomicAnd(&s.U[vs >> 5], ~(1u << (vs & 31)));
             s.R[rs_ * W + kw] |= bitk;
             s.C[cs_ * W + kw] |= bitk;
-        }
-        f = f - 1 + e;
-        const uint32_t lpart = (uint32_t)(((x & 0xFFFFFFFFULL) * 10ULL) >> 32);
-        const uint32_t tenure = lpart + (uint32_t)(a.alpha * (double)f);
-        const uint32_t ut = j + 1 + tenure;
-        if ((lane == 1 && ur >= 0) || (lane == 2 && uc >= 0)) {
+            acc += 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
+                   (improved ? 2ULL * (unsigned)nv : 0ULL);
+        } else if (lane <= 2) {
             const int u = lane == 1 ? ur : uc;
-            until[(size_t)u * w1 + ks] = ut;
-            TabuRec<W> rr = rec[u];
-            if (rr.tm[kw] & bitk) rr.exact = 0;
-            rr.tm[kw] |= bitk;
-            rr.umax = max(rr.umax, ut);
-            rec[u] = rr;
+            if (u >= 0) {
+                nr = rec[u];
+                col[u] = 0;
+                atomicOr(&s.U[u >> 5], 1u << (u & 31));
+                if (lane == 1)
+                    s.C[(g.cell[u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
+                else
+                    s.R[(g.cell[u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
+                until[(size_t)u * w1 + ks] = ut;
+                cache_forbid(nr, ks, ut, t);
+                rec[u] = nr;
+                acc += 4ULL * g.deg[u] + 2ULL;
+            }
         }
-        bt += 4ULL * (unsigned)deg_bytes + 2ULL * (unsigned)(1 + e);
-        const bool improved = f < bestf;
+        // ---- sparse slot list: new sorted list = old - {v*} + {ur, uc}
+        if (sparse) {
+            if (f_new > 32) {
+                sparse = false;
+            } else {
+                const int vl = (int)(svc & 0xFFFFu);
+                const bool old_ok = lane < f && lane != wl;
+                const int pr_ = ur >= 0 ? __popc(__ballot_sync(kFull, old_ok && vl < ur)) + (uc >= 0 && uc < ur) : -1;
+                const int pc_ = uc >= 0 ? __popc(__ballot_sync(kFull, old_ok && vl < uc)) + (ur >= 0 && ur < uc) : -1;
+                const int y = lane - (pr_ >= 0 && pr_ < lane) - (pc_ >= 0 && pc_ < lane);
+                const int src = (y >= wl ? y + 1 : y) & 31;
+                const uint32_t mvc = __shfl_sync(kFull, svc, src);
+                const uint32_t mu1 = __shfl_sync(kFull, su1, src);
+                const uint32_t mu2 = __shfl_sync(kFull, su2, src);
+                const uint32_t mkk = __shfl_sync(kFull, skk, src);
+                const int from = lane == pr_ ? 1 : 2;  // evictee caches come from lanes 1 / 2
+                const uint32_t nu1 = __shfl_sync(kFull, nr.u1, from);
+                const uint32_t nu2 = __shfl_sync(kFull, nr.u2, from);
+                const uint32_t nkk = __shfl_sync(kFull, nr.kk, from);
+                if (lane == pr_ || lane == pc_) {
+                    const int u = lane == pr_ ? ur : uc;
+                    const uint16_t rc = g.cell[u];
+                    svc = (uint32_t)u | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24);
+                    su1 = nu1;
+                    su2 = nu2;
+                    skk = nkk;
+                } else {
+                    svc = mvc;
+                    su1 = mu1;
+                    su2 = mu2;
+                    skk = mkk;
+                }
+            }
+        }
+        f = f_new;
         if (improved) {
             bestf = f;
             pending = true;
-            bt += 2ULL * (unsigned)nv;
         }
-        bytes += bt;
         if (tracing && lane == 0 && (int64_t)j < a.trace_cap) {
             plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + j;
             // CSR order of N(v*): row-mates first iff row <= col (lsgraph.hpp:202-209)
@@ -442,19 +603,48 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         }
         __syncwarp();
         ++j;
+        if (prof) {
+            const unsigned long long dt = (unsigned long long)(clock64() - t_step);
+            if (step_sparse) {
+                pc_sparse += dt;
+                ++pn_sparse;
+            } else {
+                pc_dense += dt;
+                ++pn_dense;
+                pf_dense += (unsigned)f_before;
+            }
+        }
     }
     if (pending) snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+    {
+        // lanes 0..2 hold the byte-counter parts
+        const unsigned long long a1 = __shfl_sync(kFull, acc, 1), a2 = __shfl_sync(kFull, acc, 2);
+        acc += a1 + a2;
+    }
     if (lane == 0) {
         a.best_f[i] = bestf;
         a.repaired_f[i] = repaired_f;
         a.iters[i] = (int64_t)j;
-        a.bytes[i] = bytes;
+        a.bytes[i] = acc;
+        // every until written by this individual is < base + j + 1 + tenure_cap
+        *slot_clock = base + j + 2 + a.tenure_cap;
+    }
+    if (prof && lane == 0) {
+        atomicAdd(prof + 0, 1ULL);
+        atomicAdd(prof + 1, (unsigned long long)t_prologue);
+        atomicAdd(prof + 2, pn_dense);
+        atomicAdd(prof + 3, pc_dense);
+        atomicAdd(prof + 4, pn_sparse);
+        atomicAdd(prof + 5, pc_sparse);
+        atomicAdd(prof + 6, pf_dense);
+        atomicAdd(prof + 7, pn_enter);
+        atomicAdd(prof + 8, (unsigned long long)(clock64() - t_start));
     }
     __syncwarp();
 }
 
 template <int W>
-__global__ void __launch_bounds__(kImproveMaxThreads) k_improve(const ImproveArgs a) {
+__global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_improve(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int n = a.n, nv = a.nv;
@@ -465,17 +655,23 @@ __global__ void __launch_bounds__(kImproveMaxThreads) k_improve(const ImproveArg
     uint16_t* s_cl = reinterpret_cast<uint16_t*>(smem + L.cl);
     uint64_t* s_pr = reinterpret_cast<uint64_t*>(smem + L.pr);
     uint64_t* s_pc = reinterpret_cast<uint64_t*>(smem + L.pc);
-    for (int t = threadIdx.x; t < nv; t += blockDim.x) {
-        s_cell[t] = a.cell[t];
-        s_cl[t] = a.col_list[t];
+    uint8_t* s_deg = smem + L.deg;
+    for (int x = threadIdx.x; x < nv; x += blockDim.x) {
+        s_cell[x] = a.cell[x];
+        s_cl[x] = a.col_list[x];
     }
-    for (int t = threadIdx.x; t <= n; t += blockDim.x) {
-        s_rs[t] = a.row_start[t];
-        s_cs[t] = a.col_start[t];
+    for (int x = threadIdx.x; x <= n; x += blockDim.x) {
+        s_rs[x] = a.row_start[x];
+        s_cs[x] = a.col_start[x];
     }
-    for (int t = threadIdx.x; t < n * W; t += blockDim.x) {
-        s_pr[t] = a.pre_row[t];
-        s_pc[t] = a.pre_col[t];
+    for (int x = threadIdx.x; x < n * W; x += blockDim.x) {
+        s_pr[x] = a.pre_row[x];
+        s_pc[x] = a.pre_col[x];
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < nv; x += blockDim.x) {
+        const int r = s_cell[x] >> 8, c = s_cell[x] & 0xFF;
+        s_deg[x] = (uint8_t)((s_rs[r + 1] - s_rs[r] - 1) + (s_cs[c + 1] - s_cs[c] - 1));
     }
     __syncthreads();
 
@@ -485,6 +681,7 @@ __global__ void __launch_bounds__(kImproveMaxThreads) k_improve(const ImproveArg
     g.nvpad = a.nvpad;
     g.lane_words = a.lane_words;
     g.cell = s_cell;
+    g.deg = s_deg;
     g.rs = s_rs;
     g.cs = s_cs;
     g.cl = s_cl;
@@ -509,7 +706,7 @@ __global__ void __launch_bounds__(kImproveMaxThreads) k_improve(const ImproveArg
     s.U = reinterpret_cast<uint32_t*>(wbase + L.w_U);
 
     const int slot = blockIdx.x * nwarps + warp;
-    TabuRec<W>* rec = reinterpret_cast<TabuRec<W>*>(reinterpret_cast<char*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
+    TabuRec* rec = reinterpret_cast<TabuRec*>(reinterpret_cast<char*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
 
     for (;;) {
@@ -517,13 +714,13 @@ __global__ void __launch_bounds__(kImproveMaxThreads) k_improve(const ImproveArg
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
         i = __shfl_sync(kFull, i, 0);
         if (i >= a.p) break;
-        improve_one<W>(a, g, s, rec, until, i, lane);
+        improve_one<W>(a, g, s, rec, until, a.slot_clock + slot, i, lane);
     }
 }
 
 // W = 64-bit words per colour mask: 1 for n <= 63, 2 for n <= 127 (the u8 conflict
 // counters of the repair bound n at 127; capi.cu rejects larger orders).
-size_t tabu_rec_bytes(int W) { return W == 1 ? sizeof(TabuRec<1>) : sizeof(TabuRec<2>); }
+size_t tabu_rec_bytes(int) { return sizeof(TabuRec); }
 
 const void* improve_kernel_ptr(int W) {
     if (W == 1) return reinterpret_cast<const void*>(&k_improve<1>);

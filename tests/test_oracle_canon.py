@@ -27,16 +27,31 @@ def _replay_legal(orc, grid, start, trace):
     return cur
 
 
-def test_canon_draw_is_splitmix_sequence(orc):
-    s = 0x1234_5678_9ABC_DEF0
-    st = s
-    for j in range(50):
-        st = (st + 0x9E3779B97F4A7C15) & (2**64 - 1)
-        z = st
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
-        z ^= z >> 31
-        assert orc.canon_draw(s, j) == z
+def _fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+    return h ^ (h >> 16)
+
+
+def test_canon_draw_definition(orc):
+    """DESIGN.md: h1 = fmix32(fold(s) + (j+1)*0x9E3779B9), h2 = fmix32(h1 + 0x632BE5AB)"""
+    for s in (0, 1, 0x1234_5678_9ABC_DEF0, 2**64 - 1):
+        s32 = (s ^ (s >> 32)) & 0xFFFFFFFF
+        for j in range(40):
+            h1 = _fmix32((s32 + (j + 1) * 0x9E3779B9) & 0xFFFFFFFF)
+            h2 = _fmix32((h1 + 0x632BE5AB) & 0xFFFFFFFF)
+            assert orc.canon_draw(s, j) == (h1 << 32) | h2
+
+
+def test_canon_draws_are_uniform(orc):
+    hi = np.array([orc.canon_draw(77, j) >> 32 for j in range(20000)], np.uint64)
+    lo = np.array([orc.canon_draw(77, j) & 0xFFFFFFFF for j in range(20000)], np.uint64)
+    for x in (hi, lo):
+        h = np.bincount((x * 16 >> 32).astype(np.int64), minlength=16)
+        exp = len(x) / 16
+        assert ((h - exp) ** 2 / exp).sum() < 45.0  # 15 dof
 
 
 def test_partialcol_keeps_legal_and_accounts_f(orc):
