@@ -356,7 +356,8 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_work = dalloc<int>(1);
 
     // ---- improve launch shape: maximise resident warps per SM (one individual per warp)
-    const void* kern = improve_kernel_ptr(W);
+    const void* kern = improve_kernel_ptr(W, false);
+    const void* kern_dbg = improve_kernel_ptr(W, true);
     const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
     int best_warps = 0;
     int force_wpc = 0;
@@ -379,6 +380,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     }
     if (best_warps == 0) throw Unsupported("instance too large for the shared-memory resident search");
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    CK(cudaFuncSetAttribute(kern_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     c->threads = 32 * c->wpc;
     c->warps_per_sm = best_warps;
     c->slots = c->grid * c->wpc;

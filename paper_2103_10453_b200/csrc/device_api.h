@@ -95,7 +95,7 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
 }
 
 size_t tabu_rec_bytes(int W);
-const void* improve_kernel_ptr(int W);
+const void* improve_kernel_ptr(int W, bool debug);
 cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 
 // ---- distances (K3)

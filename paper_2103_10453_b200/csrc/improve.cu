@@ -199,7 +199,8 @@ __device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int n
     for (int t = lane; t < nvpad / 16; t += 32) d4[t] = s4[t];
 }
 
-template <int W>
+// kDebug: per-step trace (plse_trace) and clock64 instrumentation (PLSE_PROFILE)
+template <int W, bool kDebug>
 __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
                             uint32_t* until, uint32_t* slot_clock, int i, int lane) {
     const int n = g.n, nv = g.nv, w1 = n + 1;
@@ -208,7 +209,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     const int v_hi = min(nv, v_lo + B);
     uint8_t* col = s.col;
     uint8_t* conf = s.conf;
-    unsigned long long* prof = a.prof;
+    unsigned long long* prof = kDebug ? a.prof : nullptr;
     long long t_start = prof ? clock64() : 0, t_step = 0;
     unsigned long long pc_dense = 0, pc_sparse = 0, pn_dense = 0, pn_sparse = 0, pf_dense = 0, pn_enter = 0;
 
@@ -314,7 +315,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     unsigned long long acc = 0;
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
     const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
-    const bool tracing = (i == a.trace_idx) && a.trace != nullptr;
+    const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     bool sparse = false;
     // sparse-mode slot (valid on lanes < f): vertex | row << 16 | col << 24, tabu cache
     uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
@@ -385,13 +386,13 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 #pragma unroll
             for (int z = 0; z < W; ++z) m[z] = (lane < f) ? (lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z]) : 0ULL;
             const int cnt = lc == 3 ? 0 : popc_w<W>(m);
+            // inclusive warp scan over the f occupied lanes only (f <= 32)
             int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+            for (int d = 1; d < f; d <<= 1) {
                 const int x = __shfl_up_sync(kFull, incl, d);
                 if (lane >= d) incl += x;
             }
-            N = __shfl_sync(kFull, incl, 31);
+            N = __shfl_sync(kFull, incl, f - 1);
             const uint32_t r = __umulhi(h1, (uint32_t)N);
             wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
             if (wl < 0) wl = 0;
@@ -519,7 +520,9 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         const bool improved = f_new < bestf;
         __syncwarp();
         // distributed update: lane 0 colours v*, lanes 1 / 2 evict the row / column holder
+        const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
         TabuRec nr{0, 0, 0, 0};
+        if (my_u >= 0) nr = rec[my_u];  // issued early: consumed after the slot bookkeeping below
         if (lane == 0) {
             col[vs] = (uint8_t)ks;
             atomicAnd(&s.U[vs >> 5], ~(1u << (vs & 31)));
@@ -527,21 +530,15 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             s.C[cs_ * W + kw] |= bitk;
             acc += 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
                    (improved ? 2ULL * (unsigned)nv : 0ULL);
-        } else if (lane <= 2) {
-            const int u = lane == 1 ? ur : uc;
-            if (u >= 0) {
-                nr = rec[u];
-                col[u] = 0;
-                atomicOr(&s.U[u >> 5], 1u << (u & 31));
-                if (lane == 1)
-                    s.C[(g.cell[u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
-                else
-                    s.R[(g.cell[u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
-                until[(size_t)u * w1 + ks] = ut;
-                cache_forbid(nr, ks, ut, t);
-                rec[u] = nr;
-                acc += 4ULL * g.deg[u] + 2ULL;
-            }
+        } else if (my_u >= 0) {
+            col[my_u] = 0;
+            atomicOr(&s.U[my_u >> 5], 1u << (my_u & 31));
+            if (lane == 1)
+                s.C[(g.cell[my_u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
+            else
+                s.R[(g.cell[my_u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
+            until[(size_t)my_u * w1 + ks] = ut;
+            acc += 4ULL * g.deg[my_u] + 2ULL;
         }
         // ---- sparse slot list: new sorted list = old - {v*} + {ur, uc}
         if (sparse) {
@@ -558,6 +555,10 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 const uint32_t mu1 = __shfl_sync(kFull, su1, src);
                 const uint32_t mu2 = __shfl_sync(kFull, su2, src);
                 const uint32_t mkk = __shfl_sync(kFull, skk, src);
+                if (my_u >= 0) {
+                    cache_forbid(nr, ks, ut, t);
+                    rec[my_u] = nr;
+                }
                 const int from = lane == pr_ ? 1 : 2;  // evictee caches come from lanes 1 / 2
                 const uint32_t nu1 = __shfl_sync(kFull, nr.u1, from);
                 const uint32_t nu2 = __shfl_sync(kFull, nr.u2, from);
@@ -576,6 +577,11 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                     skk = mkk;
                 }
             }
+        }
+        if (!sparse && my_u >= 0) {
+            // dense step (or sparse mode just left): record the forbid here
+            cache_forbid(nr, ks, ut, t);
+            rec[my_u] = nr;
         }
         f = f_new;
         if (improved) {
@@ -643,7 +649,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     __syncwarp();
 }
 
-template <int W>
+template <int W, bool kDebug>
 __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_improve(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -714,7 +720,7 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
         i = __shfl_sync(kFull, i, 0);
         if (i >= a.p) break;
-        improve_one<W>(a, g, s, rec, until, a.slot_clock + slot, i, lane);
+        improve_one<W, kDebug>(a, g, s, rec, until, a.slot_clock + slot, i, lane);
     }
 }
 
@@ -722,16 +728,26 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
 // counters of the repair bound n at 127; capi.cu rejects larger orders).
 size_t tabu_rec_bytes(int) { return sizeof(TabuRec); }
 
-const void* improve_kernel_ptr(int W) {
-    if (W == 1) return reinterpret_cast<const void*>(&k_improve<1>);
-    return reinterpret_cast<const void*>(&k_improve<2>);
+const void* improve_kernel_ptr(int W, bool debug) {
+    if (W == 1) return debug ? reinterpret_cast<const void*>(&k_improve<1, true>)
+                             : reinterpret_cast<const void*>(&k_improve<1, false>);
+    return debug ? reinterpret_cast<const void*>(&k_improve<2, true>)
+                 : reinterpret_cast<const void*>(&k_improve<2, false>);
 }
 
 cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    if (W == 1)
-        k_improve<1><<<grid, threads, smem, st>>>(a);
-    else
-        k_improve<2><<<grid, threads, smem, st>>>(a);
+    const bool debug = a.trace != nullptr || a.prof != nullptr;
+    if (W == 1) {
+        if (debug)
+            k_improve<1, true><<<grid, threads, smem, st>>>(a);
+        else
+            k_improve<1, false><<<grid, threads, smem, st>>>(a);
+    } else {
+        if (debug)
+            k_improve<2, true><<<grid, threads, smem, st>>>(a);
+        else
+            k_improve<2, false><<<grid, threads, smem, st>>>(a);
+    }
     return cudaGetLastError();
 }
 
