@@ -142,6 +142,9 @@ class Oracle:
         L.or_offspring.argtypes = [C.c_void_p, C.c_int, u16p, i32p, C.c_int, C.c_double, C.c_int, C.c_int,
                                    u8p, C.c_uint64, C.c_uint64, u16p, i32p]
         L.or_init_population.argtypes = [C.c_void_p, C.c_int, C.c_uint64, u16p]
+        L.or_init_population_ex.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, u16p]
+        L.or_offspring_ex.argtypes = [C.c_void_p, C.c_int, u16p, i32p, C.c_int, C.c_double, C.c_int, C.c_int,
+                                      u8p, C.c_uint64, C.c_uint64, u16p, i32p]
         L.or_run.argtypes = [C.c_int, u16p, C.POINTER(OrConfig), C.POINTER(OrResult), u16p,
                              C.c_void_p, C.c_int64]
         self._handles = {}
@@ -247,11 +250,21 @@ class Oracle:
                               exclusion, excl.reshape(-1), master_seed, generation, out, part)
         return out.reshape(p, nv), part
 
-    def init_population(self, grid, p, master_seed):
+    def init_population(self, grid, p, master_seed, offset=0):
         g = self.preprocess(grid)
         out = np.zeros(p * g.nv, np.uint16)
-        self.lib.or_init_population(self._h(grid), p, master_seed, out)
+        self.lib.or_init_population_ex(self._h(grid), p, master_seed, offset, out)
         return out.reshape(p, g.nv)
+
+    def offspring_ex(self, grid, members, dist, excl, master_seed, stream_base, crossover=X_AUX, beta=20.0,
+                     matching=M_NEAREST, exclusion=E_RUN):
+        p, nv = members.shape
+        out = np.zeros(p * nv, np.uint16)
+        part = np.zeros(p, np.int32)
+        self.lib.or_offspring_ex(self._h(grid), p, np.ascontiguousarray(members, np.uint16).reshape(-1),
+                                 np.ascontiguousarray(dist, np.int32).reshape(-1), crossover, beta, matching,
+                                 exclusion, excl.reshape(-1), master_seed, stream_base, out, part)
+        return out.reshape(p, nv), part
 
     def run(self, grid, p=64, alpha=0.6, gamma=10.0, beta=20.0, phase1_iters=0, crossover=X_AUX,
             matching=M_NEAREST, exclusion=E_RUN, seed=0, iteration_limit=0, generation_limit=0,

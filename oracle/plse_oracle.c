@@ -754,6 +754,14 @@ int or_nearest_neighbor(int p, const int32_t* dist, int i, uint8_t* excl) {
 int or_offspring(const or_graph* g, int p, const uint16_t* members, const int32_t* dist,
                  int crossover, double beta, int matching, int exclusion, uint8_t* excl,
                  uint64_t master_seed, uint64_t generation, uint16_t* offspring, int32_t* partner) {
+    return or_offspring_ex(g, p, members, dist, crossover, beta, matching, exclusion, excl, master_seed,
+                           generation * (uint64_t)p, offspring, partner);
+}
+
+/* island form: stream index = stream_base + i (stream_base = gen*p_total + offset) */
+int or_offspring_ex(const or_graph* g, int p, const uint16_t* members, const int32_t* dist,
+                    int crossover, double beta, int matching, int exclusion, uint8_t* excl,
+                    uint64_t master_seed, uint64_t stream_base, uint16_t* offspring, int32_t* partner) {
     const int nv = g->nv;
     if (crossover == OR_X_NONE) {
         memcpy(offspring, members, sizeof(uint16_t) * (size_t)p * nv);
@@ -766,7 +774,7 @@ int or_offspring(const or_graph* g, int p, const uint16_t* members, const int32_
         int j;
         if (matching == OR_M_RANDOM) {
             or_rng m;
-            or_rng_seed(&m, or_derive_seed(master_seed, 6, generation * (uint64_t)p + (uint64_t)i));
+            or_rng_seed(&m, or_derive_seed(master_seed, 6, stream_base + (uint64_t)i));
             j = (int)or_rng_below(&m, (uint64_t)(p - 1));
             if (j >= i) ++j;
         } else {
@@ -777,7 +785,7 @@ int or_offspring(const or_graph* g, int p, const uint16_t* members, const int32_
     }
     for (int i = 0; i < p; ++i) {
         or_rng st;
-        or_rng_seed(&st, or_derive_seed(master_seed, 3, generation * (uint64_t)p + (uint64_t)i));
+        or_rng_seed(&st, or_derive_seed(master_seed, 3, stream_base + (uint64_t)i));
         const uint16_t* first = members + (size_t)i * nv;
         const uint16_t* second = members + (size_t)part[i] * nv;
         uint16_t* child = offspring + (size_t)i * nv;
@@ -800,10 +808,14 @@ int or_offspring(const or_graph* g, int p, const uint16_t* members, const int32_
 
 /* engine.hpp:88-106 (distances are separate: or_full_distances) */
 void or_init_population(const or_graph* g, int p, uint64_t master_seed, uint16_t* members) {
+    or_init_population_ex(g, p, master_seed, 0, members);
+}
+
+void or_init_population_ex(const or_graph* g, int p, uint64_t master_seed, uint64_t offset, uint16_t* members) {
     const int nv = g->nv;
     for (int i = 0; i < p; ++i) {
         or_rng r;
-        or_rng_seed(&r, or_derive_seed(master_seed, 1, (uint64_t)i));
+        or_rng_seed(&r, or_derive_seed(master_seed, 1, offset + (uint64_t)i));
         for (int v = 0; v < nv; ++v) {
             const int begin = g->dom_off[v] + 1;
             const int choices = g->dom_off[v + 1] - begin;

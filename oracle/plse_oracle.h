@@ -124,6 +124,11 @@ int or_offspring(const or_graph* g, int p, const uint16_t* members, const int32_
                  int crossover, double beta, int matching, int exclusion, uint8_t* excl,
                  uint64_t master_seed, uint64_t generation, uint16_t* offspring, int32_t* partner);
 void or_init_population(const or_graph* g, int p, uint64_t master_seed, uint16_t* members);
+/* island forms: stream indices offset+i and stream_base+i */
+int or_offspring_ex(const or_graph* g, int p, const uint16_t* members, const int32_t* dist,
+                    int crossover, double beta, int matching, int exclusion, uint8_t* excl,
+                    uint64_t master_seed, uint64_t stream_base, uint16_t* offspring, int32_t* partner);
+void or_init_population_ex(const or_graph* g, int p, uint64_t master_seed, uint64_t offset, uint16_t* members);
 
 /* ---- engine.hpp:114-262 (partial variant) ------------------------------ */
 typedef struct {

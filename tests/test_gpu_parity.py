@@ -153,3 +153,39 @@ def test_run_matches_oracle(plse, orc, n, r, s, p):
         assert getattr(res, k) == o[k], k
     assert bool(res.proven_optimal) == bool(o["proven_optimal"])
     assert np.array_equal(res.best_solution, o["best_colors"])
+
+
+def test_two_device_islands_match_island_restatement(plse, orc):
+    """Island model at G=2 on one GPU (sequentially, no cross-kernel waits): stream offsets,
+    elite export / migrant import and the per-island phases vs tests/island_sim.py."""
+    import sys
+    import os
+    import torch
+    sys.path.insert(0, os.path.dirname(__file__))
+    import island_sim as S
+
+    n, r, s, p, seed, gens, budget, elites = 10, 0.5, 3, 12, 21, 3, 400, 3
+    grid = orc.generate_instance(n, r, s)
+    g = plse.preprocess(grid)
+    pops = [plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=seed, phase1_iters=budget,
+                                                       p_total=2 * p, offset=rk * p)) for rk in range(2)]
+    for pop in pops:
+        pop.initialize_population()
+        pop.offspring = pop.members
+    rb = pops[0].row_bytes
+    for gen in range(1, gens + 1):
+        for pop in pops:
+            pop.improve(gen)
+            pop.compute_cross_distances()
+            pop.update_population()
+        bufs = [torch.empty((elites, rb), dtype=torch.uint8, device="cuda") for _ in pops]
+        for pop, b in zip(pops, bufs):
+            pop.export_elites(elites, b.data_ptr())
+        torch.cuda.synchronize()
+        pops[0].import_migrants(elites, bufs[1].data_ptr())
+        pops[1].import_migrants(elites, bufs[0].data_ptr())
+        for pop in pops:
+            pop.build_offspring(gen)
+    want = S.simulate(orc, grid, p, 2, seed, gens, budget, elites)
+    for pop, w in zip(pops, want):
+        assert np.array_equal(pop.members, w)

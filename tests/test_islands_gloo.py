@@ -1,0 +1,85 @@
+"""N > 1 island path with world_size 2 over gloo on CPU:
+each rank evolves its island with the oracle and exchanges elites through
+torch.distributed (the same all-gather bench.py does over NCCL); the result
+must equal the sequential island restatement."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out_dir, cfg):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import island_sim as S
+    import oracle
+    from paper_2103_10453_b200 import islands
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = oracle.Oracle()
+    grid = orc.generate_instance(cfg["n"], cfg["r"], cfg["s"])
+    st = S.island_init(orc, grid, cfg["p"], cfg["seed"], rank, world)
+    for gen in range(1, cfg["gens"] + 1):
+        S.island_improve_update(orc, grid, st, cfg["seed"], gen, cfg["budget"])
+        f, c = S.fc(orc, grid, st["members"])
+        mine = torch.from_numpy(st["members"][islands.elite_order(f, c)[:cfg["elites"]]].astype(np.int32))
+        gathered = islands.allgather_rows(mine)
+        incoming = islands.others(gathered, rank, world).numpy().astype(np.uint16)
+        st["members"] = islands.migrate_host(st["members"], f, c, incoming)
+        st["dist"] = orc.full_distances(st["members"])
+        S.island_offspring(orc, grid, st, cfg["seed"], gen)
+    np.save(os.path.join(out_dir, f"rank{rank}.npy"), st["members"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_islands_over_gloo_match_sequential_restatement(tmp_path, orc):
+    import torch.multiprocessing as mp
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import island_sim as S
+
+    cfg = dict(n=10, r=0.5, s=3, p=12, seed=21, gens=3, budget=400, elites=3)
+    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), cfg), nprocs=2, join=True,
+                       start_method="spawn")
+    got = [np.load(tmp_path / f"rank{r}.npy") for r in range(2)]
+    grid = orc.generate_instance(cfg["n"], cfg["r"], cfg["s"])
+    want = S.simulate(orc, grid, cfg["p"], 2, cfg["seed"], cfg["gens"], cfg["budget"], cfg["elites"])
+    for g_, w_ in zip(got, want):
+        assert np.array_equal(g_, w_)
+    # islands exchanged genetic material: each island holds the other's elites after generation 1
+    assert not np.array_equal(got[0], got[1])
+
+
+def test_single_island_is_the_reference_population(orc):
+    """N = 1: stream coordinates reduce to the reference's (gen*p + i) keying"""
+    from paper_2103_10453_b200 import islands
+    assert islands.stream_coords(0, 1, 64) == (64, 0)
+    grid = orc.generate_instance(10, 0.5, 3)
+    a = orc.init_population(grid, 8, 5)
+    b = orc.init_population(grid, 8, 5, offset=0)
+    assert np.array_equal(a, b)
+
+
+def test_elite_and_victim_orders():
+    from paper_2103_10453_b200 import islands
+    f = np.array([5, 3, 3, 9, 1])
+    c = np.array([0, 0, 0, 0, 2])
+    assert islands.elite_order(f, c).tolist() == [1, 2, 0, 3, 4]
+    assert islands.victim_order(f, c).tolist() == [4, 3, 0, 2, 1]
