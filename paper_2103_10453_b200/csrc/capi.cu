@@ -73,6 +73,11 @@ struct plse_ctx {
     std::vector<int64_t> h_iters;
     uint32_t* d_excl = nullptr;
     int excl_words = 0;
+    // K3 on tcgen05: one-hot operands (p x Kpad u8) and the column tables of the domain CSR
+    bool use_tc = true;
+    int kdom = 0, kpad = 0;
+    uint16_t* d_colvert = nullptr;
+    uint8_t *d_hA = nullptr, *d_hB = nullptr;
     int32_t* d_partner = nullptr;
     // improve launch
     void* d_rec = nullptr;
@@ -99,7 +104,7 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_order,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_colvert, d_hA, d_hB, d_order,
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -203,8 +208,20 @@ void eval_into(plse_ctx* c, const uint8_t* colors, std::vector<int32_t>& f, std:
     CK(cudaStreamSynchronize(c->st));
 }
 
+// K3: D = hamming(A rows, B rows) -- tcgen05 one-hot GEMM, or the CUDA-core kernel (PLSE_TC=0)
 void hamming(plse_ctx* c, const uint8_t* A, const uint8_t* B, uint16_t* D) {
-    c->launched(launch_hamming(A, c->prm.p, B, c->prm.p, c->nv, c->nvpad, D, c->prm.p, c->st));
+    const int p = c->prm.p;
+    if (!c->use_tc) {
+        c->launched(launch_hamming(A, p, B, p, c->nv, c->nvpad, D, p, c->st));
+        return;
+    }
+    c->launched(launch_onehot(A, p, c->nvpad, c->d_colvert, c->d_dom, c->kdom, c->kpad, c->d_hA, c->st));
+    const uint8_t* hb = c->d_hA;
+    if (B != A) {
+        c->launched(launch_onehot(B, p, c->nvpad, c->d_colvert, c->d_dom, c->kdom, c->kpad, c->d_hB, c->st));
+        hb = c->d_hB;
+    }
+    c->launched(launch_similarity_tc(c->d_hA, p, hb, p, c->kpad, c->nv, D, p, c->st));
 }
 
 void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_ctx** out) {
@@ -291,6 +308,12 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
             dom8[a] = (uint8_t)k;
         }
     }
+    c->kdom = gr->dom_offsets[nv];
+    c->kpad = (int)up((size_t)c->kdom, 128);
+    std::vector<uint16_t> colvert(c->kdom);
+    for (int v = 0; v < nv; ++v)
+        for (int a = gr->dom_offsets[v]; a < gr->dom_offsets[v + 1]; ++a) colvert[a] = (uint16_t)v;
+    if (const char* env = std::getenv("PLSE_TC")) c->use_tc = env[0] != '0';
     std::vector<uint64_t> below(n + 1, 0);
     for (int b = 1; b <= n; ++b) below[b] = (0 - (uint64_t)b) % (uint64_t)b;
 
@@ -312,6 +335,8 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     CK(cudaMemcpy(c->d_below, below.data(), 8 * below.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_dom_off, gr->dom_offsets, 4 * (nv + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_dom, dom8.data(), dom8.size(), cudaMemcpyHostToDevice));
+    c->d_colvert = dalloc<uint16_t>(c->kdom);
+    CK(cudaMemcpy(c->d_colvert, colvert.data(), 2 * colvert.size(), cudaMemcpyHostToDevice));
 
     // ---- population buffers
     const size_t p = (size_t)c->prm.p;
@@ -328,6 +353,10 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_cross = dalloc<uint16_t>(p * p);
     c->d_fresh = dalloc<uint16_t>(p * p);
     c->d_dnext = dalloc<uint16_t>(p * p);
+    if (c->use_tc) {
+        c->d_hA = dalloc<uint8_t>(p * (size_t)c->kpad);
+        c->d_hB = dalloc<uint8_t>(p * (size_t)c->kpad);
+    }
     CK(cudaMemset(c->d_dist, 0, 2 * p * p));
     c->d_best_f = dalloc<int32_t>(p);
     c->d_rep_f = dalloc<int32_t>(p);

@@ -103,6 +103,12 @@ cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, s
 cudaError_t launch_hamming(const uint8_t* A, int na, const uint8_t* B, int nb, int nv, int nvpad, uint16_t* D,
                            int ldd, cudaStream_t st);
 
+// K3 on tcgen05 (similarity_tc.cu): one-hot expansion + i8 UMMA GEMM, D = |V| - A.B^T
+cudaError_t launch_onehot(const uint8_t* X, int rows, int nvpad, const uint16_t* col_vert, const uint8_t* col_color,
+                          int K, int Kpad, uint8_t* H, cudaStream_t st);
+cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, int N, int Kpad, int nv, uint16_t* D,
+                                 int ldd, cudaStream_t st);
+
 // ---- population kernels (population.cu)
 struct PopGraph {
     int n, nv, nvpad;

@@ -189,3 +189,28 @@ def test_two_device_islands_match_island_restatement(plse, orc):
     want = S.simulate(orc, grid, p, 2, seed, gens, budget, elites)
     for pop, w in zip(pops, want):
         assert np.array_equal(pop.members, w)
+
+
+@pytest.mark.parametrize("p", [300, 1024])
+def test_tensor_core_distances_match_cuda_core(plse, orc, p, monkeypatch):
+    """K3 on tcgen05 (one-hot i8 UMMA) vs the CUDA-core Hamming kernel, both exact, at a size with
+    partial 128x256 tiles (p=300) and full tiles (p=1024)."""
+    grid = orc.generate_instance(60, 0.5, 12345)
+    g = plse.preprocess(grid)
+    rng = np.random.default_rng(p)
+    mem = orc.init_population(grid, p, 5)
+    # mix fully coloured, partially uncoloured and repaired (legal) rows
+    for i in range(0, p, 3):
+        mem[i, rng.random(g.vertex_count) < 0.4] = 0
+    monkeypatch.setenv("PLSE_TC", "1")
+    a = plse.DevicePopulation(g, plse.SolverConfig(p=p))
+    monkeypatch.setenv("PLSE_TC", "0")
+    b = plse.DevicePopulation(g, plse.SolverConfig(p=p))
+    for pop in (a, b):
+        pop.members = mem
+        pop.compute_full_distances()
+    da, db = a.dist, b.dist
+    assert np.array_equal(da, db)
+    sample = rng.integers(0, p, size=(64, 2))
+    for i, j in sample:
+        assert da[i, j] == int((mem[i] != mem[j]).sum())
