@@ -145,6 +145,24 @@ def ncu_traffic(config_key: str):
     return None
 
 
+def k3_roofline(ph, tensor_cores):
+    """similarity GEMM (one-hot i8 tcgen05): algorithmic ops 2*M*N*Kpad per GEMM over the phase time."""
+    if ph["distances"] <= 0 or ph["k3_ops"] <= 0:
+        return None
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        src = "2 x measured bf16 burst (i8 dense rate = 2x bf16 on sm_100; i8 not measured by the driver)"
+    except (OSError, KeyError, ValueError):
+        bf16, src = 1590.0, "2 x fallback bf16 (B200_PROFILING.md)"
+    achieved = ph["k3_ops"] / (ph["distances"] / 1e3) / 1e12
+    peak = 2 * bf16
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
+            "kernel": "k_onehot + k_sim_tc" if tensor_cores else "k_hamming (CUDA cores)", "peak_source": src,
+            "includes": "one-hot expansion of both operands"}
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -228,6 +246,8 @@ def run_ours(a):
         if dist is not None:
             dist.barrier()
 
+    phase = {"improve": 0.0, "distances": 0.0, "update": 0.0, "offspring": 0.0, "k3_ops": 0.0}
+
     def generation():
         nonlocal gen
         gen += 1
@@ -243,6 +263,12 @@ def run_ours(a):
             others = torch.cat([elite_buf[r * a.elites:(r + 1) * a.elites] for r in range(world) if r != rank])
             pop.import_migrants(others.shape[0], others.data_ptr())
         pop.build_offspring(gen)
+        c2 = pop.counters()
+        phase["improve"] += ctr.improve_ms
+        phase["distances"] += c2.distances_ms
+        phase["update"] += c2.update_ms
+        phase["offspring"] += c2.offspring_ms
+        phase["k3_ops"] += c2.k3_ops
         return it, bf, ctr.improve_ms, ctr.alg_bytes
 
     # gen-1 improve rate (for the CPU-baseline comparison, same generation as the reference sample)
@@ -253,6 +279,8 @@ def run_ours(a):
             gen1 = {"moves": it, "improve_ms": ims, "moves_per_s": it / (ims / 1e3)}
 
     launches0 = pop.counters().kernel_launches
+    for k in phase:
+        phase[k] = 0.0
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -272,6 +300,7 @@ def run_ours(a):
     clk = clocks.stop()
     launches = pop.counters().kernel_launches - launches0
 
+    timed_phase = dict(phase)
     # e2e through the public API with host buffers: H2D offspring, generation, D2H next offspring + stats
     host_off = pop.offspring
     e2e_moves = 0
@@ -324,6 +353,8 @@ def run_ours(a):
                          "bytes_def": "SURVEY 8(d) B_t summed over every step of the launch",
                          "kernel_share_of_step": imp_ms / ms},
             "improve_moves_per_s": moves / (imp_ms / 1e3),
+            "phase_ms_per_step": {k: v / a.steps for k, v in timed_phase.items() if k != "k3_ops"},
+            "k3_roofline": k3_roofline(timed_phase, pop.counters().k3_tensor_cores),
             "best_f_seen": best,
             "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": a.e2e_steps},

@@ -113,6 +113,11 @@ typedef struct {
     int32_t grid, threads, warps_per_sm, slots;
     int64_t smem_bytes;
     int64_t kernel_launches;    /* this context's kernel launches so far */
+    double distances_ms;        /* last plse_distances (K3: one-hot expansion + tcgen05 GEMM) */
+    double update_ms;           /* last plse_update */
+    double offspring_ms;        /* last plse_offspring */
+    double k3_ops;              /* 2 * M * N * Kpad summed over the last plse_distances GEMMs */
+    int32_t k3_tensor_cores;    /* 1 if K3 ran on tcgen05 */
 } plse_counters;
 
 /* RunResult (engine.hpp:59-71) */

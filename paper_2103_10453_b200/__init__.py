@@ -83,7 +83,9 @@ class Step(C.Structure):
 class Counters(C.Structure):
     _fields_ = [("improve_ms", C.c_double), ("alg_bytes", C.c_double), ("moves", C.c_int64),
                 ("grid", C.c_int32), ("threads", C.c_int32), ("warps_per_sm", C.c_int32), ("slots", C.c_int32),
-                ("smem_bytes", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("smem_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("distances_ms", C.c_double),
+                ("update_ms", C.c_double), ("offspring_ms", C.c_double), ("k3_ops", C.c_double),
+                ("k3_tensor_cores", C.c_int32)]
 
 
 class _RunResult(C.Structure):

@@ -209,6 +209,19 @@ void eval_into(plse_ctx* c, const uint8_t* colors, std::vector<int32_t>& f, std:
 }
 
 // K3: D = hamming(A rows, B rows) -- tcgen05 one-hot GEMM, or the CUDA-core kernel (PLSE_TC=0)
+struct PhaseTimer {
+    plse_ctx* c;
+    double* out;
+    PhaseTimer(plse_ctx* c_, double* o) : c(c_), out(o) { CK(cudaEventRecord(c->ev0, c->st)); }
+    void stop() {
+        CK(cudaEventRecord(c->ev1, c->st));
+        CK(cudaEventSynchronize(c->ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        *out = ms;
+    }
+};
+
 void hamming(plse_ctx* c, const uint8_t* A, const uint8_t* B, uint16_t* D) {
     const int p = c->prm.p;
     if (!c->use_tc) {
@@ -222,6 +235,7 @@ void hamming(plse_ctx* c, const uint8_t* A, const uint8_t* B, uint16_t* D) {
         hb = c->d_hB;
     }
     c->launched(launch_similarity_tc(c->d_hA, p, hb, p, c->kpad, c->nv, D, p, c->st));
+    c->ctr.k3_ops += 2.0 * p * (double)p * c->kpad;
 }
 
 void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_ctx** out) {
@@ -855,9 +869,12 @@ int plse_distances(plse_ctx* c) {
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
+        c->ctr.k3_ops = 0;
+        c->ctr.k3_tensor_cores = c->use_tc ? 1 : 0;
+        PhaseTimer t(c, &c->ctr.distances_ms);
         hamming(c, c->d_members, c->d_improved, c->d_cross);
         hamming(c, c->d_improved, c->d_improved, c->d_fresh);
-        CK(cudaStreamSynchronize(c->st));
+        t.stop();
     });
 }
 
@@ -865,7 +882,9 @@ int plse_update(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
+        PhaseTimer t(c, &c->ctr.update_ms);
         update_impl(c, pool_best_f, n_shortfall, shortfall_slots);
+        t.stop();
     });
 }
 
@@ -882,7 +901,9 @@ int plse_offspring(plse_ctx* c, uint64_t generation) {
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
+        PhaseTimer t(c, &c->ctr.offspring_ms);
         offspring_impl(c, generation);
+        t.stop();
     });
 }
 
