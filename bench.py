@@ -54,6 +54,7 @@ def args_():
     ap.add_argument("--n", type=int, default=60)
     ap.add_argument("--r", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--lsc", action="store_true", help="LSC instance builders::lsc_instance(n, r, seed) (config C5)")
     ap.add_argument("--master-seed", type=int, default=1)
     ap.add_argument("--budget", type=int, default=0, help="PartialCol iterations per individual (0 = 100|V|)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -145,6 +146,13 @@ def ncu_traffic(config_key: str):
     return None
 
 
+def lsc_grid(a):
+    """C5: the order-n LSC stand-in builders::lsc_instance (tests/support/builders.hpp:46-58), restated with
+    the library's xoshiro (same stream as the reference builder)."""
+    from paper_2103_10453_b200 import lsc_instance
+    return lsc_instance(a.n, a.r, a.seed)
+
+
 def k3_roofline(ph, tensor_cores):
     """similarity GEMM (one-hot i8 tcgen05): algorithmic ops 2*M*N*Kpad per GEMM over the phase time."""
     if ph["distances"] <= 0 or ph["k3_ops"] <= 0:
@@ -226,7 +234,7 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2103_10453_b200 as P
 
-    grid = P.generate_instance(a.n, a.r, a.seed)
+    grid = lsc_grid(a) if a.lsc else P.generate_instance(a.n, a.r, a.seed)
     graph = P.preprocess(grid)
     nv = graph.vertex_count
     budget = a.budget if a.budget > 0 else 100 * nv
@@ -398,7 +406,14 @@ def ttb(a, P, grid):
     res = P.run(grid, P.SolverConfig(p=a.pop, master_seed=a.master_seed, target_score=float(target or 0),
                                      time_limit=300.0))
     out["ours"] = {"pop": a.pop, "best_score": res.best_score, "seconds_to_best": res.time_to_best_seconds,
-                   "generations": res.generations, "stop": res.stop_reason, "moves": res.total_iterations}
+                   "generations": res.generations, "stop": res.stop_reason, "moves": res.total_iterations,
+                   "mode": "parity (every individual runs its full budget)"}
+    if target is not None:
+        rr = P.run(grid, P.SolverConfig(p=a.pop, master_seed=a.master_seed, target_score=float(target),
+                                        race=True, time_limit=300.0))
+        out["ours_race"] = {"pop": a.pop, "best_score": rr.best_score, "seconds_to_best": rr.time_to_best_seconds,
+                            "generations": rr.generations, "stop": rr.stop_reason, "moves": rr.total_iterations,
+                            "mode": "race (device-global early exit at the target)"}
     if target is not None:
         out["target_score"] = target
         out["ours_reached_target"] = res.best_score >= target

@@ -138,6 +138,8 @@ typedef struct {
     int32_t device;
     int32_t disable_optimal_stop; /* harness flag */
     double target_score;        /* >0: stop as soon as best_score >= target (time-to-target) */
+    int32_t race;               /* with target_score: end the improve phase as soon as ANY individual
+                                   reaches the target (device-global early exit; not parity mode) */
 } plse_solver_config;
 
 /* per-generation callback (GenerationCallback, engine.hpp:108) */

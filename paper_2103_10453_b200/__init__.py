@@ -40,7 +40,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PLSE_LIB") or os.path.join(HERE, "libplse_b200.so")  # PLSE_LIB: A/B experiments
 
 __all__ = [
-    "generate_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
+    "generate_instance", "lsc_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
     "SolverConfig", "RunResult", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
     "lib_path", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
 ]
@@ -98,7 +98,7 @@ class _RunResult(C.Structure):
 class _SolverConfig(C.Structure):
     _fields_ = [("params", _Params), ("variant", C.c_int32), ("time_limit", C.c_double),
                 ("iteration_limit", C.c_int64), ("generation_limit", C.c_int64), ("device", C.c_int32),
-                ("disable_optimal_stop", C.c_int32), ("target_score", C.c_double)]
+                ("disable_optimal_stop", C.c_int32), ("target_score", C.c_double), ("race", C.c_int32)]
 
 
 _GEN_CB = C.CFUNCTYPE(None, C.c_int64, C.c_int32, C.c_int64, C.c_double, C.c_int32, C.c_void_p)
@@ -185,6 +185,65 @@ def generate_instance(n: int, r: float, seed: int) -> np.ndarray:
     return g.reshape(n, n)
 
 
+class _Xoshiro:
+    """xoshiro256++ seeded by splitmix64 (rng.hpp:21-58) -- host-side, for instance builders only."""
+    M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        sm = seed & self.M
+        self.s = []
+        for _ in range(4):
+            sm = (sm + 0x9E3779B97F4A7C15) & self.M
+            z = sm
+            z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & self.M
+            z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & self.M
+            self.s.append(z ^ (z >> 31))
+
+    def next(self) -> int:
+        s, M = self.s, self.M
+        rotl = lambda x, k: ((x << k) | (x >> (64 - k))) & M
+        result = (rotl((s[0] + s[3]) & M, 23) + s[0]) & M
+        t = (s[1] << 17) & M
+        s[2] ^= s[0]
+        s[3] ^= s[1]
+        s[1] ^= s[2]
+        s[0] ^= s[3]
+        s[2] ^= t
+        s[3] = rotl(s[3], 45)
+        return result
+
+    def below(self, bound: int) -> int:
+        threshold = ((1 << 64) - bound) % bound
+        while True:
+            x = self.next()
+            if x >= threshold:
+                return x % bound
+
+
+def lsc_instance(n: int, r: float, seed: int) -> np.ndarray:
+    """Latin-square-completion instance (config C5's stand-in for qwhdec.order70): a permuted cyclic
+    square with cells deleted, so a full completion exists -- builders::lsc_instance
+    (tests/support/builders.hpp:30-58)."""
+    rng = _Xoshiro(seed)
+
+    def perm(m):
+        a = list(range(m))
+        for i in range(m - 1, 0, -1):
+            j = rng.below(i + 1)
+            a[i], a[j] = a[j], a[i]
+        return a
+
+    rows, cols, syms = perm(n), perm(n), perm(n)
+    grid = np.array([[syms[(rows[a] + cols[b]) % n] + 1 for b in range(n)] for a in range(n)], np.uint16)
+    rng = _Xoshiro(seed ^ 0x5DEECE66D)
+    keep = int(r * n * n)
+    cells = perm(n * n)
+    flat = grid.reshape(-1)
+    for c in cells[keep:]:
+        flat[c] = 0
+    return grid
+
+
 def parse_instance(text: str) -> np.ndarray:
     """instance.hpp:107 -- 'n' then n rows of n symbols (0 = empty)."""
     n = C.c_int32()
@@ -262,6 +321,7 @@ class SolverConfig:
     offset: int = 0
     disable_optimal_stop: bool = False
     target_score: float = 0.0
+    race: bool = False  # with target_score: device-global early exit (time-to-target, not parity mode)
 
     def _params(self) -> _Params:
         return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,
@@ -292,7 +352,7 @@ def run(grid: np.ndarray, config: SolverConfig,
     n = grid.shape[0]
     cfg = _SolverConfig(config._params(), config.variant, config.time_limit, config.iteration_limit,
                         config.generation_limit, config.device, int(config.disable_optimal_stop),
-                        config.target_score)
+                        config.target_score, int(config.race))
     res = _RunResult()
     best = np.zeros(n * n + 1, np.uint16)
     errors: List[BaseException] = []

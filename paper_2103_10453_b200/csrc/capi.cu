@@ -86,9 +86,13 @@ struct plse_ctx {
     uint32_t tenure_cap = 0;
     size_t rec_stride = 0, until_stride = 0;
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
+    bool half_warp = false;  // k_improve (one individual per warp) vs k_improve_hw (PLSE_IMPROVE_KERNEL=hw)
+    int lane_words16 = 1;
     size_t smem = 0;
     int* d_work = nullptr;
     unsigned long long* d_prof = nullptr;  // PLSE_PROFILE instrumentation counters
+    int* d_race = nullptr;                 // race-mode flag (plse_solve with race)
+    int race_f = -1;
     // pool update scratch
     int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
     uint32_t* d_conf = nullptr;
@@ -104,7 +108,7 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_colvert, d_hA, d_hB, d_order,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_race, d_colvert, d_hA, d_hB, d_order,
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -398,35 +402,47 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_admitted = dalloc<uint8_t>(2 * p);
     c->d_work = dalloc<int>(1);
 
-    // ---- improve launch shape: maximise resident warps per SM (one individual per warp)
-    const void* kern = improve_kernel_ptr(W, false);
-    const void* kern_dbg = improve_kernel_ptr(W, true);
-    const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
-    int best_warps = 0;
+    // ---- improve launch shape: maximise resident individuals per SM
+    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL")) c->half_warp = std::string(env) == "hw";
+    c->lane_words16 = (nwords + 15) / 16;
+    const void* kern = c->half_warp ? improve_hw_kernel_ptr(W, false) : improve_kernel_ptr(W, false);
+    const void* kern_dbg = c->half_warp ? improve_hw_kernel_ptr(W, true) : improve_kernel_ptr(W, true);
+    size_t graph_bytes = 0, warp_bytes = 0;
+    if (c->half_warp) {
+        const HwSmemLayout L = improve_hw_smem_layout(n, nv, c->nvpad, c->lane_words16, W);
+        graph_bytes = L.graph_bytes;
+        warp_bytes = L.warp_bytes;
+    } else {
+        const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+        graph_bytes = L.graph_bytes;
+        warp_bytes = L.warp_bytes;
+    }
+    const int per_warp = c->half_warp ? 2 : 1;
+    int best_ind = 0;
     int force_wpc = 0;
     if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (int wpc : {8, 4, 2, 1}) {
         if (force_wpc && wpc != force_wpc) continue;
-        const size_t smem = L.graph_bytes + (size_t)wpc * L.warp_bytes;
+        const size_t smem = graph_bytes + (size_t)wpc * warp_bytes;
         if (smem > (size_t)max_optin) continue;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bps = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * wpc, smem));
-        if (bps * wpc > best_warps) {
-            best_warps = bps * wpc;
+        if (bps * wpc * per_warp > best_ind) {
+            best_ind = bps * wpc * per_warp;
             c->wpc = wpc;
             c->smem = smem;
             c->grid = bps * c->nsm;
         }
     }
-    if (best_warps == 0) throw Unsupported("instance too large for the shared-memory resident search");
+    if (best_ind == 0) throw Unsupported("instance too large for the shared-memory resident search");
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     CK(cudaFuncSetAttribute(kern_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     c->threads = 32 * c->wpc;
-    c->warps_per_sm = best_warps;
-    c->slots = c->grid * c->wpc;
+    c->warps_per_sm = best_ind / per_warp;
+    c->slots = c->grid * c->wpc * per_warp;
     c->rec_stride = up((size_t)nv * tabu_rec_bytes(W), 256);
     c->until_stride = up((size_t)nv * (n + 1), 64);
     c->d_rec = dalloc<uint8_t>((size_t)c->slots * c->rec_stride);
@@ -481,6 +497,7 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.nv = c->nv;
     a.nvpad = c->nvpad;
     a.lane_words = c->lane_words;
+    a.lane_words16 = c->lane_words16;
     a.cell = c->d_cell;
     a.row_start = c->d_rs;
     a.col_start = c->d_cs;
@@ -512,6 +529,8 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.trace_cap = trace_cap;
     a.trace = d_trace;
     a.prof = nullptr;
+    a.race_flag = c->race_f >= 0 ? c->d_race : nullptr;
+    a.race_f = c->race_f;
     if (const char* env = std::getenv("PLSE_PROFILE")) {
         if (env[0] == '1') {
             if (!c->d_prof) c->d_prof = dalloc<unsigned long long>(16);
@@ -521,7 +540,10 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     }
     CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->ev0, c->st));
-    c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
+    if (c->half_warp)
+        c->launched(launch_improve_hw(a, c->W, c->grid, c->threads, c->smem, c->st));
+    else
+        c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
     CK(cudaEventRecord(c->ev1, c->st));
 }
 
@@ -553,10 +575,11 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));
         std::fprintf(stderr,
                      "[plse-prof] indiv %llu prologue %.0f cyc/indiv | dense %llu steps %.0f cyc/step mean f %.1f | "
-                     "sparse %llu steps %.0f cyc/step | enter %llu | total %.3g cyc/indiv\n",
+                     "sparse %llu steps %.0f cyc/step | enter %llu | total %.3g cyc/indiv | f<=8 %llu f<=16 %llu "
+                     "f<=24 %llu f<=32 %llu\n",
                      pr[0], (double)pr[1] / pr[0], pr[2], pr[2] ? (double)pr[3] / pr[2] : 0.0,
                      pr[2] ? (double)pr[6] / pr[2] : 0.0, pr[4], pr[4] ? (double)pr[5] / pr[4] : 0.0, pr[7],
-                     (double)pr[8] / pr[0]);
+                     (double)pr[8] / pr[0], pr[9], pr[10], pr[11], pr[12]);
     }
     c->ctr.improve_ms = ms;
     c->ctr.alg_bytes = by;
@@ -1038,6 +1061,11 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
         }
         CK(cudaMemcpy(c->d_offspring, c->d_members, (size_t)p * c->nvpad, cudaMemcpyDeviceToDevice));
         CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
+        if (cfg->race && cfg->target_score > 0) {
+            c->d_race = dalloc<int>(1);
+            CK(cudaMemset(c->d_race, 0, sizeof(int)));
+            c->race_f = std::max(0, (int)std::floor((double)(n * n - g.l) - cfg->target_score));
+        }
         for (int64_t gen = 1;; ++gen) {
             int64_t it = 0;
             int32_t bf = 0, bi = -1;

@@ -14,7 +14,7 @@ constexpr int kImproveMinBlocks = 4;  // 32 resident warps per SM -> <= 64 regis
 
 struct ImproveArgs {
     // graph (global copies; the kernel stages them in shared memory)
-    int n, nv, nvpad, lane_words;
+    int n, nv, nvpad, lane_words, lane_words16;
     const uint16_t* cell;       // [nv] row << 8 | col
     const uint16_t* row_start;  // [n+1] survivors of row r are ids [row_start[r], row_start[r+1])
     const uint16_t* col_start;  // [n+1]
@@ -42,6 +42,9 @@ struct ImproveArgs {
     int64_t budget;
     int stop_f;
     double alpha;
+    // race mode (time-to-target): stop every search once any individual reaches best f <= race_f
+    int* race_flag;             // nullptr = off
+    int race_f;
     // optional clock64 instrumentation (PLSE_PROFILE=1): 16 counters, see capi.cu
     unsigned long long* prof;
     // parity probe
@@ -93,6 +96,60 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     L.warp_bytes = align_up(w, 16);
     return L;
 }
+
+// two individuals per warp (improve_hw.cu): graph part + per-warp block of two half blocks
+constexpr int kHwMaxThreads = 256;
+constexpr int kHwMinBlocks = 2;  // 16 warps (32 individuals) per SM -> <= 128 registers
+
+struct HwSmemLayout {
+    size_t cell, rs, cs, cl, colpos, deg, pr, pc, graph_bytes;
+    size_t warp0, warp_bytes, half_bytes, h_col, h_colT, h_R, h_C, h_U, h_list;
+};
+
+__host__ __device__ inline HwSmemLayout improve_hw_smem_layout(int n, int nv, int nvpad, int lane_words16, int W) {
+    HwSmemLayout L;
+    size_t o = 0;
+    L.cell = o;
+    o += (size_t)nv * 2;
+    L.rs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cl = o;
+    o += (size_t)nv * 2;
+    L.colpos = o;
+    o += (size_t)nv * 2;
+    L.deg = o;
+    o += (size_t)nv;
+    o = align_up(o, 16);
+    L.pr = o;
+    o += (size_t)n * W * 8;
+    L.pc = o;
+    o += (size_t)n * W * 8;
+    o = align_up(o, 16);
+    L.graph_bytes = o;
+    L.warp0 = o;
+    size_t h = 0;
+    L.h_col = h;
+    h += (size_t)nvpad;
+    L.h_colT = h;  // the repair's conflict counters live here until the column-major copy is built
+    h += (size_t)nvpad;
+    h = align_up(h, 16);
+    L.h_R = h;
+    h += (size_t)n * W * 8;
+    L.h_C = h;
+    h += (size_t)n * W * 8;
+    L.h_U = h;
+    h += (size_t)16 * lane_words16 * 4;
+    L.h_list = h;
+    h += 64;
+    L.half_bytes = align_up(h, 16);
+    L.warp_bytes = 2 * L.half_bytes;
+    return L;
+}
+
+const void* improve_hw_kernel_ptr(int W, bool debug);
+cudaError_t launch_improve_hw(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 
 size_t tabu_rec_bytes(int W);
 const void* improve_kernel_ptr(int W, bool debug);

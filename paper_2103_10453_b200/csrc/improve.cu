@@ -31,175 +31,10 @@
 //     r = floor(h1 * N / 2^32) from a counter hash of (stream seed, step); the
 //     lane holding the r-th candidate in ascending (v, k) order recovers it
 //     with a popcount search.
-#include "common.cuh"
-#include "device_api.h"
+#include "improve_common.cuh"
 
 namespace plse_dev {
 
-// per-vertex tabu cache: (k1, u1), (k2, u2) exact until values of the two
-// most recently forbidden colours; kk = k1 | k2 << 8 | ovf << 16.  ovf: a
-// third colour was forbidden while both pairs were live -> consult until[][].
-struct alignas(16) TabuRec {
-    uint32_t u1, u2, kk, pad;
-};
-
-struct WarpSmem {
-    uint8_t* col;
-    uint8_t* conf;
-    uint64_t* R;
-    uint64_t* C;
-    uint32_t* U;
-};
-
-template <int W>
-struct Graph {
-    int n, nv, nvpad, lane_words;
-    const uint16_t* cell;
-    const uint8_t* deg;  // |N(v)| = row-mates + column-mates (for the 8(d) byte counter)
-    const uint16_t* rs;
-    const uint16_t* cs;
-    const uint16_t* cl;
-    const uint64_t* pr;
-    const uint64_t* pc;
-    uint64_t full[W];
-};
-
-template <int W>
-__device__ __forceinline__ void dom_mask(const Graph<W>& g, int r, int c, uint64_t (&d)[W]) {
-#pragma unroll
-    for (int q = 0; q < W; ++q) d[q] = ~(g.pr[r * W + q] | g.pc[c * W + q]) & g.full[q];
-}
-
-// exact tabu mask at clock t from a (u1, u2, kk) cache; the overflow case reads
-// the dense table for every colour of D(v) and rebuilds the cache when <= 2 remain
-template <int W>
-__device__ __forceinline__ void tabu_of(uint32_t& u1, uint32_t& u2, uint32_t& kk, const uint32_t* until_row,
-                                        const uint64_t (&dom)[W], uint32_t t, uint64_t (&T)[W]) {
-#pragma unroll
-    for (int q = 0; q < W; ++q) T[q] = 0;
-    if (!(kk >> 16)) {
-        const int k1 = kk & 0xFF, k2 = (kk >> 8) & 0xFF;
-        if (u1 > t) T[k1 >> 6] |= 1ULL << (k1 & 63);
-        if (u2 > t) T[k2 >> 6] |= 1ULL << (k2 & 63);
-        return;
-    }
-    int n_live = 0, ka = 0, kb = 0;
-    uint32_t ua = 0, ub = 0;
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-        uint64_t m = dom[q];
-        while (m) {
-            const int b = __ffsll((long long)m) - 1;
-            m &= m - 1;
-            const int k = q * 64 + b;
-            const uint32_t u = until_row[k];
-            if (u > t) {
-                T[q] |= 1ULL << b;
-                if (n_live == 0) {
-                    ka = k;
-                    ua = u;
-                } else if (n_live == 1) {
-                    kb = k;
-                    ub = u;
-                }
-                ++n_live;
-            }
-        }
-    }
-    if (n_live <= 2) {
-        u1 = ua;
-        u2 = ub;
-        kk = (uint32_t)ka | ((uint32_t)kb << 8);
-    }
-}
-
-// forbid (k, until = ut) in a vertex's cache (search_util.hpp:73-75 overwrite semantics)
-__device__ __forceinline__ void cache_forbid(TabuRec& r, int k, uint32_t ut, uint32_t t) {
-    const int k1 = r.kk & 0xFF, k2 = (r.kk >> 8) & 0xFF;
-    uint32_t ovf = r.kk & 0xFF0000u;
-    int n1 = k1, n2 = k2;
-    if (k1 == k && r.u1) {
-        r.u1 = ut;
-    } else if (k2 == k && r.u2) {
-        r.u2 = ut;
-    } else if (r.u1 <= t) {
-        n1 = k;
-        r.u1 = ut;
-    } else if (r.u2 <= t) {
-        n2 = k;
-        r.u2 = ut;
-    } else {
-        ovf = 1u << 16;  // both cached colours still tabu: the dense table is now authoritative
-        if (r.u1 <= r.u2) {
-            n1 = k;
-            r.u1 = ut;
-        } else {
-            n2 = k;
-            r.u2 = ut;
-        }
-    }
-    r.kk = (uint32_t)n1 | ((uint32_t)n2 << 8) | ovf;
-}
-
-// admissible candidate masks of an uncoloured vertex at the three delta levels
-template <int W>
-__device__ __forceinline__ void level_masks(const WarpSmem& s, int r, int c, const uint64_t (&dom)[W],
-                                            const uint64_t (&T)[W], bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
-                                            uint64_t (&m2)[W]) {
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-        const uint64_t Rr = s.R[r * W + q], Cc = s.C[c * W + q];
-        const uint64_t fr = dom[q] & ~Rr & ~Cc;
-        m0[q] = asp ? fr : (fr & ~T[q]);
-        m1[q] = dom[q] & (Rr ^ Cc) & ~T[q];
-        m2[q] = dom[q] & Rr & Cc & ~T[q];
-    }
-}
-
-// dense mode: masks of vertex v with its tabu cache read from (and written back to) HBM
-template <int W>
-__device__ __forceinline__ void dense_masks(const Graph<W>& g, const WarpSmem& s, TabuRec* rec, const uint32_t* until,
-                                            int v, uint32_t t, bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
-                                            uint64_t (&m2)[W]) {
-    const uint16_t rc = g.cell[v];
-    const int r = rc >> 8, c = rc & 0xFF;
-    uint64_t dom[W], T[W];
-    dom_mask<W>(g, r, c, dom);
-    TabuRec tr = rec[v];
-    const uint32_t kk0 = tr.kk;
-    tabu_of<W>(tr.u1, tr.u2, tr.kk, until + (size_t)v * (g.n + 1), dom, t, T);
-    if (tr.kk != kk0) rec[v] = tr;
-    level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
-}
-
-template <int W>
-__device__ __forceinline__ int popc_w(const uint64_t (&m)[W]) {
-    int c = 0;
-#pragma unroll
-    for (int q = 0; q < W; ++q) c += __popcll(m[q]);
-    return c;
-}
-
-// 0-based rr-th set bit of a W-word mask (rr < popc)
-template <int W>
-__device__ __forceinline__ int nth_bit_w(const uint64_t (&m)[W], int rr) {
-    int k = 0;
-#pragma unroll
-    for (int z = 0; z < W; ++z) {
-        const int pz = __popcll(m[z]);
-        if (rr >= 0 && rr < pz) k = z * 64 + nth_bit64(m[z], rr);
-        rr -= pz;
-    }
-    return k;
-}
-
-__device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int nvpad, int lane) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(col);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (int t = lane; t < nvpad / 16; t += 32) d4[t] = s4[t];
-}
-
-// kDebug: per-step trace (plse_trace) and clock64 instrumentation (PLSE_PROFILE)
 template <int W, bool kDebug>
 __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
                             uint32_t* until, uint32_t* slot_clock, int i, int lane) {
@@ -212,6 +47,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     long long t_start = prof ? clock64() : 0, t_step = 0;
     unsigned long long pc_dense = 0, pc_sparse = 0, pn_dense = 0, pn_sparse = 0, pf_dense = 0, pn_enter = 0;
+    unsigned long long fh[4] = {0, 0, 0, 0};  // sparse-step |V0| histogram: <=8, <=16, <=24, <=32
 
     // ---- tabu clock of this warp slot: every until[][] left by earlier individuals is <= base
     uint32_t base = *slot_clock;
@@ -321,6 +157,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
 
     while ((int64_t)j < a.budget && bestf > a.stop_f && f > 0) {
+        if (a.race_flag && (j & 63) == 0 && *reinterpret_cast<volatile int*>(a.race_flag)) break;
         if (prof) t_step = clock64();
         const bool step_sparse = f <= 32;
         const bool asp = (f == bestf);
@@ -587,6 +424,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         if (improved) {
             bestf = f;
             pending = true;
+            if (a.race_flag && bestf <= a.race_f && lane == 0) atomicExch(a.race_flag, 1);
         }
         if (tracing && lane == 0 && (int64_t)j < a.trace_cap) {
             plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + j;
@@ -614,6 +452,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             if (step_sparse) {
                 pc_sparse += dt;
                 ++pn_sparse;
+                fh[(f_before - 1) >> 3] += 1;
             } else {
                 pc_dense += dt;
                 ++pn_dense;
@@ -645,6 +484,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         atomicAdd(prof + 6, pf_dense);
         atomicAdd(prof + 7, pn_enter);
         atomicAdd(prof + 8, (unsigned long long)(clock64() - t_start));
+        for (int q = 0; q < 4; ++q) atomicAdd(prof + 9 + q, fh[q]);
     }
     __syncwarp();
 }

@@ -1,0 +1,175 @@
+// improve_common.cuh -- device helpers shared by the improve kernels
+// (improve.cu: one individual per warp; improve_hw.cu: one per half-warp).
+#pragma once
+#include "common.cuh"
+#include "device_api.h"
+
+namespace plse_dev {
+
+// per-vertex tabu cache: (k1, u1), (k2, u2) exact until values of the two
+// most recently forbidden colours; kk = k1 | k2 << 8 | ovf << 16.  ovf: a
+// third colour was forbidden while both pairs were live -> consult until[][].
+struct alignas(16) TabuRec {
+    uint32_t u1, u2, kk, pad;
+};
+
+struct WarpSmem {
+    uint8_t* col;
+    uint8_t* conf;
+    uint64_t* R;
+    uint64_t* C;
+    uint32_t* U;
+};
+
+template <int W>
+struct Graph {
+    int n, nv, nvpad, lane_words;
+    const uint16_t* cell;
+    const uint8_t* deg;  // |N(v)| = row-mates + column-mates (for the 8(d) byte counter)
+    const uint16_t* rs;
+    const uint16_t* cs;
+    const uint16_t* cl;
+    const uint16_t* colpos;  // position of v in the column-major list cl (improve_hw only)
+    const uint64_t* pr;
+    const uint64_t* pc;
+    uint64_t full[W];
+};
+
+template <int W>
+__device__ __forceinline__ void dom_mask(const Graph<W>& g, int r, int c, uint64_t (&d)[W]) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) d[q] = ~(g.pr[r * W + q] | g.pc[c * W + q]) & g.full[q];
+}
+
+// exact tabu mask at clock t from a (u1, u2, kk) cache; the overflow case reads
+// the dense table for every colour of D(v) and rebuilds the cache when <= 2 remain
+template <int W>
+__device__ __forceinline__ void tabu_of(uint32_t& u1, uint32_t& u2, uint32_t& kk, const uint32_t* until_row,
+                                        const uint64_t (&dom)[W], uint32_t t, uint64_t (&T)[W]) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) T[q] = 0;
+    if (!(kk >> 16)) {
+        const int k1 = kk & 0xFF, k2 = (kk >> 8) & 0xFF;
+        if (u1 > t) T[k1 >> 6] |= 1ULL << (k1 & 63);
+        if (u2 > t) T[k2 >> 6] |= 1ULL << (k2 & 63);
+        return;
+    }
+    int n_live = 0, ka = 0, kb = 0;
+    uint32_t ua = 0, ub = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t m = dom[q];
+        while (m) {
+            const int b = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int k = q * 64 + b;
+            const uint32_t u = until_row[k];
+            if (u > t) {
+                T[q] |= 1ULL << b;
+                if (n_live == 0) {
+                    ka = k;
+                    ua = u;
+                } else if (n_live == 1) {
+                    kb = k;
+                    ub = u;
+                }
+                ++n_live;
+            }
+        }
+    }
+    if (n_live <= 2) {
+        u1 = ua;
+        u2 = ub;
+        kk = (uint32_t)ka | ((uint32_t)kb << 8);
+    }
+}
+
+// forbid (k, until = ut) in a vertex's cache (search_util.hpp:73-75 overwrite semantics)
+__device__ __forceinline__ void cache_forbid(TabuRec& r, int k, uint32_t ut, uint32_t t) {
+    const int k1 = r.kk & 0xFF, k2 = (r.kk >> 8) & 0xFF;
+    uint32_t ovf = r.kk & 0xFF0000u;
+    int n1 = k1, n2 = k2;
+    if (k1 == k && r.u1) {
+        r.u1 = ut;
+    } else if (k2 == k && r.u2) {
+        r.u2 = ut;
+    } else if (r.u1 <= t) {
+        n1 = k;
+        r.u1 = ut;
+    } else if (r.u2 <= t) {
+        n2 = k;
+        r.u2 = ut;
+    } else {
+        ovf = 1u << 16;  // both cached colours still tabu: the dense table is now authoritative
+        if (r.u1 <= r.u2) {
+            n1 = k;
+            r.u1 = ut;
+        } else {
+            n2 = k;
+            r.u2 = ut;
+        }
+    }
+    r.kk = (uint32_t)n1 | ((uint32_t)n2 << 8) | ovf;
+}
+
+// admissible candidate masks of an uncoloured vertex at the three delta levels
+template <int W>
+__device__ __forceinline__ void level_masks(const WarpSmem& s, int r, int c, const uint64_t (&dom)[W],
+                                            const uint64_t (&T)[W], bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
+                                            uint64_t (&m2)[W]) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const uint64_t Rr = s.R[r * W + q], Cc = s.C[c * W + q];
+        const uint64_t fr = dom[q] & ~Rr & ~Cc;
+        m0[q] = asp ? fr : (fr & ~T[q]);
+        m1[q] = dom[q] & (Rr ^ Cc) & ~T[q];
+        m2[q] = dom[q] & Rr & Cc & ~T[q];
+    }
+}
+
+// dense mode: masks of vertex v with its tabu cache read from (and written back to) HBM
+template <int W>
+__device__ __forceinline__ void dense_masks(const Graph<W>& g, const WarpSmem& s, TabuRec* rec, const uint32_t* until,
+                                            int v, uint32_t t, bool asp, uint64_t (&m0)[W], uint64_t (&m1)[W],
+                                            uint64_t (&m2)[W]) {
+    const uint16_t rc = g.cell[v];
+    const int r = rc >> 8, c = rc & 0xFF;
+    uint64_t dom[W], T[W];
+    dom_mask<W>(g, r, c, dom);
+    TabuRec tr = rec[v];
+    const uint32_t kk0 = tr.kk;
+    tabu_of<W>(tr.u1, tr.u2, tr.kk, until + (size_t)v * (g.n + 1), dom, t, T);
+    if (tr.kk != kk0) rec[v] = tr;
+    level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
+}
+
+template <int W>
+__device__ __forceinline__ int popc_w(const uint64_t (&m)[W]) {
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) c += __popcll(m[q]);
+    return c;
+}
+
+// 0-based rr-th set bit of a W-word mask (rr < popc)
+template <int W>
+__device__ __forceinline__ int nth_bit_w(const uint64_t (&m)[W], int rr) {
+    int k = 0;
+#pragma unroll
+    for (int z = 0; z < W; ++z) {
+        const int pz = __popcll(m[z]);
+        if (rr >= 0 && rr < pz) k = z * 64 + nth_bit64(m[z], rr);
+        rr -= pz;
+    }
+    return k;
+}
+
+__device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int nvpad, int lane) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(col);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int t = lane; t < nvpad / 16; t += 32) d4[t] = s4[t];
+}
+
+// kDebug: per-step trace (plse_trace) and clock64 instrumentation (PLSE_PROFILE)
+
+}  // namespace plse_dev

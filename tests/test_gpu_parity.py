@@ -214,3 +214,13 @@ def test_tensor_core_distances_match_cuda_core(plse, orc, p, monkeypatch):
     sample = rng.integers(0, p, size=(64, 2))
     for i, j in sample:
         assert da[i, j] == int((mem[i] != mem[j]).sum())
+
+
+def test_race_mode_reaches_target_and_stops_early(plse, orc):
+    grid = orc.generate_instance(30, 0.5, 12345)
+    full = plse.run(grid, plse.SolverConfig(p=256, master_seed=3, generation_limit=3))
+    race = plse.run(grid, plse.SolverConfig(p=256, master_seed=3, generation_limit=3,
+                                           target_score=float(full.best_score), race=True))
+    assert race.best_score >= full.best_score
+    assert race.total_iterations <= full.total_iterations
+    assert race.stop_reason in ("optimal", "target")

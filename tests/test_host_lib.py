@@ -105,3 +105,9 @@ def test_trivial_instance_runs_without_device(plse):
     full = np.array([[1, 2], [2, 1]], np.uint16)
     r = plse.run(full, plse.SolverConfig(p=4))
     assert r.stop_reason == "optimal" and r.best_score == 4 and r.vertex_count == 0
+
+
+def test_lsc_instance_matches_reference_builder(plse):
+    """config C5's LSC stand-in (builders.hpp:30-58)"""
+    assert np.array_equal(plse.lsc_instance(20, 0.4, 7), G["lsc_20_0.4_7"])
+    assert np.array_equal(plse.lsc_instance(70, 0.4, 7), G["lsc_70_0.4_7"])
