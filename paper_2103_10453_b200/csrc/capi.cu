@@ -83,6 +83,7 @@ struct plse_ctx {
     void* d_rec = nullptr;
     uint32_t* d_until = nullptr;
     uint32_t* d_slot_clock = nullptr;
+    uint8_t* d_conf_scratch = nullptr;
     uint32_t tenure_cap = 0;
     size_t rec_stride = 0, until_stride = 0;
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
@@ -108,7 +109,7 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_work, d_prof, d_race, d_colvert, d_hA, d_hB, d_order,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_conf_scratch, d_work, d_prof, d_race, d_colvert, d_hA, d_hB, d_order,
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -448,6 +449,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_rec = dalloc<uint8_t>((size_t)c->slots * c->rec_stride);
     c->d_until = dalloc<uint32_t>((size_t)c->slots * c->until_stride);
     CK(cudaMemset(c->d_until, 0, sizeof(uint32_t) * (size_t)c->slots * c->until_stride));
+    c->d_conf_scratch = dalloc<uint8_t>((size_t)c->slots * c->nvpad);
     c->d_slot_clock = dalloc<uint32_t>(c->slots);
     CK(cudaMemset(c->d_slot_clock, 0, sizeof(uint32_t) * c->slots));
     c->ctr.grid = c->grid;
@@ -516,6 +518,8 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.until = c->d_until;
     a.until_stride = c->until_stride;
     a.slot_clock = c->d_slot_clock;
+    a.conf_scratch = c->d_conf_scratch;
+    a.conf_stride = (size_t)c->nvpad;
     a.tenure_cap = c->tenure_cap;
     a.work_counter = c->d_work;
     a.master = c->prm.master_seed;

@@ -42,6 +42,9 @@ struct ImproveArgs {
     int64_t budget;
     int stop_f;
     double alpha;
+    // per-slot repair counters (nvpad bytes each; the warp kernel keeps them out of shared memory)
+    uint8_t* conf_scratch;
+    size_t conf_stride;
     // race mode (time-to-target): stop every search once any individual reaches best f <= race_f
     int* race_flag;             // nullptr = off
     int race_f;
@@ -54,8 +57,8 @@ struct ImproveArgs {
 };
 
 struct ImproveSmemLayout {
-    size_t cell, rs, cs, cl, deg, pr, pc, graph_bytes;
-    size_t warp0, warp_bytes, w_col, w_conf, w_R, w_C, w_U;
+    size_t cell, rs, cs, cl, colpos, deg, pr, pc, graph_bytes;
+    size_t warp0, warp_bytes, w_col, w_colT, w_list, w_R, w_C, w_U;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -71,6 +74,8 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     o += (size_t)(n + 1) * 2;
     L.cl = o;
     o += (size_t)nv * 2;
+    L.colpos = o;
+    o += (size_t)nv * 2;
     L.deg = o;
     o += (size_t)nv;
     o = align_up(o, 16);
@@ -84,8 +89,10 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     size_t w = 0;
     L.w_col = w;
     w += (size_t)nvpad;
-    L.w_conf = w;  // repair counters; afterwards the 32-entry u16 list that seeds sparse mode
-    w += nvpad > 64 ? (size_t)nvpad : 64;
+    L.w_colT = w;  // column-major colour copy (ordered like the column lists)
+    w += (size_t)nvpad;
+    L.w_list = w;  // the 32-entry u16 list that seeds sparse mode (repair counters live in HBM scratch)
+    w += 64;
     w = align_up(w, 16);
     L.w_R = w;
     w += (size_t)n * W * 8;

@@ -8,12 +8,13 @@
 //
 // Data layout:
 //   * The individual's colours (u8) live in shared memory for the whole
-//     search, with per-row / per-column colour-occupancy bitmasks R[r], C[c]
-//     (W x u64) and the uncoloured set U as a bitmask.  In a legal colouring
-//     gamma[v][k] = [k in R[row v]] + [k in C[col v]] for every uncoloured v,
-//     so the three move classes of an uncoloured vertex (delta -1 / 0 / +1)
-//     are three W-word mask expressions: the gamma rows the north star puts in
-//     HBM are never materialised.
+//     search -- row-major (col) and column-major (colT, ordered like the
+//     graph's column lists) -- with per-row / per-column colour-occupancy
+//     bitmasks R[r], C[c] (W x u64) and the uncoloured set U as a bitmask.
+//     In a legal colouring gamma[v][k] = [k in R[row v]] + [k in C[col v]]
+//     for every uncoloured v, so the three move classes of an uncoloured
+//     vertex (delta -1 / 0 / +1) are three W-word mask expressions: the gamma
+//     rows the north star puts in HBM are never materialised.
 //   * The domain of v is ~(PR[row] | PC[col]) over the prefilled-symbol masks
 //     (lsgraph.hpp:152-156), shared by the CTA in shared memory.
 //   * Tabu state (search_util.hpp:54-81): the reference's dense until[v][k]
@@ -23,9 +24,14 @@
 //     an overflow flag; only a vertex with three or more live tabu colours
 //     reads the dense table.
 //   * Sparse mode (|V0| <= 32, i.e. everything after the first ~1% of the
-//     descent): lane l holds the l-th uncoloured vertex (ascending id) and its
-//     tabu pairs in registers, so scoring a step costs two shared loads per
-//     lane.  Dense mode scans the U bitmask (lane-owned 32*lane_words blocks).
+//     descent) is a tight, branch-light inner loop: lane l holds the l-th
+//     uncoloured vertex (ascending id, with its row / column packed in) and
+//     its tabu pairs in registers, so scoring costs four shared loads per
+//     lane; the row / column holder of k* is one word-parallel pass over the
+//     row-major / column-major colour copies; the update is a predicated
+//     five-lane XOR (colour bytes, U bits, R / C bits) and the slot list is
+//     re-sorted with one computed-source shuffle per field.  Dense mode
+//     (|V0| > 32) scans the U bitmask (lane-owned 32*lane_words blocks).
 //   * Selection is the canonical order-free rule: the lowest
 //     admissible delta level, per-lane counts, a warp prefix sum, and
 //     r = floor(h1 * N / 2^32) from a counter hash of (stream seed, step); the
@@ -35,19 +41,43 @@
 
 namespace plse_dev {
 
+// position of the unique byte == k in bytes [a, b) of buf, or -1 (warp-uniform result)
+__device__ __forceinline__ int warp_find_byte(const uint8_t* buf, int a, int b, int k, bool enable, int lane) {
+    if (!enable) return -1;
+    const uint32_t k4 = (uint32_t)k * 0x01010101u;
+    for (int base = a & ~3; base < b; base += 128) {
+        const int wpos = base + 4 * lane;
+        uint32_t hit = 0;
+        if (wpos < b) {
+            const uint32_t w = reinterpret_cast<const uint32_t*>(buf)[wpos >> 2] ^ k4;
+            const uint32_t z = ~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;  // 0x80 where byte == k
+            const int lo = a - wpos, hi = b - wpos;  // valid bytes q: lo <= q < hi
+            uint32_t valid = 0x80808080u;
+            if (lo > 0) valid &= 0x80808080u << (8 * min(lo, 4));
+            if (hi < 4) valid &= 0x80808080u >> (8 * (4 - max(hi, 0)));
+            hit = z & valid;
+        }
+        const unsigned bal = __ballot_sync(kFull, hit != 0);
+        if (bal) {
+            const int src = __ffs(bal) - 1;
+            return __shfl_sync(kFull, wpos + ((__ffs(hit) - 1) >> 3), src);
+        }
+    }
+    return -1;
+}
+
 template <int W, bool kDebug>
 __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
-                            uint32_t* until, uint32_t* slot_clock, int i, int lane) {
+                            uint32_t* until, uint32_t* slot_clock, uint8_t* conf, int i, int lane) {
     const int n = g.n, nv = g.nv, w1 = n + 1;
     const int B = 32 * g.lane_words;
     const int v_lo = lane * B;
     const int v_hi = min(nv, v_lo + B);
     uint8_t* col = s.col;
-    uint8_t* conf = s.conf;
+    uint8_t* colT = s.colT;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     long long t_start = prof ? clock64() : 0, t_step = 0;
     unsigned long long pc_dense = 0, pc_sparse = 0, pn_dense = 0, pn_sparse = 0, pf_dense = 0, pn_enter = 0;
-    unsigned long long fh[4] = {0, 0, 0, 0};  // sparse-step |V0| histogram: <=8, <=16, <=24, <=32
 
     // ---- tabu clock of this warp slot: every until[][] left by earlier individuals is <= base
     uint32_t base = *slot_clock;
@@ -113,7 +143,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         __syncwarp();
     }
 
-    // ---- occupancy masks R/C and uncoloured bitmask U of the (now legal) colouring
+    // ---- occupancy masks R/C, uncoloured bitmask U and the column-major copy
     for (int x = lane; x < n * W; x += 32) {
         s.R[x] = 0;
         s.C[x] = 0;
@@ -138,6 +168,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         s.U[lane * g.lane_words + q] = bits;
         fl += __popc(bits);
     }
+    for (int x = lane; x < nv; x += 32) colT[x] = col[g.cl[x]];
     int f = (int)__reduce_add_sync(kFull, (unsigned)fl);
     __syncwarp();
 
@@ -152,92 +183,44 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
     const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
-    bool sparse = false;
-    // sparse-mode slot (valid on lanes < f): vertex | row << 16 | col << 24, tabu cache
-    uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
+    const int64_t budget = a.budget;
+    const int stop_f = a.stop_f;
+    const double alpha = a.alpha;
+    const int* race_flag = a.race_flag;
+    const int race_f = a.race_f;
 
-    while ((int64_t)j < a.budget && bestf > a.stop_f && f > 0) {
-        if (a.race_flag && (j & 63) == 0 && *reinterpret_cast<volatile int*>(a.race_flag)) break;
-        if (prof) t_step = clock64();
-        const bool step_sparse = f <= 32;
+    // step record of the parity probe
+    auto trace_step = [&](uint32_t jj, int vs, int ks, int ur, int uc, int rs_, int cs_, int fb, int fa, int bf,
+                          int ten, int N, int lvl) {
+        plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + jj;
+        const int e = (ur >= 0) + (uc >= 0);
+        // CSR order of N(v*): row-mates first iff row <= col (lsgraph.hpp:202-209)
+        const bool row_first = rs_ <= cs_;
+        tr->step = jj;
+        tr->v = vs;
+        tr->k = ks;
+        tr->e = e;
+        tr->ev0 = vs < 0 ? -1 : row_first ? (ur >= 0 ? ur : uc) : (uc >= 0 ? uc : ur);
+        tr->ev1 = e == 2 ? (row_first ? uc : ur) : -1;
+        tr->f_before = fb;
+        tr->f_after = fa;
+        tr->best_f = bf;
+        tr->tenure = ten;
+        tr->n_adm = N;
+        tr->level = lvl;
+    };
+
+    for (;;) {
+        if (!((int64_t)j < budget && bestf > stop_f && f > 0)) break;
+        if (race_flag && *reinterpret_cast<const volatile int*>(race_flag)) break;
+        const int f_before = f;
         const bool asp = (f == bestf);
-        const uint32_t t = base + j;  // tabu clock of this step's scan
-        if (f <= 32 && !sparse) {
-            // enter sparse mode: lane l takes the l-th uncoloured vertex (ascending v)
-            if (prof) ++pn_enter;
-            int cnt = 0;
-            for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += x;
-            }
-            uint16_t* list = reinterpret_cast<uint16_t*>(conf);
-            int at = incl - cnt;
-            for (int q = 0; q < g.lane_words; ++q) {
-                uint32_t bits = s.U[lane * g.lane_words + q];
-                while (bits) {
-                    list[at++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
-                    bits &= bits - 1;
-                }
-            }
-            __syncwarp();
-            if (lane < f) {
-                const int v = list[lane];
-                const TabuRec tr = rec[v];
-                const uint16_t rc = g.cell[v];
-                svc = (uint32_t)v | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24);
-                su1 = tr.u1;
-                su2 = tr.u2;
-                skk = tr.kk;
-            }
-            __syncwarp();
-            sparse = true;
-        }
+        const uint32_t t = base + j;
         const uint32_t h1 = fmix32(s32 + (j + 1) * 0x9E3779B9u);
         const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
-        int lvl, N, vs, ks = 0, wl = 0;
-        if (sparse) {
-            // ---- sparse: each lane scores its own slot
-            uint64_t m[W];
-            int lv = 3;
-            uint64_t m0[W], m1[W], m2[W];
-            if (lane < f) {
-                const int r = (svc >> 16) & 0xFF, c = svc >> 24;
-                uint64_t dom[W], T[W];
-                dom_mask<W>(g, r, c, dom);
-                tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, t, T);
-                level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
-                uint64_t o0 = 0, o1 = 0, o2 = 0;
-#pragma unroll
-                for (int z = 0; z < W; ++z) {
-                    o0 |= m0[z];
-                    o1 |= m1[z];
-                    o2 |= m2[z];
-                }
-                lv = o0 ? 0 : o1 ? 1 : o2 ? 2 : 3;
-            }
-            const int lc = (int)__reduce_min_sync(kFull, (unsigned)lv);
-            lvl = lc - 1;
-#pragma unroll
-            for (int z = 0; z < W; ++z) m[z] = (lane < f) ? (lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z]) : 0ULL;
-            const int cnt = lc == 3 ? 0 : popc_w<W>(m);
-            // inclusive warp scan over the f occupied lanes only (f <= 32)
-            int incl = cnt;
-            for (int d = 1; d < f; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += x;
-            }
-            N = __shfl_sync(kFull, incl, f - 1);
-            const uint32_t r = __umulhi(h1, (uint32_t)N);
-            wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
-            if (wl < 0) wl = 0;
-            if (lane == wl && N > 0) ks = nth_bit_w<W>(m, (int)r - (incl - cnt));
-            vs = (int)(__shfl_sync(kFull, svc, wl) & 0xFFFFu);
-            ks = __shfl_sync(kFull, ks, wl);
-        } else {
-            // ---- dense: each lane scans its bitmask words (start of the descent, |V0| > 32)
+        if (f > 32) {
+            // ============================================== dense step (start of the descent)
+            if (prof) t_step = clock64();
             int c0 = 0, c1 = 0, c2 = 0;
             for (int q = 0; q < g.lane_words; ++q) {
                 uint32_t bits = s.U[lane * g.lane_words + q];
@@ -254,7 +237,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const unsigned b0 = __ballot_sync(kFull, c0 > 0);
             const unsigned b1 = __ballot_sync(kFull, c1 > 0);
             const unsigned b2 = __ballot_sync(kFull, c2 > 0);
-            lvl = b0 ? -1 : b1 ? 0 : b2 ? 1 : 2;
+            const int lvl = b0 ? -1 : b1 ? 0 : b2 ? 1 : 2;
             const int cnt = lvl == -1 ? c0 : lvl == 0 ? c1 : lvl == 1 ? c2 : 0;
             int incl = cnt;
 #pragma unroll
@@ -262,12 +245,18 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 const int x = __shfl_up_sync(kFull, incl, d);
                 if (lane >= d) incl += x;
             }
-            N = __shfl_sync(kFull, incl, 31);
-            vs = -1;
+            const int N = __shfl_sync(kFull, incl, 31);
+            if (N == 0) {
+                if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
+                if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
+                    trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
+                ++j;
+                continue;
+            }
             const uint32_t r = __umulhi(h1, (uint32_t)N);
-            wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
-            if (wl < 0) wl = 0;
-            if (lane == wl && N > 0) {
+            const int wl = __ffs(__ballot_sync(kFull, (uint32_t)(incl - cnt) <= r && r < (uint32_t)incl)) - 1;
+            int vs = -1, ks = 0;
+            if (lane == wl) {
                 int rr = (int)r - (incl - cnt);
                 for (int q = 0; q < g.lane_words && vs < 0; ++q) {
                     uint32_t bits = s.U[lane * g.lane_words + q];
@@ -291,173 +280,252 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             }
             vs = __shfl_sync(kFull, vs, wl);
             ks = __shfl_sync(kFull, ks, wl);
-        }
-        const int f_before = f;
-        if (N == 0) {
-            // every candidate tabu: no move, the clock still advances (partial.hpp:121-122)
-            if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
-            if (tracing && lane == 0 && (int64_t)j < a.trace_cap) {
-                plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + j;
-                tr->step = j;
-                tr->v = -1;
-                tr->k = 0;
-                tr->e = 0;
-                tr->ev0 = tr->ev1 = -1;
-                tr->f_before = tr->f_after = f;
-                tr->best_f = bestf;
-                tr->tenure = -1;
-                tr->n_adm = 0;
-                tr->level = 2;
+            if (pending && lvl >= 0) {
+                snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+                pending = false;
             }
+            const uint16_t rcs = g.cell[vs];
+            const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
+            const int kw = ks >> 6;
+            const uint64_t bitk = 1ULL << (ks & 63);
+            const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
+            const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
+            const int ur = warp_find_byte(col, g.rs[rs_], g.rs[rs_ + 1], ks, inR, lane);
+            const int xc = warp_find_byte(colT, g.cs[cs_], g.cs[cs_ + 1], ks, inC, lane);
+            const int uc = xc >= 0 ? (int)g.cl[xc] : -1;
+            const int e = (ur >= 0) + (uc >= 0);
+            const int f_new = f - 1 + e;
+            const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(alpha * (double)f_new);
+            const uint32_t ut = t + 1 + tenure;
+            const bool improved = f_new < bestf;
+            __syncwarp();
+            if (lane < 3) {
+                const int u = lane == 0 ? vs : lane == 1 ? ur : uc;
+                if (u >= 0) {
+                    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+                    col[u] = nc;
+                    colT[g.colpos[u]] = nc;
+                    atomicXor(&s.U[u >> 5], 1u << (u & 31));
+                    acc += lane == 0 ? 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
+                                           (improved ? 2ULL * (unsigned)nv : 0ULL)
+                                     : 4ULL * g.deg[u] + 2ULL;
+                    if (lane > 0) {
+                        until[(size_t)u * w1 + ks] = ut;
+                        TabuRec nr = rec[u];
+                        cache_forbid(nr, ks, ut, t);
+                        rec[u] = nr;
+                        if (lane == 1)
+                            s.C[(g.cell[u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
+                        else
+                            s.R[(g.cell[u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
+                    } else {
+                        s.R[rs_ * W + kw] |= bitk;
+                        s.C[cs_ * W + kw] |= bitk;
+                    }
+                }
+            }
+            f = f_new;
+            if (improved) {
+                bestf = f;
+                pending = true;
+                if (race_flag && bestf <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
+            }
+            if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
+                trace_step(j, vs, ks, ur, uc, rs_, cs_, f_before, f, bestf, (int)tenure, N, lvl);
+            __syncwarp();
             ++j;
+            if (prof) {
+                pc_dense += (unsigned long long)(clock64() - t_step);
+                ++pn_dense;
+                pf_dense += (unsigned)f_before;
+            }
             continue;
         }
 
-        // ---- apply (partial.hpp:124-141)
-        if (pending && lvl >= 0) {
-            // the current colouring is the best one and is about to change without improving
-            snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
-            pending = false;
+        // ================================================== sparse phase (|V0| <= 32)
+        if (prof) ++pn_enter;
+        // lane l takes the l-th uncoloured vertex (ascending v) with its tabu cache
+        uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
+        {
+            int cnt = 0;
+            for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += x;
+            }
+            int at = incl - cnt;
+            for (int q = 0; q < g.lane_words; ++q) {
+                uint32_t bits = s.U[lane * g.lane_words + q];
+                while (bits) {
+                    s.list[at++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
+                    bits &= bits - 1;
+                }
+            }
+            __syncwarp();
+            if (lane < f) {
+                const int v = s.list[lane];
+                const TabuRec tr = rec[v];
+                const uint16_t rc = g.cell[v];
+                svc = (uint32_t)v | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24);
+                su1 = tr.u1;
+                su2 = tr.u2;
+                skk = tr.kk;
+            }
+            __syncwarp();
         }
-        const uint16_t rcs = g.cell[vs];
-        const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-        const int kw = ks >> 6;
-        const uint64_t bitk = 1ULL << (ks & 63);
-        int ur = -1, uc = -1;
-        if (lvl >= 0) {
-            // the row / column holder of k* (at most one each: the colouring is legal)
+        for (;;) {
+            if (prof) t_step = clock64();
+            const int fb = f;
+            const bool asp_s = (f == bestf);
+            const uint32_t ts = base + j;
+            const uint32_t g1 = fmix32(s32 + (j + 1) * 0x9E3779B9u);
+            const uint32_t g2 = fmix32(g1 + 0x632BE5ABu);
+            // ---- score this lane's slot
+            const int r = (svc >> 16) & 0xFF, c = svc >> 24;
+            uint64_t dom[W], T[W], m0[W], m1[W], m2[W];
+            dom_mask<W>(g, r, c, dom);
+            tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
+            level_masks<W>(s, r, c, dom, T, asp_s, m0, m1, m2);
+            const bool mine = lane < f;
+            uint64_t o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+            for (int z = 0; z < W; ++z) {
+                o0 |= m0[z];
+                o1 |= m1[z];
+                o2 |= m2[z];
+            }
+            const unsigned lv = !mine ? 3u : o0 ? 0u : o1 ? 1u : o2 ? 2u : 3u;
+            const int lc = (int)__reduce_min_sync(kFull, lv);
+            uint64_t m[W];
+#pragma unroll
+            for (int z = 0; z < W; ++z) m[z] = !mine ? 0ULL : lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z];
+            const int cnt = popc_w<W>(m);
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                incl += lane >= d ? x : 0;
+            }
+            const int N = __shfl_sync(kFull, incl, 31);
+            if (N == 0) {
+                // every candidate tabu: no move, the clock still advances (partial.hpp:121-122)
+                if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
+                if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
+                    trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
+                ++j;
+                if (!((int64_t)j < budget) || (race_flag && (j & 63) == 0 &&
+                                               *reinterpret_cast<const volatile int*>(race_flag)))
+                    break;
+                continue;
+            }
+            const uint32_t rnk = __umulhi(g1, (uint32_t)N);
+            const int excl = incl - cnt;
+            const int wl = __ffs(__ballot_sync(kFull, (uint32_t)excl <= rnk && rnk < (uint32_t)incl)) - 1;
+            const int kmine = nth_bit_w<W>(m, min(max((int)rnk - excl, 0), max(cnt - 1, 0)));
+            const int ks = __shfl_sync(kFull, kmine, wl);
+            const uint32_t vcs = __shfl_sync(kFull, svc, wl);
+            const int vs = (int)(vcs & 0xFFFFu), rs_ = (vcs >> 16) & 0xFF, cs_ = vcs >> 24;
+            const int lvl = lc - 1;
+            if (pending && lvl >= 0) {
+                // the current colouring is the best one and is about to change without improving
+                snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+                pending = false;
+            }
+            const int kw = ks >> 6;
+            const uint64_t bitk = 1ULL << (ks & 63);
             const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
             const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
-            if (inR) {
-                for (int b0 = g.rs[rs_]; b0 < g.rs[rs_ + 1]; b0 += 32) {
-                    const int u = b0 + lane;
-                    const unsigned hit = __ballot_sync(kFull, u < g.rs[rs_ + 1] && col[u] == ks);
-                    if (hit) {
-                        ur = b0 + __ffs(hit) - 1;
-                        break;
-                    }
+            // ---- the row / column holder of k* (at most one each: the colouring is legal)
+            const int ur = warp_find_byte(col, g.rs[rs_], g.rs[rs_ + 1], ks, inR, lane);
+            const int xc = warp_find_byte(colT, g.cs[cs_], g.cs[cs_ + 1], ks, inC, lane);
+            const int uc = xc >= 0 ? (int)g.cl[xc] : -1;
+            const int e = (ur >= 0) + (uc >= 0);
+            const int f_new = f - 1 + e;
+            const uint32_t tenure = __umulhi(g2, 10u) + (uint32_t)(alpha * (double)f_new);
+            const uint32_t ut = ts + 1 + tenure;
+            const bool improved = f_new < bestf;
+            const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
+            TabuRec nr{0, 0, 0, 0};
+            if (my_u >= 0) nr = rec[my_u];  // issued early, consumed after the updates
+            __syncwarp();
+            // ---- predicated five-lane update:
+            //   lanes 0-2: colour byte (row- and column-major) and U bit of v*, ur, uc
+            //   lanes 1/2 also clear k* from the evictee's other line
+            //   lane 3: R[row v*] gains k* unless ur held it; lane 4: C[col v*] likewise unless uc did
+            {
+                const int u = lane == 0 ? vs : my_u;
+                if (lane < 3 && u >= 0) {
+                    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+                    col[u] = nc;
+                    colT[g.colpos[u]] = nc;
+                    atomicXor(&s.U[u >> 5], 1u << (u & 31));
+                    const uint16_t cu = g.cell[u];
+                    uint64_t* line = lane == 1 ? &s.C[(cu & 0xFF) * W + kw] : &s.R[(cu >> 8) * W + kw];
+                    if (lane > 0) *line ^= bitk;
+                    acc += lane == 0 ? 2ULL * (unsigned)w1 * (unsigned)fb + 4ULL * g.deg[u] + 2ULL +
+                                           (improved ? 2ULL * (unsigned)nv : 0ULL)
+                                     : 4ULL * g.deg[u] + 2ULL;
                 }
+                if (lane == 3 && !inR) s.R[rs_ * W + kw] ^= bitk;
+                if (lane == 4 && !inC) s.C[cs_ * W + kw] ^= bitk;
             }
-            if (inC) {
-                for (int b0 = g.cs[cs_]; b0 < g.cs[cs_ + 1]; b0 += 32) {
-                    const int x = b0 + lane;
-                    const int u = x < g.cs[cs_ + 1] ? g.cl[x] : 0;
-                    const unsigned hit = __ballot_sync(kFull, x < g.cs[cs_ + 1] && col[u] == ks);
-                    if (hit) {
-                        uc = __shfl_sync(kFull, u, __ffs(hit) - 1);
-                        break;
-                    }
-                }
+            if (my_u >= 0) {
+                until[(size_t)my_u * w1 + ks] = ut;
+                cache_forbid(nr, ks, ut, ts);
+                rec[my_u] = nr;
             }
-        }
-        const int e = (ur >= 0) + (uc >= 0);
-        const int f_new = f - 1 + e;
-        const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(a.alpha * (double)f_new);
-        const uint32_t ut = t + 1 + tenure;
-        const bool improved = f_new < bestf;
-        __syncwarp();
-        // distributed update: lane 0 colours v*, lanes 1 / 2 evict the row / column holder
-        const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
-        TabuRec nr{0, 0, 0, 0};
-        if (my_u >= 0) nr = rec[my_u];  // issued early: consumed after the slot bookkeeping below
-        if (lane == 0) {
-            col[vs] = (uint8_t)ks;
-            atomicAnd(&s.U[vs >> 5], ~(1u << (vs & 31)));
-            s.R[rs_ * W + kw] |= bitk;
-            s.C[cs_ * W + kw] |= bitk;
-            acc += 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
-                   (improved ? 2ULL * (unsigned)nv : 0ULL);
-        } else if (my_u >= 0) {
-            col[my_u] = 0;
-            atomicOr(&s.U[my_u >> 5], 1u << (my_u & 31));
-            if (lane == 1)
-                s.C[(g.cell[my_u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
-            else
-                s.R[(g.cell[my_u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
-            until[(size_t)my_u * w1 + ks] = ut;
-            acc += 4ULL * g.deg[my_u] + 2ULL;
-        }
-        // ---- sparse slot list: new sorted list = old - {v*} + {ur, uc}
-        if (sparse) {
+            f = f_new;
+            if (improved) {
+                bestf = f;
+                pending = true;
+                if (race_flag && bestf <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
+            }
+            if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
+                trace_step(j, vs, ks, ur, uc, rs_, cs_, fb, f, bestf, (int)tenure, N, lvl);
+            ++j;
             if (f_new > 32) {
-                sparse = false;
-            } else {
+                __syncwarp();
+                if (prof) {
+                    pc_sparse += (unsigned long long)(clock64() - t_step);
+                    ++pn_sparse;
+                }
+                break;  // back to dense mode; the slot list is rebuilt on re-entry
+            }
+            // ---- re-sort the slot list: new = old - {v*} + {ur, uc}
+            {
                 const int vl = (int)(svc & 0xFFFFu);
-                const bool old_ok = lane < f && lane != wl;
-                const int pr_ = ur >= 0 ? __popc(__ballot_sync(kFull, old_ok && vl < ur)) + (uc >= 0 && uc < ur) : -1;
-                const int pc_ = uc >= 0 ? __popc(__ballot_sync(kFull, old_ok && vl < uc)) + (ur >= 0 && ur < uc) : -1;
+                const bool old_ok = mine && lane != wl;
+                const unsigned br = __ballot_sync(kFull, old_ok && vl < ur);
+                const unsigned bc = __ballot_sync(kFull, old_ok && vl < uc);
+                const int pr_ = ur >= 0 ? __popc(br) + (uc >= 0 && uc < ur) : -1;
+                const int pc_ = uc >= 0 ? __popc(bc) + (ur >= 0 && ur < uc) : -1;
                 const int y = lane - (pr_ >= 0 && pr_ < lane) - (pc_ >= 0 && pc_ < lane);
                 const int src = (y >= wl ? y + 1 : y) & 31;
                 const uint32_t mvc = __shfl_sync(kFull, svc, src);
                 const uint32_t mu1 = __shfl_sync(kFull, su1, src);
                 const uint32_t mu2 = __shfl_sync(kFull, su2, src);
                 const uint32_t mkk = __shfl_sync(kFull, skk, src);
-                if (my_u >= 0) {
-                    cache_forbid(nr, ks, ut, t);
-                    rec[my_u] = nr;
-                }
                 const int from = lane == pr_ ? 1 : 2;  // evictee caches come from lanes 1 / 2
                 const uint32_t nu1 = __shfl_sync(kFull, nr.u1, from);
                 const uint32_t nu2 = __shfl_sync(kFull, nr.u2, from);
                 const uint32_t nkk = __shfl_sync(kFull, nr.kk, from);
-                if (lane == pr_ || lane == pc_) {
-                    const int u = lane == pr_ ? ur : uc;
-                    const uint16_t rc = g.cell[u];
-                    svc = (uint32_t)u | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24);
-                    su1 = nu1;
-                    su2 = nu2;
-                    skk = nkk;
-                } else {
-                    svc = mvc;
-                    su1 = mu1;
-                    su2 = mu2;
-                    skk = mkk;
-                }
+                const bool take_new = lane == pr_ || lane == pc_;
+                const int u = lane == pr_ ? ur : uc;
+                const uint16_t rc = g.cell[take_new ? u : 0];
+                svc = take_new ? ((uint32_t)u | ((uint32_t)(rc >> 8) << 16) | ((uint32_t)(rc & 0xFF) << 24)) : mvc;
+                su1 = take_new ? nu1 : mu1;
+                su2 = take_new ? nu2 : mu2;
+                skk = take_new ? nkk : mkk;
             }
-        }
-        if (!sparse && my_u >= 0) {
-            // dense step (or sparse mode just left): record the forbid here
-            cache_forbid(nr, ks, ut, t);
-            rec[my_u] = nr;
-        }
-        f = f_new;
-        if (improved) {
-            bestf = f;
-            pending = true;
-            if (a.race_flag && bestf <= a.race_f && lane == 0) atomicExch(a.race_flag, 1);
-        }
-        if (tracing && lane == 0 && (int64_t)j < a.trace_cap) {
-            plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + j;
-            // CSR order of N(v*): row-mates first iff row <= col (lsgraph.hpp:202-209)
-            const bool row_first = rs_ <= cs_;
-            const int e0 = row_first ? (ur >= 0 ? ur : uc) : (uc >= 0 ? uc : ur);
-            const int e1 = e == 2 ? (row_first ? uc : ur) : -1;
-            tr->step = j;
-            tr->v = vs;
-            tr->k = ks;
-            tr->e = e;
-            tr->ev0 = e0;
-            tr->ev1 = e1;
-            tr->f_before = f_before;
-            tr->f_after = f;
-            tr->best_f = bestf;
-            tr->tenure = (int32_t)tenure;
-            tr->n_adm = N;
-            tr->level = lvl;
-        }
-        __syncwarp();
-        ++j;
-        if (prof) {
-            const unsigned long long dt = (unsigned long long)(clock64() - t_step);
-            if (step_sparse) {
-                pc_sparse += dt;
+            __syncwarp();
+            if (prof) {
+                pc_sparse += (unsigned long long)(clock64() - t_step);
                 ++pn_sparse;
-                fh[(f_before - 1) >> 3] += 1;
-            } else {
-                pc_dense += dt;
-                ++pn_dense;
-                pf_dense += (unsigned)f_before;
             }
+            if (!((int64_t)j < budget && bestf > stop_f)) break;
+            if (race_flag && (j & 63) == 0 && *reinterpret_cast<const volatile int*>(race_flag)) break;
         }
     }
     if (pending) snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
@@ -484,7 +552,6 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         atomicAdd(prof + 6, pf_dense);
         atomicAdd(prof + 7, pn_enter);
         atomicAdd(prof + 8, (unsigned long long)(clock64() - t_start));
-        for (int q = 0; q < 4; ++q) atomicAdd(prof + 9 + q, fh[q]);
     }
     __syncwarp();
 }
@@ -499,12 +566,15 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
     uint16_t* s_rs = reinterpret_cast<uint16_t*>(smem + L.rs);
     uint16_t* s_cs = reinterpret_cast<uint16_t*>(smem + L.cs);
     uint16_t* s_cl = reinterpret_cast<uint16_t*>(smem + L.cl);
+    uint16_t* s_cp = reinterpret_cast<uint16_t*>(smem + L.colpos);
     uint64_t* s_pr = reinterpret_cast<uint64_t*>(smem + L.pr);
     uint64_t* s_pc = reinterpret_cast<uint64_t*>(smem + L.pc);
     uint8_t* s_deg = smem + L.deg;
     for (int x = threadIdx.x; x < nv; x += blockDim.x) {
         s_cell[x] = a.cell[x];
-        s_cl[x] = a.col_list[x];
+        const uint16_t v = a.col_list[x];
+        s_cl[x] = v;
+        s_cp[v] = (uint16_t)x;
     }
     for (int x = threadIdx.x; x <= n; x += blockDim.x) {
         s_rs[x] = a.row_start[x];
@@ -531,6 +601,7 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
     g.rs = s_rs;
     g.cs = s_cs;
     g.cl = s_cl;
+    g.colpos = s_cp;
     g.pr = s_pr;
     g.pc = s_pc;
 #pragma unroll
@@ -546,7 +617,9 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
     uint8_t* wbase = smem + L.warp0 + (size_t)warp * L.warp_bytes;
     WarpSmem s;
     s.col = wbase + L.w_col;
-    s.conf = wbase + L.w_conf;
+    s.conf = nullptr;
+    s.colT = wbase + L.w_colT;
+    s.list = reinterpret_cast<uint16_t*>(wbase + L.w_list);
     s.R = reinterpret_cast<uint64_t*>(wbase + L.w_R);
     s.C = reinterpret_cast<uint64_t*>(wbase + L.w_C);
     s.U = reinterpret_cast<uint32_t*>(wbase + L.w_U);
@@ -554,13 +627,14 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
     const int slot = blockIdx.x * nwarps + warp;
     TabuRec* rec = reinterpret_cast<TabuRec*>(reinterpret_cast<char*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
+    uint8_t* conf = a.conf_scratch + (size_t)slot * a.conf_stride;
 
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
         i = __shfl_sync(kFull, i, 0);
         if (i >= a.p) break;
-        improve_one<W, kDebug>(a, g, s, rec, until, a.slot_clock + slot, i, lane);
+        improve_one<W, kDebug>(a, g, s, rec, until, a.slot_clock + slot, conf, i, lane);
     }
 }
 

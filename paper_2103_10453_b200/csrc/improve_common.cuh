@@ -14,11 +14,13 @@ struct alignas(16) TabuRec {
 };
 
 struct WarpSmem {
-    uint8_t* col;
-    uint8_t* conf;
+    uint8_t* col;    // colour of vertex v
+    uint8_t* conf;   // improve_hw: repair counters / column-major copy
     uint64_t* R;
     uint64_t* C;
     uint32_t* U;
+    uint8_t* colT;   // improve: colour of vertex cl[x] (column-major copy)
+    uint16_t* list;  // improve: 32-entry seed list of sparse mode
 };
 
 template <int W>
