@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PLSE_ABI_VERSION 1
+#define PLSE_ABI_VERSION 2
 
 typedef enum {
     PLSE_OK = 0,
@@ -142,9 +142,19 @@ typedef struct {
                                    reaches the target (device-global early exit; not parity mode) */
 } plse_solver_config;
 
+/* per-generation statistics (GenerationStats, engine.hpp:49-57) */
+typedef struct {
+    int64_t generation;
+    int32_t best_f;          /* best f ever seen (legal) */
+    double mean_f;           /* mean f of the (updated) population */
+    double mean_distance;    /* mean pairwise Hamming distance over i < j */
+    int64_t iterations;      /* total tabu iterations so far */
+    double elapsed_seconds;
+    int32_t shortfall;       /* slots the pool update could not fill */
+} plse_generation_stats;
+
 /* per-generation callback (GenerationCallback, engine.hpp:108) */
-typedef void (*plse_generation_cb)(int64_t generation, int32_t best_f, int64_t iterations,
-                                   double elapsed_seconds, int32_t shortfall, void* user);
+typedef void (*plse_generation_cb)(const plse_generation_stats* stats, void* user);
 
 int plse_abi_version(void);
 const char* plse_last_error(const plse_ctx* ctx); /* ctx may be NULL: last global error */
@@ -155,6 +165,13 @@ int plse_parse_instance(const char* text, int32_t* n, uint16_t* grid /* cap n*n 
 int plse_preprocess(int32_t n, const uint16_t* grid, plse_graph_h** out);
 void plse_graph_free(plse_graph_h* g);
 int plse_graph_view(const plse_graph_h* g, plse_graph* view); /* borrowed arrays, valid until free */
+/* coloring.hpp:171 to_grid: certificate grid [n*n] from a |V|-colouring (colours are symbols, 0 = empty) */
+int plse_to_grid(const plse_graph_h* g, const uint16_t* colors, uint16_t* grid);
+/* verify.hpp:20 verify_certificate: problems joined by '\n' (NUL-terminated, truncated to cap;
+   *problems_len = full length); legal = no problems, score = filled cells of the certificate */
+int plse_verify_certificate(int32_t n, const uint16_t* instance, int32_t m, const uint16_t* certificate,
+                            int32_t* legal, int32_t* score, char* problems, int64_t problems_cap,
+                            int64_t* problems_len);
 
 /* ---- device context */
 int plse_create(const plse_graph* graph, const plse_params* params, int32_t device, plse_ctx** out);

@@ -70,7 +70,7 @@ class OrResult(C.Structure):
 
 class OrGenLog(C.Structure):
     _fields_ = [("generation", C.c_int64), ("best_f", C.c_int32), ("shortfall", C.c_int32),
-                ("iterations", C.c_int64)]
+                ("iterations", C.c_int64), ("mean_f", C.c_double), ("mean_distance", C.c_double)]
 
 
 class RefRunResult(C.Structure):
@@ -330,6 +330,15 @@ class Reference:
         L.ref_improve_phase.argtypes = [C.c_void_p, C.c_int, u16p, C.c_void_p, C.c_uint64, C.c_uint64,
                                         C.c_int64, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_default_workers.restype = C.c_int
+        L.ref_set_log.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_log_count.restype = C.c_int64
+        L.ref_verify_certificate.argtypes = [C.c_int, u16p, C.c_int, u16p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ref_to_grid.argtypes = [C.c_int, u16p, u16p, u16p]
+        if hasattr(L, "ref_result_json"):
+            L.ref_result_json.argtypes = [C.c_char_p, C.c_int, C.POINTER(RefRunResult), C.c_char_p, C.c_int,
+                                          C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int,
+                                          C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int64,
+                                          C.c_int64, C.c_int, C.c_char_p, C.c_int]
         self._handles = {}
 
     def generate_instance(self, n, r, seed):
@@ -433,16 +442,25 @@ class Reference:
 
     def run(self, grid, p=64, alpha=0.6, gamma=10.0, beta=20.0, phase1_iters=0, variant=1, crossover=X_AUX,
             matching=M_NEAREST, exclusion=E_RUN, seed=0, workers=1, time_limit=0.0, iteration_limit=0,
-            generation_limit=0):
+            generation_limit=0, log_cap=0):
         grid = np.ascontiguousarray(grid, np.uint16)
         n = grid.shape[0]
         res = RefRunResult()
         best = np.zeros(n * n + 1, np.uint16)
-        self.lib.ref_run(n, grid.reshape(-1), p, alpha, gamma, beta, phase1_iters, variant, crossover, matching,
-                         exclusion, seed, workers, time_limit, iteration_limit, generation_limit, C.byref(res), best)
+        log = (OrGenLog * log_cap)() if log_cap else None  # same layout as ref_gen_log
+        self.lib.ref_set_log(C.cast(log, C.c_void_p) if log is not None else None, log_cap)
+        try:
+            self.lib.ref_run(n, grid.reshape(-1), p, alpha, gamma, beta, phase1_iters, variant, crossover,
+                             matching, exclusion, seed, workers, time_limit, iteration_limit, generation_limit,
+                             C.byref(res), best)
+            n_log = self.lib.ref_log_count()
+        finally:
+            self.lib.ref_set_log(None, 0)
         out = {k: getattr(res, k) for k, _ in RefRunResult._fields_}
         out["stop_reason"] = STOP_NAMES[res.stop_reason]
         out["best_colors"] = best[:res.vertex_count]
+        if log is not None:
+            out["log"] = [{k: getattr(log[i], k) for k, _ in OrGenLog._fields_} for i in range(n_log)]
         return out
 
     def improve_phase(self, grid, offspring, master_seed, generation, budget, alpha=0.6, stop_f=0, workers=0):
@@ -455,3 +473,39 @@ class Reference:
 
     def default_workers(self):
         return self.lib.ref_default_workers()
+
+    def verify_certificate(self, instance, certificate):
+        """verify.hpp:20 -> (legal, score, problems)"""
+        a = np.ascontiguousarray(instance, np.uint16)
+        b = np.ascontiguousarray(certificate, np.uint16)
+        score = C.c_int()
+        buf = C.create_string_buffer(1 << 20)
+        legal = self.lib.ref_verify_certificate(a.shape[0], a.reshape(-1), b.shape[0], b.reshape(-1),
+                                                C.byref(score), buf, len(buf))
+        text = buf.value.decode()
+        return bool(legal), score.value, (text.split("\n") if text else [])
+
+    def to_grid(self, instance, colors):
+        """coloring.hpp:171"""
+        a = np.ascontiguousarray(instance, np.uint16)
+        out = np.zeros_like(a)
+        self.lib.ref_to_grid(a.shape[0], a.reshape(-1), np.ascontiguousarray(colors, np.uint16), out.reshape(-1))
+        return out
+
+    def has_result_json(self):
+        return hasattr(self.lib, "ref_result_json")
+
+    def result_json(self, name, order, result, stop_reason, p, alpha, gamma, beta, phase1, phase2, variant,
+                    crossover, matching, exclusion, seed, workers, time_limit, iteration_limit, generation_limit,
+                    timing=False):
+        """report.hpp:85 result_to_json(...).dump(2) for the given result fields (a dict with
+        RefRunResult's keys)."""
+        res = RefRunResult()
+        for k, _ in RefRunResult._fields_:
+            if k in result and k != "stop_reason":
+                setattr(res, k, result[k])
+        buf = C.create_string_buffer(1 << 16)
+        self.lib.ref_result_json(name.encode(), order, C.byref(res), stop_reason.encode(), p, alpha, gamma, beta,
+                                 phase1, phase2, variant, crossover, matching, exclusion, seed, workers, time_limit,
+                                 iteration_limit, generation_limit, int(timing), buf, len(buf))
+        return buf.value.decode()

@@ -912,6 +912,16 @@ int or_run(int n, const uint16_t* grid, const or_config* cfg, or_result* res, ui
                 log[nlog].best_f = res->best_f;
                 log[nlog].shortfall = nsf;
                 log[nlog].iterations = res->total_iterations;
+                /* engine.hpp:219-225: f over members, distance over i < j */
+                double f_sum = 0, d_sum = 0;
+                for (int i = 0; i < p; ++i) {
+                    int f, c;
+                    or_eval(g, members + (size_t)i * nv, &f, &c);
+                    f_sum += f;
+                    for (int j = i + 1; j < p; ++j) d_sum += dist[(size_t)i * p + j];
+                }
+                log[nlog].mean_f = f_sum / p;
+                log[nlog].mean_distance = d_sum / (0.5 * p * (p - 1));
                 ++nlog;
             }
             if (optimal || iters_up || gens_up) {

@@ -147,12 +147,15 @@ typedef struct {
     int64_t generations, total_iterations;
 } or_result;
 
-/* per-generation log: best_f after the improve phase, iterations so far */
+/* per-generation log (GenerationStats, engine.hpp:49-57 / emit_stats 214-233): best_f after the
+   improve phase, iterations so far, and the population's mean f and mean pairwise distance */
 typedef struct {
     int64_t generation;
     int32_t best_f;
     int32_t shortfall;
     int64_t iterations;
+    double mean_f;
+    double mean_distance;
 } or_gen_log;
 
 int or_run(int n, const uint16_t* grid, const or_config* cfg, or_result* res, uint16_t* best_colors,

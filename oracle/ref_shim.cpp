@@ -14,6 +14,11 @@
 #include <vector>
 
 #include "plse/engine.hpp"
+#if __has_include(<json.hpp>)
+#include "plse/report.hpp"
+#define PLSE_REF_HAVE_JSON 1
+#endif
+#include "plse/verify.hpp"
 #include "plse/oracle.hpp"
 #include "support/builders.hpp"
 
@@ -224,6 +229,23 @@ int ref_solve_exact(const ref_graph* h, int* exact) {
     return r.optimum_f;
 }
 
+// GenerationStats capture for the next ref_run (engine.hpp:49-57)
+struct ref_gen_log {
+    int64_t generation;
+    int32_t best_f, shortfall;
+    int64_t iterations;
+    double mean_f, mean_distance;
+};
+static ref_gen_log* g_log = nullptr;
+static int64_t g_log_cap = 0, g_log_n = 0;
+
+void ref_set_log(ref_gen_log* log, int64_t cap) {
+    g_log = log;
+    g_log_cap = cap;
+    g_log_n = 0;
+}
+int64_t ref_log_count(void) { return g_log_n; }
+
 struct ref_run_result {
     int32_t best_f, best_score, proven_optimal, stop_reason, l, upper_bound, vertex_count;
     int64_t generations, total_iterations;
@@ -255,6 +277,8 @@ int ref_run(int n, const uint16_t* grid, int p, double alpha, double gamma, doub
     int last_best = -1;
     double first_at = 0;
     RunResult r = run(grid_instance(n, grid), cfg, [&](const GenerationStats& s) {
+        if (g_log && g_log_n < g_log_cap)
+            g_log[g_log_n++] = {s.generation, s.best_f, s.shortfall, s.iterations, s.mean_f, s.mean_distance};
         if (s.best_f != last_best) {
             last_best = s.best_f;
             first_at = s.elapsed_seconds;
@@ -309,5 +333,75 @@ int64_t ref_improve_phase(const ref_graph* h, int p, const uint16_t* offspring, 
 }
 
 int ref_default_workers() { return default_workers(); }
+
+
+static void copy_out(const std::string& s, char* out, int cap) {
+    if (!out || cap <= 0) return;
+    const std::size_t n = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+    std::memcpy(out, s.data(), n);
+    out[n] = 0;
+}
+
+// verify.hpp:20 verify_certificate; problems joined by '\n'.  Returns legal.
+int ref_verify_certificate(int n, const uint16_t* instance, int m, const uint16_t* certificate, int* score,
+                           char* problems, int cap) {
+    VerifyReport r = verify_certificate(grid_instance(n, instance), grid_instance(m, certificate));
+    std::string joined;
+    for (std::size_t i = 0; i < r.problems.size(); ++i) joined += (i ? "\n" : "") + r.problems[i];
+    copy_out(joined, problems, cap);
+    if (score) *score = r.score;
+    return r.legal ? 1 : 0;
+}
+
+// coloring.hpp:171 to_grid
+int ref_to_grid(int n, const uint16_t* grid, const uint16_t* colors, uint16_t* out) {
+    PlsInstance inst = grid_instance(n, grid);
+    ReducedGraph g = preprocess(build_graph(inst));
+    Coloring c(g);
+    c.assign(std::vector<Color>(colors, colors + g.vertex_count()));
+    PlsInstance res = to_grid(inst, g, c);
+    for (int r = 0; r < n; ++r)
+        for (int col = 0; col < n; ++col) out[r * n + col] = res.at(r, col);
+    return 0;
+}
+
+#ifdef PLSE_REF_HAVE_JSON
+// report.hpp:85 result_to_json, printed as plse.cpp:154 does (dump(2)).
+int ref_result_json(const char* name, int order, const ref_run_result* res, const char* stop_reason, int p,
+                    double alpha, double gamma, double beta, int64_t phase1, int64_t phase2, int variant,
+                    int crossover, int matching, int exclusion, uint64_t seed, int workers, double time_limit,
+                    int64_t iteration_limit, int64_t generation_limit, int timing, char* out, int cap) {
+    SolverConfig cfg;
+    cfg.p = p;
+    cfg.alpha = alpha;
+    cfg.gamma = gamma;
+    cfg.crossover.beta = beta;
+    cfg.phase1_iters = phase1;
+    cfg.phase2_iters = phase2;
+    cfg.variant = variant == 1 ? Variant::PartialMPMA : Variant::MPMA;
+    cfg.crossover.mode = crossover == 0 ? CrossoverMode::AUX : crossover == 1 ? CrossoverMode::UX : CrossoverMode::None;
+    cfg.crossover.matching = matching == 0 ? MatchingStrategy::NearestNeighbor : MatchingStrategy::Random;
+    cfg.crossover.exclusion =
+        exclusion == 0 ? ExclusionScope::Run : exclusion == 1 ? ExclusionScope::Generation : ExclusionScope::Off;
+    cfg.master_seed = seed;
+    cfg.workers = workers;
+    cfg.limits.time_seconds = time_limit;
+    cfg.limits.total_iterations = iteration_limit;
+    cfg.limits.generations = generation_limit;
+    RunResult r;
+    r.best_f = res->best_f;
+    r.best_score = res->best_score;
+    r.proven_optimal = res->proven_optimal != 0;
+    r.stop_reason = stop_reason;
+    r.l = res->l;
+    r.upper_bound = res->upper_bound;
+    r.vertex_count = res->vertex_count;
+    r.generations = res->generations;
+    r.total_iterations = res->total_iterations;
+    r.elapsed_seconds = res->elapsed_seconds;
+    copy_out(result_to_json(name, order, r, cfg, timing != 0).dump(2), out, cap);
+    return 0;
+}
+#endif
 
 }  // extern "C"

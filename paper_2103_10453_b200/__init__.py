@@ -18,6 +18,10 @@ this module                       reference
   ``.update_population()``        population.hpp:103 update_population
   ``.build_offspring(gen)``       crossover.hpp:54  build_offspring
 ``run``                           engine.hpp:114    run (variant=partial)
+``to_grid``                       coloring.hpp:171  to_grid (certificate)
+``verify_certificate``            verify.hpp:20     verify_certificate
+``report.result_to_json``         report.hpp:85     result_to_json
+``python -m paper_2103_10453_b200``  tools/plse.cpp  generate / solve / verify
 ================================  =======================================
 
 Errors map like the reference's exceptions: ``std::invalid_argument`` ->
@@ -41,8 +45,8 @@ LIB_PATH = os.environ.get("PLSE_LIB") or os.path.join(HERE, "libplse_b200.so")  
 
 __all__ = [
     "generate_instance", "lsc_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
-    "SolverConfig", "RunResult", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
-    "lib_path", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
+    "SolverConfig", "RunResult", "GenerationStats", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
+    "lib_path", "derive_seed", "to_grid", "verify_certificate", "VerifyReport", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
 ]
 
 AUX, UX, NONE = 0, 1, 2
@@ -101,7 +105,17 @@ class _SolverConfig(C.Structure):
                 ("disable_optimal_stop", C.c_int32), ("target_score", C.c_double), ("race", C.c_int32)]
 
 
-_GEN_CB = C.CFUNCTYPE(None, C.c_int64, C.c_int32, C.c_int64, C.c_double, C.c_int32, C.c_void_p)
+class GenerationStats(C.Structure):
+    """plse_generation_stats (GenerationStats, engine.hpp:49-57)"""
+    _fields_ = [("generation", C.c_int64), ("best_f", C.c_int32), ("mean_f", C.c_double),
+                ("mean_distance", C.c_double), ("iterations", C.c_int64), ("elapsed_seconds", C.c_double),
+                ("shortfall", C.c_int32)]
+
+    def __repr__(self):
+        return "GenerationStats(" + ", ".join(f"{k}={getattr(self, k)!r}" for k, _ in self._fields_) + ")"
+
+
+_GEN_CB = C.CFUNCTYPE(None, C.POINTER(GenerationStats), C.c_void_p)
 
 
 def lib_path() -> str:
@@ -126,6 +140,9 @@ def _load() -> C.CDLL:
         "plse_preprocess": ([C.c_int32, u16p, C.POINTER(vp)], C.c_int),
         "plse_graph_free": ([vp], None),
         "plse_graph_view": ([vp, C.POINTER(_Graph)], C.c_int),
+        "plse_to_grid": ([vp, u16p, u16p], C.c_int),
+        "plse_verify_certificate": ([C.c_int32, u16p, C.c_int32, u16p, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32), vp, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
         "plse_create": ([C.POINTER(_Graph), C.POINTER(_Params), C.c_int32, C.POINTER(vp)], C.c_int),
         "plse_destroy": ([ctx], None),
         "plse_set_colors": ([ctx, C.c_int32, u16p, C.c_int64], C.c_int),
@@ -156,7 +173,7 @@ def _load() -> C.CDLL:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
-    if L.plse_abi_version() != 1:
+    if L.plse_abi_version() != 2:
         raise ImportError("libplse_b200.so ABI mismatch")
     return L
 
@@ -259,6 +276,47 @@ def serialize_instance(grid: np.ndarray) -> str:
     return f"{n}\n" + "".join(" ".join(str(int(x)) for x in row) + "\n" for row in grid)
 
 
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(state: int):
+    state = (state + 0x9E3779B97F4A7C15) & _M64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return state, z ^ (z >> 31)
+
+
+def derive_seed(master: int, tag: int, index: int) -> int:
+    """rng.hpp:81-88 -- the (master, purpose tag, index) stream seed."""
+    s, h = _splitmix64(master & _M64)
+    s, h = _splitmix64(h ^ ((tag * 0xD1B54A32D192ED03) & _M64))
+    s, h = _splitmix64(h ^ ((index * 0x8CB92BA72F3D8DD7) & _M64))
+    return h
+
+
+@dataclasses.dataclass
+class VerifyReport:
+    """verify.hpp:11-15"""
+    legal: bool
+    score: int
+    problems: List[str]
+
+
+def verify_certificate(instance: np.ndarray, certificate: np.ndarray) -> VerifyReport:
+    """verify.hpp:20-73 -- order, pre-filled cells, Latin condition; score = filled cells."""
+    a = np.ascontiguousarray(instance, np.uint16)
+    b = np.ascontiguousarray(certificate, np.uint16)
+    legal, score, length = C.c_int32(), C.c_int32(), C.c_int64()
+    _check(_lib.plse_verify_certificate(a.shape[0], a.reshape(-1), b.shape[0], b.reshape(-1), C.byref(legal),
+                                        C.byref(score), None, 0, C.byref(length)))
+    buf = C.create_string_buffer(length.value + 1)
+    _check(_lib.plse_verify_certificate(a.shape[0], a.reshape(-1), b.shape[0], b.reshape(-1), C.byref(legal),
+                                        C.byref(score), C.cast(buf, C.c_void_p), len(buf), C.byref(length)))
+    text = buf.value.decode()
+    return VerifyReport(bool(legal.value), int(score.value), text.split("\n") if text else [])
+
+
 @dataclasses.dataclass
 class ReducedGraph:
     """lsgraph.hpp:67 (cells row-major, CSR domains starting with 0, prefilled triples)."""
@@ -299,6 +357,22 @@ def preprocess(grid: np.ndarray) -> ReducedGraph:
         _lib.plse_graph_free(h)
 
 
+def to_grid(instance: np.ndarray, graph: "ReducedGraph", solution: np.ndarray) -> np.ndarray:
+    """coloring.hpp:171-183 -- the certificate: pre-filled symbols plus the solution's coloured cells."""
+    inst = np.ascontiguousarray(instance, np.uint16)
+    colors = np.ascontiguousarray(solution, np.uint16).reshape(-1)
+    if colors.size != graph.vertex_count:
+        raise ValueError("solution size differs from the graph's vertex count")
+    h = C.c_void_p()
+    _check(_lib.plse_preprocess(inst.shape[0], inst.reshape(-1), C.byref(h)))
+    try:
+        out = np.zeros(inst.size, np.uint16)
+        _check(_lib.plse_to_grid(h, colors, out))
+    finally:
+        _lib.plse_graph_free(h)
+    return out.reshape(inst.shape)
+
+
 # ------------------------------------------------------------------ config
 @dataclasses.dataclass
 class SolverConfig:
@@ -306,6 +380,7 @@ class SolverConfig:
     p: int = 12288
     alpha: float = 0.6
     phase1_iters: int = 0
+    phase2_iters: int = 0  # MPMA (PLITS) phase-2 budget, 0 -> 2|V|
     gamma: float = 10.0
     beta: float = 20.0
     crossover: int = AUX
@@ -322,6 +397,7 @@ class SolverConfig:
     disable_optimal_stop: bool = False
     target_score: float = 0.0
     race: bool = False  # with target_score: device-global early exit (time-to-target, not parity mode)
+    workers: int = 1  # reported in the result JSON (report.hpp:76); the device path uses one host thread
 
     def _params(self) -> _Params:
         return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,
@@ -346,7 +422,7 @@ class RunResult:
 
 
 def run(grid: np.ndarray, config: SolverConfig,
-        on_generation: Optional[Callable[[int, int, int, float, int], None]] = None) -> RunResult:
+        on_generation: Optional[Callable[["GenerationStats"], None]] = None) -> RunResult:
     """engine.hpp:114 -- the whole Partial-MPMA run on one B200."""
     grid = np.ascontiguousarray(grid, np.uint16)
     n = grid.shape[0]
@@ -357,15 +433,15 @@ def run(grid: np.ndarray, config: SolverConfig,
     best = np.zeros(n * n + 1, np.uint16)
     errors: List[BaseException] = []
 
-    def cb(gen, best_f, iters, elapsed, shortfall, _user):
+    def cb(stats_ptr, _user):
         if on_generation is None:
             return
         try:
-            on_generation(gen, best_f, iters, elapsed, shortfall)
+            on_generation(GenerationStats.from_buffer_copy(stats_ptr.contents))
         except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
             errors.append(e)
 
-    cfun = _GEN_CB(cb)
+    cfun = _GEN_CB(cb) if on_generation is not None else _GEN_CB()  # NULL: no per-generation stats work
     _check(_lib.plse_solve(n, grid.reshape(-1), C.byref(cfg), C.byref(res), best, cfun, None))
     if errors:
         raise errors[0]

@@ -24,6 +24,20 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// run()'s deadline on the device clock: now + remaining (engine.hpp:148-151)
+__global__ void k_set_deadline(unsigned long long* deadline, unsigned long long remaining_ns) {
+    *deadline = globaltimer_ns() + remaining_ns;
+}
+
+// sum of dist(i, j) over i < j (engine.hpp:222-225)
+__global__ void k_upper_sum(const uint16_t* __restrict__ d, int p, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (int i = blockIdx.x; i < p; i += gridDim.x)
+        for (int j = i + 1 + threadIdx.x; j < p; j += blockDim.x) s += d[(size_t)i * p + j];
+    for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -94,6 +108,8 @@ struct plse_ctx {
     unsigned long long* d_prof = nullptr;  // PLSE_PROFILE instrumentation counters
     int* d_race = nullptr;                 // race-mode flag (plse_solve with race)
     int race_f = -1;
+    unsigned long long* d_deadline = nullptr;  // %globaltimer deadline of plse_solve's time limit
+    unsigned long long* d_dsum = nullptr;      // GenerationStats::mean_distance reduction
     // pool update scratch
     int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
     uint32_t* d_conf = nullptr;
@@ -109,7 +125,7 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_conf_scratch, d_work, d_prof, d_race, d_colvert, d_hA, d_hB, d_order,
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_conf_scratch, d_work, d_prof, d_race, d_deadline, d_dsum, d_colvert, d_hA, d_hB, d_order,
                         d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -535,6 +551,7 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.prof = nullptr;
     a.race_flag = c->race_f >= 0 ? c->d_race : nullptr;
     a.race_f = c->race_f;
+    a.deadline = c->d_deadline;
     if (const char* env = std::getenv("PLSE_PROFILE")) {
         if (env[0] == '1') {
             if (!c->d_prof) c->d_prof = dalloc<unsigned long long>(16);
@@ -745,6 +762,33 @@ int plse_graph_view(const plse_graph_h* h, plse_graph* v) {
         v->dom = g.dom.data();
         v->n_prefilled = (int32_t)(g.prefilled.size() / 3);
         v->prefilled = g.prefilled.data();
+    });
+}
+
+int plse_to_grid(const plse_graph_h* h, const uint16_t* colors, uint16_t* grid) {
+    return guard(nullptr, [&] {
+        if (!h || !colors || !grid) throw std::invalid_argument("null argument");
+        auto g = plse_host::to_grid(h->g, colors);
+        std::memcpy(grid, g.data(), 2 * g.size());
+    });
+}
+
+int plse_verify_certificate(int32_t n, const uint16_t* instance, int32_t m, const uint16_t* certificate,
+                            int32_t* legal, int32_t* score, char* problems, int64_t problems_cap,
+                            int64_t* problems_len) {
+    return guard(nullptr, [&] {
+        if (!instance || !certificate || n <= 0 || m <= 0) throw std::invalid_argument("bad arguments");
+        auto r = plse_host::verify_certificate(n, instance, m, certificate);
+        std::string joined;
+        for (size_t i = 0; i < r.problems.size(); ++i) joined += (i ? "\n" : "") + r.problems[i];
+        if (legal) *legal = r.legal ? 1 : 0;
+        if (score) *score = r.score;
+        if (problems_len) *problems_len = (int64_t)joined.size();
+        if (problems && problems_cap > 0) {
+            const size_t k = std::min<size_t>(joined.size(), (size_t)(problems_cap - 1));
+            std::memcpy(problems, joined.data(), k);
+            problems[k] = 0;
+        }
     });
 }
 
@@ -1070,6 +1114,34 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
             CK(cudaMemset(c->d_race, 0, sizeof(int)));
             c->race_f = std::max(0, (int)std::floor((double)(n * n - g.l) - cfg->target_score));
         }
+        if (cfg->time_limit > 0) {
+            // partial.hpp:165: each search checks the deadline every 4096 steps
+            c->d_deadline = dalloc<unsigned long long>(1);
+            const double remaining = std::max(0.0, cfg->time_limit - elapsed());
+            k_set_deadline<<<1, 1, 0, c->st>>>(c->d_deadline, (unsigned long long)(remaining * 1e9));
+            CK(cudaGetLastError());
+        }
+        auto emit_stats = [&](int64_t gen, int shortfall) {
+            if (!cb) return;
+            plse_generation_stats st{};
+            st.generation = gen;
+            st.best_f = res->best_f;
+            double fs = 0;
+            for (int i = 0; i < p; ++i) fs += c->h_mf[i];
+            st.mean_f = fs / p;
+            if (!c->d_dsum) c->d_dsum = dalloc<unsigned long long>(1);
+            CK(cudaMemsetAsync(c->d_dsum, 0, 8, c->st));
+            k_upper_sum<<<std::min(p, 4 * 148), 256, 0, c->st>>>(c->d_dist, p, c->d_dsum);
+            CK(cudaGetLastError());
+            unsigned long long ds = 0;
+            CK(cudaMemcpyAsync(&ds, c->d_dsum, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            st.mean_distance = (double)ds / (0.5 * p * (p - 1));
+            st.iterations = res->total_iterations;
+            st.elapsed_seconds = elapsed();
+            st.shortfall = shortfall;
+            cb(&st, user);
+        };
         for (int64_t gen = 1;; ++gen) {
             int64_t it = 0;
             int32_t bf = 0, bi = -1;
@@ -1088,7 +1160,7 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
             const bool gens_up = cfg->generation_limit > 0 && gen >= cfg->generation_limit;
             const bool target = cfg->target_score > 0 && (n * n - g.l - res->best_f) >= cfg->target_score;
             if (optimal || time_up || iters_up || gens_up || target) {
-                if (cb) cb(gen, res->best_f, res->total_iterations, elapsed(), 0, user);
+                emit_stats(gen, 0);
                 finalize(optimal ? PLSE_STOP_OPTIMAL
                          : time_up ? PLSE_STOP_TIME
                          : iters_up ? PLSE_STOP_ITERS
@@ -1102,7 +1174,7 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
             update_impl(c, &pbf, &nsf, nullptr);
             if (c->prm.exclusion == PLSE_E_GENERATION) CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
             offspring_impl(c, (uint64_t)gen);
-            if (cb) cb(gen, res->best_f, res->total_iterations, elapsed(), nsf, user);
+            emit_stats(gen, nsf);
         }
     });
     delete ctx;

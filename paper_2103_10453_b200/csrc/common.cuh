@@ -40,6 +40,15 @@ __host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t master, uint64
 // murmur3 finaliser; the canonical tie-break draw of step j is
 //   h1 = fmix32(fold(s) + (j+1) * 0x9E3779B9), h2 = fmix32(h1 + 0x632BE5AB)
 // with fold(s) = lo32(s ^ (s >> 32)); h1 ranks the move, h2 the tenure offset.
+#ifdef __CUDACC__
+// %globaltimer (ns): the device clock the run's time limit is checked against
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 __host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
     h ^= h >> 16;
     h *= 0x85EBCA6Bu;

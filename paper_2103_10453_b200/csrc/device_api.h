@@ -48,6 +48,8 @@ struct ImproveArgs {
     // race mode (time-to-target): stop every search once any individual reaches best f <= race_f
     int* race_flag;             // nullptr = off
     int race_f;
+    // time limit (partial.hpp:165): after every 4096th step, stop once %globaltimer >= *deadline
+    const unsigned long long* deadline;  // nullptr = no limit
     // optional clock64 instrumentation (PLSE_PROFILE=1): 16 counters, see capi.cu
     unsigned long long* prof;
     // parity probe

@@ -4,6 +4,7 @@
 // for this library; exported through include/plse_b200.h.
 #include <cstring>
 #include <sstream>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -151,6 +152,62 @@ GraphH preprocess(int n, const uint16_t* grid) {
     }
     g.nv = static_cast<int>(g.cell_row.size());
     return g;
+}
+
+
+// coloring.hpp:171-183 to_grid: prefilled symbols plus the solution's
+// coloured cells (colours are symbols; 0 leaves the cell empty).
+std::vector<uint16_t> to_grid(const GraphH& g, const uint16_t* colors) {
+    std::vector<uint16_t> out(static_cast<size_t>(g.n) * g.n, 0);
+    for (size_t t = 0; t + 2 < g.prefilled.size(); t += 3)
+        out[g.prefilled[t] * g.n + g.prefilled[t + 1]] = static_cast<uint16_t>(g.prefilled[t + 2]);
+    for (int v = 0; v < g.nv; ++v) {
+        const int k = colors[v];
+        if (k == 0) continue;
+        // Coloring::assign (coloring.hpp:44-48) rejects colours outside the domain
+        if (!std::binary_search(g.dom.begin() + g.dom_off[v], g.dom.begin() + g.dom_off[v + 1], (uint16_t)k))
+            throw std::invalid_argument("assignment leaves vertex domain");
+        out[g.cell_row[v] * g.n + g.cell_col[v]] = static_cast<uint16_t>(k);
+    }
+    return out;
+}
+
+// verify.hpp:20-73: order, pre-filled cells, then row and column duplicates,
+// in that order and with the same wording.
+VerifyResult verify_certificate(int n, const uint16_t* inst, int m, const uint16_t* cert) {
+    VerifyResult r;
+    if (m != n) {
+        r.problems.push_back("order mismatch: instance " + std::to_string(n) + ", certificate " + std::to_string(m));
+        return r;
+    }
+    auto cell = [](int a, int b) { return "(" + std::to_string(a) + "," + std::to_string(b) + ")"; };
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            const int e = inst[a * n + b], got = cert[a * n + b];
+            if (e != 0 && got != e)
+                r.problems.push_back("pre-filled cell " + cell(a, b) + " altered: expected " + std::to_string(e) +
+                                     ", got " + std::to_string(got));
+        }
+    std::vector<int> first(static_cast<size_t>(n) + 1);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int line = 0; line < n; ++line) {
+            std::fill(first.begin(), first.end(), -1);
+            for (int t = 0; t < n; ++t) {
+                const int s = pass == 0 ? cert[line * n + t] : cert[t * n + line];
+                if (s == 0) continue;
+                if (s > n) throw std::invalid_argument("symbol out of range");
+                if (first[s] < 0) {
+                    first[s] = t;
+                    continue;
+                }
+                r.problems.push_back("duplicate symbol " + std::to_string(s) + (pass == 0 ? " in row " : " in column ") +
+                                     std::to_string(line) + (pass == 0 ? " at columns " : " at rows ") +
+                                     std::to_string(first[s]) + " and " + std::to_string(t));
+            }
+        }
+    for (int q = 0; q < n * n; ++q) r.score += cert[q] != 0;
+    r.legal = r.problems.empty();
+    return r;
 }
 
 }  // namespace plse_host

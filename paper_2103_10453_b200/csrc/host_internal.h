@@ -21,6 +21,14 @@ std::vector<uint16_t> generate_instance(int n, double r, uint64_t seed);
 std::vector<uint16_t> parse_instance(const std::string& text, int& n_out);
 GraphH preprocess(int n, const uint16_t* grid);
 
+struct VerifyResult {
+    bool legal = false;
+    int score = 0;
+    std::vector<std::string> problems;
+};
+std::vector<uint16_t> to_grid(const GraphH& g, const uint16_t* colors);
+VerifyResult verify_certificate(int n, const uint16_t* inst, int m, const uint16_t* cert);
+
 }  // namespace plse_host
 
 struct plse_graph_h {

@@ -188,6 +188,15 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     const double alpha = a.alpha;
     const int* race_flag = a.race_flag;
     const int race_f = a.race_f;
+    // partial.hpp:164-165: `++iterations; if ((iterations & 0xFFF) == 0 && deadline_passed) break;`
+    // lane 0 reads the clock so the whole warp takes the same decision
+    const unsigned long long* deadline = a.deadline;
+    // polled every 64 steps: the race flag, and the deadline at multiples of 4096
+    auto poll_stop = [race_flag, deadline](uint32_t jj) -> bool {
+        if (race_flag && *reinterpret_cast<const volatile int*>(race_flag)) return true;
+        if (!deadline || jj == 0 || (jj & 0xFFFu)) return false;
+        return __shfl_sync(kFull, globaltimer_ns() >= *deadline ? 1 : 0, 0) != 0;
+    };
 
     // step record of the parity probe
     auto trace_step = [&](uint32_t jj, int vs, int ks, int ur, int uc, int rs_, int cs_, int fb, int fa, int bf,
@@ -212,7 +221,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 
     for (;;) {
         if (!((int64_t)j < budget && bestf > stop_f && f > 0)) break;
-        if (race_flag && *reinterpret_cast<const volatile int*>(race_flag)) break;
+        if ((j & 63) == 0 && poll_stop(j)) break;
         const int f_before = f;
         const bool asp = (f == bestf);
         const uint32_t t = base + j;
@@ -415,8 +424,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                     trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
                 ++j;
-                if (!((int64_t)j < budget) || (race_flag && (j & 63) == 0 &&
-                                               *reinterpret_cast<const volatile int*>(race_flag)))
+                if (!((int64_t)j < budget) ||
+                    ((j & 63) == 0 && poll_stop(j)))
                     break;
                 continue;
             }
@@ -525,7 +534,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 ++pn_sparse;
             }
             if (!((int64_t)j < budget && bestf > stop_f)) break;
-            if (race_flag && (j & 63) == 0 && *reinterpret_cast<const volatile int*>(race_flag)) break;
+            if ((j & 63) == 0 && poll_stop(j)) break;
         }
     }
     if (pending) snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);

@@ -280,7 +280,11 @@ __global__ void __launch_bounds__(kHwMaxThreads, kHwMinBlocks) k_improve_hw(cons
         if (__ballot_sync(kFull, state == 2) == kFull) break;
         if (state != 1) continue;
 
-        const bool raced = a.race_flag && (j & 63) == 0 && *reinterpret_cast<volatile int*>(a.race_flag);
+        bool raced = a.race_flag && (j & 63) == 0 && *reinterpret_cast<volatile int*>(a.race_flag);
+        if (a.deadline && j != 0 && (j & 0xFFFu) == 0) {  // partial.hpp:165, decided by the half's lane 0
+            const int hit = hl == 0 ? (globaltimer_ns() >= *a.deadline) : 0;
+            raced |= __shfl_sync(hm, hit, 0, 16) != 0;
+        }
         if (raced || !((int64_t)j < a.budget && bestf > a.stop_f && f > 0)) {
             // ---------------------------------------------------------- finish the individual
             if (pending) half_snapshot<W>(col, a.improved + (size_t)i * nvpad, nvpad, hl);

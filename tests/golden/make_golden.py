@@ -112,6 +112,45 @@ def main():
         suite.append([n, seed & 0xFFFFFFFFFFFF, f, n * n - gr.l - f, gr.l])
         out[f"suite_{i}"] = gg
     out["suite"] = np.array(suite, np.int64)
+
+    # --- per-generation GenerationStats of a run (engine.hpp:214-233)
+    gg = out["run_inst_20"]
+    rr = R.run(gg, p=16, seed=7, generation_limit=5, workers=1, log_cap=8)
+    out["run_log_20"] = np.array([[e["generation"], e["best_f"], e["shortfall"], e["iterations"]]
+                                  for e in rr["log"]], np.int64)
+    out["run_log_20_means"] = np.array([[e["mean_f"], e["mean_distance"]] for e in rr["log"]], np.float64)
+
+    # --- certificates (coloring.hpp:171) and verify_certificate (verify.hpp:20)
+    rng = np.random.default_rng(171)
+    for n, r, s in [(10, 0.3, 606), (20, 0.7, 505)]:
+        g = out[f"inst_{n}_{r}_{s}"]
+        gr = R.preprocess(g)
+        cols = np.zeros(gr.nv, np.uint16)
+        for v in range(gr.nv):
+            d = gr.dom[gr.dom_off[v]:gr.dom_off[v + 1]]
+            cols[v] = d[rng.integers(0, len(d))]
+        cert = R.to_grid(g, cols)
+        out[f"cert_colors_{n}"] = cols
+        out[f"cert_grid_{n}"] = cert
+        for t, bad in enumerate([cert, g]):
+            legal, score, probs = R.verify_certificate(g, bad)
+            out[f"verify_{n}_{t}"] = np.frombuffer(("\n".join(probs)).encode() or b"\0", np.uint8)
+            out[f"verify_{n}_{t}_ls"] = np.array([legal, score], np.int64)
+        alt = cert.copy()
+        alt[np.nonzero(g)[0][0], np.nonzero(g)[1][0]] = 0
+        legal, score, probs = R.verify_certificate(g, alt)
+        out[f"verify_{n}_alt"] = np.frombuffer(("\n".join(probs)).encode(), np.uint8)
+        out[f"verify_{n}_alt_ls"] = np.array([legal, score], np.int64)
+
+    # --- result_to_json(...).dump(2) (report.hpp:85, plse.cpp:154)
+    if R.has_result_json():
+        res = dict(best_f=3, best_score=80, proven_optimal=0, l=2, upper_bound=83, vertex_count=50, generations=5,
+                   total_iterations=12345, elapsed_seconds=1.25)
+        out["json_a"] = np.frombuffer(R.result_json("instance.txt", 12, res, "generation_limit", 16, 0.6, 10.0, 20.0,
+                                                    0, 0, 0, 0, 0, 0, 31337, 2, 0.0, 0, 5).encode(), np.uint8)
+        out["json_b"] = np.frombuffer(R.result_json("QC-60-50-0.txt", 60, res, "time_limit", 12288, 0.35, 12.5,
+                                                    25.0, 1000, 7, 1, 1, 1, 2, 2**64 - 1, 144, 1e-3, 10**12, 0,
+                                                    True).encode(), np.uint8)
     path = os.path.join(HERE, "ref_golden.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes,", len(out), "arrays")

@@ -1,0 +1,107 @@
+"""§8(f) rank 2 on the GPU: the driver around the device kernels.
+
+* ``python -m paper_2103_10453_b200 solve`` twice with the same seed and flags writes
+  byte-identical JSON and certificates, and the certificate verifies (acceptance.cpp
+  criterion 8, plse.cpp:132-174);
+* the JSON's numbers are the canonical-tie oracle's run (engine.hpp:114-262);
+* per-generation GenerationStats (mean f, mean distance, shortfall, iterations) equal the
+  oracle's, which tests/test_report_cli.py pins to the reference;
+* the time limit is honoured inside the search the way partial.hpp:165 does it.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _cli(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2103_10453_b200", *args], capture_output=True, text=True,
+                          cwd=ROOT, timeout=900)
+
+
+def test_cli_solve_is_byte_identical_and_certified(plse, orc, tmp_path):
+    grid = orc.generate_instance(12, 0.6, 88)
+    inst = tmp_path / "instance.txt"
+    inst.write_text(plse.serialize_instance(grid))
+    outs = []
+    for tag in "ab":
+        r = _cli("solve", str(inst), "--seed", "31337", "--pop", "16", "--gen-limit", "5", "--workers", "2",
+                 "--variant", "partial", "--json", str(tmp_path / f"{tag}.json"), "--cert", str(tmp_path / f"{tag}.cert"))
+        assert r.returncode in (0, 2), r.stderr
+        outs.append(r.returncode)
+    assert outs[0] == outs[1]
+    ja, jb = (tmp_path / "a.json").read_bytes(), (tmp_path / "b.json").read_bytes()
+    ca, cb = (tmp_path / "a.cert").read_bytes(), (tmp_path / "b.cert").read_bytes()
+    assert ja and ja == jb
+    assert ca and ca == cb
+    cert = plse.parse_instance(ca.decode())
+    rep = plse.verify_certificate(grid, cert)
+    assert rep.legal, rep.problems
+    j = json.loads(ja)
+    o = orc.run(grid, p=16, seed=31337, generation_limit=5, tie=oracle.TIE_CANON)
+    for k, ok in [("best_score", "best_score"), ("f", "best_f"), ("generations", "generations"),
+                  ("total_iterations", "total_iterations"), ("l", "l"), ("upper_bound", "upper_bound"),
+                  ("vertices", "vertex_count"), ("stop_reason", "stop_reason")]:
+        assert j[k] == o[ok], k
+    assert rep.score == j["best_score"]
+    assert j["config"]["workers"] == 2 and j["config"]["variant"] == "partial" and j["instance"] == "instance.txt"
+    assert outs[0] == (0 if j["proven_optimal"] else 2)
+    # stdout form (no --json) is the same text
+    r = _cli("solve", str(inst), "--seed", "31337", "--pop", "16", "--gen-limit", "5", "--workers", "2",
+             "--variant", "partial")
+    assert r.stdout.encode() == ja
+    assert r.stderr.strip().startswith(f"score {j['best_score']}/{j['upper_bound']}")
+
+
+@pytest.mark.parametrize("n,r,s,p", [(20, 0.6, 9, 12), (30, 0.5, 4, 24)])
+def test_generation_stats_match_oracle(plse, orc, n, r, s, p):
+    grid = orc.generate_instance(n, r, s)
+    seen = []
+    res = plse.run(grid, plse.SolverConfig(p=p, master_seed=s, generation_limit=4, phase1_iters=400,
+                                           disable_optimal_stop=True), seen.append)
+    o = orc.run(grid, p=p, seed=s, generation_limit=4, phase1_iters=400, tie=oracle.TIE_CANON,
+                disable_optimal_stop=True, log_cap=8)
+    assert res.generations == o["generations"] and len(seen) == len(o["log"])
+    for st, e in zip(seen, o["log"]):
+        assert (st.generation, st.best_f, st.shortfall, st.iterations) == \
+            (e["generation"], e["best_f"], e["shortfall"], e["iterations"])
+        assert st.mean_f == e["mean_f"] and st.mean_distance == e["mean_distance"]
+        assert st.elapsed_seconds >= 0
+
+
+def test_time_limit_stops_inside_the_search(plse, orc):
+    """partial.hpp:165: with a huge phase-1 budget, the deadline ends the first generation;
+    every search stops at a multiple of 4096 steps (or at its target)."""
+    grid = orc.generate_instance(60, 0.5, 12345)
+    g = plse.preprocess(grid)
+    limit = 1.0
+    res = plse.run(grid, plse.SolverConfig(p=512, master_seed=1, phase1_iters=10**9, time_limit=limit))
+    assert res.stop_reason in ("time_limit", "optimal")
+    assert res.generations == 1
+    assert res.elapsed_seconds < limit + 5.0
+    if res.stop_reason == "time_limit":
+        assert res.total_iterations > 0
+        assert res.best_f >= 0 and res.best_score == 3600 - g.l - res.best_f
+
+
+def test_time_limit_iteration_accounting_matches_stride(plse, orc):
+    """Individuals that neither reach f = 0 nor exhaust the budget stop at j % 4096 == 0."""
+    grid = orc.generate_instance(60, 0.5, 12345)
+    g = plse.preprocess(grid)
+    cfg = plse.SolverConfig(p=256, master_seed=3, phase1_iters=10**9, time_limit=0.5)
+    seen = []
+    res = plse.run(grid, cfg, seen.append)
+    assert res.stop_reason in ("time_limit", "optimal")
+    if res.stop_reason == "time_limit":
+        # total = sum of per-individual counts; with no individual at f = 0 each is a multiple of 4096
+        if res.best_f > 0:
+            assert res.total_iterations % 4096 == 0
+        assert seen and seen[-1].iterations == res.total_iterations

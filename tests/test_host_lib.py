@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol(plse):
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.plse_abi_version() == 1
+    assert lib.plse_abi_version() == 2
 
 
 def test_oracle_library_is_not_linked_into_product(plse):
