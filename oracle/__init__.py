@@ -58,7 +58,7 @@ class OrConfig(C.Structure):
                 ("phase1_iters", C.c_int64), ("crossover", C.c_int32), ("matching", C.c_int32),
                 ("exclusion", C.c_int32), ("master_seed", C.c_uint64), ("iteration_limit", C.c_int64),
                 ("generation_limit", C.c_int64), ("tie_mode", C.c_int32),
-                ("disable_optimal_stop", C.c_int32)]
+                ("disable_optimal_stop", C.c_int32), ("variant", C.c_int32), ("phase2_iters", C.c_int64)]
 
 
 class OrResult(C.Structure):
@@ -71,6 +71,18 @@ class OrResult(C.Structure):
 class OrGenLog(C.Structure):
     _fields_ = [("generation", C.c_int64), ("best_f", C.c_int32), ("shortfall", C.c_int32),
                 ("iterations", C.c_int64), ("mean_f", C.c_double), ("mean_distance", C.c_double)]
+
+
+class OrPlitsStep(C.Structure):
+    _fields_ = [("step", C.c_int64), ("phase", C.c_int32), ("v", C.c_int32), ("k", C.c_int32),
+                ("from_", C.c_int32), ("df", C.c_int32), ("dc", C.c_int32), ("delta", C.c_int64),
+                ("cur_scaled", C.c_int64), ("best_scaled", C.c_int64), ("n_adm", C.c_int32),
+                ("tenure", C.c_int32), ("active", C.c_int32), ("f", C.c_int32), ("c", C.c_int32)]
+
+
+class OrPlitsStats(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("phase1_iterations", C.c_int64), ("hit_target", C.c_int32),
+                ("repaired", C.c_int32), ("final_f", C.c_int32), ("alg_bytes", C.c_double)]
 
 
 class RefRunResult(C.Structure):
@@ -133,6 +145,8 @@ class Oracle:
         L.or_eval.argtypes = [C.c_void_p, u16p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_gamma_build.argtypes = [C.c_void_p, u16p, i32p]
         L.or_repair.argtypes = [C.c_void_p, u16p]
+        L.or_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                               C.c_int, C.POINTER(OrPlitsStats), C.c_void_p, C.c_int64]
         L.or_improve.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int,
                                  C.c_int, C.POINTER(OrImproveStats), C.c_void_p, C.c_int64]
         L.or_cross_distances.argtypes = [C.c_int, C.c_int, u16p, u16p, i32p, i32p]
@@ -212,6 +226,23 @@ class Oracle:
             res["trace"] = [{k: getattr(tr[i], k) for k, _ in OrStep._fields_} for i in range(m)]
         return res
 
+    def plits(self, grid, colors, stream_seed, iters1=0, iters2=0, alpha=0.6, stop_f=0, tie=TIE_CANON,
+              trace_cap=0):
+        """plits.hpp:276 plits_run"""
+        nv = len(colors)
+        out = np.zeros(max(nv, 1), np.uint16)
+        st = OrPlitsStats()
+        tr = (OrPlitsStep * trace_cap)() if trace_cap else None
+        self.lib.or_plits(self._h(grid), np.ascontiguousarray(colors, np.uint16), out, stream_seed, iters1, iters2,
+                          alpha, stop_f, tie, C.byref(st), C.cast(tr, C.c_void_p) if tr is not None else None,
+                          trace_cap)
+        res = {k: getattr(st, k) for k, _ in OrPlitsStats._fields_}
+        res["best"] = out[:nv]
+        if tr is not None:
+            m = min(trace_cap, st.iterations)
+            res["trace"] = [{k: getattr(tr[i], k) for k, _ in OrPlitsStep._fields_} for i in range(m)]
+        return res
+
     # -- population phases
     def cross_distances(self, members, improved):
         p, nv = members.shape
@@ -268,11 +299,11 @@ class Oracle:
 
     def run(self, grid, p=64, alpha=0.6, gamma=10.0, beta=20.0, phase1_iters=0, crossover=X_AUX,
             matching=M_NEAREST, exclusion=E_RUN, seed=0, iteration_limit=0, generation_limit=0,
-            tie=TIE_CANON, disable_optimal_stop=False, log_cap=0):
+            tie=TIE_CANON, disable_optimal_stop=False, log_cap=0, variant=1, phase2_iters=0):
         grid = np.ascontiguousarray(grid, np.uint16)
         n = grid.shape[0]
         cfg = OrConfig(p, alpha, gamma, beta, phase1_iters, crossover, matching, exclusion, seed,
-                       iteration_limit, generation_limit, tie, int(disable_optimal_stop))
+                       iteration_limit, generation_limit, tie, int(disable_optimal_stop), variant, phase2_iters)
         res = OrResult()
         best = np.zeros(n * n + 1, np.uint16)
         log = (OrGenLog * log_cap)() if log_cap else None
@@ -323,13 +354,19 @@ class Reference:
                                     C.c_void_p, C.c_uint64, C.c_uint64, u16p]
         L.ref_init_population.argtypes = [C.c_void_p, C.c_int, C.c_uint64, u16p, C.c_void_p]
         L.ref_solve_exact.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
-        L.ref_run.argtypes = [C.c_int, u16p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int,
+        L.ref_run.argtypes = [C.c_int, u16p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64,
+                              C.c_int,
                               C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int64, C.c_int64,
                               C.POINTER(RefRunResult), u16p]
         L.ref_improve_phase.restype = C.c_int64
         L.ref_improve_phase.argtypes = [C.c_void_p, C.c_int, u16p, C.c_void_p, C.c_uint64, C.c_uint64,
                                         C.c_int64, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_default_workers.restype = C.c_int
+        L.ref_plits.restype = C.c_int64
+        L.ref_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int]
+        L.ref_plits_trace.restype = C.c_int64
+        L.ref_plits_trace.argtypes = [C.c_void_p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                      i32p, np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"), C.c_int64, u16p]
         L.ref_set_log.argtypes = [C.c_void_p, C.c_int64]
         L.ref_log_count.restype = C.c_int64
         L.ref_verify_certificate.argtypes = [C.c_int, u16p, C.c_int, u16p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
@@ -441,6 +478,7 @@ class Reference:
         return f, bool(ex.value)
 
     def run(self, grid, p=64, alpha=0.6, gamma=10.0, beta=20.0, phase1_iters=0, variant=1, crossover=X_AUX,
+            phase2_iters=0,
             matching=M_NEAREST, exclusion=E_RUN, seed=0, workers=1, time_limit=0.0, iteration_limit=0,
             generation_limit=0, log_cap=0):
         grid = np.ascontiguousarray(grid, np.uint16)
@@ -450,7 +488,7 @@ class Reference:
         log = (OrGenLog * log_cap)() if log_cap else None  # same layout as ref_gen_log
         self.lib.ref_set_log(C.cast(log, C.c_void_p) if log is not None else None, log_cap)
         try:
-            self.lib.ref_run(n, grid.reshape(-1), p, alpha, gamma, beta, phase1_iters, variant, crossover,
+            self.lib.ref_run(n, grid.reshape(-1), p, alpha, gamma, beta, phase1_iters, phase2_iters, variant, crossover,
                              matching, exclusion, seed, workers, time_limit, iteration_limit, generation_limit,
                              C.byref(res), best)
             n_log = self.lib.ref_log_count()
@@ -473,6 +511,25 @@ class Reference:
 
     def default_workers(self):
         return self.lib.ref_default_workers()
+
+    def plits(self, grid, colors, stream_seed, iters1=0, iters2=0, alpha=0.6, stop_f=0):
+        """plits.hpp:276 plits_run -> (coloring, iterations)"""
+        nv = len(colors)
+        out = np.zeros(max(nv, 1), np.uint16)
+        it = self.lib.ref_plits(self._h(grid), np.ascontiguousarray(colors, np.uint16), out, stream_seed, iters1,
+                                iters2, alpha, stop_f)
+        return out[:nv], it
+
+    def plits_trace(self, grid, colors, stream_seed, iters1=0, iters2=0, alpha=0.6, stop_f=0, cap=100000):
+        """per-step (phase, v, to, df, dc, f, c), best_scaled, final coloring"""
+        nv = len(colors)
+        rec = np.zeros(7 * cap, np.int32)
+        bs = np.zeros(cap, np.int64)
+        out = np.zeros(max(nv, 1), np.uint16)
+        n = self.lib.ref_plits_trace(self._h(grid), np.ascontiguousarray(colors, np.uint16), stream_seed, iters1,
+                                     iters2, alpha, stop_f, rec, bs, cap, out)
+        m = min(n, cap)
+        return rec[:7 * m].reshape(m, 7), bs[:m], out[:nv], n
 
     def verify_certificate(self, instance, certificate):
         """verify.hpp:20 -> (legal, score, problems)"""

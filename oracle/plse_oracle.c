@@ -609,6 +609,254 @@ int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uin
     return 0;
 }
 
+
+/* ----------------------------------------------------------------- plits */
+
+typedef struct {
+    const or_graph* g;
+    state s;
+    indexset un, cf;   /* uncoloured / conflicting sets (plits.hpp:74-75), REF iteration order */
+    int64_t* until;    /* phase-local tabu clock: until > j <=> tabu at step j */
+    int64_t wf, wc;
+} plits_phase_state;
+
+/* plits.hpp:193-212 update_membership_around */
+static void plits_membership(plits_phase_state* ps, int v, int from, int to) {
+    const or_graph* g = ps->g;
+    const int w = ps->s.w;
+    if (from == 0) is_erase(&ps->un, v);
+    if (to == 0) {
+        is_insert(&ps->un, v);
+        is_erase(&ps->cf, v);
+    } else if (ps->s.gamma[(size_t)v * w + to] > 0) {
+        is_insert(&ps->cf, v);
+    } else {
+        is_erase(&ps->cf, v);
+    }
+    for (int a = g->adj_off[v]; a < g->adj_off[v + 1]; ++a) {
+        const int u = g->adj[a];
+        const int cu = ps->s.col[u];
+        if (cu == 0 || (cu != from && cu != to)) continue;
+        if (ps->s.gamma[(size_t)u * w + cu] > 0)
+            is_insert(&ps->cf, u);
+        else
+            is_erase(&ps->cf, u);
+    }
+}
+
+/* plits.hpp:255-270 detail::run_phase with PlitsSearch (96-191) inlined.
+ * col is the phase input and receives search.best(). Returns hit_target. */
+static int plits_phase(const or_graph* g, uint16_t* col, int phase, int64_t wf, int64_t wc, int64_t budget,
+                       double alpha, int stop_f, int tie_mode, or_rng* rng, uint64_t seed, int64_t* J,
+                       int64_t* iters, double* bytes, or_plits_step* trace, int64_t trace_cap) {
+    const int nv = g->nv;
+    plits_phase_state ps;
+    ps.g = g;
+    ps.wf = wf;
+    ps.wc = wc;
+    state_init(&ps.s, g, col);
+    const int w = ps.s.w;
+    ps.un.pos = (int32_t*)malloc(sizeof(int32_t) * (nv + 1));
+    ps.un.el = (int32_t*)malloc(sizeof(int32_t) * (nv + 1));
+    ps.cf.pos = (int32_t*)malloc(sizeof(int32_t) * (nv + 1));
+    ps.cf.el = (int32_t*)malloc(sizeof(int32_t) * (nv + 1));
+    ps.un.size = ps.cf.size = 0;
+    for (int v = 0; v < nv; ++v) ps.un.pos[v] = ps.cf.pos[v] = -1;
+    /* plits.hpp:109-115 */
+    for (int v = 0; v < nv; ++v) {
+        const int k = ps.s.col[v];
+        if (k == 0)
+            is_insert(&ps.un, v);
+        else if (ps.s.gamma[(size_t)v * w + k] > 0)
+            is_insert(&ps.cf, v);
+    }
+    /* fresh tabu per phase == PlitsScratch::prepare's skip_past(16 + 2|V|) (plits.hpp:81)
+       whenever every tenure 9 + alpha*active stays below 17 + 2|V| (alpha < 2) */
+    ps.until = (int64_t*)calloc((size_t)nv * w + 1, sizeof(int64_t));
+    uint16_t* best = (uint16_t*)malloc(sizeof(uint16_t) * (nv + 1));
+    memcpy(best, ps.s.col, sizeof(uint16_t) * nv);
+    int best_f = ps.s.f, best_c = ps.s.c;
+    int64_t best_scaled = wf * ps.s.f + wc * ps.s.c;
+    int64_t it = 0;
+    int hit = 0;
+    while (it < budget) {
+        if (best_c == 0 && best_f <= stop_f) {
+            hit = 1;
+            break;
+        }
+        if (ps.un.size == 0 && ps.cf.size == 0) break; /* StepResult::Exhausted, not counted */
+        const int64_t j = it;                           /* tabu clock of this step's scan */
+        const int64_t cur_scaled = wf * ps.s.f + wc * ps.s.c;
+        int bv = -1, bk = 0, bdf = 0, bdc = 0;
+        int64_t bd = 0;
+        int64_t nadm = 0;
+        uint64_t x = 0;
+        double bt = 2.0 * w * (ps.un.size + ps.cf.size);
+        if (tie_mode == OR_TIE_REF) {
+            /* plits.hpp:135-176: uncoloured set, then conflicting set, each in IndexSet order */
+            uint64_t ties = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                const indexset* set = pass == 0 ? &ps.un : &ps.cf;
+                for (int idx = 0; idx < set->size; ++idx) {
+                    const int v = set->el[idx];
+                    const int cur = ps.s.col[v];
+                    const int32_t* row = ps.s.gamma + (size_t)v * w;
+                    for (int a = g->dom_off[v]; a < g->dom_off[v + 1]; ++a) {
+                        const int k = g->dom[a];
+                        if (pass == 0 ? (k == 0) : (k == cur)) continue;
+                        const int df = (k == 0) - (cur == 0);
+                        const int dc = (k ? row[k] : 0) - (cur ? row[cur] : 0);
+                        const int64_t d = wf * df + wc * dc;
+                        if (bv >= 0 && d > bd) continue;
+                        if (ps.until[(size_t)v * w + k] > j && cur_scaled + d >= best_scaled) continue;
+                        if (bv < 0 || d < bd) {
+                            bv = v, bk = k, bdf = df, bdc = dc, bd = d;
+                            ties = 1;
+                        } else if (or_rng_below(rng, ++ties) == 0) {
+                            bv = v, bk = k, bdf = df, bdc = dc;
+                        }
+                    }
+                }
+            }
+            nadm = (int64_t)ties;
+        } else {
+            /* canonical rule: minimum admissible delta, count N, the r-th in ascending (v, k) */
+            int64_t dmin = INT64_MAX;
+            for (int pass = 0; pass < 2; ++pass) {
+                int64_t r = 0;
+                if (pass == 1) {
+                    if (nadm == 0) break;
+                    x = or_canon_draw(seed, (uint64_t)*J);
+                    r = (int64_t)(((x >> 32) * (uint64_t)nadm) >> 32);
+                }
+                for (int v = 0; v < nv && bv < 0; ++v) {
+                    const int cur = ps.s.col[v];
+                    const int32_t* row = ps.s.gamma + (size_t)v * w;
+                    if (cur != 0 && row[cur] == 0) continue; /* not in the neighbourhood (plits.hpp:47-63) */
+                    for (int a = g->dom_off[v]; a < g->dom_off[v + 1]; ++a) {
+                        const int k = g->dom[a];
+                        if (k == cur) continue;
+                        const int df = (k == 0) - (cur == 0);
+                        const int dc = (k ? row[k] : 0) - (cur ? row[cur] : 0);
+                        const int64_t d = wf * df + wc * dc;
+                        if (ps.until[(size_t)v * w + k] > j && cur_scaled + d >= best_scaled) continue;
+                        if (pass == 0) {
+                            if (d < dmin) {
+                                dmin = d;
+                                nadm = 1;
+                            } else if (d == dmin) {
+                                ++nadm;
+                            }
+                        } else if (d == dmin) {
+                            if (r == 0) {
+                                bv = v, bk = k, bdf = df, bdc = dc, bd = d;
+                                break;
+                            }
+                            --r;
+                        }
+                    }
+                }
+            }
+        }
+        /* tick (plits.hpp:178): the next scan uses clock j+1 */
+        or_plits_step rec;
+        memset(&rec, 0, sizeof(rec));
+        rec.step = *J;
+        rec.phase = phase;
+        rec.v = bv;
+        rec.k = bk;
+        rec.from = bv >= 0 ? ps.s.col[bv] : 0;
+        rec.n_adm = (int32_t)nadm;
+        rec.tenure = -1;
+        if (bv >= 0) {
+            const int from = ps.s.col[bv];
+            apply_move(&ps.s, bv, bk);
+            plits_membership(&ps, bv, from, bk);
+            const uint64_t active = (uint64_t)ps.un.size + (uint64_t)ps.cf.size;
+            const uint64_t lpart = (tie_mode == OR_TIE_REF) ? or_rng_below(rng, 10)
+                                                            : (((uint64_t)(uint32_t)x * 10ULL) >> 32);
+            const uint64_t tenure = lpart + (uint64_t)(alpha * (double)active);
+            ps.until[(size_t)bv * w + from] = j + 1 + (int64_t)tenure;
+            const int64_t now = cur_scaled + bd;
+            bt += 4.0 * (g->adj_off[bv + 1] - g->adj_off[bv]) + 2.0;
+            if (now < best_scaled) {
+                best_scaled = now;
+                memcpy(best, ps.s.col, sizeof(uint16_t) * nv);
+                best_f = ps.s.f;
+                best_c = ps.s.c;
+                bt += 2.0 * nv;
+            }
+            rec.df = bdf;
+            rec.dc = bdc;
+            rec.delta = bd;
+            rec.tenure = (int32_t)tenure;
+        }
+        rec.cur_scaled = wf * ps.s.f + wc * ps.s.c;
+        rec.best_scaled = best_scaled;
+        rec.active = ps.un.size + ps.cf.size;
+        rec.f = ps.s.f;
+        rec.c = ps.s.c;
+        if (trace && *J < trace_cap) trace[*J] = rec;
+        *bytes += bt;
+        ++it;
+        ++*J;
+    }
+    if (best_c == 0 && best_f <= stop_f) hit = 1;
+    memcpy(col, best, sizeof(uint16_t) * nv);
+    *iters += it;
+    free(best);
+    free(ps.until);
+    free(ps.un.pos);
+    free(ps.un.el);
+    free(ps.cf.pos);
+    free(ps.cf.el);
+    state_free(&ps.s);
+    return hit;
+}
+
+/* plits.hpp:276-292 plits_run */
+int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
+             int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
+             or_plits_step* trace, int64_t trace_cap) {
+    const int nv = g->nv;
+    or_plits_stats z;
+    memset(&z, 0, sizeof(z));
+    if (nv == 0) {
+        if (st) *st = z;
+        return 0;
+    }
+    if (iters1 <= 0) iters1 = 100LL * nv;
+    if (iters2 <= 0) iters2 = 2LL * nv;
+    uint16_t* col = (uint16_t*)malloc(sizeof(uint16_t) * (nv + 1));
+    memcpy(col, input, sizeof(uint16_t) * nv);
+    or_rng rng;
+    or_rng_seed(&rng, stream_seed);
+    int64_t J = 0, iters = 0;
+    double bytes = 0;
+    const int done = plits_phase(g, col, 1, 2, 1, iters1, alpha, stop_f, tie_mode, &rng, stream_seed, &J, &iters,
+                                 &bytes, trace, trace_cap);
+    z.phase1_iterations = iters;
+    z.hit_target = done;
+    if (!done)
+        plits_phase(g, col, 2, 2, 2LL * nv, iters2, alpha, stop_f, tie_mode, &rng, stream_seed, &J, &iters, &bytes,
+                    trace, trace_cap);
+    int f, c;
+    or_eval(g, col, &f, &c);
+    if (c > 0) {
+        or_repair(g, col);
+        or_eval(g, col, &f, &c);
+        z.repaired = 1;
+        bytes += 2.0 * nv;
+    }
+    memcpy(out, col, sizeof(uint16_t) * nv);
+    z.iterations = iters;
+    z.final_f = f;
+    z.alg_bytes = bytes;
+    if (st) *st = z;
+    free(col);
+    return 0;
+}
+
 /* ----------------------------------------------------------- population */
 
 /* population.hpp:41-61 */
@@ -881,11 +1129,18 @@ int or_run(int n, const uint16_t* grid, const or_config* cfg, or_result* res, ui
         int64_t nlog = 0;
         for (int64_t gen = 1;; ++gen) {
             for (int i = 0; i < p; ++i) {
-                or_improve_stats st;
-                or_improve(g, offspring + (size_t)i * nv, improved + (size_t)i * nv,
-                           or_derive_seed(cfg->master_seed, 2, (uint64_t)gen * p + i), budget, cfg->alpha,
-                           target_f, cfg->tie_mode, &st, NULL, 0);
-                res->total_iterations += st.iterations;
+                const uint64_t sd = or_derive_seed(cfg->master_seed, 2, (uint64_t)gen * p + i);
+                if (cfg->variant == 0) {
+                    or_plits_stats ps;
+                    or_plits(g, offspring + (size_t)i * nv, improved + (size_t)i * nv, sd, cfg->phase1_iters,
+                             cfg->phase2_iters, cfg->alpha, target_f, cfg->tie_mode, &ps, NULL, 0);
+                    res->total_iterations += ps.iterations;
+                } else {
+                    or_improve_stats st;
+                    or_improve(g, offspring + (size_t)i * nv, improved + (size_t)i * nv, sd, budget, cfg->alpha,
+                               target_f, cfg->tie_mode, &st, NULL, 0);
+                    res->total_iterations += st.iterations;
+                }
             }
             res->generations = gen;
             for (int i = 0; i < p; ++i) {

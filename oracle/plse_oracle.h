@@ -111,6 +111,40 @@ int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uin
                int64_t budget, double alpha, int stop_f, int tie_mode, or_improve_stats* st,
                or_step* trace, int64_t trace_cap);
 
+/* ---- plits.hpp:96-292 (the MPMA variant's improve operator) ------------ */
+typedef struct {
+    int64_t step;       /* 0-based step index over both phases (the CANON draw key) */
+    int32_t phase;      /* 1 or 2 */
+    int32_t v, k, from; /* chosen move; v = -1 on an all-tabu step */
+    int32_t df, dc;
+    int64_t delta;      /* wf*df + wc*dc */
+    int64_t cur_scaled, best_scaled; /* after the step */
+    int32_t n_adm;      /* CANON: admissible candidates at the minimum; REF: ties */
+    int32_t tenure;     /* -1 on an all-tabu step */
+    int32_t active;     /* |uncoloured| + |conflicting| after the step */
+    int32_t f, c;       /* after the step */
+} or_plits_step;
+
+typedef struct {
+    int64_t iterations;        /* both phases (SearchStats::iterations) */
+    int64_t phase1_iterations;
+    int32_t hit_target;        /* phase 1 reached a legal best with f <= stop_f */
+    int32_t repaired;          /* the final greedy repair ran (phase 2 ended illegal) */
+    int32_t final_f;           /* f of the returned (legal) colouring */
+    double alg_bytes;          /* DESIGN.md "PLITS" byte model */
+} or_plits_stats;
+
+/* plits_run(scratch, input, Rng(stream_seed), {iters1, iters2, alpha, stop_f}, &stats):
+ * phase 1 (phi = 0.5: 2F = 2f + c) then, unless it hit the target, phase 2
+ * (phi = |V|: 2F = 2f + 2|V|c) from phase 1's best with a fresh tabu table,
+ * then the greedy repair if the result still conflicts.  iters <= 0 take the
+ * defaults 100|V| and 2|V| (plits.hpp:243-244).  OR_TIE_REF = the reference's
+ * reservoir sampling over IndexSet order; OR_TIE_CANON = the GPU's rule, with
+ * the draw keyed by the step index over both phases. */
+int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
+             int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
+             or_plits_step* trace, int64_t trace_cap);
+
 /* ---- population.hpp:41-228, crossover.hpp:26-104, engine.hpp:88-106 --- */
 void or_cross_distances(int nv, int p, const uint16_t* members, const uint16_t* improved,
                         int32_t* cross, int32_t* fresh);
@@ -140,6 +174,8 @@ typedef struct {
     int64_t iteration_limit, generation_limit;
     int32_t tie_mode;
     int32_t disable_optimal_stop; /* harness flag */
+    int32_t variant;              /* 0 = MPMA (PLITS improve), 1 = Partial-MPMA (engine.hpp:193-203) */
+    int64_t phase2_iters;         /* MPMA phase-2 budget, 0 -> 2|V| */
 } or_config;
 
 typedef struct {

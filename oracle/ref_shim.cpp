@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "plse/engine.hpp"
+#include "plse/plits.hpp"
 #if __has_include(<json.hpp>)
 #include "plse/report.hpp"
 #define PLSE_REF_HAVE_JSON 1
@@ -140,6 +141,72 @@ int64_t ref_improve_states(const ref_graph* h, const uint16_t* input, uint64_t s
     return t;
 }
 
+// plits.hpp:276 plits_run(scratch, input, Rng(stream_seed), params, &stats).  A scratch is
+// reused across calls on the same thread, as engine.hpp:176 does per worker.
+int64_t ref_plits(const ref_graph* h, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
+                  int64_t iters2, double alpha, int stop_f) {
+    thread_local PlitsScratch scratch;
+    Rng rng(stream_seed);
+    PlitsParams params;
+    params.phase1_iters = iters1;
+    params.phase2_iters = iters2;
+    params.alpha = alpha;
+    params.stop_f = stop_f;
+    SearchStats stats;
+    Coloring res = plits_run(scratch, make(h->g, input), rng, params, &stats);
+    std::memcpy(out, res.colors().data(), sizeof(uint16_t) * h->g.vertex_count());
+    return stats.iterations;
+}
+
+// plits_run's two phases (plits.hpp:255-292) driven step by step through
+// PlitsSearch::step(&applied), recording every step: (phase, v, to, df, dc,
+// current f, c, best_scaled).  Returns the number of steps recorded.
+int64_t ref_plits_trace(const ref_graph* h, const uint16_t* input, uint64_t stream_seed, int64_t iters1,
+                        int64_t iters2, double alpha, int stop_f, int32_t* rec /* 7 per step */,
+                        int64_t* best_scaled, int64_t cap, uint16_t* out) {
+    const int nv = h->g.vertex_count();
+    PlitsScratch scratch;
+    Rng rng(stream_seed);
+    Coloring col = make(h->g, input);
+    if (iters1 <= 0) iters1 = phase1_default(nv);
+    if (iters2 <= 0) iters2 = phase2_default(nv);
+    int64_t n = 0;
+    auto phase = [&](int ph, PhaseWeights w, int64_t budget) {
+        PlitsSearch search(scratch, col, w, rng, alpha);
+        int64_t it = 0;
+        bool hit = false;
+        while (it < budget) {
+            if (search.best().legal() && search.best().f() <= stop_f) {
+                hit = true;
+                break;
+            }
+            CandidateMove m;
+            const StepResult r = search.step(&m);
+            if (r == StepResult::Exhausted) break;
+            if (n < cap) {
+                int32_t* q = rec + 7 * n;
+                q[0] = ph;
+                q[1] = r == StepResult::Moved ? m.v : -1;
+                q[2] = r == StepResult::Moved ? m.to : 0;
+                q[3] = r == StepResult::Moved ? m.df : 0;
+                q[4] = r == StepResult::Moved ? m.dc : 0;
+                q[5] = search.current().f();
+                q[6] = search.current().c();
+                best_scaled[n] = search.best_scaled();
+            }
+            ++n;
+            ++it;
+        }
+        hit = hit || (search.best().legal() && search.best().f() <= stop_f);
+        col = search.best();
+        return hit;
+    };
+    if (!phase(1, PhaseWeights::from_phi(0.5), iters1)) phase(2, PhaseWeights::from_phi((double)nv), iters2);
+    if (!col.legal()) col = repair(std::move(col));
+    std::memcpy(out, col.colors().data(), sizeof(uint16_t) * nv);
+    return n;
+}
+
 // population.hpp:41 compute_cross_distances
 void ref_cross_distances(const ref_graph* h, int p, const uint16_t* members, const uint16_t* improved,
                          int32_t* cross, int32_t* fresh) {
@@ -255,7 +322,7 @@ struct ref_run_result {
 
 // engine.hpp:114 run(), Partial-MPMA or MPMA, optional limits
 int ref_run(int n, const uint16_t* grid, int p, double alpha, double gamma, double beta, int64_t phase1,
-            int variant, int crossover, int matching, int exclusion, uint64_t seed, int workers,
+            int64_t phase2, int variant, int crossover, int matching, int exclusion, uint64_t seed, int workers,
             double time_limit, int64_t iteration_limit, int64_t generation_limit, ref_run_result* out,
             uint16_t* best_colors) {
     SolverConfig cfg;
@@ -264,6 +331,7 @@ int ref_run(int n, const uint16_t* grid, int p, double alpha, double gamma, doub
     cfg.gamma = gamma;
     cfg.crossover.beta = beta;
     cfg.phase1_iters = phase1;
+    cfg.phase2_iters = phase2;
     cfg.variant = variant == 1 ? Variant::PartialMPMA : Variant::MPMA;
     cfg.crossover.mode = crossover == 0 ? CrossoverMode::AUX : crossover == 1 ? CrossoverMode::UX : CrossoverMode::None;
     cfg.crossover.matching = matching == 0 ? MatchingStrategy::NearestNeighbor : MatchingStrategy::Random;

@@ -151,6 +151,30 @@ def main():
         out["json_b"] = np.frombuffer(R.result_json("QC-60-50-0.txt", 60, res, "time_limit", 12288, 0.35, 12.5,
                                                     25.0, 1000, 7, 1, 1, 1, 2, 2**64 - 1, 144, 1e-3, 10**12, 0,
                                                     True).encode(), np.uint8)
+
+    # --- PLITS (plits.hpp:276) and the MPMA run (engine.hpp:193-197)
+    rng = np.random.default_rng(276)
+    for tag, (n, r, s) in enumerate([(8, 0.4, 17), (12, 0.5, 606), (20, 0.6, 505), (9, 0.3, 3)]):
+        g = R.generate_instance(n, r, s)
+        gr = R.preprocess(g)
+        cols = np.array([gr.dom[gr.dom_off[v] + 1 + rng.integers(0, gr.dom_off[v + 1] - gr.dom_off[v] - 1)]
+                         for v in range(gr.nv)], np.uint16)
+        seed = int(rng.integers(0, 2**62))
+        i1, i2 = [(0, 0), (300, 10), (2000, 0), (50, 5)][tag]
+        stop = 1 if gr.l == 1 else 0
+        res, its = R.plits(g, cols, seed, i1, i2, 0.6, stop)
+        out[f"plits_grid_{tag}"] = g
+        out[f"plits_in_{tag}"] = cols
+        out[f"plits_out_{tag}"] = res
+        out[f"plits_meta_{tag}"] = np.array([seed, i1, i2, stop, its], np.int64)
+    mruns = []
+    for n, r, s, pp in [(10, 0.5, 3, 8), (20, 0.6, 9, 12)]:
+        g = R.generate_instance(n, r, s)
+        rr = R.run(g, p=pp, seed=s, generation_limit=4, phase1_iters=400, variant=0, workers=1)
+        out[f"mpma_inst_{n}"] = g
+        out[f"mpma_best_{n}"] = rr["best_colors"]
+        mruns.append([n, pp, s, rr["best_f"], rr["total_iterations"], rr["generations"]])
+    out["mpma_runs"] = np.array(mruns, np.int64)
     path = os.path.join(HERE, "ref_golden.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes,", len(out), "arrays")
