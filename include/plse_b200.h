@@ -95,6 +95,8 @@ typedef struct {
     uint64_t master_seed;
     int64_t p_total;        /* stream index space: gen*p_total + offset + i; 0 -> p */
     int64_t offset;         /* first global individual of this shard */
+    int32_t variant;        /* PLSE_V_PARTIAL (PartialCol improve) or PLSE_V_MPMA (PLITS improve, plits.hpp) */
+    int64_t phase2_iters;   /* MPMA phase-2 budget, 0 -> 2|V| (plits.hpp:244) */
 } plse_params;
 
 /* One PartialCol step, for the per-step parity probe (partial.hpp:92-143). */
@@ -131,7 +133,7 @@ typedef struct {
 /* SolverConfig + RunLimits for plse_solve */
 typedef struct {
     plse_params params;
-    int32_t variant;            /* PLSE_V_PARTIAL (MPMA/PLITS -> PLSE_ERR_UNSUPPORTED) */
+    int32_t variant;            /* PLSE_V_PARTIAL or PLSE_V_MPMA (overrides params.variant) */
     double time_limit;          /* seconds, 0 = unlimited */
     int64_t iteration_limit;    /* 0 = unlimited */
     int64_t generation_limit;   /* 0 = unlimited */

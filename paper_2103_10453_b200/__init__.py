@@ -74,7 +74,7 @@ class _Params(C.Structure):
     _fields_ = [("p", C.c_int32), ("alpha", C.c_double), ("gamma", C.c_double), ("beta", C.c_double),
                 ("phase1_iters", C.c_int64), ("crossover", C.c_int32), ("matching", C.c_int32),
                 ("exclusion", C.c_int32), ("tie_mode", C.c_int32), ("master_seed", C.c_uint64),
-                ("p_total", C.c_int64), ("offset", C.c_int64)]
+                ("p_total", C.c_int64), ("offset", C.c_int64), ("variant", C.c_int32), ("phase2_iters", C.c_int64)]
 
 
 class Step(C.Structure):
@@ -401,7 +401,8 @@ class SolverConfig:
 
     def _params(self) -> _Params:
         return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,
-                       self.exclusion, 0, self.master_seed & (2**64 - 1), self.p_total, self.offset)
+                       self.exclusion, 0, self.master_seed & (2**64 - 1), self.p_total, self.offset, self.variant,
+                       self.phase2_iters)
 
 
 @dataclasses.dataclass

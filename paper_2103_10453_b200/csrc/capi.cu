@@ -102,6 +102,8 @@ struct plse_ctx {
     size_t rec_stride = 0, until_stride = 0;
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
     bool half_warp = false;  // k_improve (one individual per warp) vs k_improve_hw (PLSE_IMPROVE_KERNEL=hw)
+    bool plits = false;      // variant MPMA: k_plits (plits.cu) is the improve kernel
+    int64_t budget2 = 0;     // PLITS phase-2 budget
     int lane_words16 = 1;
     size_t smem = 0;
     int* d_work = nullptr;
@@ -211,7 +213,8 @@ void validate_params(const plse_params& p) {
     if (!(p.gamma > 1.0)) throw std::invalid_argument("gamma must exceed 1");
     if (p.crossover == PLSE_X_AUX && !(p.beta > p.gamma)) throw std::invalid_argument("beta must exceed gamma");
     if (!(p.alpha >= 0.0)) throw std::invalid_argument("alpha must be non-negative");
-    if (p.phase1_iters < 0) throw std::invalid_argument("phase budgets must be positive");
+    if (p.phase1_iters < 0 || p.phase2_iters < 0) throw std::invalid_argument("phase budgets must be positive");
+    if (p.variant != PLSE_V_PARTIAL && p.variant != PLSE_V_MPMA) throw std::invalid_argument("unknown variant");
     if (p.crossover < 0 || p.crossover > 2) throw std::invalid_argument("unknown crossover mode");
     if (p.matching < 0 || p.matching > 1) throw std::invalid_argument("unknown matching strategy");
     if (p.exclusion < 0 || p.exclusion > 2) throw std::invalid_argument("unknown exclusion scope");
@@ -288,7 +291,9 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->prm = *pp;
     if (c->prm.p_total == 0) c->prm.p_total = c->prm.p;
     c->budget = pp->phase1_iters > 0 ? pp->phase1_iters : 100LL * nv;
-    if (c->budget >= (1LL << 30)) throw Unsupported("budget must be < 2^30 iterations");
+    c->budget2 = pp->phase2_iters > 0 ? pp->phase2_iters : 2LL * nv;
+    c->plits = pp->variant == PLSE_V_MPMA;
+    if (c->budget + (c->plits ? c->budget2 : 0) >= (1LL << 30)) throw Unsupported("budget must be < 2^30 iterations");
     if (pp->alpha * nv >= (double)(1 << 29)) throw Unsupported("alpha * |V| must be < 2^29 (tabu tenure range)");
     c->tenure_cap = 10u + (uint32_t)(pp->alpha * (double)nv);
     c->stop_f = gr->l == 1 ? 1 : 0;
@@ -420,12 +425,20 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_work = dalloc<int>(1);
 
     // ---- improve launch shape: maximise resident individuals per SM
-    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL")) c->half_warp = std::string(env) == "hw";
+    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL")) c->half_warp = std::string(env) == "hw" && !c->plits;
     c->lane_words16 = (nwords + 15) / 16;
-    const void* kern = c->half_warp ? improve_hw_kernel_ptr(W, false) : improve_kernel_ptr(W, false);
-    const void* kern_dbg = c->half_warp ? improve_hw_kernel_ptr(W, true) : improve_kernel_ptr(W, true);
+    const void* kern = c->plits       ? plits_kernel_ptr(W, false)
+                       : c->half_warp ? improve_hw_kernel_ptr(W, false)
+                                      : improve_kernel_ptr(W, false);
+    const void* kern_dbg = c->plits       ? plits_kernel_ptr(W, true)
+                           : c->half_warp ? improve_hw_kernel_ptr(W, true)
+                                          : improve_kernel_ptr(W, true);
     size_t graph_bytes = 0, warp_bytes = 0;
-    if (c->half_warp) {
+    if (c->plits) {
+        const PlitsSmemLayout L = plits_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+        graph_bytes = L.graph_bytes;
+        warp_bytes = L.warp_bytes;
+    } else if (c->half_warp) {
         const HwSmemLayout L = improve_hw_smem_layout(n, nv, c->nvpad, c->lane_words16, W);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
@@ -543,6 +556,7 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.p_total = (uint64_t)c->prm.p_total;
     a.offset = (uint64_t)c->prm.offset;
     a.budget = c->budget;
+    a.budget2 = c->budget2;
     a.stop_f = c->stop_f;
     a.alpha = c->prm.alpha;
     a.trace_idx = trace_idx;
@@ -561,7 +575,9 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     }
     CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->ev0, c->st));
-    if (c->half_warp)
+    if (c->plits)
+        c->launched(launch_plits(a, c->W, c->grid, c->threads, c->smem, c->st));
+    else if (c->half_warp)
         c->launched(launch_improve_hw(a, c->W, c->grid, c->threads, c->smem, c->st));
     else
         c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
@@ -1050,9 +1066,9 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
     plse_ctx* ctx = nullptr;
     const int rc = guard(nullptr, [&] {
         if (!grid || !cfg || !res) throw std::invalid_argument("null argument");
-        validate_params(cfg->params);
-        if (cfg->variant != PLSE_V_PARTIAL)
-            throw Unsupported("only the Partial-MPMA variant runs on the device (PLITS/MPMA is out of scope)");
+        plse_params prm = cfg->params;
+        prm.variant = cfg->variant;  // plse_solver_config::variant selects the improve operator
+        validate_params(prm);
         const auto t0 = std::chrono::steady_clock::now();
         auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
         const plse_host::GraphH g = plse_host::preprocess(n, grid);
@@ -1086,7 +1102,7 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
         view.dom = g.dom.data();
         view.n_prefilled = (int32_t)(g.prefilled.size() / 3);
         view.prefilled = g.prefilled.data();
-        create_impl(&view, &cfg->params, cfg->device, &ctx);
+        create_impl(&view, &prm, cfg->device, &ctx);
         plse_ctx* c = ctx;
         const int p = c->prm.p;
         const bool opt_stop = !cfg->disable_optimal_stop;

@@ -40,6 +40,7 @@ struct ImproveArgs {
     // streams (engine.hpp:189-191): seed = derive(master, 2, gen*p_total + offset + i)
     uint64_t master, generation, p_total, offset;
     int64_t budget;
+    int64_t budget2;            // PLITS phase-2 budget (plits.hpp:244); unused by PartialCol
     int stop_f;
     double alpha;
     // per-slot repair counters (nvpad bytes each; the warp kernel keeps them out of shared memory)
@@ -156,6 +157,34 @@ __host__ __device__ inline HwSmemLayout improve_hw_smem_layout(int n, int nv, in
     L.warp_bytes = 2 * L.half_bytes;
     return L;
 }
+
+// PLITS (plits.cu): graph part as improve_smem_layout, per warp: colours, row / column
+// colour counts (u8 [n][n+1] each) and the active-vertex bitmask
+struct PlitsSmemLayout {
+    size_t graph_bytes, warp0, warp_bytes, w_col, w_rcnt, w_ccnt, w_A;
+};
+
+__host__ __device__ inline PlitsSmemLayout plits_smem_layout(int n, int nv, int nvpad, int lane_words, int W) {
+    const ImproveSmemLayout G = improve_smem_layout(n, nv, nvpad, lane_words, W);
+    PlitsSmemLayout L;
+    L.graph_bytes = G.graph_bytes;
+    L.warp0 = G.warp0;
+    size_t w = 0;
+    L.w_col = w;
+    w += (size_t)nvpad;
+    L.w_rcnt = w;
+    w += (size_t)n * (n + 1);
+    L.w_ccnt = w;
+    w += (size_t)n * (n + 1);
+    w = align_up(w, 16);
+    L.w_A = w;
+    w += (size_t)32 * lane_words * 4;
+    L.warp_bytes = align_up(w, 16);
+    return L;
+}
+
+const void* plits_kernel_ptr(int W, bool debug);
+cudaError_t launch_plits(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 
 const void* improve_hw_kernel_ptr(int W, bool debug);
 cudaError_t launch_improve_hw(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);

@@ -93,8 +93,10 @@ def test_device_path_fails_loudly_without_gpu(plse):
 
 
 def test_unsupported_requests(plse):
-    with pytest.raises(NotImplementedError):
-        plse.run(G["inst_10_0.3_606"], plse.SolverConfig(p=8, variant=plse.MPMA))
+    with pytest.raises(ValueError, match="unknown variant"):
+        plse.run(G["inst_10_0.3_606"], plse.SolverConfig(p=8, variant=7))
+    with pytest.raises(ValueError, match="phase budgets"):
+        plse.run(G["inst_10_0.3_606"], plse.SolverConfig(p=8, variant=plse.MPMA, phase2_iters=-1))
     big = np.zeros((130, 130), np.uint16)
     with pytest.raises(NotImplementedError):
         plse.DevicePopulation(plse.preprocess(big), plse.SolverConfig(p=4))
