@@ -23,6 +23,11 @@ ranks all-gather 32 elites each over NCCL every 2 generations.
 /root/reference compiled in place; parallel_for over all host threads,
 partial_mpma_improve, engine.hpp:184-206), each step a bounded sample of the
 same C3 workload.
+
+--variant mpma: the same generation with the MPMA variant's improve operator
+(PLITS, plits.hpp:276-292; the GPU kernel k_plits), budgets 100|V| + 2|V|; the
+CPU legs then time the reference's plits_run phase.  Not the headline (the
+north star names the PartialCol path); reported for the §8(f) PLITS row.
 """
 from __future__ import annotations
 
@@ -57,6 +62,9 @@ def args_():
     ap.add_argument("--lsc", action="store_true", help="LSC instance builders::lsc_instance(n, r, seed) (config C5)")
     ap.add_argument("--master-seed", type=int, default=1)
     ap.add_argument("--budget", type=int, default=0, help="PartialCol iterations per individual (0 = 100|V|)")
+    ap.add_argument("--variant", default="partial", choices=["partial", "mpma"],
+                    help="improve operator: PartialCol (headline) or PLITS (MPMA)")
+    ap.add_argument("--budget2", type=int, default=0, help="PLITS phase-2 iterations (0 = 2|V|)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--migrate-every", type=int, default=2)
     ap.add_argument("--elites", type=int, default=32)
@@ -200,10 +208,14 @@ def run_reference(a):
     ref = oracle.Reference()
     grid = ref.generate_instance(a.n, a.r, a.seed)
     members, budget, threads, s = reference_sample(a, ref, grid)
+    mpma = a.variant == "mpma"
     moves = 0
     secs = 0.0
     for step in range(a.warmup + a.steps):
-        it, t = ref.improve_phase(grid, members, a.master_seed, step + 1, budget, workers=threads)
+        if mpma:
+            it, t = ref.plits_phase(grid, members, a.master_seed, step + 1, a.budget, a.budget2, workers=threads)
+        else:
+            it, t = ref.improve_phase(grid, members, a.master_seed, step + 1, budget, workers=threads)
         if step >= a.warmup:
             moves += it
             secs += t
@@ -213,12 +225,14 @@ def run_reference(a):
         "ms_per_step": 1000 * secs / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic (generate_instance(60,0.5,12345), random initial population)",
         "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}: reference improve phase "
-                               f"(partial_mpma_improve, parallel_for) on {s} individuals x {budget} iterations",
-                   "pop_sample": s, "budget": budget},
+                               + (f"(plits_run, parallel_for) on {s} individuals, budgets 100|V| + 2|V|" if mpma else
+                                  f"(partial_mpma_improve, parallel_for) on {s} individuals x {budget} iterations"),
+                   "pop_sample": s, "budget": budget, "variant": a.variant},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{s} generation-1 individuals of the C3 population, budget 100|V|, per step"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "variant": a.variant,
     }
     print(json.dumps(line))
     return 0
@@ -238,8 +252,10 @@ def run_ours(a):
     graph = P.preprocess(grid)
     nv = graph.vertex_count
     budget = a.budget if a.budget > 0 else 100 * nv
+    mpma = a.variant == "mpma"
     cfg = P.SolverConfig(p=a.pop, master_seed=a.master_seed, phase1_iters=a.budget, device=local,
-                         p_total=a.pop * world, offset=a.pop * rank)
+                         p_total=a.pop * world, offset=a.pop * rank, variant=P.MPMA if mpma else P.PARTIAL,
+                         phase2_iters=a.budget2)
     pop = P.DevicePopulation(graph, cfg)
     pop.initialize_population()
     pop.offspring = pop.members  # generation-0 offspring are the initial individuals (engine.hpp:163)
@@ -345,8 +361,11 @@ def run_ours(a):
             "warmup": a.warmup, "ms_per_step": t_max / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (generate_instance(60,0.5,12345); random initial population, seeds fixed)",
-            "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}, Partial-MPMA generation "
-                                   f"(improve+distances+update+offspring), pop {a.pop}/GPU, budget {budget}",
+            "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}, "
+                                   + ("MPMA (PLITS) generation" if mpma else "Partial-MPMA generation")
+                                   + f" (improve+distances+update+offspring), pop {a.pop}/GPU, budget {budget}"
+                                   + (" + 2|V|" if mpma else ""),
+                       "variant": a.variant,
                        "global_batch": a.pop * world, "vertices": nv, "budget": budget,
                        "parallelism": f"islands x{world}" + (f", {a.elites} elites all-gathered every "
                                                              f"{a.migrate_every} gens" if world > 1 else ""),
@@ -356,9 +375,11 @@ def run_ours(a):
             "gpu_launches": launches,
             "clocks": clk,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(key), "kernel": "k_improve",
+                         "frac": achieved / peak, "traffic": None if mpma else ncu_traffic(key),
+                         "kernel": "k_plits" if mpma else "k_improve",
                          "peak_source": peak_src, "config_key": key,
-                         "bytes_def": "SURVEY 8(d) B_t summed over every step of the launch",
+                         "bytes_def": ("DESIGN.md PLITS byte model summed over every step of the launch" if mpma
+                                       else "SURVEY 8(d) B_t summed over every step of the launch"),
                          "kernel_share_of_step": imp_ms / ms},
             "improve_moves_per_s": moves / (imp_ms / 1e3),
             "phase_ms_per_step": {k: v / a.steps for k, v in timed_phase.items() if k != "k3_ops"},
@@ -385,7 +406,10 @@ def cpu_baseline(a, grid):
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
     ref = oracle.Reference()
     members, budget, threads, s = reference_sample(a, ref, grid)
-    it, secs = ref.improve_phase(grid, members, a.master_seed, 1, budget, workers=threads)
+    if a.variant == "mpma":
+        it, secs = ref.plits_phase(grid, members, a.master_seed, 1, a.budget, a.budget2, workers=threads)
+    else:
+        it, secs = ref.improve_phase(grid, members, a.master_seed, 1, budget, workers=threads)
     return {"value": it / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{s} generation-1 individuals of the C3 population (reference init), budget {budget}: "
                       f"{it} moves in {secs:.1f} s"}
@@ -398,19 +422,21 @@ def ttb(a, P, grid):
     target = None
     if oracle.Reference.available():
         ref = oracle.Reference()
-        r = ref.run(grid, p=a.ttb_ref_pop, seed=a.master_seed, workers=cpu_threads(), time_limit=300.0)
+        r = ref.run(grid, p=a.ttb_ref_pop, seed=a.master_seed, workers=cpu_threads(), time_limit=300.0,
+                    variant=0 if a.variant == "mpma" else 1)
         target = r["best_score"]
         out["reference"] = {"pop": a.ttb_ref_pop, "best_score": r["best_score"], "cores": cpu_threads(),
                             "seconds_to_best": r["first_best_seconds"], "generations": r["generations"],
                             "stop": r["stop_reason"]}
+    var = P.MPMA if a.variant == "mpma" else P.PARTIAL
     res = P.run(grid, P.SolverConfig(p=a.pop, master_seed=a.master_seed, target_score=float(target or 0),
-                                     time_limit=300.0))
+                                     time_limit=300.0, variant=var))
     out["ours"] = {"pop": a.pop, "best_score": res.best_score, "seconds_to_best": res.time_to_best_seconds,
                    "generations": res.generations, "stop": res.stop_reason, "moves": res.total_iterations,
                    "mode": "parity (every individual runs its full budget)"}
     if target is not None:
         rr = P.run(grid, P.SolverConfig(p=a.pop, master_seed=a.master_seed, target_score=float(target),
-                                        race=True, time_limit=300.0))
+                                        race=True, time_limit=300.0, variant=var))
         out["ours_race"] = {"pop": a.pop, "best_score": rr.best_score, "seconds_to_best": rr.time_to_best_seconds,
                             "generations": rr.generations, "stop": rr.stop_reason, "moves": rr.total_iterations,
                             "mode": "race (device-global early exit at the target)"}

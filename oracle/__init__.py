@@ -362,6 +362,9 @@ class Reference:
         L.ref_improve_phase.argtypes = [C.c_void_p, C.c_int, u16p, C.c_void_p, C.c_uint64, C.c_uint64,
                                         C.c_int64, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_default_workers.restype = C.c_int
+        L.ref_plits_phase.restype = C.c_int64
+        L.ref_plits_phase.argtypes = [C.c_void_p, C.c_int, u16p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64,
+                                      C.c_int64, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.ref_plits.restype = C.c_int64
         L.ref_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int]
         L.ref_plits_trace.restype = C.c_int64
@@ -507,6 +510,16 @@ class Reference:
         it = self.lib.ref_improve_phase(self._h(grid), p, np.ascontiguousarray(offspring, np.uint16).reshape(-1),
                                         None, master_seed, generation, budget, alpha, stop_f, workers,
                                         C.byref(secs))
+        return it, secs.value
+
+    def plits_phase(self, grid, offspring, master_seed, generation, iters1=0, iters2=0, alpha=0.6, stop_f=0,
+                    workers=0):
+        """engine.hpp:184-199 with variant MPMA -> (iterations, seconds)"""
+        p = offspring.shape[0]
+        secs = C.c_double()
+        it = self.lib.ref_plits_phase(self._h(grid), p, np.ascontiguousarray(offspring, np.uint16).reshape(-1),
+                                      None, master_seed, generation, iters1, iters2, alpha, stop_f, workers,
+                                      C.byref(secs))
         return it, secs.value
 
     def default_workers(self):

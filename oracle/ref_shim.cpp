@@ -400,6 +400,39 @@ int64_t ref_improve_phase(const ref_graph* h, int p, const uint16_t* offspring, 
     return total;
 }
 
+// engine.hpp:184-199 for the MPMA variant: plits_run per individual, per-worker PlitsScratch
+int64_t ref_plits_phase(const ref_graph* h, int p, const uint16_t* offspring, uint16_t* improved,
+                        uint64_t master_seed, uint64_t generation, int64_t iters1, int64_t iters2, double alpha,
+                        int stop_f, int workers, double* seconds) {
+    const int nv = h->g.vertex_count();
+    if (workers <= 0) workers = default_workers();
+    std::vector<PlitsScratch> scratch((size_t)workers);
+    std::vector<int64_t> iters((size_t)p, 0);
+    PlitsParams params;
+    params.phase1_iters = iters1;
+    params.phase2_iters = iters2;
+    params.alpha = alpha;
+    params.stop_f = stop_f;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t chunk = (p + workers - 1) / workers;
+    parallel_for(0, workers, workers, [&](int64_t w) {
+        const int64_t lo = w * chunk;
+        const int64_t hi = std::min<int64_t>(p, lo + chunk);
+        for (int64_t i = lo; i < hi; ++i) {
+            Rng rng = derive_stream(master_seed, stream_tag::kImprove, generation * (uint64_t)p + (uint64_t)i);
+            SearchStats st;
+            Coloring out = plits_run(scratch[(size_t)w], make(h->g, offspring + (size_t)i * nv), rng, params, &st);
+            if (improved) std::memcpy(improved + (size_t)i * nv, out.colors().data(), sizeof(uint16_t) * nv);
+            iters[(size_t)i] = st.iterations;
+        }
+    });
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    int64_t total = 0;
+    for (int64_t x : iters) total += x;
+    return total;
+}
+
 int ref_default_workers() { return default_workers(); }
 
 
