@@ -158,10 +158,14 @@ __host__ __device__ inline HwSmemLayout improve_hw_smem_layout(int n, int nv, in
     return L;
 }
 
-// PLITS (plits.cu): graph part as improve_smem_layout, per warp: colours, row / column
-// colour counts (u8 [n][n+1] each) and the active-vertex bitmask
+// PLITS (plits.cu): graph part as improve_smem_layout, per warp: colours, bit-sliced row /
+// column colour counts ((5 + W) planes of W words per line), the active-vertex bitmask, the
+// compacted active list and a per-listed-vertex scratch word
+constexpr int kPlitsMaxThreads = 256;
+constexpr int kPlitsMinBlocks = 2;  // <= 128 registers
+
 struct PlitsSmemLayout {
-    size_t graph_bytes, warp0, warp_bytes, w_col, w_rcnt, w_ccnt, w_A;
+    size_t graph_bytes, warp0, warp_bytes, w_col, w_rp, w_cp, w_A, w_list, w_vmin, w_vcnt;
 };
 
 __host__ __device__ inline PlitsSmemLayout plits_smem_layout(int n, int nv, int nvpad, int lane_words, int W) {
@@ -169,16 +173,23 @@ __host__ __device__ inline PlitsSmemLayout plits_smem_layout(int n, int nv, int 
     PlitsSmemLayout L;
     L.graph_bytes = G.graph_bytes;
     L.warp0 = G.warp0;
+    const size_t planes = (size_t)n * (5 + W) * W * 8;
     size_t w = 0;
     L.w_col = w;
     w += (size_t)nvpad;
-    L.w_rcnt = w;
-    w += (size_t)n * (n + 1);
-    L.w_ccnt = w;
-    w += (size_t)n * (n + 1);
     w = align_up(w, 16);
+    L.w_rp = w;
+    w += planes;
+    L.w_cp = w;
+    w += planes;
     L.w_A = w;
     w += (size_t)32 * lane_words * 4;
+    L.w_list = w;
+    w += align_up((size_t)nv * 2, 16);
+    L.w_vmin = w;
+    w += (size_t)nv * 4;
+    L.w_vcnt = w;
+    w += (size_t)nv;
     L.warp_bytes = align_up(w, 16);
     return L;
 }

@@ -4,32 +4,36 @@
 // Replaces engine.hpp:193-197 (plits_run per individual) with ONE WARP PER
 // INDIVIDUAL, persistent over a work counter, like the PartialCol kernel
 // (improve.cu).  Data layout:
-//   * colours (u8) in shared memory; gamma is never materialised: for a
-//     vertex v in row r / column c and any colour k != col(v),
-//       gamma[v][k] = rcnt[r][k] + ccnt[c][k]
-//     and gamma[v][col(v)] = rcnt[r][col v] + ccnt[c][col v] - 2, over the
-//     per-row / per-column colour counts (u8 [n][n+1] each, shared memory).
-//     PLITS colourings are illegal, so counts (not the occupancy bits of the
-//     legal PartialCol state) are what the step needs.
-//   * the neighbourhood N0 u Nc (plits.hpp:47-63) is an active-vertex
-//     bitmask A: v is active iff col(v) = 0 or its row / column holds col(v)
-//     twice.  A move changes counts in one row and one column only, so only
-//     those cells are re-classified.
-//   * tabu: the reference's dense until[v][k] (search_util.hpp:54-81) per
-//     warp slot in HBM on the slot's monotone clock; a phase switch (fresh
-//     table, plits.hpp:81) advances the clock past every live entry.  The scan
-//     reads until[][] only for candidates at or below the lane's running
-//     minimum, so the table costs a handful of loads per step.
-//   * the objective is the integer 2F = wf*f + wc*c (plits.hpp:22-36):
-//     (2, 1) in phase 1, (2, 2|V|) in phase 2; aspiration compares against
-//     the phase best (plits.hpp:147).
-//   * selection is the canonical order-free rule: the
-//     minimum admissible delta, N candidates at it, r = floor(h1 * N / 2^32)
-//     from the counter hash keyed by (stream seed, step over both phases),
-//     the r-th candidate in ascending (v, k) order with k = 0 first; tenure
-//     floor(h2 * 10 / 2^32) + floor(alpha * active) (plits.hpp:182-185).
-//   * best tracking: deferred snapshot into the improved row (the row is
-//     written only before a move that does not improve on the phase best).
+//   * colours (u8) in shared memory.  gamma is never materialised: for a
+//     vertex v in row r / column c and any colour k != col(v)
+//       gamma[v][k] = cnt_row[r][k] + cnt_col[c][k]
+//     and gamma[v][col v] is the same sum minus 2.  The colour counts are kept
+//     BIT-SLICED: plane b of row r is the W-word mask of colours whose count
+//     has bit b set (NP = 5 + W planes, counts <= n).  One ripple-carry add of
+//     the row and column planes gives gamma for all colours of v at once, and
+//     a bit-sliced minimum over the candidate mask gives v's best move class
+//     and its multiplicity -- about 80 word ops per vertex instead of a loop
+//     over its domain.
+//   * the neighbourhood N0 u Nc (plits.hpp:47-63) is an active-vertex bitmask:
+//     v is active iff col(v) = 0 or col(v) occurs twice in its row or column.
+//     Every step compacts it into an ascending id list dealt round-robin to
+//     the lanes, so the scan is balanced however the active set clusters.
+//   * tabu: the reference's dense until[v][k] (search_util.hpp:54-81) per warp
+//     slot in HBM on the slot's monotone clock; a phase switch (fresh table,
+//     plits.hpp:81) advances the clock past every live entry.  The step finds
+//     the lowest delta LEVEL with an admissible candidate: the level minimum
+//     is computed tabu-blind from shared memory, then only the candidates AT
+//     that level read until[][] (batched, independent loads); when all of them
+//     are tabu and not aspirating (plits.hpp:147) the next level is tried.
+//   * objective: the integer 2F = wf*f + wc*c (plits.hpp:22-36), (2, 1) in
+//     phase 1 and (2, 2|V|) in phase 2; aspiration against the phase best.
+//   * selection: the canonical order-free rule: N
+//     admissible candidates at the level, r = floor(h1 * N / 2^32) from the
+//     counter hash keyed by (stream seed, step over both phases), the r-th in
+//     ascending (v, k) order with k = 0 first; tenure floor(h2 * 10 / 2^32) +
+//     floor(alpha * active) (plits.hpp:182-185).
+//   * best tracking: deferred snapshot into the improved row (written only
+//     before a move that does not improve on the phase best).
 #include <climits>
 
 #include "improve_common.cuh"
@@ -37,35 +41,244 @@
 namespace plse_dev {
 
 struct PlitsWarp {
-    uint8_t* col;   // [nvpad]
-    uint8_t* rcnt;  // [n][n+1] colour counts per row (index 0 counts uncoloured cells)
-    uint8_t* ccnt;  // [n][n+1] per column
-    uint32_t* A;    // [32 * lane_words] active vertices; word v >> 5 (lane-owned blocks)
+    uint8_t* col;     // [nvpad]
+    uint64_t* rp;     // [n][NP][W] row colour-count planes
+    uint64_t* cp;     // [n][NP][W] column colour-count planes
+    uint32_t* A;      // [32 * lane_words] active vertices; word v >> 5 (lane-owned blocks)
+    uint16_t* list;   // [nv] active ids, ascending
+    int32_t* vmin;    // [nv] per active vertex: tabu-blind minimum delta of its moves (refreshed when its
+                      //      row or column changes)
+    uint8_t* vcnt;    // [nv] per listed vertex: admissible moves at the step's level
 };
 
 template <int W>
-__device__ __forceinline__ bool plits_is_active(const Graph<W>& g, const PlitsWarp& s, int u, int w1) {
+struct PlitsK {
+    static constexpr int NP = 5 + W;  // count bits: counts <= n <= 63 (W = 1) or 127 (W = 2)
+    static constexpr int NB = NP + 1; // bits of gamma = row count + column count
+};
+
+// count of colour k in a plane stack
+template <int W, int NP>
+__device__ __forceinline__ int plane_val(const uint64_t* P, int k) {
+    int v = 0;
+#pragma unroll
+    for (int b = 0; b < NP; ++b) v |= (int)((P[b * W + (k >> 6)] >> (k & 63)) & 1ULL) << b;
+    return v;
+}
+
+// mask of colours whose count is >= 2 (any plane above bit 0)
+template <int W, int NP>
+__device__ __forceinline__ bool plane_multi(const uint64_t* P, int k) {
+    uint64_t m = 0;
+#pragma unroll
+    for (int b = 1; b < NP; ++b) m |= P[b * W + (k >> 6)];
+    return (m >> (k & 63)) & 1ULL;
+}
+
+// S = R + C, bit-sliced (gamma of every colour against a vertex in that row / column)
+template <int W, int NP>
+__device__ __forceinline__ void plane_sum(const uint64_t* R, const uint64_t* C, uint64_t (&S)[NP + 1][W]) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int b = 0; b < NP; ++b) {
+            const uint64_t x = R[b * W + q], y = C[b * W + q], t = x ^ y;
+            S[b][q] = t ^ carry;
+            carry = (x & y) | (carry & t);
+        }
+        S[NP][q] = carry;
+    }
+}
+
+// word q of a register array without dynamic indexing (W <= 2)
+template <int W>
+__device__ __forceinline__ uint64_t word_of(const uint64_t (&x)[W], int q) {
+    return (W == 1 || q == 0) ? x[0] : x[W - 1];
+}
+
+template <int W, int NB>
+__device__ __forceinline__ int sliced_val(const uint64_t (&S)[NB][W], int k) {
+    int v = 0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) v |= (int)((word_of<W>(S[b], k >> 6) >> (k & 63)) & 1ULL) << b;
+    return v;
+}
+
+// minimum of S over a non-empty mask; sel becomes the argmin set
+template <int W, int NB>
+__device__ __forceinline__ int sliced_min(const uint64_t (&S)[NB][W], uint64_t (&sel)[W]) {
+    int val = 0;
+#pragma unroll
+    for (int b = NB - 1; b >= 0; --b) {
+        uint64_t z[W], any = 0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            z[q] = sel[q] & ~S[b][q];
+            any |= z[q];
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q) sel[q] = any ? z[q] : sel[q];
+        val |= any ? 0 : (1 << b);
+    }
+    return val;
+}
+
+// m &= {k : S_k >= th}
+template <int W, int NB>
+__device__ __forceinline__ void sliced_ge(const uint64_t (&S)[NB][W], int th, uint64_t (&m)[W]) {
+    if (th <= 0) return;
+    if (th >= (1 << NB)) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) m[q] = 0;
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t lt = 0, eq = ~0ULL;
+#pragma unroll
+        for (int b = NB - 1; b >= 0; --b) {
+            const uint64_t tb = ((th >> b) & 1) ? ~0ULL : 0ULL;
+            lt |= eq & ~S[b][q] & tb;
+            eq &= ~(S[b][q] ^ tb);
+        }
+        m[q] &= ~lt;
+    }
+}
+
+// m &= {k : S_k == val}
+template <int W, int NB>
+__device__ __forceinline__ void sliced_eq(const uint64_t (&S)[NB][W], int val, uint64_t (&m)[W]) {
+    if (val < 0 || val >= (1 << NB)) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) m[q] = 0;
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t eq = ~0ULL;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) eq &= ~(S[b][q] ^ (((val >> b) & 1) ? ~0ULL : 0ULL));
+        m[q] &= eq;
+    }
+}
+
+__device__ __forceinline__ int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// one vertex's move classes: gamma planes, current-colour gamma, delta offsets, candidate mask
+template <int W>
+struct VertexMoves {
+    static constexpr int NB = PlitsK<W>::NB;
+    uint64_t S[NB][W];
+    uint64_t M[W];  // colours k != col(v) of D(v) \ {0}
+    int cur, dbase, d0;
+};
+
+template <int W>
+__device__ __forceinline__ void vertex_moves(const Graph<W>& g, const PlitsWarp& s, int v, int wf, int wc,
+                                             VertexMoves<W>& m) {
+    constexpr int NP = PlitsK<W>::NP;
+    const uint16_t rc = g.cell[v];
+    const int r = rc >> 8, c = rc & 0xFF;
+    plane_sum<W, NP>(s.rp + (size_t)r * NP * W, s.cp + (size_t)c * NP * W, m.S);
+    m.cur = s.col[v];
+    const int gcur = m.cur ? sliced_val<W, NP + 1>(m.S, m.cur) - 2 : 0;
+    m.dbase = (m.cur ? 0 : -wf) - wc * gcur;  // to k != 0: delta = dbase + wc * gamma[v][k]
+    m.d0 = wf - wc * gcur;                    // to 0 (coloured v only): df = +1, dc = -gamma[v][cur]
+    dom_mask<W>(g, r, c, m.M);
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+        if (m.cur && (m.cur >> 6) == q) m.M[q] &= ~(1ULL << (m.cur & 63));
+}
+
+// ripple +-1 of colour k's count in a plane stack (lanes may update different colours of the
+// same stack concurrently: each lane only reads its own bit and flips it with atomicXor)
+template <int W, int NP>
+__device__ __forceinline__ void plane_step(uint64_t* P, int k, bool inc) {
+    // the colour's bit lives in one 32-bit half of each plane word: native 32-bit shared atomics
+    uint32_t* P32 = reinterpret_cast<uint32_t*>(P) + 2 * (k >> 6) + ((k >> 5) & 1);
+    const uint32_t bit = 1u << (k & 31);
+#pragma unroll
+    for (int b = 0; b < NP; ++b) {
+        const uint32_t x = atomicXor(P32 + 2 * W * b, bit);  // returns the old word
+        if (inc ? !(x & bit) : (x & bit)) break;            // no carry / borrow out of this bit
+    }
+}
+
+template <int W>
+__device__ __forceinline__ bool plits_is_active(const Graph<W>& g, const PlitsWarp& s, int u) {
+    constexpr int NP = PlitsK<W>::NP;
     const int k = s.col[u];
     if (!k) return true;
     const uint16_t rc = g.cell[u];
-    return s.rcnt[(rc >> 8) * w1 + k] >= 2 || s.ccnt[(rc & 0xFF) * w1 + k] >= 2;
+    return plane_multi<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k) ||
+           plane_multi<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k);
 }
 
-// counts, active set, f and c of the colouring in s.col (plits.hpp:104-116, coloring.hpp:59-73)
+// tabu-blind minimum delta over v's candidates (plits.hpp:135-176 without the tabu test)
 template <int W>
-__device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int cnt_bytes, int lane, int& f, int& c,
-                            int& active) {
-    const int n = g.n, nv = g.nv, w1 = n + 1;
-    uint4* z = reinterpret_cast<uint4*>(s.rcnt);
-    for (int x = lane; x < cnt_bytes / 16; x += 32) z[x] = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    for (int r = lane; r < n; r += 32) {
-        uint8_t* row = s.rcnt + r * w1;
-        for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) row[s.col[u]] += 1;
+__device__ __forceinline__ int vertex_min(const Graph<W>& g, const PlitsWarp& s, int v, int wf, int wc) {
+    constexpr int NB = PlitsK<W>::NB;
+    VertexMoves<W> m;
+    vertex_moves<W>(g, s, v, wf, wc, m);
+    int vm = m.cur ? m.d0 : INT_MAX;
+    if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
+    return vm;
+}
+
+// after a move in row r / column c: re-classify those cells (plits.hpp:193-212) and refresh the
+// cached minimum of every active one -- no other vertex's gamma changed
+template <int W>
+__device__ __forceinline__ void plits_membership(const Graph<W>& g, const PlitsWarp& s, int r, int c, int wf, int wc,
+                                                 int lane) {
+    const int nr = g.rs[r + 1] - g.rs[r];
+    const int tot = nr + g.cs[c + 1] - g.cs[c];
+    for (int x = lane; x < tot; x += 32) {
+        const int u = x < nr ? g.rs[r] + x : g.cl[g.cs[c] + x - nr];
+        const uint32_t bit = 1u << (u & 31);
+        if (plits_is_active<W>(g, s, u)) {
+            atomicOr(&s.A[u >> 5], bit);
+            s.vmin[u] = vertex_min<W>(g, s, u, wf, wc);
+        } else {
+            atomicAnd(&s.A[u >> 5], ~bit);
+        }
     }
-    for (int cc = lane; cc < n; cc += 32) {
-        uint8_t* row = s.ccnt + cc * w1;
-        for (int x = g.cs[cc]; x < g.cs[cc + 1]; ++x) row[s.col[g.cl[x]]] += 1;
+}
+
+// count planes, active set, f and c of the colouring in s.col (plits.hpp:104-116, coloring.hpp:59-73)
+template <int W>
+__device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int lane, int wf, int wc, int& f, int& c,
+                            int& active) {
+    constexpr int NP = PlitsK<W>::NP;
+    const int n = g.n, nv = g.nv;
+    for (int line = lane; line < 2 * n; line += 32) {
+        const bool is_row = line < n;
+        const int idx = is_row ? line : line - n;
+        uint64_t P[NP][W];
+#pragma unroll
+        for (int b = 0; b < NP; ++b)
+#pragma unroll
+            for (int q = 0; q < W; ++q) P[b][q] = 0;
+        const int lo = is_row ? g.rs[idx] : g.cs[idx], hi = is_row ? g.rs[idx + 1] : g.cs[idx + 1];
+        for (int x = lo; x < hi; ++x) {
+            const int k = s.col[is_row ? x : g.cl[x]];
+            if (!k) continue;
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                uint64_t carry = (k >> 6) == q ? 1ULL << (k & 63) : 0ULL;
+#pragma unroll
+                for (int b = 0; b < NP; ++b) {
+                    const uint64_t t = P[b][q] & carry;
+                    P[b][q] ^= carry;
+                    carry = t;
+                }
+            }
+        }
+        uint64_t* dst = (is_row ? s.rp : s.cp) + (size_t)idx * NP * W;
+#pragma unroll
+        for (int b = 0; b < NP; ++b)
+#pragma unroll
+            for (int q = 0; q < W; ++q) dst[b * W + q] = P[b][q];
     }
     __syncwarp();
     const int v_lo = lane * 32 * g.lane_words;
@@ -81,13 +294,19 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int cnt_bytes
                 ++fl;
             } else {
                 const uint16_t rc = g.cell[v];
-                const int gv = s.rcnt[(rc >> 8) * w1 + k] + s.ccnt[(rc & 0xFF) * w1 + k] - 2;
+                const int gv = plane_val<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k) +
+                               plane_val<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k) - 2;
                 cl2 += gv;
                 if (gv) bits |= 1u << b;
             }
         }
         s.A[lane * g.lane_words + q] = bits;
         al += __popc(bits);
+        while (bits) {
+            const int v = v_lo + 32 * q + __ffs(bits) - 1;
+            bits &= bits - 1;
+            s.vmin[v] = vertex_min<W>(g, s, v, wf, wc);
+        }
     }
     f = (int)__reduce_add_sync(kFull, (unsigned)fl);
     c = (int)__reduce_add_sync(kFull, (unsigned)cl2) / 2;
@@ -95,12 +314,52 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int cnt_bytes
     __syncwarp();
 }
 
+// the admissible moves of one vertex at delta level dl (plits.hpp:146-147): adm = colours k != 0,
+// adm0 = the move to 0.  Tabu candidates read until[][] in independent batches of four.
+template <int W>
+__device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
+                                         uint32_t t, uint64_t (&adm)[W], bool& adm0) {
+    constexpr int NB = PlitsK<W>::NB;
+    adm0 = m.cur && m.d0 == dl && (asp_all || urow[0] <= t);
+    const int qv = dl - m.dbase;
+#pragma unroll
+    for (int q = 0; q < W; ++q) adm[q] = m.M[q];
+    if (qv < 0 || qv % wc) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) adm[q] = 0;
+    } else {
+        sliced_eq<W, NB>(m.S, qv / wc, adm);
+    }
+    if (!asp_all) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            uint64_t x = adm[q];
+            while (x) {
+                int ks[4];
+                uint32_t us[4];
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    ks[z] = x ? __ffsll((long long)x) - 1 : -1;
+                    x &= x - 1;
+                }
+#pragma unroll
+                for (int z = 0; z < 4; ++z) us[z] = ks[z] >= 0 ? urow[q * 64 + ks[z]] : 0u;
+#pragma unroll
+                for (int z = 0; z < 4; ++z)
+                    if (ks[z] >= 0 && us[z] > t) adm[q] &= ~(1ULL << ks[z]);
+            }
+        }
+    }
+    return popc_w<W>(adm) + (adm0 ? 1 : 0);
+}
+
 template <int W, bool kDebug>
-__device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWarp& s, int cnt_bytes,
-                          uint32_t* until, uint32_t* slot_clock, int i, int lane) {
+__device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWarp& s, uint32_t* until,
+                          uint32_t* slot_clock, int i, int lane) {
+    constexpr int NP = PlitsK<W>::NP;
+    constexpr int NB = PlitsK<W>::NB;
     const int n = g.n, nv = g.nv, w1 = n + 1;
     const int v_lo = lane * 32 * g.lane_words;
-    const int v_hi = min(nv, v_lo + 32 * g.lane_words);
     uint8_t* col = s.col;
     uint8_t* best_row = a.improved + (size_t)i * g.nvpad;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
@@ -112,12 +371,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         for (size_t x = lane; x < a.until_stride / 4; x += 32) u4[x] = make_uint4(0, 0, 0, 0);
         base = 0;
     }
-
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(a.offspring + (size_t)i * g.nvpad);
-        uint4* d4 = reinterpret_cast<uint4*>(col);
-        for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
-    }
+    snapshot(a.offspring + (size_t)i * g.nvpad, col, g.nvpad, lane);
     __syncwarp();
 
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
@@ -134,12 +388,12 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     };
 
     int f = 0, c = 0, active = 0;
-    plits_build<W>(g, s, cnt_bytes, lane, f, c, active);
+    plits_build<W>(g, s, lane, 2, 1, f, c, active);
     const int initial_f = f;
-    uint32_t J = 0;        // step index over both phases: the canonical draw's key
+    uint32_t J = 0;  // step index over both phases: the canonical draw's key
     int64_t iters = 0;
     bool hit = false;
-    bool pending = true;   // the phase best equals the current colouring
+    bool pending = true;  // the phase best equals the current colouring
     int best_f = f, best_c = c;
     unsigned long long acc = 0;
 
@@ -147,16 +401,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         const int wf = 2;
         const int wc = phase == 1 ? 1 : 2 * nv;  // PhaseWeights::from_phi(0.5 / |V|), plits.hpp:27-33
         const int64_t budget = phase == 1 ? a.budget : a.budget2;
-        if (phase == 2) {
-            // plits.hpp:285-288: phase 2 starts from phase 1's best with a fresh tabu table
-            if (!pending) {
-                const uint4* src = reinterpret_cast<const uint4*>(best_row);
-                uint4* d4 = reinterpret_cast<uint4*>(col);
-                for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
-                __syncwarp();
-            }
-            plits_build<W>(g, s, cnt_bytes, lane, f, c, active);
-        }
+        if (phase == 2) plits_build<W>(g, s, lane, wf, wc, f, c, active);  // from phase 1's best
         int64_t best_scaled = (int64_t)wf * f + (int64_t)wc * c;
         best_f = f;
         best_c = c;
@@ -174,60 +419,90 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             const uint32_t h1 = fmix32(s32 + (J + 1) * 0x9E3779B9u);
             const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
             const int64_t cur_scaled = (int64_t)wf * f + (int64_t)wc * c;
-            const int64_t thr64 = best_scaled - cur_scaled;  // tabu move admissible iff delta < thr
+            const int64_t thr64 = best_scaled - cur_scaled;  // a tabu move is admissible iff delta < thr
             const int thr = (int)max(min(thr64, (int64_t)INT_MAX), (int64_t)INT_MIN);
             const int active_before = active;
 
-            // ---- pass 1: each lane's minimum admissible delta and its multiplicity
-            int lmin = INT_MAX, lcnt = 0;
-            for (int q = 0; q < g.lane_words; ++q) {
-                uint32_t bits = s.A[lane * g.lane_words + q];
-                while (bits) {
-                    const int v = v_lo + 32 * q + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const uint16_t rc = g.cell[v];
-                    const int r = rc >> 8, cc = rc & 0xFF;
-                    const int cur = col[v];
-                    const uint8_t* rrow = s.rcnt + r * w1;
-                    const uint8_t* crow = s.ccnt + cc * w1;
-                    const uint32_t* urow = until + (size_t)v * w1;
-                    const int gcur = cur ? rrow[cur] + crow[cur] - 2 : 0;
-                    if (cur) {
-                        const int d = wf - wc * gcur;  // to 0: df = +1, dc = -gamma[v][cur]
-                        if (d <= lmin && !(urow[0] > t && !(d < thr))) {
-                            if (d < lmin) {
-                                lmin = d;
-                                lcnt = 1;
-                            } else {
-                                ++lcnt;
-                            }
-                        }
-                    }
-                    const int dbase = (cur ? 0 : -wf) - wc * gcur;
-                    uint64_t dom[W];
-                    dom_mask<W>(g, r, cc, dom);
-                    if (cur) dom[cur >> 6] &= ~(1ULL << (cur & 63));
+            // ---- compact the active set into ascending ids; lane L takes the L-th contiguous block
+            int na = 0;
+            {
+                int my = 0;
+                for (int q = 0; q < g.lane_words; ++q) my += __popc(s.A[lane * g.lane_words + q]);
+                int incl = my;
 #pragma unroll
-                    for (int qq = 0; qq < W; ++qq) {
-                        uint64_t m = dom[qq];
-                        while (m) {
-                            const int k = qq * 64 + __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            const int d = dbase + wc * (rrow[k] + crow[k]);
-                            if (d > lmin) continue;
-                            if (urow[k] > t && !(d < thr)) continue;
-                            if (d < lmin) {
-                                lmin = d;
-                                lcnt = 1;
-                            } else {
-                                ++lcnt;
-                            }
-                        }
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int x = __shfl_up_sync(kFull, incl, d);
+                    incl += lane >= d ? x : 0;
+                }
+                na = __shfl_sync(kFull, incl, 31);
+                int pos = incl - my;
+                for (int q = 0; q < g.lane_words; ++q) {
+                    uint32_t bits = s.A[lane * g.lane_words + q];
+                    while (bits) {
+                        s.list[pos++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
+                        bits &= bits - 1;
                     }
                 }
             }
-            const int dmin = __reduce_min_sync(kFull, lmin);
-            if (dmin == INT_MAX) {
+            __syncwarp();
+            const int per = (na + 31) >> 5;
+            const int i_lo = min(na, lane * per), i_hi = min(na, i_lo + per);
+
+            // ---- the lowest delta level holding an admissible candidate: its tabu-blind minimum from
+            // the cached per-vertex minima, then the until[][] reads of the candidates at that level only
+            bool has_prev = false;
+            int prev = 0, dl = INT_MAX, N = 0, lc = 0;
+            bool asp_all = false;
+            int c_idx = -1;   // first listed vertex of this lane with admissible moves, and its masks
+            uint64_t c_adm[W];
+            bool c_adm0 = false;
+            for (;;) {
+                int lmin = INT_MAX;
+                for (int idx = i_lo; idx < i_hi; ++idx) {
+                    const int v = s.list[idx];
+                    int vm;
+                    if (!has_prev) {
+                        vm = s.vmin[v];
+                    } else {
+                        VertexMoves<W> m;
+                        vertex_moves<W>(g, s, v, wf, wc, m);
+                        sliced_ge<W, NB>(m.S, floor_div(prev - m.dbase, wc) + 1, m.M);
+                        vm = (m.cur && m.d0 > prev) ? m.d0 : INT_MAX;
+                        if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
+                    }
+                    lmin = min(lmin, vm);
+                }
+                dl = __reduce_min_sync(kFull, lmin);
+                if (dl == INT_MAX) break;  // every candidate tabu
+                asp_all = dl < thr;
+                lc = 0;
+                c_idx = -1;
+                for (int idx = i_lo; idx < i_hi; ++idx) {
+                    const int v = s.list[idx];
+                    int cnt = 0;
+                    if (has_prev || s.vmin[v] <= dl) {
+                        VertexMoves<W> m;
+                        vertex_moves<W>(g, s, v, wf, wc, m);
+                        uint64_t adm[W];
+                        bool adm0;
+                        cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, t, adm, adm0);
+                        if (cnt && c_idx < 0) {
+                            c_idx = idx;
+                            c_adm0 = adm0;
+#pragma unroll
+                            for (int q = 0; q < W; ++q) c_adm[q] = adm[q];
+                        }
+                    }
+                    s.vcnt[idx] = (uint8_t)cnt;
+                    lc += cnt;
+                }
+                N = (int)__reduce_add_sync(kFull, (unsigned)lc);
+                if (N > 0) break;
+                has_prev = true;
+                prev = dl;
+            }
+            __syncwarp();
+            if (N == 0) {
                 // every candidate tabu: the clock still advances (plits.hpp:178-179)
                 if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)active_before;
                 if (tracing && lane == 0 && (int64_t)J < a.trace_cap) {
@@ -238,69 +513,45 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 ++J;
                 continue;
             }
-            const int cnt = lmin == dmin ? lcnt : 0;
-            int incl = cnt;
+
+            // ---- the r-th admissible candidate in ascending (v, k): lane blocks are in id order
+            const uint32_t rnk = __umulhi(h1, (uint32_t)N);
+            int incl = lc;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int x = __shfl_up_sync(kFull, incl, d);
                 incl += lane >= d ? x : 0;
             }
-            const int N = __shfl_sync(kFull, incl, 31);
-            const uint32_t rnk = __umulhi(h1, (uint32_t)N);
-            const int excl = incl - cnt;
-            const bool owner = (uint32_t)excl <= rnk && rnk < (uint32_t)incl;
-            int sv = -1, sk = 0, sdc = 0;
+            const bool owner = (uint32_t)(incl - lc) <= rnk && rnk < (uint32_t)incl;
+            int sel_idx = -1, sv = -1, sk = 0, sdc = 0;
             if (owner) {
-                // ---- pass 2 (one lane): the (rnk - excl)-th admissible candidate at dmin, ascending (v, k)
-                int left = (int)rnk - excl;
-                for (int q = 0; q < g.lane_words && sv < 0; ++q) {
-                    uint32_t bits = s.A[lane * g.lane_words + q];
-                    while (bits && sv < 0) {
-                        const int v = v_lo + 32 * q + __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        const uint16_t rc = g.cell[v];
-                        const int r = rc >> 8, cc = rc & 0xFF;
-                        const int cur = col[v];
-                        const uint8_t* rrow = s.rcnt + r * w1;
-                        const uint8_t* crow = s.ccnt + cc * w1;
-                        const uint32_t* urow = until + (size_t)v * w1;
-                        const int gcur = cur ? rrow[cur] + crow[cur] - 2 : 0;
-                        if (cur) {
-                            const int d = wf - wc * gcur;
-                            if (d == dmin && !(urow[0] > t && !(d < thr))) {
-                                if (left == 0) {
-                                    sv = v;
-                                    sk = 0;
-                                    sdc = -gcur;
-                                    break;
-                                }
-                                --left;
-                            }
-                        }
-                        const int dbase = (cur ? 0 : -wf) - wc * gcur;
-                        uint64_t dom[W];
-                        dom_mask<W>(g, r, cc, dom);
-                        if (cur) dom[cur >> 6] &= ~(1ULL << (cur & 63));
-                        for (int qq = 0; qq < W && sv < 0; ++qq) {
-                            uint64_t m = dom[qq];
-                            while (m) {
-                                const int k = qq * 64 + __ffsll((long long)m) - 1;
-                                m &= m - 1;
-                                const int gk = rrow[k] + crow[k];
-                                const int d = dbase + wc * gk;
-                                if (d != dmin) continue;
-                                if (urow[k] > t && !(d < thr)) continue;
-                                if (left == 0) {
-                                    sv = v;
-                                    sk = k;
-                                    sdc = gk - gcur;
-                                    break;
-                                }
-                                --left;
-                            }
-                        }
+                int local = (int)rnk - (incl - lc);
+                for (int idx = i_lo; idx < i_hi; ++idx) {
+                    const int cnt = s.vcnt[idx];
+                    if (local < cnt) {
+                        sel_idx = idx;
+                        break;
                     }
+                    local -= cnt;
                 }
+                sv = s.list[sel_idx];
+                VertexMoves<W> m;
+                vertex_moves<W>(g, s, sv, wf, wc, m);
+                uint64_t adm[W];
+                bool adm0;
+                if (sel_idx == c_idx) {
+                    adm0 = c_adm0;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) adm[q] = c_adm[q];
+                } else {
+                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, t, adm, adm0);
+                }
+                if (adm0 && local == 0)
+                    sk = 0;
+                else
+                    sk = nth_bit_w<W>(adm, local - (adm0 ? 1 : 0));
+                const int gcur = m.cur ? sliced_val<W, NB>(m.S, m.cur) - 2 : 0;
+                sdc = (sk ? sliced_val<W, NB>(m.S, sk) : 0) - gcur;
             }
             const int wl = __ffs(__ballot_sync(kFull, owner)) - 1;
             const int vs = __shfl_sync(kFull, sv, wl);
@@ -308,41 +559,22 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             const int dcs = __shfl_sync(kFull, sdc, wl);
             const int from = col[vs];
             const int dfs = (ks == 0) - (from == 0);
-            const int64_t now = cur_scaled + dmin;
+            const int64_t now = cur_scaled + dl;
             if (now >= best_scaled && pending) {
                 // deferred snapshot: the colouring about to change is the phase best
-                const uint4* src = reinterpret_cast<const uint4*>(col);
-                uint4* d4 = reinterpret_cast<uint4*>(best_row);
-                for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
+                snapshot(col, best_row, g.nvpad, lane);
                 pending = false;
             }
             __syncwarp();
             const uint16_t rcs = g.cell[vs];
             const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-            if (lane == 0) {
-                col[vs] = (uint8_t)ks;
-                s.rcnt[rs_ * w1 + from] -= 1;
-                s.ccnt[cs_ * w1 + from] -= 1;
-                s.rcnt[rs_ * w1 + ks] += 1;
-                s.ccnt[cs_ * w1 + ks] += 1;
-            }
+            if (lane == 0) col[vs] = (uint8_t)ks;
+            if (lane == 0 && from) plane_step<W, NP>(s.rp + (size_t)rs_ * NP * W, from, false);
+            if (lane == 1 && ks) plane_step<W, NP>(s.rp + (size_t)rs_ * NP * W, ks, true);
+            if (lane == 2 && from) plane_step<W, NP>(s.cp + (size_t)cs_ * NP * W, from, false);
+            if (lane == 3 && ks) plane_step<W, NP>(s.cp + (size_t)cs_ * NP * W, ks, true);
             __syncwarp();
-            // ---- membership around the move (plits.hpp:193-212): re-classify v's row and column
-            for (int u = g.rs[rs_] + lane; u < g.rs[rs_ + 1]; u += 32) {
-                const uint32_t bit = 1u << (u & 31);
-                if (plits_is_active<W>(g, s, u, w1))
-                    atomicOr(&s.A[u >> 5], bit);
-                else
-                    atomicAnd(&s.A[u >> 5], ~bit);
-            }
-            for (int x = g.cs[cs_] + lane; x < g.cs[cs_ + 1]; x += 32) {
-                const int u = g.cl[x];
-                const uint32_t bit = 1u << (u & 31);
-                if (plits_is_active<W>(g, s, u, w1))
-                    atomicOr(&s.A[u >> 5], bit);
-                else
-                    atomicAnd(&s.A[u >> 5], ~bit);
-            }
+            plits_membership<W>(g, s, rs_, cs_, wf, wc, lane);
             __syncwarp();
             {
                 int al = 0;
@@ -368,7 +600,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             if (tracing && lane == 0 && (int64_t)J < a.trace_cap) {
                 plse_step* tr = reinterpret_cast<plse_step*>(a.trace) + J;
                 *tr = plse_step{(int64_t)J, vs, ks, phase, from, active, f, c, (int32_t)best_scaled, (int32_t)tenure,
-                                N, dmin};
+                                N, dl};
             }
             __syncwarp();
             ++j;
@@ -378,9 +610,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         iters += j;
         // the phase's result is its best colouring (plits.hpp:268)
         if (!pending) {
-            const uint4* src = reinterpret_cast<const uint4*>(best_row);
-            uint4* d4 = reinterpret_cast<uint4*>(col);
-            for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
+            snapshot(best_row, col, g.nvpad, lane);
             __syncwarp();
             pending = true;
         }
@@ -388,45 +618,49 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         if (hit) break;                // plits.hpp:284: phase 2 only when phase 1 missed the target
     }
 
-    // ---- final greedy repair when the result still conflicts (plits.hpp:289, partial.hpp:22-39)
+    // ---- final greedy repair when the result still conflicts (plits.hpp:289, partial.hpp:22-39):
+    // argmax gamma[v][col v] over the conflicting (active, coloured) vertices, lowest id on ties
     if (best_c > 0) {
-        plits_build<W>(g, s, cnt_bytes, lane, f, c, active);
+        plits_build<W>(g, s, lane, 2, 2 * nv, f, c, active);
         for (;;) {
             int bc = 0, bv = -1;
-            for (int v = v_lo; v < v_hi; ++v) {
-                const int k = col[v];
-                if (!k) continue;
-                const uint16_t rc = g.cell[v];
-                const int gv = s.rcnt[(rc >> 8) * w1 + k] + s.ccnt[(rc & 0xFF) * w1 + k] - 2;
-                if (gv > bc) {
-                    bc = gv;
-                    bv = v;
+            for (int q = 0; q < g.lane_words; ++q) {
+                uint32_t bits = s.A[lane * g.lane_words + q];
+                while (bits) {
+                    const int v = v_lo + 32 * q + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int k = col[v];
+                    if (!k) continue;
+                    const uint16_t rc = g.cell[v];
+                    const int gv = plane_val<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k) +
+                                   plane_val<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k) - 2;
+                    if (gv > bc) {
+                        bc = gv;
+                        bv = v;
+                    }
                 }
             }
             const int mx = (int)__reduce_max_sync(kFull, (unsigned)bc);
             if (mx == 0) break;
             const int wl = __ffs(__ballot_sync(kFull, bc == mx)) - 1;
             const int w = __shfl_sync(kFull, bv, wl);
+            const int k = col[w];
+            const uint16_t rc = g.cell[w];
+            __syncwarp();
             if (lane == 0) {
-                const uint16_t rc = g.cell[w];
-                const int k = col[w];
                 col[w] = 0;
-                s.rcnt[(rc >> 8) * w1 + k] -= 1;
-                s.ccnt[(rc & 0xFF) * w1 + k] -= 1;
-                s.rcnt[(rc >> 8) * w1] += 1;
-                s.ccnt[(rc & 0xFF) * w1] += 1;
+                plane_step<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k, false);
             }
+            if (lane == 1) plane_step<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k, false);
+            __syncwarp();
+            plits_membership<W>(g, s, rc >> 8, rc & 0xFF, 2, 2 * nv, lane);
             ++f;
             __syncwarp();
         }
         best_f = f;
         if (lane == 0) acc += 2ULL * (unsigned)nv;
     }
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(col);
-        uint4* d4 = reinterpret_cast<uint4*>(best_row);
-        for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
-    }
+    snapshot(col, best_row, g.nvpad, lane);
     if (lane == 0) {
         a.best_f[i] = best_f;
         a.repaired_f[i] = initial_f;
@@ -439,7 +673,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 }
 
 template <int W, bool kDebug>
-__global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_plits(const ImproveArgs a) {
+__global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int n = a.n, nv = a.nv;
@@ -497,10 +731,12 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_plits
     uint8_t* wbase = smem + L.warp0 + (size_t)warp * L.warp_bytes;
     PlitsWarp s;
     s.col = wbase + L.w_col;
-    s.rcnt = wbase + L.w_rcnt;
-    s.ccnt = wbase + L.w_ccnt;
+    s.rp = reinterpret_cast<uint64_t*>(wbase + L.w_rp);
+    s.cp = reinterpret_cast<uint64_t*>(wbase + L.w_cp);
     s.A = reinterpret_cast<uint32_t*>(wbase + L.w_A);
-    const int cnt_bytes = (int)(L.w_A - L.w_rcnt);
+    s.list = reinterpret_cast<uint16_t*>(wbase + L.w_list);
+    s.vmin = reinterpret_cast<int32_t*>(wbase + L.w_vmin);
+    s.vcnt = wbase + L.w_vcnt;
 
     const int slot = blockIdx.x * nwarps + warp;
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
@@ -509,7 +745,7 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_plits
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
         i = __shfl_sync(kFull, i, 0);
         if (i >= a.p) break;
-        plits_one<W, kDebug>(a, g, s, cnt_bytes, until, a.slot_clock + slot, i, lane);
+        plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane);
     }
 }
 
