@@ -374,6 +374,10 @@ class Reference:
         L.ref_log_count.restype = C.c_int64
         L.ref_verify_certificate.argtypes = [C.c_int, u16p, C.c_int, u16p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
         L.ref_to_grid.argtypes = [C.c_int, u16p, u16p, u16p]
+        if hasattr(L, "ref_bench"):
+            L.ref_bench.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, C.c_int64, C.c_int64, C.c_int,
+                                    C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         if hasattr(L, "ref_result_json"):
             L.ref_result_json.argtypes = [C.c_char_p, C.c_int, C.POINTER(RefRunResult), C.c_char_p, C.c_int,
                                           C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int,
@@ -561,6 +565,16 @@ class Reference:
         out = np.zeros_like(a)
         self.lib.ref_to_grid(a.shape[0], a.reshape(-1), np.ascontiguousarray(colors, np.uint16), out.reshape(-1))
         return out
+
+    def bench(self, suite_dir, repeats, master_seed, p, gen_limit, phase1=0, variant=1, crossovers="aux",
+              matchings="nearest", pops="", jobs=1, workers=1):
+        """bench.hpp run_bench + write_rows_csv / write_aggregates_csv / report_to_json(...).dump(2)"""
+        bufs = [C.create_string_buffer(1 << 20) for _ in range(3)]
+        self.lib.ref_bench(suite_dir.encode(), repeats, master_seed, p, gen_limit, phase1, variant, crossovers.encode(),
+                           matchings.encode(), pops.encode(), jobs, workers, C.cast(bufs[0], C.c_void_p),
+                           len(bufs[0]), C.cast(bufs[1], C.c_void_p), len(bufs[1]), C.cast(bufs[2], C.c_void_p),
+                           len(bufs[2]))
+        return tuple(b.value.decode() for b in bufs)
 
     def has_result_json(self):
         return hasattr(self.lib, "ref_result_json")

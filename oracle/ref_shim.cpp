@@ -16,9 +16,14 @@
 #include "plse/engine.hpp"
 #include "plse/plits.hpp"
 #if __has_include(<json.hpp>)
+#include "plse/bench.hpp"
 #include "plse/report.hpp"
 #define PLSE_REF_HAVE_JSON 1
 #endif
+#include <dirent.h>
+#include <sys/stat.h>
+
+#include <sstream>
 #include "plse/verify.hpp"
 #include "plse/oracle.hpp"
 #include "support/builders.hpp"
@@ -501,6 +506,79 @@ int ref_result_json(const char* name, int order, const ref_run_result* res, cons
     r.total_iterations = res->total_iterations;
     r.elapsed_seconds = res->elapsed_seconds;
     copy_out(result_to_json(name, order, r, cfg, timing != 0).dump(2), out, cap);
+    return 0;
+}
+
+static std::vector<std::string> split_csv(const char* s) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (const char* q = s; q && *q; ++q) {
+        if (*q == ',') {
+            out.push_back(cur);
+            cur.clear();
+        } else {
+            cur += *q;
+        }
+    }
+    if (!cur.empty()) out.push_back(cur);
+    return out;
+}
+
+// plse.cpp:199-250 cmd_bench through bench.hpp run_bench (CPU reference), all outputs as text
+int ref_bench(const char* suite_dir, int repeats, uint64_t master_seed, int p, int64_t gen_limit, int64_t phase1,
+              int variant, const char* crossovers, const char* matchings, const char* pops, int jobs, int workers,
+              char* rows_csv, int cap1, char* agg_csv, int cap2, char* json_out, int cap3) {
+    // plse.cpp:203-211 with POSIX directory calls (std::filesystem clashes with the libstdc++ some
+    // Python extensions preload)
+    std::vector<BenchTask> tasks;
+    std::vector<std::string> files;
+    if (DIR* d = opendir(suite_dir)) {
+        while (dirent* e = readdir(d)) {
+            const std::string name = e->d_name;
+            const std::string path = std::string(suite_dir) + "/" + name;
+            struct stat st;
+            if (name.size() > 4 && name.compare(name.size() - 4, 4, ".txt") == 0 && stat(path.c_str(), &st) == 0 &&
+                S_ISREG(st.st_mode))
+                files.push_back(path);
+        }
+        closedir(d);
+    }
+    std::sort(files.begin(), files.end());
+    for (const std::string& file : files) {
+        const std::string base = file.substr(file.rfind('/') + 1);
+        tasks.push_back({file, base.substr(0, base.size() - 4), static_cast<int>(tasks.size())});
+    }
+    SolverConfig base;
+    base.p = p;
+    base.phase1_iters = phase1;
+    base.variant = variant == 1 ? Variant::PartialMPMA : Variant::MPMA;
+    base.limits.generations = gen_limit;
+    base.master_seed = master_seed;
+    base.workers = workers;
+    std::vector<SolverConfig> sweep;
+    auto cl = split_csv(crossovers), ml = split_csv(matchings), pl = split_csv(pops);
+    if (cl.empty()) cl = {"aux"};
+    if (ml.empty()) ml = {"nearest"};
+    std::vector<int> pv;
+    for (auto& x : pl) pv.push_back(std::stoi(x));
+    if (pv.empty()) pv = {p};
+    for (auto& c : cl)
+        for (auto& m : ml)
+            for (int pp : pv) {
+                SolverConfig config = base;
+                config.crossover.mode = parse_crossover(c);
+                config.crossover.matching = parse_matching(m);
+                config.p = pp;
+                config.validate();
+                sweep.push_back(config);
+            }
+    const BenchReport report = run_bench(tasks, sweep, repeats, master_seed, jobs, nullptr);
+    std::ostringstream a, b;
+    write_rows_csv(report, a);
+    write_aggregates_csv(report, b);
+    copy_out(a.str(), rows_csv, cap1);
+    copy_out(b.str(), agg_csv, cap2);
+    copy_out(report_to_json(report).dump(2), json_out, cap3);
     return 0;
 }
 #endif

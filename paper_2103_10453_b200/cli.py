@@ -1,9 +1,9 @@
 """``python -m paper_2103_10453_b200`` -- the solver front-end of tools/plse.cpp on the device path.
 
 Subcommands and flags follow plse.cpp:245-311 (``generate``, ``solve``,
-``verify``); output files, stdout/stderr lines and exit codes follow
-cmd_generate (plse.cpp:111-130), cmd_solve (132-174) and cmd_verify
-(175-198).  ``solve`` runs :func:`paper_2103_10453_b200.run` on one B200;
+``verify``, ``bench``); output files, stdout/stderr lines and exit codes follow
+cmd_generate (plse.cpp:111-130), cmd_solve (132-174), cmd_verify (175-198)
+and cmd_bench (199-250, the suite harness in ``suite.py``).  ``solve`` runs :func:`paper_2103_10453_b200.run` on one B200;
 its JSON is report.hpp's ``result_to_json`` printed as ``dump(2)``, so two
 runs with the same seed and flags write byte-identical JSON and certificates
 (acceptance.cpp criterion 8).
@@ -11,6 +11,7 @@ runs with the same seed and flags write byte-identical JSON and certificates
 from __future__ import annotations
 
 import argparse
+import math
 import os
 import secrets
 import sys
@@ -125,7 +126,7 @@ def cmd_generate(args) -> int:
     """plse.cpp:111-130"""
     master = _resolve_seed(args)
     os.makedirs(args.out_dir, exist_ok=True)
-    r_tag = int(round(100.0 * args.ratio))
+    r_tag = int(math.floor(100.0 * args.ratio + 0.5))  # std::lround (r > 0)
     for i in range(args.count):
         grid = generate_instance(args.order, args.ratio, derive_seed(master, _KINSTANCE_GEN, i))
         path = os.path.join(args.out_dir, f"QC-{args.order}-{r_tag}-{i}.txt")
@@ -189,6 +190,44 @@ def cmd_verify(args) -> int:
     return 0
 
 
+def cmd_bench(args) -> int:
+    """plse.cpp:199-250"""
+    import dataclasses
+    from . import suite as S
+    tasks = S.suite_tasks(args.suite)
+    if not tasks:
+        print(f"error: no .txt instances under {args.suite}", file=sys.stderr)
+        return 1
+    base = make_config(args)
+    cross = args.sweep_crossover or [args.crossover]
+    match = args.sweep_matching or [args.matching]
+    pops = args.sweep_pop or [base.p]
+    sweep = []
+    for cname in cross:
+        for mname in match:
+            for p in pops:
+                cfg = dataclasses.replace(base, crossover=R.parse_crossover(cname), matching=R.parse_matching(mname),
+                                          p=int(p))
+                validate_config(cfg)
+                sweep.append(cfg)
+    rep = S.run_bench(tasks, sweep, args.repeats, base.master_seed, args.jobs, sys.stderr)
+    import io
+    if args.csv:
+        with open(args.csv, "w") as fh:
+            S.write_rows_csv(rep, fh)
+        print(f"rows -> {args.csv}", file=sys.stderr)
+    else:
+        S.write_rows_csv(rep, sys.stdout)
+    if args.json:
+        with open(args.json, "w") as fh:
+            fh.write(R.dumps(S.report_to_json(rep)) + "\n")
+        print(f"report -> {args.json}", file=sys.stderr)
+    agg = io.StringIO()
+    S.write_aggregates_csv(rep, agg)
+    sys.stderr.write(agg.getvalue())
+    return 0
+
+
 def main(argv: Optional[List[str]] = None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2103_10453_b200",
                                  description="partial Latin square extension solver")
@@ -211,12 +250,24 @@ def main(argv: Optional[List[str]] = None) -> int:
     v.add_argument("certificate", help="certificate file")
     v.add_argument("--exact", action="store_true", help="also compute the exact optimum (small instances)")
     v.add_argument("--node-budget", type=int, default=50_000_000, help="search-node cap for --exact")
+    b = sub.add_parser("bench", help="solve a directory of instances")
+    b.add_argument("suite", help="directory of instance files")
+    b.add_argument("--repeats", type=int, default=5, help="independent runs per instance (default 5)")
+    b.add_argument("--csv", default="", help="write per-run rows CSV here (default: stdout)")
+    b.add_argument("--json", default="", help="write the full report JSON here")
+    b.add_argument("--sweep-crossover", nargs="+", default=[], help="ablation: crossover modes to sweep")
+    b.add_argument("--sweep-matching", nargs="+", default=[], help="ablation: matching strategies to sweep")
+    b.add_argument("--sweep-pop", nargs="+", type=int, default=[], help="ablation: population sizes to sweep")
+    b.add_argument("--jobs", type=int, default=1, help="instances solved concurrently (default 1)")
+    _add_solver_flags(b)
     args = ap.parse_args(argv)
     try:
         if args.cmd == "generate":
             return cmd_generate(args)
         if args.cmd == "solve":
             return cmd_solve(args)
+        if args.cmd == "bench":
+            return cmd_bench(args)
         return cmd_verify(args)
     except Exception as e:  # noqa: BLE001 -- plse.cpp:312-315
         print(f"error: {e}", file=sys.stderr)

@@ -105,3 +105,33 @@ def test_time_limit_iteration_accounting_matches_stride(plse, orc):
         if res.best_f > 0:
             assert res.total_iterations % 4096 == 0
         assert seen and seen[-1].iterations == res.total_iterations
+
+
+def test_cli_bench_suite_rows_match_oracle(plse, orc, tmp_path):
+    """plse.cpp:199-250 / bench.hpp:196-250 on the device: every row is the canonical-tie run of
+    its kBench seed; aggregates and JSON follow the rows; reruns reproduce every non-timing field."""
+    import csv as _csv
+    suite = tmp_path / "suite"
+    r = _cli("generate", "-n", "8", "-r", "0.5", "-c", "2", "-o", str(suite), "--seed", "9")
+    assert r.returncode == 0
+    outs = []
+    for tag in "ab":
+        r = _cli("bench", str(suite), "--repeats", "2", "--pop", "8", "--gen-limit", "3", "--phase1-iters", "300",
+                 "--variant", "partial", "--seed", "4", "--sweep-crossover", "aux", "ux",
+                 "--csv", str(tmp_path / f"{tag}.csv"), "--json", str(tmp_path / f"{tag}.json"))
+        assert r.returncode == 0, r.stderr
+        outs.append(list(_csv.DictReader(open(tmp_path / f"{tag}.csv"))))
+    rows = outs[0]
+    assert len(rows) == 2 * 2 * 2
+    for a, b in zip(*outs):
+        assert {k: v for k, v in a.items() if k != "elapsed_seconds"} == \
+               {k: v for k, v in b.items() if k != "elapsed_seconds"}
+    for row in rows:
+        grid = plse.parse_instance(open(suite / f"{row['instance']}.txt").read())
+        o = orc.run(grid, p=8, seed=int(row["seed"]), generation_limit=3, phase1_iters=300, tie=oracle.TIE_CANON,
+                    crossover=oracle.X_AUX if row["crossover"] == "aux" else oracle.X_UX)
+        assert (int(row["score"]), int(row["f"]), int(row["iterations"]), int(row["generations"])) == \
+            (o["best_score"], o["best_f"], o["total_iterations"], o["generations"]), row
+    j = json.loads((tmp_path / "a.json").read_text())
+    assert [x["seed"] for x in j["rows"]] == [int(x["seed"]) for x in rows]
+    assert len(j["aggregates"]) == 2

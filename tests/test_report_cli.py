@@ -218,3 +218,52 @@ def test_generation_stats_match_reference(orc, ref):
         a = orc.run(gg, p=p, seed=s, generation_limit=4, phase1_iters=300, tie=oracle.TIE_REF, log_cap=8)
         b = ref.run(gg, p=p, seed=s, generation_limit=4, phase1_iters=300, log_cap=8)
         assert a["log"] == b["log"]
+
+
+def _bench_rows_from_ref_json(js):
+    from paper_2103_10453_b200 import suite as S
+    import json as J
+    d = J.loads(js)
+    return [S.BenchRow(instance=r["instance"], n=r["n"], r_percent=r["r"], id=r["id"], repeat=r["repeat"],
+                       seed=r["seed"], p=r["p"], crossover=r["crossover"], matching=r["matching"],
+                       variant=r["variant"], score=r["score"], f=r["f"], upper_bound=r["upper_bound"],
+                       proven_optimal=r["proven_optimal"], generations=r["generations"], iterations=r["iterations"],
+                       elapsed_seconds=r["elapsed_seconds"]) for r in d["rows"]]
+
+
+def test_bench_report_format_matches_reference(plse, ref, tmp_path):
+    """bench.hpp: rows CSV, aggregates CSV and report JSON of the same rows, byte for byte; the
+    kBench seed derivation and the QC-name parsing (bench.hpp:64-81, 228-233)."""
+    import io
+    from paper_2103_10453_b200 import report as R
+    from paper_2103_10453_b200 import suite as S
+    if not hasattr(ref.lib, "ref_bench"):
+        pytest.skip("nlohmann/json not found when oracle/_ref was built")
+    out = _cli("generate", "-n", "6", "-r", "0.45", "-c", "2", "-o", str(tmp_path), "--seed", "5")
+    assert out.returncode == 0
+    (tmp_path / "odd-name.txt").write_text(plse.serialize_instance(G["inst_6_0.8_3"]))
+    (tmp_path / "QC-7-10-zz.txt").write_text(plse.serialize_instance(G["inst_6_0.8_3"]))  # n mismatch -> fallback
+    rows_csv, agg_csv, js = ref.bench(str(tmp_path), 2, 77, 8, 2, phase1=200, crossovers="aux,ux",
+                                      matchings="nearest", pops="8,6")
+    rows = _bench_rows_from_ref_json(js)
+    assert len(rows) == 4 * 2 * 2 * 2
+    rep = S.BenchReport(rows=rows)
+    S.compute_aggregates(rep)
+    a, b = io.StringIO(), io.StringIO()
+    S.write_rows_csv(rep, a)
+    S.write_aggregates_csv(rep, b)
+    assert a.getvalue() == rows_csv
+    assert b.getvalue() == agg_csv
+    assert R.dumps(S.report_to_json(rep)) == js
+    tasks = S.suite_tasks(str(tmp_path))
+    assert [t.stem for t in tasks] == sorted({r.instance for r in rows})
+    k = 0
+    for t in tasks:
+        grid = plse.parse_instance(open(t.path).read())
+        for sidx in range(4):
+            for rep_i in range(2):
+                row = rows[k]
+                assert row.instance == t.stem and row.repeat == rep_i
+                assert row.seed == plse.derive_seed(77, 5, (t.instance_index * 4 + sidx) * 2 + rep_i)
+                assert (row.n, row.r_percent, row.id) == S.parse_instance_name(t.stem, grid)
+                k += 1
