@@ -169,6 +169,10 @@ void plse_graph_free(plse_graph_h* g);
 int plse_graph_view(const plse_graph_h* g, plse_graph* view); /* borrowed arrays, valid until free */
 /* coloring.hpp:171 to_grid: certificate grid [n*n] from a |V|-colouring (colours are symbols, 0 = empty) */
 int plse_to_grid(const plse_graph_h* g, const uint16_t* colors, uint16_t* grid);
+/* oracle.hpp:134 solve_exact (host, CPU): exact minimum f by branch and bound, one optimal certificate
+   (|V| colours), exact = 0 when the node budget ran out (default budget in the reference: 50'000'000) */
+int plse_solve_exact(const plse_graph_h* g, int64_t node_budget, int32_t* optimum_f, int32_t* exact, int64_t* nodes,
+                     uint16_t* certificate /* |V| */);
 /* verify.hpp:20 verify_certificate: problems joined by '\n' (NUL-terminated, truncated to cap;
    *problems_len = full length); legal = no problems, score = filled cells of the certificate */
 int plse_verify_certificate(int32_t n, const uint16_t* instance, int32_t m, const uint16_t* certificate,

@@ -85,6 +85,10 @@ class OrPlitsStats(C.Structure):
                 ("repaired", C.c_int32), ("final_f", C.c_int32), ("alg_bytes", C.c_double)]
 
 
+class OrExact(C.Structure):
+    _fields_ = [("optimum_f", C.c_int32), ("exact", C.c_int32), ("nodes", C.c_int64)]
+
+
 class RefRunResult(C.Structure):
     _fields_ = [("best_f", C.c_int32), ("best_score", C.c_int32), ("proven_optimal", C.c_int32),
                 ("stop_reason", C.c_int32), ("l", C.c_int32), ("upper_bound", C.c_int32),
@@ -145,6 +149,8 @@ class Oracle:
         L.or_eval.argtypes = [C.c_void_p, u16p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_gamma_build.argtypes = [C.c_void_p, u16p, i32p]
         L.or_repair.argtypes = [C.c_void_p, u16p]
+        L.or_solve_exact.argtypes = [C.c_void_p, C.c_int64, C.POINTER(OrExact), u16p]
+        L.or_enumerate_exact.argtypes = [C.c_void_p, C.POINTER(OrExact), u16p]
         L.or_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                C.c_int, C.POINTER(OrPlitsStats), C.c_void_p, C.c_int64]
         L.or_improve.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int,
@@ -225,6 +231,18 @@ class Oracle:
             m = min(trace_cap, st.iterations)
             res["trace"] = [{k: getattr(tr[i], k) for k, _ in OrStep._fields_} for i in range(m)]
         return res
+
+    def solve_exact(self, grid, node_budget=50_000_000, enumerate=False):
+        """oracle.hpp:134 solve_exact / 141 enumerate_exact -> (f, exact, nodes, certificate)"""
+        h = self._h(grid)
+        nv = self.lib.or_graph_nv(h)
+        cert = np.zeros(max(nv, 1), np.uint16)
+        r = OrExact()
+        if enumerate:
+            self.lib.or_enumerate_exact(h, C.byref(r), cert)
+        else:
+            self.lib.or_solve_exact(h, node_budget, C.byref(r), cert)
+        return r.optimum_f, bool(r.exact), r.nodes, cert[:nv]
 
     def plits(self, grid, colors, stream_seed, iters1=0, iters2=0, alpha=0.6, stop_f=0, tie=TIE_CANON,
               trace_cap=0):
@@ -354,6 +372,8 @@ class Reference:
                                     C.c_void_p, C.c_uint64, C.c_uint64, u16p]
         L.ref_init_population.argtypes = [C.c_void_p, C.c_int, C.c_uint64, u16p, C.c_void_p]
         L.ref_solve_exact.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+        L.ref_solve_exact_full.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.POINTER(C.c_int),
+                                           C.POINTER(C.c_int64), u16p]
         L.ref_run.argtypes = [C.c_int, u16p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64,
                               C.c_int,
                               C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int64, C.c_int64,
@@ -483,6 +503,15 @@ class Reference:
         ex = C.c_int()
         f = self.lib.ref_solve_exact(self._h(grid), C.byref(ex))
         return f, bool(ex.value)
+
+    def solve_exact_full(self, grid, node_budget=50_000_000, enumerate=False):
+        """-> (f, exact, nodes, certificate)"""
+        h = self._h(grid)
+        nv = self.lib.ref_graph_nv(h)
+        cert = np.zeros(max(nv, 1), np.uint16)
+        ex, nodes = C.c_int(), C.c_int64()
+        f = self.lib.ref_solve_exact_full(h, node_budget, int(enumerate), C.byref(ex), C.byref(nodes), cert)
+        return f, bool(ex.value), nodes.value, cert[:nv]
 
     def run(self, grid, p=64, alpha=0.6, gamma=10.0, beta=20.0, phase1_iters=0, variant=1, crossover=X_AUX,
             phase2_iters=0,

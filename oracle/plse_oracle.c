@@ -857,6 +857,133 @@ int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t s
     return 0;
 }
 
+
+/* ---------------------------------------------------------------- exact */
+
+typedef struct {
+    const or_graph* g;
+    int64_t budget, nodes;
+    int exhausted, best_f, prune;
+    int16_t* assign;
+    int32_t* used; /* [nv][n+1]: neighbours of v coloured k */
+    int16_t* best;
+} exact_state;
+
+static void exact_adjust(exact_state* x, int v, int k, int d) {
+    if (k == 0) return;
+    const or_graph* g = x->g;
+    for (int a = g->adj_off[v]; a < g->adj_off[v + 1]; ++a) x->used[(size_t)g->adj[a] * (g->n + 1) + k] += d;
+}
+
+/* oracle.hpp:64-119 ExactSolver::descend */
+static void exact_descend(exact_state* x, int zeros) {
+    const or_graph* g = x->g;
+    if (x->exhausted) return;
+    if (++x->nodes > x->budget) {
+        x->exhausted = 1;
+        return;
+    }
+    int pick = -1, pick_feasible = 0, forced = 0;
+    for (int v = 0; v < g->nv; ++v) {
+        if (x->assign[v] != -1) continue;
+        int feasible = 0;
+        for (int a = g->dom_off[v]; a < g->dom_off[v + 1]; ++a)
+            if (g->dom[a] != 0 && x->used[(size_t)v * (g->n + 1) + g->dom[a]] == 0) ++feasible;
+        if (feasible == 0) {
+            ++forced;
+            continue;
+        }
+        if (pick < 0 || feasible < pick_feasible) {
+            pick = v;
+            pick_feasible = feasible;
+        }
+    }
+    if (x->prune && zeros + forced >= x->best_f) return;
+    if (pick < 0) {
+        const int f = zeros + forced;
+        if (f < x->best_f) {
+            x->best_f = f;
+            for (int v = 0; v < g->nv; ++v) x->best[v] = x->assign[v] == -1 ? 0 : x->assign[v];
+        }
+        return;
+    }
+    for (int a = g->dom_off[pick]; a < g->dom_off[pick + 1]; ++a) {
+        const int k = g->dom[a];
+        if (k == 0 || x->used[(size_t)pick * (g->n + 1) + k] != 0) continue;
+        x->assign[pick] = (int16_t)k;
+        exact_adjust(x, pick, k, +1);
+        exact_descend(x, zeros);
+        exact_adjust(x, pick, k, -1);
+        if (x->exhausted) break;
+    }
+    if (!x->exhausted) {
+        x->assign[pick] = 0;
+        exact_descend(x, zeros + 1);
+    }
+    x->assign[pick] = -1;
+}
+
+int or_solve_exact(const or_graph* g, int64_t node_budget, or_exact_result* res, uint16_t* certificate) {
+    exact_state x;
+    memset(&x, 0, sizeof(x));
+    x.g = g;
+    x.budget = node_budget;
+    x.prune = 1;
+    x.best_f = g->nv;
+    x.assign = (int16_t*)malloc(sizeof(int16_t) * (g->nv + 1));
+    x.best = (int16_t*)calloc((size_t)g->nv + 1, sizeof(int16_t));
+    x.used = (int32_t*)calloc((size_t)g->nv * (g->n + 1) + 1, sizeof(int32_t));
+    for (int v = 0; v < g->nv; ++v) x.assign[v] = -1;
+    exact_descend(&x, 0);
+    res->optimum_f = x.best_f;
+    res->exact = !x.exhausted;
+    res->nodes = x.nodes;
+    for (int v = 0; v < g->nv; ++v) certificate[v] = (uint16_t)x.best[v];
+    free(x.assign);
+    free(x.best);
+    free(x.used);
+    return 0;
+}
+
+/* oracle.hpp:141-177 enumerate_exact */
+static void enum_rec(const or_graph* g, int v, int zeros, uint16_t* asg, uint16_t* best, int* best_f, int64_t* nodes) {
+    ++*nodes;
+    if (v == g->nv) {
+        if (zeros < *best_f) {
+            *best_f = zeros;
+            memcpy(best, asg, sizeof(uint16_t) * g->nv);
+        }
+        return;
+    }
+    for (int a = g->dom_off[v]; a < g->dom_off[v + 1]; ++a) {
+        const int k = g->dom[a];
+        if (k != 0) {
+            int ok = 1;
+            for (int b = g->adj_off[v]; b < g->adj_off[v + 1] && ok; ++b)
+                if (g->adj[b] < v && asg[g->adj[b]] == k) ok = 0;
+            if (!ok) continue;
+        }
+        asg[v] = (uint16_t)k;
+        enum_rec(g, v + 1, zeros + (k == 0), asg, best, best_f, nodes);
+    }
+    asg[v] = 0;
+}
+
+int or_enumerate_exact(const or_graph* g, or_exact_result* res, uint16_t* certificate) {
+    uint16_t* asg = (uint16_t*)calloc((size_t)g->nv + 1, sizeof(uint16_t));
+    uint16_t* best = (uint16_t*)calloc((size_t)g->nv + 1, sizeof(uint16_t));
+    int best_f = g->nv + 1;
+    int64_t nodes = 0;
+    enum_rec(g, 0, 0, asg, best, &best_f, &nodes);
+    res->optimum_f = best_f;
+    res->exact = 1;
+    res->nodes = nodes;
+    memcpy(certificate, best, sizeof(uint16_t) * g->nv);
+    free(asg);
+    free(best);
+    return 0;
+}
+
 /* ----------------------------------------------------------- population */
 
 /* population.hpp:41-61 */

@@ -145,6 +145,17 @@ int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t s
              int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
              or_plits_step* trace, int64_t trace_cap);
 
+/* ---- oracle.hpp:24-179 (exact optimum; recursive, for small |V|) ---------- */
+typedef struct {
+    int32_t optimum_f;
+    int32_t exact;   /* 0 when the node budget ran out */
+    int64_t nodes;
+} or_exact_result;
+/* solve_exact: fail-first branch and bound with pruning; certificate = |V| colours */
+int or_solve_exact(const or_graph* g, int64_t node_budget, or_exact_result* res, uint16_t* certificate);
+/* enumerate_exact: every legal colouring, vertices in index order, no pruning */
+int or_enumerate_exact(const or_graph* g, or_exact_result* res, uint16_t* certificate);
+
 /* ---- population.hpp:41-228, crossover.hpp:26-104, engine.hpp:88-106 --- */
 void or_cross_distances(int nv, int p, const uint16_t* members, const uint16_t* improved,
                         int32_t* cross, int32_t* fresh);

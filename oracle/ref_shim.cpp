@@ -294,6 +294,16 @@ void ref_init_population(const ref_graph* h, int p, uint64_t master_seed, uint16
     if (dist) std::memcpy(dist, pop.dist.data.data(), sizeof(int32_t) * p * p);
 }
 
+// oracle.hpp:134 solve_exact / 141 enumerate_exact with node counts and certificates
+int ref_solve_exact_full(const ref_graph* h, int64_t budget, int enumerate, int* exact, int64_t* nodes,
+                         uint16_t* cert) {
+    OracleResult r = enumerate ? enumerate_exact(h->g) : solve_exact(h->g, budget);
+    if (exact) *exact = r.exact ? 1 : 0;
+    if (nodes) *nodes = r.nodes;
+    if (cert) std::memcpy(cert, r.certificate.colors().data(), sizeof(uint16_t) * h->g.vertex_count());
+    return r.optimum_f;
+}
+
 // oracle.hpp:134 solve_exact
 int ref_solve_exact(const ref_graph* h, int* exact) {
     OracleResult r = solve_exact(h->g);

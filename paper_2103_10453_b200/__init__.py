@@ -20,6 +20,7 @@ this module                       reference
 ``run``                           engine.hpp:114    run (variant=partial)
 ``to_grid``                       coloring.hpp:171  to_grid (certificate)
 ``verify_certificate``            verify.hpp:20     verify_certificate
+``solve_exact``                   oracle.hpp:134    solve_exact (host branch and bound)
 ``report.result_to_json``         report.hpp:85     result_to_json
 ``python -m paper_2103_10453_b200``  tools/plse.cpp  generate / solve / verify
 ================================  =======================================
@@ -46,7 +47,7 @@ LIB_PATH = os.environ.get("PLSE_LIB") or os.path.join(HERE, "libplse_b200.so")  
 __all__ = [
     "generate_instance", "lsc_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
     "SolverConfig", "RunResult", "GenerationStats", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
-    "lib_path", "derive_seed", "to_grid", "verify_certificate", "VerifyReport", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
+    "lib_path", "derive_seed", "to_grid", "verify_certificate", "VerifyReport", "solve_exact", "ExactResult", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
 ]
 
 AUX, UX, NONE = 0, 1, 2
@@ -141,6 +142,8 @@ def _load() -> C.CDLL:
         "plse_graph_free": ([vp], None),
         "plse_graph_view": ([vp, C.POINTER(_Graph)], C.c_int),
         "plse_to_grid": ([vp, u16p, u16p], C.c_int),
+        "plse_solve_exact": ([vp, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                              u16p], C.c_int),
         "plse_verify_certificate": ([C.c_int32, u16p, C.c_int32, u16p, C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32), vp, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
         "plse_create": ([C.POINTER(_Graph), C.POINTER(_Params), C.c_int32, C.POINTER(vp)], C.c_int),
@@ -355,6 +358,31 @@ def preprocess(grid: np.ndarray) -> ReducedGraph:
                             arr(v.dom, int(dom_off[-1])), arr(v.prefilled, 3 * v.n_prefilled).reshape(-1, 3))
     finally:
         _lib.plse_graph_free(h)
+
+
+@dataclasses.dataclass
+class ExactResult:
+    """oracle.hpp:11-16"""
+    optimum_f: int
+    certificate: np.ndarray
+    exact: bool
+    nodes: int
+
+
+def solve_exact(instance: np.ndarray, node_budget: int = 50_000_000) -> ExactResult:
+    """oracle.hpp:134 solve_exact on the instance's reduced graph (host C++, branch and bound)."""
+    inst = np.ascontiguousarray(instance, np.uint16)
+    h = C.c_void_p()
+    _check(_lib.plse_preprocess(inst.shape[0], inst.reshape(-1), C.byref(h)))
+    try:
+        view = _Graph()
+        _check(_lib.plse_graph_view(h, C.byref(view)))
+        cert = np.zeros(max(view.vertex_count, 1), np.uint16)
+        f, ex, nodes = C.c_int32(), C.c_int32(), C.c_int64()
+        _check(_lib.plse_solve_exact(h, node_budget, C.byref(f), C.byref(ex), C.byref(nodes), cert))
+    finally:
+        _lib.plse_graph_free(h)
+    return ExactResult(int(f.value), cert[:view.vertex_count].copy(), bool(ex.value), int(nodes.value))
 
 
 def to_grid(instance: np.ndarray, graph: "ReducedGraph", solution: np.ndarray) -> np.ndarray:

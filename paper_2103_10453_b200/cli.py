@@ -171,9 +171,8 @@ def cmd_solve(args) -> int:
 
 
 def cmd_verify(args) -> int:
-    """plse.cpp:175-198 (without --exact: the exact oracle is CPU test infrastructure, oracle/)"""
-    if args.exact:
-        raise NotImplementedError("--exact needs the CPU exact oracle, which is test infrastructure here")
+    """plse.cpp:175-198"""
+    from . import solve_exact
     inst = load_instance(args.instance)
     cert = load_instance(args.certificate)
     rep = verify_certificate(inst, cert)
@@ -185,8 +184,12 @@ def cmd_verify(args) -> int:
     print(f"legal, score {rep.score}")
     g = preprocess(inst)
     n = inst.shape[0]
-    ub = n * n - 2 if g.l == 1 else n * n - g.l  # lsgraph.hpp compute_bounds
+    ub = n * n - 2 if g.l == 1 else n * n - g.l  # lsgraph.hpp:220-225 compute_bounds
     print(f"upper bound {ub} (l = {g.l})")
+    if args.exact:
+        ex = solve_exact(inst, args.node_budget)
+        optimum = n * n - g.l - ex.optimum_f
+        print(f"exact optimum {optimum}{'' if ex.exact else ' (budget exhausted)'}, gap {optimum - rep.score}")
     return 0
 
 

@@ -789,6 +789,18 @@ int plse_to_grid(const plse_graph_h* h, const uint16_t* colors, uint16_t* grid) 
     });
 }
 
+int plse_solve_exact(const plse_graph_h* h, int64_t node_budget, int32_t* optimum_f, int32_t* exact, int64_t* nodes,
+                     uint16_t* certificate) {
+    return guard(nullptr, [&] {
+        if (!h || node_budget < 0) throw std::invalid_argument("bad arguments");
+        auto r = plse_host::solve_exact(h->g, node_budget);
+        if (optimum_f) *optimum_f = r.optimum_f;
+        if (exact) *exact = r.exact ? 1 : 0;
+        if (nodes) *nodes = r.nodes;
+        if (certificate && !r.certificate.empty()) std::memcpy(certificate, r.certificate.data(), 2 * r.certificate.size());
+    });
+}
+
 int plse_verify_certificate(int32_t n, const uint16_t* instance, int32_t m, const uint16_t* certificate,
                             int32_t* legal, int32_t* score, char* problems, int64_t problems_cap,
                             int64_t* problems_len) {

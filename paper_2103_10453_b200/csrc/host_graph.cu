@@ -5,6 +5,7 @@
 #include <cstring>
 #include <sstream>
 #include <algorithm>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -208,6 +209,104 @@ VerifyResult verify_certificate(int n, const uint16_t* inst, int m, const uint16
     for (int q = 0; q < n * n; ++q) r.score += cert[q] != 0;
     r.legal = r.problems.empty();
     return r;
+}
+
+// oracle.hpp:24-136 ExactSolver / solve_exact: fail-first branch and bound (fewest feasible non-zero
+// colours first, lowest id on ties), colours ascending with 0 last, pruning on zeros + forced zeros
+// >= incumbent, node budget.  used(v, k) -- neighbours of v coloured k -- is the row + column count of
+// k, since the neighbours of a cell are exactly the vertices of its row and column.  The recursion of
+// the reference is an explicit stack here (|V| can be deep).
+ExactResult solve_exact(const GraphH& g, int64_t node_budget) {
+    const int n = g.n, nv = g.nv, w = n + 1;
+    ExactResult res;
+    std::vector<int16_t> assign(nv, -1), best(nv, 0);
+    std::vector<int32_t> rcnt((size_t)n * w, 0), ccnt((size_t)n * w, 0);
+    int best_f = nv;
+    bool exhausted = false;
+    int64_t nodes = 0;
+    auto used = [&](int v, int k) { return rcnt[(size_t)g.cell_row[v] * w + k] + ccnt[(size_t)g.cell_col[v] * w + k]; };
+    auto adjust = [&](int v, int k, int d) {
+        rcnt[(size_t)g.cell_row[v] * w + k] += d;
+        ccnt[(size_t)g.cell_col[v] * w + k] += d;
+    };
+    struct Frame {
+        int zeros, pick, ki, applied;
+        int stage;  // 0 = enter, 1 = colours, 2 = zero branch done
+    };
+    std::vector<Frame> st;
+    st.push_back({0, -1, 0, 0, 0});
+    while (!st.empty()) {
+        Frame& fr = st.back();
+        if (fr.stage == 0) {
+            if (exhausted || ++nodes > node_budget) {
+                exhausted = true;
+                st.pop_back();
+                continue;
+            }
+            int pick = -1, pick_feasible = 0, forced = 0;
+            for (int v = 0; v < nv; ++v) {
+                if (assign[v] != -1) continue;
+                int feasible = 0;
+                for (int a = g.dom_off[v]; a < g.dom_off[v + 1]; ++a)
+                    if (g.dom[a] != 0 && used(v, g.dom[a]) == 0) ++feasible;
+                if (feasible == 0) {
+                    ++forced;
+                    continue;
+                }
+                if (pick < 0 || feasible < pick_feasible) {
+                    pick = v;
+                    pick_feasible = feasible;
+                }
+            }
+            if (fr.zeros + forced >= best_f) {  // prune (solve_exact sets prune)
+                st.pop_back();
+                continue;
+            }
+            if (pick < 0) {
+                best_f = fr.zeros + forced;
+                for (int v = 0; v < nv; ++v) best[v] = assign[v] == -1 ? 0 : assign[v];
+                st.pop_back();
+                continue;
+            }
+            fr.pick = pick;
+            fr.ki = g.dom_off[pick];
+            fr.stage = 1;
+        }
+        if (fr.stage == 1) {
+            if (fr.applied) {
+                adjust(fr.pick, fr.applied, -1);
+                fr.applied = 0;
+                if (exhausted) fr.ki = g.dom_off[fr.pick + 1];
+            }
+            while (fr.ki < g.dom_off[fr.pick + 1]) {
+                const int k = g.dom[fr.ki++];
+                if (k == 0 || used(fr.pick, k) != 0) continue;
+                assign[fr.pick] = (int16_t)k;
+                adjust(fr.pick, k, +1);
+                fr.applied = k;
+                break;
+            }
+            if (fr.applied) {
+                const int z = fr.zeros;
+                st.push_back({z, -1, 0, 0, 0});
+                continue;
+            }
+            fr.stage = 2;
+            if (!exhausted) {
+                assign[fr.pick] = 0;
+                const int z = fr.zeros + 1;
+                st.push_back({z, -1, 0, 0, 0});
+                continue;
+            }
+        }
+        assign[fr.pick] = -1;
+        st.pop_back();
+    }
+    res.optimum_f = best_f;
+    res.exact = !exhausted;
+    res.nodes = nodes;
+    res.certificate.assign(best.begin(), best.end());
+    return res;
 }
 
 }  // namespace plse_host

@@ -29,6 +29,14 @@ struct VerifyResult {
 std::vector<uint16_t> to_grid(const GraphH& g, const uint16_t* colors);
 VerifyResult verify_certificate(int n, const uint16_t* inst, int m, const uint16_t* cert);
 
+struct ExactResult {
+    int optimum_f = 0;
+    bool exact = true;
+    int64_t nodes = 0;
+    std::vector<uint16_t> certificate;  // |V| colours
+};
+ExactResult solve_exact(const GraphH& g, int64_t node_budget);
+
 }  // namespace plse_host
 
 struct plse_graph_h {
