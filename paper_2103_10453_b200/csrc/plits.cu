@@ -45,10 +45,11 @@ struct PlitsWarp {
     uint64_t* rp;     // [n][NP][W] row colour-count planes
     uint64_t* cp;     // [n][NP][W] column colour-count planes
     uint32_t* A;      // [32 * lane_words] active vertices; word v >> 5 (lane-owned blocks)
-    uint16_t* list;   // [nv] active ids, ascending
+    uint16_t* list;   // [nv] the step's active ids (ascending); after the selection: scratch for the
+                      //      cells whose cached minimum is refreshed
     int32_t* vmin;    // [nv] per active vertex: tabu-blind minimum delta of its moves (refreshed when its
                       //      row or column changes)
-    uint8_t* vcnt;    // [nv] per listed vertex: admissible moves at the step's level
+    uint8_t* vcnt;    // [nv] per active vertex at the step's level: its admissible moves
 };
 
 template <int W>
@@ -205,6 +206,35 @@ __device__ __forceinline__ void plane_step(uint64_t* P, int k, bool inc) {
     }
 }
 
+// one lane moves a cell of this line from colour `from` to `to`: the two single-bit ripples (-1 at
+// `from`, +1 at `to`; 0 = uncoloured is not counted) computed in registers, NP x W words stored back
+template <int W, int NP>
+__device__ __forceinline__ void plane_move(uint64_t* P, int from, int to) {
+    uint64_t x[NP][W];
+#pragma unroll
+    for (int b = 0; b < NP; ++b)
+#pragma unroll
+        for (int q = 0; q < W; ++q) x[b][q] = P[b * W + q];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t borrow = (from && (from >> 6) == q) ? 1ULL << (from & 63) : 0ULL;
+        uint64_t carry = (to && (to >> 6) == q) ? 1ULL << (to & 63) : 0ULL;
+#pragma unroll
+        for (int b = 0; b < NP; ++b) {
+            const uint64_t old = x[b][q];
+            x[b][q] = old ^ borrow;
+            borrow &= ~old;
+            const uint64_t mid = x[b][q];
+            x[b][q] = mid ^ carry;
+            carry &= mid;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NP; ++b)
+#pragma unroll
+        for (int q = 0; q < W; ++q) P[b * W + q] = x[b][q];
+}
+
 template <int W>
 __device__ __forceinline__ bool plits_is_active(const Graph<W>& g, const PlitsWarp& s, int u) {
     constexpr int NP = PlitsK<W>::NP;
@@ -226,22 +256,53 @@ __device__ __forceinline__ int vertex_min(const Graph<W>& g, const PlitsWarp& s,
     return vm;
 }
 
-// after a move in row r / column c: re-classify those cells (plits.hpp:193-212) and refresh the
-// cached minimum of every active one -- no other vertex's gamma changed
+// after a move of colour `from` -> `to` in row r / column c: re-classify those cells
+// (plits.hpp:193-212) and refresh the cached minimum of each active one whose moves could have
+// changed: it was inactive, or its own colour or a colour of its domain is `from` or `to` (only the
+// counts of those two colours changed, and only in its row or column).  Nothing else moved.
 template <int W>
-__device__ __forceinline__ void plits_membership(const Graph<W>& g, const PlitsWarp& s, int r, int c, int wf, int wc,
-                                                 int lane) {
+__device__ __forceinline__ void plits_membership(const Graph<W>& g, const PlitsWarp& s, int r, int c, int from, int to,
+                                                 int wf, int wc, int lane) {
     const int nr = g.rs[r + 1] - g.rs[r];
     const int tot = nr + g.cs[c + 1] - g.cs[c];
-    for (int x = lane; x < tot; x += 32) {
-        const int u = x < nr ? g.rs[r] + x : g.cl[g.cs[c] + x - nr];
-        const uint32_t bit = 1u << (u & 31);
-        if (plits_is_active<W>(g, s, u)) {
-            atomicOr(&s.A[u >> 5], bit);
-            s.vmin[u] = vertex_min<W>(g, s, u, wf, wc);
-        } else {
-            atomicAnd(&s.A[u >> 5], ~bit);
+    uint64_t ft[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+        ft[q] = ((from >> 6) == q && from ? 1ULL << (from & 63) : 0ULL) | ((to >> 6) == q && to ? 1ULL << (to & 63) : 0ULL);
+    // classify every cell, collect the ones whose cached minimum must be refreshed ...
+    int nredo = 0;
+    for (int x0 = 0; x0 < tot; x0 += 32) {
+        const int x = x0 + lane;
+        bool need = false;
+        int u = -1;
+        if (x < tot) {
+            u = x < nr ? g.rs[r] + x : g.cl[g.cs[c] + x - nr];
+            const uint32_t bit = 1u << (u & 31);
+            if (plits_is_active<W>(g, s, u)) {
+                const bool was = (s.A[u >> 5] & bit) != 0;
+                const int cu = s.col[u];
+                need = !was || (cu && (cu == from || cu == to));
+                if (!need) {
+                    const uint16_t rc = g.cell[u];
+                    uint64_t d[W];
+                    dom_mask<W>(g, rc >> 8, rc & 0xFF, d);
+#pragma unroll
+                    for (int q = 0; q < W; ++q) need |= (d[q] & ft[q]) != 0;
+                }
+                if (!was) atomicOr(&s.A[u >> 5], bit);
+            } else {
+                atomicAnd(&s.A[u >> 5], ~bit);
+            }
         }
+        const unsigned bal = __ballot_sync(kFull, need);
+        if (need) s.list[nredo + __popc(bal & ((1u << lane) - 1))] = (uint16_t)u;
+        nredo += __popc(bal);
+    }
+    __syncwarp();
+    // ... and refresh them in one round (the moved vertex may appear twice: same value)
+    for (int x = lane; x < nredo; x += 32) {
+        const int u = s.list[x];
+        s.vmin[u] = vertex_min<W>(g, s, u, wf, wc);
     }
 }
 
@@ -363,6 +424,9 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     uint8_t* col = s.col;
     uint8_t* best_row = a.improved + (size_t)i * g.nvpad;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
+    unsigned long long* prof = kDebug ? a.prof : nullptr;
+    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // steps, list, level, select, move, step, level iters, sum na
+    long long tp0 = 0, tp1 = 0;
 
     // ---- tabu clock of this warp slot (two phases, each followed by a skip of tenure_cap + 2)
     uint32_t base = *slot_clock;
@@ -422,8 +486,18 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             const int64_t thr64 = best_scaled - cur_scaled;  // a tabu move is admissible iff delta < thr
             const int thr = (int)max(min(thr64, (int64_t)INT_MAX), (int64_t)INT_MIN);
             const int active_before = active;
+            if (prof) tp0 = tp1 = clock64();
+            auto tick = [&](int slot) {
+                if (prof) {
+                    const long long x = clock64();
+                    pc[slot] += (unsigned long long)(x - tp1);
+                    tp1 = x;
+                }
+            };
 
-            // ---- compact the active set into ascending ids; lane L takes the L-th contiguous block
+            if (prof) pc[7] += (unsigned)active;
+            // ---- compact the active set into ascending ids; lane L takes the L-th contiguous block, so
+            // lanes in order then list order is the ascending (v, k) order of the canonical rule
             int na = 0;
             {
                 int my = 0;
@@ -447,61 +521,67 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             __syncwarp();
             const int per = (na + 31) >> 5;
             const int i_lo = min(na, lane * per), i_hi = min(na, i_lo + per);
-
+            tick(1);
             // ---- the lowest delta level holding an admissible candidate: its tabu-blind minimum from
             // the cached per-vertex minima, then the until[][] reads of the candidates at that level only
             bool has_prev = false;
             int prev = 0, dl = INT_MAX, N = 0, lc = 0;
             bool asp_all = false;
-            int c_idx = -1;   // first listed vertex of this lane with admissible moves, and its masks
+            int c_v = -1, c_d0 = 0, c_dbase = 0;  // this lane's first vertex with admissible moves at dl
             uint64_t c_adm[W];
             bool c_adm0 = false;
             for (;;) {
                 int lmin = INT_MAX;
                 for (int idx = i_lo; idx < i_hi; ++idx) {
-                    const int v = s.list[idx];
-                    int vm;
-                    if (!has_prev) {
-                        vm = s.vmin[v];
-                    } else {
-                        VertexMoves<W> m;
-                        vertex_moves<W>(g, s, v, wf, wc, m);
-                        sliced_ge<W, NB>(m.S, floor_div(prev - m.dbase, wc) + 1, m.M);
-                        vm = (m.cur && m.d0 > prev) ? m.d0 : INT_MAX;
-                        if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
+                    {
+                        const int v = s.list[idx];
+                        int vm;
+                        if (!has_prev) {
+                            vm = s.vmin[v];
+                        } else {
+                            VertexMoves<W> m;
+                            vertex_moves<W>(g, s, v, wf, wc, m);
+                            sliced_ge<W, NB>(m.S, floor_div(prev - m.dbase, wc) + 1, m.M);
+                            vm = (m.cur && m.d0 > prev) ? m.d0 : INT_MAX;
+                            if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
+                        }
+                        lmin = min(lmin, vm);
                     }
-                    lmin = min(lmin, vm);
                 }
                 dl = __reduce_min_sync(kFull, lmin);
                 if (dl == INT_MAX) break;  // every candidate tabu
                 asp_all = dl < thr;
                 lc = 0;
-                c_idx = -1;
+                c_v = -1;
                 for (int idx = i_lo; idx < i_hi; ++idx) {
-                    const int v = s.list[idx];
-                    int cnt = 0;
-                    if (has_prev || s.vmin[v] <= dl) {
+                    {
+                        const int v = s.list[idx];
+                        if (!has_prev && s.vmin[v] > dl) continue;
                         VertexMoves<W> m;
                         vertex_moves<W>(g, s, v, wf, wc, m);
                         uint64_t adm[W];
                         bool adm0;
-                        cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, t, adm, adm0);
-                        if (cnt && c_idx < 0) {
-                            c_idx = idx;
+                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, t, adm, adm0);
+                        if (cnt && c_v < 0) {
+                            c_v = v;
                             c_adm0 = adm0;
+                            c_d0 = m.d0;
+                            c_dbase = m.dbase;
 #pragma unroll
-                            for (int q = 0; q < W; ++q) c_adm[q] = adm[q];
+                            for (int qq = 0; qq < W; ++qq) c_adm[qq] = adm[qq];
                         }
+                        s.vcnt[v] = (uint8_t)cnt;
+                        lc += cnt;
                     }
-                    s.vcnt[idx] = (uint8_t)cnt;
-                    lc += cnt;
                 }
                 N = (int)__reduce_add_sync(kFull, (unsigned)lc);
                 if (N > 0) break;
                 has_prev = true;
                 prev = dl;
+                if (prof) ++pc[6];
             }
             __syncwarp();
+            tick(2);
             if (N == 0) {
                 // every candidate tabu: the clock still advances (plits.hpp:178-179)
                 if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)active_before;
@@ -514,7 +594,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 continue;
             }
 
-            // ---- the r-th admissible candidate in ascending (v, k): lane blocks are in id order
+            // ---- the r-th admissible candidate in ascending (v, k)
             const uint32_t rnk = __umulhi(h1, (uint32_t)N);
             int incl = lc;
 #pragma unroll
@@ -523,36 +603,47 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 incl += lane >= d ? x : 0;
             }
             const bool owner = (uint32_t)(incl - lc) <= rnk && rnk < (uint32_t)incl;
-            int sel_idx = -1, sv = -1, sk = 0, sdc = 0;
+            int sv = -1, sk = 0, sdc = 0;
             if (owner) {
                 int local = (int)rnk - (incl - lc);
-                for (int idx = i_lo; idx < i_hi; ++idx) {
-                    const int cnt = s.vcnt[idx];
-                    if (local < cnt) {
-                        sel_idx = idx;
-                        break;
+                for (int idx = i_lo; idx < i_hi && sv < 0; ++idx) {
+                    {
+                        const int v = s.list[idx];
+                        if (!has_prev && s.vmin[v] > dl) continue;
+                        const int cnt = s.vcnt[v];
+                        if (local < cnt) {
+                            sv = v;
+                            break;
+                        }
+                        local -= cnt;
                     }
-                    local -= cnt;
                 }
-                sv = s.list[sel_idx];
-                VertexMoves<W> m;
-                vertex_moves<W>(g, s, sv, wf, wc, m);
                 uint64_t adm[W];
                 bool adm0;
-                if (sel_idx == c_idx) {
+                int d0, dbase, cur;
+                if (sv == c_v) {
                     adm0 = c_adm0;
+                    d0 = c_d0;
+                    dbase = c_dbase;
 #pragma unroll
                     for (int q = 0; q < W; ++q) adm[q] = c_adm[q];
                 } else {
+                    VertexMoves<W> m;
+                    vertex_moves<W>(g, s, sv, wf, wc, m);
                     level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, t, adm, adm0);
+                    d0 = m.d0;
+                    dbase = m.dbase;
                 }
+                cur = col[sv];
                 if (adm0 && local == 0)
                     sk = 0;
                 else
                     sk = nth_bit_w<W>(adm, local - (adm0 ? 1 : 0));
-                const int gcur = m.cur ? sliced_val<W, NB>(m.S, m.cur) - 2 : 0;
-                sdc = (sk ? sliced_val<W, NB>(m.S, sk) : 0) - gcur;
+                // every candidate at level dl has gamma[v][k] = (dl - dbase) / wc; gamma[v][cur] from d0
+                const int gcur = cur ? (wf - d0) / wc : 0;
+                sdc = (sk ? (dl - dbase) / wc : 0) - gcur;
             }
+            tick(3);
             const int wl = __ffs(__ballot_sync(kFull, owner)) - 1;
             const int vs = __shfl_sync(kFull, sv, wl);
             const int ks = __shfl_sync(kFull, sk, wl);
@@ -568,13 +659,13 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             __syncwarp();
             const uint16_t rcs = g.cell[vs];
             const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-            if (lane == 0) col[vs] = (uint8_t)ks;
-            if (lane == 0 && from) plane_step<W, NP>(s.rp + (size_t)rs_ * NP * W, from, false);
-            if (lane == 1 && ks) plane_step<W, NP>(s.rp + (size_t)rs_ * NP * W, ks, true);
-            if (lane == 2 && from) plane_step<W, NP>(s.cp + (size_t)cs_ * NP * W, from, false);
-            if (lane == 3 && ks) plane_step<W, NP>(s.cp + (size_t)cs_ * NP * W, ks, true);
+            if (lane == 0) {
+                col[vs] = (uint8_t)ks;
+                plane_move<W, NP>(s.rp + (size_t)rs_ * NP * W, from, ks);
+            }
+            if (lane == 1) plane_move<W, NP>(s.cp + (size_t)cs_ * NP * W, from, ks);
             __syncwarp();
-            plits_membership<W>(g, s, rs_, cs_, wf, wc, lane);
+            plits_membership<W>(g, s, rs_, cs_, from, ks, wf, wc, lane);
             __syncwarp();
             {
                 int al = 0;
@@ -603,6 +694,11 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
+            tick(4);
+            if (prof) {
+                pc[5] += (unsigned long long)(clock64() - tp0);
+                ++pc[0];
+            }
             ++j;
             ++J;
         }
@@ -653,7 +749,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             }
             if (lane == 1) plane_step<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k, false);
             __syncwarp();
-            plits_membership<W>(g, s, rc >> 8, rc & 0xFF, 2, 2 * nv, lane);
+            plits_membership<W>(g, s, rc >> 8, rc & 0xFF, k, 0, 2, 2 * nv, lane);
             ++f;
             __syncwarp();
         }
@@ -668,6 +764,11 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         a.bytes[i] = acc;
         *slot_clock = base;
         if (race_flag && best_f <= a.race_f) atomicExch(const_cast<int*>(race_flag), 1);
+        if (prof) {
+#pragma unroll
+            for (int z = 0; z < 8; ++z) atomicAdd(prof + z, pc[z]);
+            atomicAdd(prof + 8, 1ULL);
+        }
     }
     __syncwarp();
 }
@@ -757,7 +858,7 @@ const void* plits_kernel_ptr(int W, bool debug) {
 }
 
 cudaError_t launch_plits(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    const bool debug = a.trace != nullptr;
+    const bool debug = a.trace != nullptr || a.prof != nullptr;
     if (W == 1) {
         if (debug)
             k_plits<1, true><<<grid, threads, smem, st>>>(a);
