@@ -61,7 +61,7 @@ enum { PLSE_X_AUX = 0, PLSE_X_UX = 1, PLSE_X_NONE = 2 };
 enum { PLSE_M_NEAREST = 0, PLSE_M_RANDOM = 1 };
 enum { PLSE_E_RUN = 0, PLSE_E_GENERATION = 1, PLSE_E_OFF = 2 };
 enum { PLSE_V_MPMA = 0, PLSE_V_PARTIAL = 1 };
-enum { PLSE_TIE_CANON = 0 };
+enum { PLSE_TIE_CANON = 0, PLSE_TIE_REF = 1 };
 enum { PLSE_STOP_OPTIMAL = 0, PLSE_STOP_TIME = 1, PLSE_STOP_ITERS = 2, PLSE_STOP_GENS = 3, PLSE_STOP_TRIVIAL = 4,
        PLSE_STOP_TARGET = 5 /* harness: target_score reached */ };
 
@@ -91,7 +91,8 @@ typedef struct {
     int32_t crossover;      /* PLSE_X_* */
     int32_t matching;       /* PLSE_M_* */
     int32_t exclusion;      /* PLSE_E_* */
-    int32_t tie_mode;       /* PLSE_TIE_CANON */
+    int32_t tie_mode;       /* PLSE_TIE_CANON (throughput) or PLSE_TIE_REF (the reference's reservoir
+                               draws: bit-exact trajectories, Partial-MPMA only) */
     uint64_t master_seed;
     int64_t p_total;        /* stream index space: gen*p_total + offset + i; 0 -> p */
     int64_t offset;         /* first global individual of this shard */

@@ -47,7 +47,7 @@ LIB_PATH = os.environ.get("PLSE_LIB") or os.path.join(HERE, "libplse_b200.so")  
 __all__ = [
     "generate_instance", "lsc_instance", "parse_instance", "serialize_instance", "preprocess", "ReducedGraph",
     "SolverConfig", "RunResult", "GenerationStats", "run", "DevicePopulation", "UpdateInfo", "PlseCudaError",
-    "lib_path", "derive_seed", "to_grid", "verify_certificate", "VerifyReport", "solve_exact", "ExactResult", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
+    "lib_path", "TIE_CANON", "TIE_REF", "derive_seed", "to_grid", "verify_certificate", "VerifyReport", "solve_exact", "ExactResult", "AUX", "UX", "NONE", "NEAREST", "RANDOM", "RUN", "GENERATION", "OFF",
 ]
 
 AUX, UX, NONE = 0, 1, 2
@@ -55,6 +55,7 @@ NEAREST, RANDOM = 0, 1
 RUN, GENERATION, OFF = 0, 1, 2
 MPMA, PARTIAL = 0, 1
 MEMBERS, OFFSPRING, IMPROVED = 0, 1, 2
+TIE_CANON, TIE_REF = 0, 1
 DIST, CROSS, FRESH = 0, 1, 2
 STOP_NAMES = ["optimal", "time_limit", "iteration_limit", "generation_limit", "trivial", "target"]
 
@@ -426,10 +427,11 @@ class SolverConfig:
     target_score: float = 0.0
     race: bool = False  # with target_score: device-global early exit (time-to-target, not parity mode)
     workers: int = 1  # reported in the result JSON (report.hpp:76); the device path uses one host thread
+    tie_mode: int = 0  # TIE_CANON (throughput) or TIE_REF (the reference's reservoir draws, bit-exact; partial only)
 
     def _params(self) -> _Params:
         return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,
-                       self.exclusion, 0, self.master_seed & (2**64 - 1), self.p_total, self.offset, self.variant,
+                       self.exclusion, self.tie_mode, self.master_seed & (2**64 - 1), self.p_total, self.offset, self.variant,
                        self.phase2_iters)
 
 

@@ -103,6 +103,7 @@ struct plse_ctx {
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
     bool half_warp = false;  // k_improve (one individual per warp) vs k_improve_hw (PLSE_IMPROVE_KERNEL=hw)
     bool plits = false;      // variant MPMA: k_plits (plits.cu) is the improve kernel
+    bool ref_ties = false;   // tie_mode REF: k_improve_ref (improve_ref.cu)
     int64_t budget2 = 0;     // PLITS phase-2 budget
     int lane_words16 = 1;
     size_t smem = 0;
@@ -218,7 +219,9 @@ void validate_params(const plse_params& p) {
     if (p.crossover < 0 || p.crossover > 2) throw std::invalid_argument("unknown crossover mode");
     if (p.matching < 0 || p.matching > 1) throw std::invalid_argument("unknown matching strategy");
     if (p.exclusion < 0 || p.exclusion > 2) throw std::invalid_argument("unknown exclusion scope");
-    if (p.tie_mode != PLSE_TIE_CANON) throw Unsupported("only the canonical tie-break runs on the device");
+    if (p.tie_mode != PLSE_TIE_CANON && p.tie_mode != PLSE_TIE_REF) throw std::invalid_argument("unknown tie mode");
+    if (p.tie_mode == PLSE_TIE_REF && p.variant == PLSE_V_MPMA)
+        throw Unsupported("the reference tie-break runs on the device for the Partial-MPMA variant only");
     if (p.p_total < 0 || p.offset < 0) throw std::invalid_argument("negative island coordinates");
 }
 
@@ -293,6 +296,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->budget = pp->phase1_iters > 0 ? pp->phase1_iters : 100LL * nv;
     c->budget2 = pp->phase2_iters > 0 ? pp->phase2_iters : 2LL * nv;
     c->plits = pp->variant == PLSE_V_MPMA;
+    c->ref_ties = pp->tie_mode == PLSE_TIE_REF;
     if (c->budget + (c->plits ? c->budget2 : 0) >= (1LL << 30)) throw Unsupported("budget must be < 2^30 iterations");
     if (pp->alpha * nv >= (double)(1 << 29)) throw Unsupported("alpha * |V| must be < 2^29 (tabu tenure range)");
     c->tenure_cap = 10u + (uint32_t)(pp->alpha * (double)nv);
@@ -425,16 +429,23 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_work = dalloc<int>(1);
 
     // ---- improve launch shape: maximise resident individuals per SM
-    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL")) c->half_warp = std::string(env) == "hw" && !c->plits;
+    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL"))
+        c->half_warp = std::string(env) == "hw" && !c->plits && !c->ref_ties;
     c->lane_words16 = (nwords + 15) / 16;
     const void* kern = c->plits       ? plits_kernel_ptr(W, false)
+                       : c->ref_ties  ? improve_ref_kernel_ptr(W, false)
                        : c->half_warp ? improve_hw_kernel_ptr(W, false)
                                       : improve_kernel_ptr(W, false);
     const void* kern_dbg = c->plits       ? plits_kernel_ptr(W, true)
+                           : c->ref_ties  ? improve_ref_kernel_ptr(W, true)
                            : c->half_warp ? improve_hw_kernel_ptr(W, true)
                                           : improve_kernel_ptr(W, true);
     size_t graph_bytes = 0, warp_bytes = 0;
-    if (c->plits) {
+    if (c->ref_ties) {
+        const RefSmemLayout L = improve_ref_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+        graph_bytes = L.graph_bytes;
+        warp_bytes = L.warp_bytes;
+    } else if (c->plits) {
         const PlitsSmemLayout L = plits_smem_layout(n, nv, c->nvpad, c->lane_words, W);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
@@ -577,6 +588,8 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     CK(cudaEventRecord(c->ev0, c->st));
     if (c->plits)
         c->launched(launch_plits(a, c->W, c->grid, c->threads, c->smem, c->st));
+    else if (c->ref_ties)
+        c->launched(launch_improve_ref(a, c->W, c->grid, c->threads, c->smem, c->st));
     else if (c->half_warp)
         c->launched(launch_improve_hw(a, c->W, c->grid, c->threads, c->smem, c->st));
     else

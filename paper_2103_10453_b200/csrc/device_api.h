@@ -197,6 +197,41 @@ __host__ __device__ inline PlitsSmemLayout plits_smem_layout(int n, int nv, int 
 const void* plits_kernel_ptr(int W, bool debug);
 cudaError_t launch_plits(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 
+// PartialCol with the reference's tie-break (improve_ref.cu): improve's layout plus the IndexSet-ordered
+// uncoloured list and a 32-vertex mask staging area per warp
+struct RefSmemLayout {
+    size_t graph_bytes, warp0, warp_bytes, w_col, w_colT, w_R, w_C, w_U, w_el, w_msk;
+};
+
+__host__ __device__ inline RefSmemLayout improve_ref_smem_layout(int n, int nv, int nvpad, int lane_words, int W) {
+    const ImproveSmemLayout G = improve_smem_layout(n, nv, nvpad, lane_words, W);
+    RefSmemLayout L;
+    L.graph_bytes = G.graph_bytes;
+    L.warp0 = G.warp0;
+    size_t w = 0;
+    L.w_col = w;
+    w += (size_t)nvpad;
+    L.w_colT = w;
+    w += (size_t)nvpad;
+    w = align_up(w, 16);
+    L.w_R = w;
+    w += (size_t)n * W * 8;
+    L.w_C = w;
+    w += (size_t)n * W * 8;
+    L.w_U = w;
+    w += (size_t)32 * lane_words * 4;
+    w = align_up(w, 16);
+    L.w_el = w;
+    w += align_up((size_t)nv * 2, 16);
+    L.w_msk = w;
+    w += (size_t)32 * 3 * W * 8;
+    L.warp_bytes = align_up(w, 16);
+    return L;
+}
+
+const void* improve_ref_kernel_ptr(int W, bool debug);
+cudaError_t launch_improve_ref(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
+
 const void* improve_hw_kernel_ptr(int W, bool debug);
 cudaError_t launch_improve_hw(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 

@@ -172,6 +172,129 @@ __device__ __forceinline__ void snapshot(const uint8_t* col, uint8_t* dst, int n
     for (int t = lane; t < nvpad / 16; t += 32) d4[t] = s4[t];
 }
 
-// kDebug: per-step trace (plse_trace) and clock64 instrumentation (PLSE_PROFILE)
+// position of the unique byte == k in bytes [a, b) of buf, or -1 (warp-uniform result)
+__device__ __forceinline__ int warp_find_byte(const uint8_t* buf, int a, int b, int k, bool enable, int lane) {
+    if (!enable) return -1;
+    const uint32_t k4 = (uint32_t)k * 0x01010101u;
+    for (int base = a & ~3; base < b; base += 128) {
+        const int wpos = base + 4 * lane;
+        uint32_t hit = 0;
+        if (wpos < b) {
+            const uint32_t w = reinterpret_cast<const uint32_t*>(buf)[wpos >> 2] ^ k4;
+            const uint32_t z = ~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;  // 0x80 where byte == k
+            const int lo = a - wpos, hi = b - wpos;  // valid bytes q: lo <= q < hi
+            uint32_t valid = 0x80808080u;
+            if (lo > 0) valid &= 0x80808080u << (8 * min(lo, 4));
+            if (hi < 4) valid &= 0x80808080u >> (8 * (4 - max(hi, 0)));
+            hit = z & valid;
+        }
+        const unsigned bal = __ballot_sync(kFull, hit != 0);
+        if (bal) {
+            const int src = __ffs(bal) - 1;
+            return __shfl_sync(kFull, wpos + ((__ffs(hit) - 1) >> 3), src);
+        }
+    }
+    return -1;
+}
+
+// Shared by the PartialCol kernels (improve.cu canonical policy, improve_ref.cu reference policy):
+// load offspring i, reset the slot's tabu caches, K1 conflict counts (coloring.hpp:105-116), K1b greedy
+// repair (partial.hpp:22-39), occupancy masks R/C, uncoloured bitmask U and the column-major copy.
+// Returns f after the repair.
+template <int W>
+__device__ int partial_prologue(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
+                                uint8_t* conf, int i, int lane) {
+    const int n = g.n, nv = g.nv;
+    const int B = 32 * g.lane_words;
+    const int v_lo = lane * B;
+    const int v_hi = min(nv, v_lo + B);
+    uint8_t* col = s.col;
+    uint8_t* colT = s.colT;
+    // ---- load the offspring (u8, row stride nvpad) and reset this slot's tabu caches
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.offspring + (size_t)i * g.nvpad);
+        uint4* d4 = reinterpret_cast<uint4*>(col);
+        for (int x = lane; x < g.nvpad / 16; x += 32) d4[x] = src[x];
+        const TabuRec z{0, 0, 0, 0};
+        for (int x = lane; x < nv; x += 32) rec[x] = z;
+    }
+    __syncwarp();
+
+    // ---- K1: conflict counts gamma[v][col v] of coloured vertices (coloring.hpp:105-116)
+    for (int v = v_lo; v < v_hi; ++v) {
+        const int k = col[v];
+        int cnt = 0;
+        if (k) {
+            const uint16_t rc = g.cell[v];
+            const int r = rc >> 8, c = rc & 0xFF;
+            for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) cnt += col[u] == k;
+            for (int x = g.cs[c]; x < g.cs[c + 1]; ++x) cnt += col[g.cl[x]] == k;
+            cnt -= 2;  // v itself in its row and its column
+        }
+        conf[v] = (uint8_t)cnt;
+    }
+    __syncwarp();
+
+    // ---- K1b: greedy repair, argmax conflicts with lowest-index ties (partial.hpp:22-39)
+    for (;;) {
+        int bc = 0, bv = -1;
+        for (int v = v_lo; v < v_hi; ++v) {
+            const int c = conf[v];
+            if (c > bc) {
+                bc = c;
+                bv = v;
+            }
+        }
+        const int mx = __reduce_max_sync(kFull, (unsigned)bc);
+        if (mx == 0) break;
+        const int wl = __ffs(__ballot_sync(kFull, bc == mx)) - 1;
+        const int w = __shfl_sync(kFull, bv, wl);
+        const int k = col[w];
+        const uint16_t rc = g.cell[w];
+        const int r = rc >> 8, c = rc & 0xFF;
+        for (int u = g.rs[r] + lane; u < g.rs[r + 1]; u += 32)
+            if (u != w && col[u] == k) conf[u] -= 1;
+        for (int x = g.cs[c] + lane; x < g.cs[c + 1]; x += 32) {
+            const int u = g.cl[x];
+            if (u != w && col[u] == k) conf[u] -= 1;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            col[w] = 0;
+            conf[w] = 0;
+        }
+        __syncwarp();
+    }
+
+    // ---- occupancy masks R/C, uncoloured bitmask U and the column-major copy
+    for (int x = lane; x < n * W; x += 32) {
+        s.R[x] = 0;
+        s.C[x] = 0;
+    }
+    __syncwarp();
+    int fl = 0;
+    for (int q = 0; q < g.lane_words; ++q) {
+        const int vb = v_lo + 32 * q;
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int v = vb + b;
+            if (v >= nv) break;
+            const int k = col[v];
+            if (!k) {
+                bits |= 1u << b;
+            } else {
+                const uint16_t rc = g.cell[v];
+                atomicOr((unsigned long long*)&s.R[(rc >> 8) * W + (k >> 6)], 1ULL << (k & 63));
+                atomicOr((unsigned long long*)&s.C[(rc & 0xFF) * W + (k >> 6)], 1ULL << (k & 63));
+            }
+        }
+        s.U[lane * g.lane_words + q] = bits;
+        fl += __popc(bits);
+    }
+    for (int x = lane; x < nv; x += 32) colT[x] = col[g.cl[x]];
+    int f = (int)__reduce_add_sync(kFull, (unsigned)fl);
+    __syncwarp();
+    return f;
+}
 
 }  // namespace plse_dev
