@@ -65,6 +65,8 @@ def args_():
     ap.add_argument("--variant", default="partial", choices=["partial", "mpma"],
                     help="improve operator: PartialCol (headline) or PLITS (MPMA)")
     ap.add_argument("--budget2", type=int, default=0, help="PLITS phase-2 iterations (0 = 2|V|)")
+    ap.add_argument("--tie", default="canon", choices=["canon", "ref"],
+                    help="PartialCol tie-break: canonical (throughput) or the reference's draws (bit-exact)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--migrate-every", type=int, default=2)
     ap.add_argument("--elites", type=int, default=32)
@@ -255,7 +257,7 @@ def run_ours(a):
     mpma = a.variant == "mpma"
     cfg = P.SolverConfig(p=a.pop, master_seed=a.master_seed, phase1_iters=a.budget, device=local,
                          p_total=a.pop * world, offset=a.pop * rank, variant=P.MPMA if mpma else P.PARTIAL,
-                         phase2_iters=a.budget2)
+                         phase2_iters=a.budget2, tie_mode=P.TIE_REF if a.tie == "ref" else P.TIE_CANON)
     pop = P.DevicePopulation(graph, cfg)
     pop.initialize_population()
     pop.offspring = pop.members  # generation-0 offspring are the initial individuals (engine.hpp:163)
@@ -365,7 +367,7 @@ def run_ours(a):
                                    + ("MPMA (PLITS) generation" if mpma else "Partial-MPMA generation")
                                    + f" (improve+distances+update+offspring), pop {a.pop}/GPU, budget {budget}"
                                    + (" + 2|V|" if mpma else ""),
-                       "variant": a.variant,
+                       "variant": a.variant, "tie_break": a.tie,
                        "global_batch": a.pop * world, "vertices": nv, "budget": budget,
                        "parallelism": f"islands x{world}" + (f", {a.elites} elites all-gathered every "
                                                              f"{a.migrate_every} gens" if world > 1 else ""),

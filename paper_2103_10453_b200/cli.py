@@ -49,6 +49,9 @@ def _add_solver_flags(ap: argparse.ArgumentParser) -> None:
     ap.add_argument("--paper-params", action="store_true",
                     help="use the published defaults (p=12288, alpha=0.6, gamma=10, beta=20)")
     ap.add_argument("--device", type=int, default=0, help="CUDA device (device path only)")
+    ap.add_argument("--tie", default="canon", choices=["canon", "ref"],
+                    help="device path: canonical tie-break (throughput) or the reference's reservoir draws "
+                         "(bit-exact with the reference; partial variant)")
 
 
 def _resolve_seed(args) -> int:
@@ -81,7 +84,7 @@ def make_config(args) -> SolverConfig:
         crossover=R.parse_crossover(args.crossover), matching=R.parse_matching(args.matching),
         exclusion=R.parse_exclusion(args.exclusion), time_limit=args.time_limit,
         iteration_limit=args.iter_limit, generation_limit=args.gen_limit, master_seed=_resolve_seed(args),
-        workers=_resolve_workers(args), device=args.device)
+        workers=_resolve_workers(args), device=args.device, tie_mode=1 if args.tie == "ref" else 0)
     validate_config(cfg)
     return cfg
 

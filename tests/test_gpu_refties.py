@@ -91,3 +91,25 @@ def test_ref_ties_rejected_for_plits(plse, orc):
     with pytest.raises(NotImplementedError):
         plse.DevicePopulation(plse.preprocess(grid), plse.SolverConfig(p=4, variant=plse.MPMA,
                                                                          tie_mode=plse.TIE_REF))
+
+
+def test_cli_json_with_ref_ties_equals_reference_json(plse, orc, ref, tmp_path):
+    """The drop-in claim end to end: `solve --variant partial --tie ref` prints the JSON the reference's
+    run() + result_to_json(...).dump(2) print for the same instance, seed and flags."""
+    import subprocess
+    import sys
+    import os
+    if not ref.has_result_json():
+        pytest.skip("nlohmann/json not found when oracle/_ref was built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    grid = orc.generate_instance(12, 0.6, 88)
+    inst = tmp_path / "instance.txt"
+    inst.write_text(plse.serialize_instance(grid))
+    out = subprocess.run([sys.executable, "-m", "paper_2103_10453_b200", "solve", str(inst), "--seed", "31337",
+                          "--pop", "16", "--gen-limit", "5", "--workers", "2", "--variant", "partial", "--tie", "ref"],
+                         capture_output=True, text=True, cwd=root, timeout=600)
+    assert out.returncode in (0, 2), out.stderr
+    r = ref.run(grid, p=16, seed=31337, generation_limit=5, workers=2)
+    want = ref.result_json("instance.txt", 12, r, r["stop_reason"], 16, 0.6, 10.0, 20.0, 0, 0, 1, 0, 0, 0, 31337, 2,
+                           0.0, 0, 5)
+    assert out.stdout == want + "\n"
