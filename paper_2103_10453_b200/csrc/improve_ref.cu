@@ -28,6 +28,23 @@ __device__ __forceinline__ uint64_t ref_below(Xoshiro& rng, uint64_t bound) {
     }
 }
 
+// next_below(bound) == 0 without a 64-bit division: x accepted (x >= bound, or x >= the rejection
+// threshold, which is < bound), then bound | x <=> the odd part o of bound divides x >> s (s = its
+// trailing zeros) and the low s bits of x are 0; o | y <=> y * o^-1 (mod 2^64) times o does not overflow
+__device__ __forceinline__ bool ref_below_is_zero(Xoshiro& rng, uint64_t bound) {
+    for (;;) {
+        const uint64_t x = rng.next();
+        if (x < bound && x < (0 - bound) % bound) continue;  // rejected (probability < bound / 2^64)
+        const int sh = __ffsll((long long)bound) - 1;
+        if (x & ((1ULL << sh) - 1)) return false;
+        const uint64_t o = bound >> sh, y = x >> sh;
+        uint64_t inv = o;  // Newton: o * inv == 1 (mod 2^64), 3 -> 6 -> 12 -> 24 -> 48 -> 96 correct bits
+#pragma unroll
+        for (int it = 0; it < 5; ++it) inv *= 2 - o * inv;
+        return __umul64hi(y * inv, o) == 0;
+    }
+}
+
 struct RefScan {
     int found, bd, cv, ck, cpos;
     uint32_t ties;
@@ -55,7 +72,7 @@ __device__ __forceinline__ void ref_walk(RefScan& st, Xoshiro& rng, const uint64
                 st.ck = q * 64 + b;
                 st.cpos = pos;
                 rel &= l < 0 ? a0 : l == 0 ? (a0 | a1) : (a0 | a1 | a2);
-            } else if (ref_below(rng, ++st.ties) == 0) {
+            } else if (ref_below_is_zero(rng, ++st.ties)) {
                 st.cv = v;
                 st.ck = q * 64 + b;
                 st.cpos = pos;
