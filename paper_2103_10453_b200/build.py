@@ -31,8 +31,30 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+CLI = os.path.join(HERE, "plse_b200")
+CLI_SRC = os.path.join(ROOT, "tools", "plse_b200.cpp")
+CXX = os.environ.get("PLSE_CXX", "g++")
+
+
+def build_cli(force: bool = False) -> str:
+    """tools/plse_b200.cpp -> plse_b200 (the C++ front-end over include/plse_b200.hpp), linked to the
+    in-tree library with an $ORIGIN rpath so it travels with the snapshot."""
+    deps = [CLI_SRC, LIB, os.path.join(ROOT, "include", "plse_b200.hpp"), os.path.join(ROOT, "include", "plse_b200.h")]
+    if not force and os.path.exists(CLI) and all(os.path.getmtime(d) <= os.path.getmtime(CLI) for d in deps
+                                                  if os.path.exists(d)):
+        return CLI
+    cmd = [CXX, "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI + ".tmp",
+           "-L" + HERE, "-lplse_b200", "-Wl,-rpath,$ORIGIN", "-pthread"]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("c++ failed:\n" + " ".join(cmd) + "\n" + out.stdout + out.stderr)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
+        build_cli()
         return LIB
     cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3", "-shared",
            "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
@@ -42,6 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(LIB + ".tmp", LIB)
     if verbose:
         sys.stderr.write(out.stderr)
+    build_cli(force=True)
     return LIB
 
 

@@ -122,6 +122,66 @@ def result_to_json(instance_name: str, order: int, result: RunResult, config: So
     return j
 
 
+def _nl_float(x: float) -> str:
+    """nlohmann::detail::dtoa_impl::format_buffer over the shortest round-trip digits: fixed notation
+    while the decimal point lies in (-4, 15] digits of the first digit, else d.ddde+XX."""
+    if x != x or x in (float("inf"), float("-inf")):
+        return "null"
+    if x == 0:
+        return "-0.0" if math.copysign(1.0, x) < 0 else "0.0"
+    sign = "-" if x < 0 else ""
+    r = repr(abs(x))
+    if "e" in r:
+        m, e = r.split("e")
+        e10 = int(e)
+    else:
+        m, e10 = r, None
+    if "." in m:
+        ip, fp = m.split(".")
+    else:
+        ip, fp = m, ""
+    if e10 is None:
+        # fixed repr: value = ip.fp
+        digits = (ip + fp).lstrip("0")
+        lead = len(ip.lstrip("0")) if ip.strip("0") else -(len(fp) - len(fp.lstrip("0")))
+        n = lead  # decimal point position relative to the first significant digit
+    else:
+        digits = (ip + fp).lstrip("0")
+        n = e10 + 1
+    digits = digits.rstrip("0") or "0"
+    k = len(digits)
+    if k <= n <= 15:
+        return sign + digits + "0" * (n - k) + ".0"
+    if 0 < n <= 15:
+        return sign + digits[:n] + "." + digits[n:]
+    if -4 < n <= 0:
+        return sign + "0." + "0" * (-n) + digits
+    m2 = digits[0] + ("." + digits[1:] if k > 1 else "")
+    ex = n - 1
+    return f"{sign}{m2}e{'-' if ex < 0 else '+'}{abs(ex):02d}"
+
+
+def _dump(v: Any, depth: int) -> str:
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        pad, end = "  " * (depth + 1), "  " * depth
+        return "{\n" + ",\n".join(f"{pad}{json.dumps(k, ensure_ascii=False)}: {_dump(x, depth + 1)}"
+                                   for k, x in v.items()) + f"\n{end}}}"
+    if isinstance(v, (list, tuple)):
+        if not v:
+            return "[]"
+        pad, end = "  " * (depth + 1), "  " * depth
+        return "[\n" + ",\n".join(f"{pad}{_dump(x, depth + 1)}" for x in v) + f"\n{end}]"
+    if isinstance(v, bool) or v is None:
+        return "true" if v is True else "false" if v is False else "null"
+    if isinstance(v, float):
+        return _nl_float(v)
+    if isinstance(v, int):
+        return str(v)
+    return json.dumps(v, ensure_ascii=False)
+
+
 def dumps(j: Dict[str, Any]) -> str:
     """nlohmann ``dump(2)``: the text plse.cpp:154 writes (without the trailing newline)."""
-    return json.dumps(j, indent=2, ensure_ascii=False, allow_nan=False)
+    return _dump(j, 0)

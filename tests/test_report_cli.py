@@ -53,21 +53,22 @@ def test_result_json_golden(plse):
                        "stop_reason", "generations", "total_iterations", "elapsed_seconds", "config"]
 
 
-@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("case", range(8))
 def test_result_json_matches_reference_bytes(plse, ref, case):
     from paper_2103_10453_b200 import report as R
     if not ref.has_result_json():
         pytest.skip("nlohmann/json not found when oracle/_ref was built")
     rng = np.random.default_rng(case)
-    alpha = [0.6, 0.1, 1 / 3, 2.5e20, 1e-7, 0.0][case]
-    tl = [0.0, 1e-7, 123456789.125, 1e300, 0.1 + 0.2, 7.0][case]
+    alpha = [0.6, 0.1, 1 / 3, 2.5e20, 1e-7, 0.0, 1e15, 100000.0][case]
+    tl = [0.0, 1e-7, 123456789.125, 1e300, 0.1 + 0.2, 7.0, 1234567890123456.0, 0.00001][case]
     seed = int(rng.integers(0, 2**63)) * (1 + case % 2)
     timing = case % 2 == 1
     fields = dict(best_f=int(rng.integers(0, 99)), best_score=int(rng.integers(0, 9999)), proven_optimal=case % 3 == 0,
                   l=int(rng.integers(0, 5)), upper_bound=int(rng.integers(0, 9999)), vertex_count=int(rng.integers(0, 5000)),
                   generations=int(rng.integers(0, 10**6)), total_iterations=int(rng.integers(0, 2**62)),
                   elapsed_seconds=float(rng.random() * 100))
-    stop = ["optimal", "time_limit", "iteration_limit", "generation_limit", "trivial", "optimal"][case]
+    stop = ["optimal", "time_limit", "iteration_limit", "generation_limit", "trivial", "optimal", "time_limit",
+            "optimal"][case]
     cfg = plse.SolverConfig(p=int(rng.integers(2, 20000)), alpha=alpha, gamma=10.0 + case, beta=20.0 + 0.5 * case,
                             phase1_iters=case * 1000, phase2_iters=case, variant=case % 2,
                             crossover=case % 3, matching=case % 2, exclusion=(case + 1) % 3, master_seed=seed,
