@@ -243,11 +243,21 @@ def run_reference(a):
 def run_ours(a):
     world, rank, local = dist_env()
     import torch
+    # functional check of the multi-rank path on a 1-GPU box (not a measurement): PLSE_BENCH_DIST=gloo
+    # moves the elite exchange through host memory, PLSE_BENCH_ONE_GPU=1 puts every rank on device 0
+    backend = os.environ.get("PLSE_BENCH_DIST", "nccl")
+    one_gpu = os.environ.get("PLSE_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll = "cuda" if backend == "nccl" else "cpu"
     import paper_2103_10453_b200 as P
 
     grid = lsc_grid(a) if a.lsc else P.generate_instance(a.n, a.r, a.seed)
@@ -284,7 +294,12 @@ def run_ours(a):
         if world > 1 and gen % a.migrate_every == 0:
             pop.export_elites(a.elites, my_elites.data_ptr())
             torch.cuda.synchronize()
-            dist.all_gather_into_tensor(elite_buf, my_elites)
+            if coll == "cuda":
+                dist.all_gather_into_tensor(elite_buf, my_elites)
+            else:
+                parts = [torch.empty_like(my_elites, device="cpu") for _ in range(world)]
+                dist.all_gather(parts, my_elites.cpu())
+                elite_buf.copy_(torch.cat(parts).to("cuda"))
             torch.cuda.synchronize()
             others = torch.cat([elite_buf[r * a.elites:(r + 1) * a.elites] for r in range(world) if r != rank])
             pop.import_migrants(others.shape[0], others.data_ptr())
@@ -346,10 +361,10 @@ def run_ours(a):
     tot_moves, tot_e2e = moves, e2e_moves
     t_max, e2e_max = ms, e2e_s
     if dist is not None:
-        t = torch.tensor([float(moves), float(e2e_moves)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(moves), float(e2e_moves)], dtype=torch.float64, device=coll)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         tot_moves, tot_e2e = t.tolist()
-        m = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
+        m = torch.tensor([ms, e2e_s], dtype=torch.float64, device=coll)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         t_max, e2e_max = m.tolist()
 
@@ -391,6 +406,9 @@ def run_ours(a):
                     "steps": a.e2e_steps},
             "gen1": gen1,
         }
+        if world > 1 and (one_gpu or backend != "nccl"):
+            line["functional_check"] = (f"{world} ranks on " + ("one GPU" if one_gpu else "separate GPUs") +
+                                        f", {backend} exchange: a code-path check, not a measurement")
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(a, grid)
         if world == 1 and not a.no_ttb:
