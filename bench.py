@@ -460,6 +460,20 @@ def ttb(a, P, grid):
         out["ours_race"] = {"pop": a.pop, "best_score": rr.best_score, "seconds_to_best": rr.time_to_best_seconds,
                             "generations": rr.generations, "stop": rr.stop_reason, "moves": rr.total_iterations,
                             "mode": "race (device-global early exit at the target)"}
+    if target is not None and a.variant != "mpma":
+        # the SAME computation as the reference run: pop 1024, reference tie-break -> identical
+        # trajectory, generations and result (tests/test_gpu_refties.py); only the wall time differs
+        rx = P.run(grid, P.SolverConfig(p=a.ttb_ref_pop, master_seed=a.master_seed, time_limit=300.0, variant=var,
+                                        tie_mode=P.TIE_REF))
+        out["ours_same_computation"] = {
+            "pop": a.ttb_ref_pop, "tie_break": "reference (bit-exact)", "best_score": rx.best_score,
+            "seconds_to_best": rx.time_to_best_seconds, "seconds_total": rx.elapsed_seconds,
+            "generations": rx.generations, "moves": rx.total_iterations, "stop": rx.stop_reason,
+            "identical_to_reference": (rx.best_score == r["best_score"] and rx.generations == r["generations"]
+                                       and rx.total_iterations == r["total_iterations"]),
+            "speedup_vs_reference": (r["elapsed_seconds"] / rx.elapsed_seconds) if rx.elapsed_seconds > 0 else None}
+        out["reference"]["seconds_total"] = r["elapsed_seconds"]
+        out["reference"]["moves"] = r["total_iterations"]
     if target is not None:
         out["target_score"] = target
         out["ours_reached_target"] = res.best_score >= target
