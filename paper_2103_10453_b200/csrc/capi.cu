@@ -620,7 +620,15 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
             bi = i;
         }
     }
-    if (c->d_prof && std::getenv("PLSE_PROFILE") && c->plits) {
+    if (c->d_prof && std::getenv("PLSE_PROFILE") && c->ref_ties) {
+        unsigned long long pr[16];
+        CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));
+        const double st = pr[0] ? (double)pr[0] : 1.0;
+        std::fprintf(stderr,
+                     "[plse-prof ref] steps %llu | cyc/step: masks %.0f walk %.0f apply %.0f | draws/step %.2f | "
+                     "mean f %.1f\n",
+                     pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st);
+    } else if (c->d_prof && std::getenv("PLSE_PROFILE") && c->plits) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));
         const double st = pr[0] ? (double)pr[0] : 1.0;

@@ -89,6 +89,9 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
     uint8_t* col = s.col;
     uint8_t* colT = s.colT;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
+    unsigned long long* prof = kDebug ? a.prof : nullptr;
+    unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};  // steps, mask cycles, walk cycles, apply cycles, draws, sum f
+    long long tq = 0;
 
     uint32_t base = *slot_clock;
     if ((uint64_t)base + (uint64_t)a.budget + a.tenure_cap + 2 >= 0xFFFFFFFFull) {
@@ -148,6 +151,11 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
 
         // ---- the reservoir scan (partial.hpp:100-119): masks in parallel, draws serially on lane 0
         RefScan st{0, 2, -1, 0, -1, 0};
+        if (prof) {
+            tq = clock64();
+            ++pc[0];
+            pc[5] += (unsigned)f;
+        }
         for (int c0 = 0; c0 < f; c0 += 32) {
             const int p = c0 + lane;
             if (p < f) {
@@ -161,6 +169,11 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 }
             }
             __syncwarp();
+            if (prof) {
+                const long long x = clock64();
+                pc[1] += (unsigned long long)(x - tq);
+                tq = x;
+            }
             if (lane == 0) {
                 const int m = min(32, f - c0);
                 for (int q = 0; q < m; ++q)
@@ -168,7 +181,13 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                                 el[c0 + q], c0 + q);
             }
             __syncwarp();
+            if (prof) {
+                const long long x = clock64();
+                pc[2] += (unsigned long long)(x - tq);
+                tq = x;
+            }
         }
+        if (prof) pc[4] += st.found ? st.ties - 1 : 0;
         const int found = __shfl_sync(kFull, st.found, 0);
         const uint32_t ties = __shfl_sync(kFull, st.ties, 0);
         if (!found) {
@@ -252,6 +271,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
             *(reinterpret_cast<plse_step*>(a.trace) + j) =
                 plse_step{(int64_t)j, vs, ks, e, ev0, ev1, f_before, f, bestf, (int)tenure, (int32_t)ties, lvl};
         __syncwarp();
+        if (prof) pc[3] += (unsigned long long)(clock64() - tq);
         ++j;
     }
     if (pending) snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
@@ -265,6 +285,10 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         a.iters[i] = (int64_t)j;
         a.bytes[i] = acc;
         *slot_clock = base + j + 2 + a.tenure_cap;
+        if (prof) {
+#pragma unroll
+            for (int z = 0; z < 6; ++z) atomicAdd(prof + z, pc[z]);
+        }
     }
     __syncwarp();
 }
@@ -361,7 +385,7 @@ const void* improve_ref_kernel_ptr(int W, bool debug) {
 }
 
 cudaError_t launch_improve_ref(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    const bool debug = a.trace != nullptr;
+    const bool debug = a.trace != nullptr || a.prof != nullptr;
     if (W == 1) {
         if (debug)
             k_improve_ref<1, true><<<grid, threads, smem, st>>>(a);
