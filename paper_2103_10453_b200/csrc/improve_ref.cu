@@ -31,18 +31,165 @@ __device__ __forceinline__ uint64_t ref_below(Xoshiro& rng, uint64_t bound) {
 // next_below(bound) == 0 without a 64-bit division: x accepted (x >= bound, or x >= the rejection
 // threshold, which is < bound), then bound | x <=> the odd part o of bound divides x >> s (s = its
 // trailing zeros) and the low s bits of x are 0; o | y <=> y * o^-1 (mod 2^64) times o does not overflow
+// 64-bit inverses of the odd parts of 0..256 (0 unused), for the common small bounds
+__constant__ uint64_t kOddInv[257] = {
+    0x0000000000000000ULL, 0x0000000000000001ULL, 0x0000000000000001ULL, 0xaaaaaaaaaaaaaaabULL,
+    0x0000000000000001ULL, 0xcccccccccccccccdULL, 0xaaaaaaaaaaaaaaabULL, 0x6db6db6db6db6db7ULL,
+    0x0000000000000001ULL, 0x8e38e38e38e38e39ULL, 0xcccccccccccccccdULL, 0x2e8ba2e8ba2e8ba3ULL,
+    0xaaaaaaaaaaaaaaabULL, 0x4ec4ec4ec4ec4ec5ULL, 0x6db6db6db6db6db7ULL, 0xeeeeeeeeeeeeeeefULL,
+    0x0000000000000001ULL, 0xf0f0f0f0f0f0f0f1ULL, 0x8e38e38e38e38e39ULL, 0x86bca1af286bca1bULL,
+    0xcccccccccccccccdULL, 0xcf3cf3cf3cf3cf3dULL, 0x2e8ba2e8ba2e8ba3ULL, 0xd37a6f4de9bd37a7ULL,
+    0xaaaaaaaaaaaaaaabULL, 0x8f5c28f5c28f5c29ULL, 0x4ec4ec4ec4ec4ec5ULL, 0x84bda12f684bda13ULL,
+    0x6db6db6db6db6db7ULL, 0x34f72c234f72c235ULL, 0xeeeeeeeeeeeeeeefULL, 0xef7bdef7bdef7bdfULL,
+    0x0000000000000001ULL, 0x0f83e0f83e0f83e1ULL, 0xf0f0f0f0f0f0f0f1ULL, 0xaf8af8af8af8af8bULL,
+    0x8e38e38e38e38e39ULL, 0x14c1bacf914c1badULL, 0x86bca1af286bca1bULL, 0x6f96f96f96f96f97ULL,
+    0xcccccccccccccccdULL, 0x8f9c18f9c18f9c19ULL, 0xcf3cf3cf3cf3cf3dULL, 0x82fa0be82fa0be83ULL,
+    0x2e8ba2e8ba2e8ba3ULL, 0x4fa4fa4fa4fa4fa5ULL, 0xd37a6f4de9bd37a7ULL, 0x51b3bea3677d46cfULL,
+    0xaaaaaaaaaaaaaaabULL, 0x7d6343eb1a1f58d1ULL, 0x8f5c28f5c28f5c29ULL, 0xfafafafafafafafbULL,
+    0x4ec4ec4ec4ec4ec5ULL, 0x21cfb2b78c13521dULL, 0x84bda12f684bda13ULL, 0x6fb586fb586fb587ULL,
+    0x6db6db6db6db6db7ULL, 0x823ee08fb823ee09ULL, 0x34f72c234f72c235ULL, 0xcbeea4e1a08ad8f3ULL,
+    0xeeeeeeeeeeeeeeefULL, 0x4fbcda3ac10c9715ULL, 0xef7bdef7bdef7bdfULL, 0xefbefbefbefbefbfULL,
+    0x0000000000000001ULL, 0x0fc0fc0fc0fc0fc1ULL, 0x0f83e0f83e0f83e1ULL, 0xf0b7672a07a44c6bULL,
+    0xf0f0f0f0f0f0f0f1ULL, 0xf128cfc4a33f128dULL, 0xaf8af8af8af8af8bULL, 0x193d4bb7e327a977ULL,
+    0x8e38e38e38e38e39ULL, 0x7e3f1f8fc7e3f1f9ULL, 0x14c1bacf914c1badULL, 0x2fc962fc962fc963ULL,
+    0x86bca1af286bca1bULL, 0x4fcace213f2b3885ULL, 0x6f96f96f96f96f97ULL, 0x9b8b577e613716afULL,
+    0xcccccccccccccccdULL, 0x2c3f35ba781948b1ULL, 0x8f9c18f9c18f9c19ULL, 0xa3784a062b2e43dbULL,
+    0xcf3cf3cf3cf3cf3dULL, 0xfcfcfcfcfcfcfcfdULL, 0x82fa0be82fa0be83ULL, 0x66fd0eb66fd0eb67ULL,
+    0x2e8ba2e8ba2e8ba3ULL, 0xf47e8fd1fa3f47e9ULL, 0x4fa4fa4fa4fa4fa5ULL, 0x2fd2fd2fd2fd2fd3ULL,
+    0xd37a6f4de9bd37a7ULL, 0x4fd3f4fd3f4fd3f5ULL, 0x51b3bea3677d46cfULL, 0x4e25b9efd4e25b9fULL,
+    0xaaaaaaaaaaaaaaabULL, 0xa3a0fd5c5f02a3a1ULL, 0x7d6343eb1a1f58d1ULL, 0xafd6a052bf5a814bULL,
+    0x8f5c28f5c28f5c29ULL, 0x3a4c0a237c32b16dULL, 0xfafafafafafafafbULL, 0xdab7ec1dd3431b57ULL,
+    0x4ec4ec4ec4ec4ec5ULL, 0x8fd8fd8fd8fd8fd9ULL, 0x21cfb2b78c13521dULL, 0x77a04c8f8d28ac43ULL,
+    0x84bda12f684bda13ULL, 0xa6c0964fda6c0965ULL, 0x6fb586fb586fb587ULL, 0xb195e8efdb195e8fULL,
+    0x6db6db6db6db6db7ULL, 0x90fdbc090fdbc091ULL, 0x823ee08fb823ee09ULL, 0x2a4bafdc61f2a4bbULL,
+    0x34f72c234f72c235ULL, 0xcfdcfdcfdcfdcfddULL, 0xcbeea4e1a08ad8f3ULL, 0xd946fdd946fdd947ULL,
+    0xeeeeeeeeeeeeeeefULL, 0x1b810ecf56be69c9ULL, 0x4fbcda3ac10c9715ULL, 0x2fdeb2fdeb2fdeb3ULL,
+    0xef7bdef7bdef7bdfULL, 0x1cac083126e978d5ULL, 0xefbefbefbefbefbfULL, 0x7efdfbf7efdfbf7fULL,
+    0x0000000000000001ULL, 0x80fe03f80fe03f81ULL, 0x0fc0fc0fc0fc0fc1ULL, 0x03e88cb3c9484e2bULL,
+    0x0f83e0f83e0f83e1ULL, 0x133f84cfe133f84dULL, 0xf0b7672a07a44c6bULL, 0x1a8c536fe1a8c537ULL,
+    0xf0f0f0f0f0f0f0f1ULL, 0xe21a291c077975b9ULL, 0xf128cfc4a33f128dULL, 0x3aef6ca970586723ULL,
+    0xaf8af8af8af8af8bULL, 0x70913f8bcd29c245ULL, 0x193d4bb7e327a977ULL, 0xefe35b4cfaa11e6fULL,
+    0x8e38e38e38e38e39ULL, 0x70fe3c070fe3c071ULL, 0x7e3f1f8fc7e3f1f9ULL, 0xd4766bf908b51d9bULL,
+    0x14c1bacf914c1badULL, 0xdf5b0f768ce2cabdULL, 0x2fc962fc962fc963ULL, 0x6fe4dfc9bf937f27ULL,
+    0x86bca1af286bca1bULL, 0x53a8fe53a8fe53a9ULL, 0x4fcace213f2b3885ULL, 0x2fe592fe592fe593ULL,
+    0x6f96f96f96f96f97ULL, 0x5b4fe5e92c0685b5ULL, 0x9b8b577e613716afULL, 0xb5efe63d2eb11b5fULL,
+    0xcccccccccccccccdULL, 0xf9a3c6c1fcd1e361ULL, 0x2c3f35ba781948b1ULL, 0x1f693a1c451ab30bULL,
+    0x8f9c18f9c18f9c19ULL, 0xcfe72cfe72cfe72dULL, 0xa3784a062b2e43dbULL, 0x8d07aa27db35a717ULL,
+    0xcf3cf3cf3cf3cf3dULL, 0xf25deacafb74a399ULL, 0xfcfcfcfcfcfcfcfdULL, 0x80bfa02fe80bfa03ULL,
+    0x82fa0be82fa0be83ULL, 0x882383b30d516325ULL, 0x66fd0eb66fd0eb67ULL, 0xefe898231bcb564fULL,
+    0x2e8ba2e8ba2e8ba3ULL, 0x43fa36f5e02e4851ULL, 0xf47e8fd1fa3f47e9ULL, 0xed6866f8d962ae7bULL,
+    0x4fa4fa4fa4fa4fa5ULL, 0x3454dca410f8ed9dULL, 0x2fd2fd2fd2fd2fd3ULL, 0x6fe99e1395aedd07ULL,
+    0xd37a6f4de9bd37a7ULL, 0x9dc0588fe9dc0589ULL, 0x4fd3f4fd3f4fd3f5ULL, 0x8a4472fea18a4473ULL,
+    0x51b3bea3677d46cfULL, 0xa53fa94fea53fa95ULL, 0x4e25b9efd4e25b9fULL, 0x1d7ca632ee936f3fULL,
+    0xaaaaaaaaaaaaaaabULL, 0x70bf015390948f41ULL, 0xa3a0fd5c5f02a3a1ULL, 0xafeafeafeafeafebULL,
+    0x7d6343eb1a1f58d1ULL, 0xc96bdb9d3d137e0dULL, 0xafd6a052bf5a814bULL, 0x2697cc8aef46c0f7ULL,
+    0x8f5c28f5c28f5c29ULL, 0xfae7cd0e028c1979ULL, 0x3a4c0a237c32b16dULL, 0x99da2ae0791064e3ULL,
+    0xfafafafafafafafbULL, 0x4fec04fec04fec05ULL, 0xdab7ec1dd3431b57ULL, 0xfb0d9a96e115062fULL,
+    0x4ec4ec4ec4ec4ec5ULL, 0xf4f9e02732385831ULL, 0x8fd8fd8fd8fd8fd9ULL, 0xc0e8f2a76e68575bULL,
+    0x21cfb2b78c13521dULL, 0xb3146e92a10d387dULL, 0x77a04c8f8d28ac43ULL, 0xe6fecf2e6fecf2e7ULL,
+    0x84bda12f684bda13ULL, 0x8fed1fda3fb47f69ULL, 0xa6c0964fda6c0965ULL, 0xd4bfb52fed4bfb53ULL,
+    0x6fb586fb586fb587ULL, 0xd774fed774fed775ULL, 0xb195e8efdb195e8fULL, 0x687763dfdb43bb1fULL,
+    0x6db6db6db6db6db7ULL, 0x0fedcba987654321ULL, 0x90fdbc090fdbc091ULL, 0x1b10ea929ba144cbULL,
+    0x823ee08fb823ee09ULL, 0x1d10c4c0478bbcedULL, 0x2a4bafdc61f2a4bbULL, 0x6fee44b5bfb912d7ULL,
+    0x34f72c234f72c235ULL, 0x63fb9aeb1fdcd759ULL, 0xcfdcfdcfdcfdcfddULL, 0x76bd8c8714b2a7c3ULL,
+    0xcbeea4e1a08ad8f3ULL, 0xde83c7d4cb125ce5ULL, 0xd946fdd946fdd947ULL, 0x64afaa4f437b2e0fULL,
+    0xeeeeeeeeeeeeeeefULL, 0xf010fef010fef011ULL, 0x1b810ecf56be69c9ULL, 0x641511e8d2b3183bULL,
+    0x4fbcda3ac10c9715ULL, 0x1913da62386cab5dULL, 0x2fdeb2fdeb2fdeb3ULL, 0xf6ac0c6fef6ac0c7ULL,
+    0xef7bdef7bdef7bdfULL, 0x367d6e020e64c149ULL, 0x1cac083126e978d5ULL, 0x28cbfbeb9a020a33ULL,
+    0xefbefbefbefbefbfULL, 0x8796c44ce6b41c55ULL, 0x7efdfbf7efdfbf7fULL, 0xfefefefefefefeffULL,
+    0x0000000000000001ULL};
+
+__device__ __forceinline__ bool divides(uint64_t bound, uint64_t x) {
+    const int sh = __ffsll((long long)bound) - 1;
+    if (x & ((1ULL << sh) - 1)) return false;
+    const uint64_t o = bound >> sh, y = x >> sh;
+    uint64_t inv;
+    if (bound <= 256) {
+        inv = kOddInv[bound];
+    } else {
+        inv = o;  // Newton: o * inv == 1 (mod 2^64), 3 -> 6 -> 12 -> 24 -> 48 -> 96 correct bits
+#pragma unroll
+        for (int it = 0; it < 5; ++it) inv *= 2 - o * inv;
+    }
+    return __umul64hi(y * inv, o) == 0;
+}
+
 __device__ __forceinline__ bool ref_below_is_zero(Xoshiro& rng, uint64_t bound) {
     for (;;) {
         const uint64_t x = rng.next();
         if (x < bound && x < (0 - bound) % bound) continue;  // rejected (probability < bound / 2^64)
-        const int sh = __ffsll((long long)bound) - 1;
-        if (x & ((1ULL << sh) - 1)) return false;
-        const uint64_t o = bound >> sh, y = x >> sh;
-        uint64_t inv = o;  // Newton: o * inv == 1 (mod 2^64), 3 -> 6 -> 12 -> 24 -> 48 -> 96 correct bits
-#pragma unroll
-        for (int it = 0; it < 5; ++it) inv *= 2 - o * inv;
-        return __umul64hi(y * inv, o) == 0;
+        return divides(bound, x);
     }
+}
+
+// ---- the same selection computed in parallel when the uncoloured set fits one warp (|V0| <= 32).
+// Levels are -1 / 0 / +1 (index 0 / 1 / 2), so the reservoir's history is a handful of segments:
+// the prefix minimum of the per-vertex minimum level says where each vertex enters; a vertex's draws
+// are the candidates at the running level between the events where the level drops; the final
+// segment is every admissible candidate at the global minimum level D from its first one c* on, and
+// its j-th member (j >= 2) draws next_below(j).  Lane 0 only generates the stream (one next() per
+// draw); the lanes test their own final-segment draws.  Any output below 2^32 (a possible rejection,
+// probability 2^-32 per draw) or an oversized final segment falls back to the serial walk.
+
+template <int W>
+__device__ __forceinline__ uint64_t word_sel(const uint64_t (&x)[W], int q) {
+    return (W == 1 || q == 0) ? x[0] : x[W - 1];
+}
+
+// first set bit of a W-word mask after position pos (-1: from the start), or -1
+template <int W>
+__device__ __forceinline__ int next_bit(const uint64_t (&m)[W], int pos) {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const int lo = pos + 1 - 64 * q;
+        uint64_t x = m[q];
+        if (lo >= 64) continue;
+        if (lo > 0) x &= ~0ULL << lo;
+        if (x) return 64 * q + __ffsll((long long)x) - 1;
+    }
+    return -1;
+}
+
+// set bits of m in the open range (pos, e) (e = -1: to the end)
+template <int W>
+__device__ __forceinline__ int popc_range(const uint64_t (&m)[W], int pos, int e) {
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t x = m[q];
+        const int lo = pos + 1 - 64 * q, hi = e < 0 ? 64 : e - 64 * q;  // keep bits [lo, hi)
+        if (lo >= 64 || hi <= 0) continue;
+        if (lo > 0) x &= ~0ULL << lo;
+        if (hi < 64) x &= (1ULL << hi) - 1;
+        c += __popcll(x);
+    }
+    return c;
+}
+
+// draws the reference makes inside one vertex entered at running level cur (3 = nothing found yet),
+// stopping at its first level-`stop` candidate when stop < 3
+template <int W>
+__device__ __forceinline__ int vertex_draws(const uint64_t (&a0)[W], const uint64_t (&a1)[W], const uint64_t (&a2)[W],
+                                            int cur, int stop) {
+    int draws = 0, pos = -1;
+    for (int it = 0; it < 4; ++it) {
+        uint64_t lower[W], atcur[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            lower[q] = cur == 3 ? (a0[q] | a1[q] | a2[q]) : cur == 2 ? (a0[q] | a1[q]) : cur == 1 ? a0[q] : 0ULL;
+            atcur[q] = cur == 0 ? a0[q] : cur == 1 ? a1[q] : cur == 2 ? a2[q] : 0ULL;
+        }
+        const int e = next_bit<W>(lower, pos);
+        if (cur != 3) draws += popc_range<W>(atcur, pos, e);
+        if (e < 0) break;
+        const uint64_t bit = 1ULL << (e & 63);
+        const int q = e >> 6;
+        const int lvl = (word_sel<W>(a0, q) & bit) ? 0 : (word_sel<W>(a1, q) & bit) ? 1 : 2;
+        if (lvl == stop) break;  // c*, the first candidate of the final level
+        cur = lvl;
+        pos = e;
+    }
+    return draws;
 }
 
 struct RefScan {
@@ -149,14 +296,106 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         const bool asp = (f == bestf);
         const int f_before = f;
 
-        // ---- the reservoir scan (partial.hpp:100-119): masks in parallel, draws serially on lane 0
+        // ---- the reservoir scan (partial.hpp:100-119)
         RefScan st{0, 2, -1, 0, -1, 0};
         if (prof) {
             tq = clock64();
             ++pc[0];
             pc[5] += (unsigned)f;
         }
-        for (int c0 = 0; c0 < f; c0 += 32) {
+        bool fast_done = false;
+        if (f <= 32) {
+            // masks of position `lane` in registers
+            uint64_t a0[W], a1[W], a2[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) a0[q] = a1[q] = a2[q] = 0;
+            if (lane < f) dense_masks<W>(g, s, rec, until, el[lane], t, asp, a0, a1, a2);
+            const int m = (lane >= f) ? 3 : popc_w<W>(a0) ? 0 : popc_w<W>(a1) ? 1 : popc_w<W>(a2) ? 2 : 3;
+            const int D = (int)__reduce_min_sync(kFull, (unsigned)m);
+            if (D == 3) {
+                fast_done = true;  // no admissible candidate: no draw at all
+            } else {
+                int pm = m;  // inclusive prefix minimum of the per-vertex minimum level
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int x = __shfl_up_sync(kFull, pm, d);
+                    if (lane >= d) pm = min(pm, x);
+                }
+                int R = __shfl_up_sync(kFull, pm, 1);
+                if (lane == 0) R = 3;
+                const int istar = __ffs(__ballot_sync(kFull, m == D)) - 1;
+                int early = 0;
+                if (lane <= istar && lane < f) early = vertex_draws<W>(a0, a1, a2, R, lane == istar ? D : 3);
+                uint64_t aD[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) aD[q] = D == 0 ? a0[q] : D == 1 ? a1[q] : a2[q];
+                const int cD = popc_w<W>(aD);
+                const int E = (int)__reduce_add_sync(kFull, (unsigned)early);
+                int sD = cD;  // inclusive prefix sum of the level-D counts
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int x = __shfl_up_sync(kFull, sD, d);
+                    if (lane >= d) sD += x;
+                }
+                const int ND = __shfl_sync(kFull, sD, 31);
+                sD -= cD;  // exclusive: index (0-based) of this lane's first level-D candidate
+                const int cap = 32 * 3 * W;
+                bool ok = ND - 1 <= cap;
+                const Xoshiro saved = rng;
+                if (ok && lane == 0) {
+                    for (int d = 0; d < E + ND - 1; ++d) {
+                        const uint64_t x = rng.next();
+                        if (x < (1ULL << 32)) ok = false;  // a rejection is possible: take the exact path
+                        if (d >= E) msk[d - E] = x;
+                    }
+                }
+                ok = __shfl_sync(kFull, (int)ok, 0) != 0;
+                __syncwarp();
+                if (ok) {
+                    // final-segment member j (1-based; c* is j = 1) keeps the choice iff next_below(j) == 0
+                    int bestj = 0, tloc = 0;
+                    uint64_t x[W];
+#pragma unroll
+                    for (int q = 0; q < W; ++q) x[q] = aD[q];
+                    for (int q = 0; q < W; ++q) {
+                        uint64_t y = word_sel<W>(x, q);
+                        while (y) {
+                            y &= y - 1;
+                            const int jj = sD + (++tloc);
+                            if (jj >= 2 && divides((uint64_t)jj, msk[jj - 2])) bestj = jj;
+                        }
+                    }
+                    int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
+                    if (J == 0) J = 1;
+                    const bool own = sD < J && J <= sD + cD;
+                    if (own) {
+                        st.found = 1;
+                        st.bd = D - 1;
+                        st.ties = (uint32_t)ND;
+                        st.cv = el[lane];
+                        st.ck = nth_bit_w<W>(aD, J - sD - 1);
+                        st.cpos = lane;
+                    }
+                    const int wl = __ffs(__ballot_sync(kFull, own)) - 1;
+                    st.found = 1;
+                    st.bd = D - 1;
+                    st.ties = (uint32_t)ND;
+                    st.cv = __shfl_sync(kFull, st.cv, wl);
+                    st.ck = __shfl_sync(kFull, st.ck, wl);
+                    st.cpos = __shfl_sync(kFull, st.cpos, wl);
+                    fast_done = true;
+                } else if (lane == 0) {
+                    rng = saved;
+                }
+                __syncwarp();
+            }
+            if (prof) {
+                const long long x = clock64();
+                pc[2] += (unsigned long long)(x - tq);
+                tq = x;
+            }
+        }
+        for (int c0 = 0; c0 < f && !fast_done; c0 += 32) {
             const int p = c0 + lane;
             if (p < f) {
                 uint64_t x0[W], x1[W], x2[W];
