@@ -22,6 +22,7 @@
 namespace plse_dev {
 
 constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 128, kTcStages = 4;
+constexpr int kTcGroupM = 12;  // tile rows per raster group
 constexpr int kTcABytes = kTcBM * kTcBK;  // 16 KB
 constexpr int kTcBBytes = kTcBN * kTcBK;  // 32 KB
 constexpr int kTcStageBytes = kTcABytes + kTcBBytes;
@@ -118,7 +119,13 @@ __global__ void __launch_bounds__(128, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kTcStages + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile_n = blockIdx.x, tile_m = blockIdx.y;
+    // grouped raster: consecutive CTAs walk kTcGroupM tile rows, then the next tile column, so one wave
+    // of resident CTAs shares ~12 A tiles and ~12 B tiles per K slab in L2 (row-major order would stream
+    // every B tile once per tile row from DRAM)
+    const int nt_n = (N + kTcBN - 1) / kTcBN, nt_m = (M + kTcBM - 1) / kTcBM;
+    const int lin = blockIdx.x, per_group = kTcGroupM * nt_n;
+    const int first_m = (lin / per_group) * kTcGroupM, gm = min(nt_m - first_m, kTcGroupM);
+    const int tile_m = first_m + (lin % per_group) % gm, tile_n = (lin % per_group) / gm;
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcStages), done = smem_u32(bars + 2 * kTcStages);
 
     if (threadIdx.x == 0) {
@@ -254,8 +261,8 @@ cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, in
     }
     CUtensorMap ma, mb;
     if (!make_map(&ma, HA, M, Kpad, kTcBM) || !make_map(&mb, HB, N, Kpad, kTcBN)) return cudaErrorInvalidValue;
-    dim3 grid((N + kTcBN - 1) / kTcBN, (M + kTcBM - 1) / kTcBM);
-    k_sim_tc<<<grid, 128, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd);
+    const int tiles = ((N + kTcBN - 1) / kTcBN) * ((M + kTcBM - 1) / kTcBM);
+    k_sim_tc<<<tiles, 128, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd);
     return cudaGetLastError();
 }
 
