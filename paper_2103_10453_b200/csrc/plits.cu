@@ -192,20 +192,6 @@ __device__ __forceinline__ void vertex_moves(const Graph<W>& g, const PlitsWarp&
         if (m.cur && (m.cur >> 6) == q) m.M[q] &= ~(1ULL << (m.cur & 63));
 }
 
-// ripple +-1 of colour k's count in a plane stack (lanes may update different colours of the
-// same stack concurrently: each lane only reads its own bit and flips it with atomicXor)
-template <int W, int NP>
-__device__ __forceinline__ void plane_step(uint64_t* P, int k, bool inc) {
-    // the colour's bit lives in one 32-bit half of each plane word: native 32-bit shared atomics
-    uint32_t* P32 = reinterpret_cast<uint32_t*>(P) + 2 * (k >> 6) + ((k >> 5) & 1);
-    const uint32_t bit = 1u << (k & 31);
-#pragma unroll
-    for (int b = 0; b < NP; ++b) {
-        const uint32_t x = atomicXor(P32 + 2 * W * b, bit);  // returns the old word
-        if (inc ? !(x & bit) : (x & bit)) break;            // no carry / borrow out of this bit
-    }
-}
-
 // one lane moves a cell of this line from colour `from` to `to`: the two single-bit ripples (-1 at
 // `from`, +1 at `to`; 0 = uncoloured is not counted) computed in registers, NP x W words stored back
 template <int W, int NP>
@@ -745,9 +731,9 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             __syncwarp();
             if (lane == 0) {
                 col[w] = 0;
-                plane_step<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k, false);
+                plane_move<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k, 0);
             }
-            if (lane == 1) plane_step<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k, false);
+            if (lane == 1) plane_move<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k, 0);
             __syncwarp();
             plits_membership<W>(g, s, rc >> 8, rc & 0xFF, k, 0, 2, 2 * nv, lane);
             ++f;
