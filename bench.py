@@ -460,7 +460,7 @@ def ttb(a, P, grid):
         out["ours_race"] = {"pop": a.pop, "best_score": rr.best_score, "seconds_to_best": rr.time_to_best_seconds,
                             "generations": rr.generations, "stop": rr.stop_reason, "moves": rr.total_iterations,
                             "mode": "race (device-global early exit at the target)"}
-    if target is not None and a.variant != "mpma":
+    if target is not None:
         # the SAME computation as the reference run: pop 1024, reference tie-break -> identical
         # trajectory, generations and result (tests/test_gpu_refties.py); only the wall time differs
         rx = P.run(grid, P.SolverConfig(p=a.ttb_ref_pop, master_seed=a.master_seed, time_limit=300.0, variant=var,

@@ -92,7 +92,7 @@ typedef struct {
     int32_t matching;       /* PLSE_M_* */
     int32_t exclusion;      /* PLSE_E_* */
     int32_t tie_mode;       /* PLSE_TIE_CANON (throughput) or PLSE_TIE_REF (the reference's reservoir
-                               draws: bit-exact trajectories, Partial-MPMA only) */
+                               draws: bit-exact trajectories, both variants) */
     uint64_t master_seed;
     int64_t p_total;        /* stream index space: gen*p_total + offset + i; 0 -> p */
     int64_t offset;         /* first global individual of this shard */

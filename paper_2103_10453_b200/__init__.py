@@ -427,7 +427,7 @@ class SolverConfig:
     target_score: float = 0.0
     race: bool = False  # with target_score: device-global early exit (time-to-target, not parity mode)
     workers: int = 1  # reported in the result JSON (report.hpp:76); the device path uses one host thread
-    tie_mode: int = 0  # TIE_CANON (throughput) or TIE_REF (the reference's reservoir draws, bit-exact; partial only)
+    tie_mode: int = 0  # TIE_CANON (throughput) or TIE_REF (the reference's reservoir draws, bit-exact)
 
     def _params(self) -> _Params:
         return _Params(self.p, self.alpha, self.gamma, self.beta, self.phase1_iters, self.crossover, self.matching,

@@ -51,7 +51,7 @@ def _add_solver_flags(ap: argparse.ArgumentParser) -> None:
     ap.add_argument("--device", type=int, default=0, help="CUDA device (device path only)")
     ap.add_argument("--tie", default="canon", choices=["canon", "ref"],
                     help="device path: canonical tie-break (throughput) or the reference's reservoir draws "
-                         "(bit-exact with the reference; partial variant)")
+                         "(bit-exact with the reference)")
 
 
 def _resolve_seed(args) -> int:

@@ -220,8 +220,6 @@ void validate_params(const plse_params& p) {
     if (p.matching < 0 || p.matching > 1) throw std::invalid_argument("unknown matching strategy");
     if (p.exclusion < 0 || p.exclusion > 2) throw std::invalid_argument("unknown exclusion scope");
     if (p.tie_mode != PLSE_TIE_CANON && p.tie_mode != PLSE_TIE_REF) throw std::invalid_argument("unknown tie mode");
-    if (p.tie_mode == PLSE_TIE_REF && p.variant == PLSE_V_MPMA)
-        throw Unsupported("the reference tie-break runs on the device for the Partial-MPMA variant only");
     if (p.p_total < 0 || p.offset < 0) throw std::invalid_argument("negative island coordinates");
 }
 
@@ -432,16 +430,20 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL"))
         c->half_warp = std::string(env) == "hw" && !c->plits && !c->ref_ties;
     c->lane_words16 = (nwords + 15) / 16;
-    const void* kern = c->plits       ? plits_kernel_ptr(W, false)
+    const void* kern = c->plits       ? (c->ref_ties ? plits_ref_kernel_ptr(W, false) : plits_kernel_ptr(W, false))
                        : c->ref_ties  ? improve_ref_kernel_ptr(W, false)
                        : c->half_warp ? improve_hw_kernel_ptr(W, false)
                                       : improve_kernel_ptr(W, false);
-    const void* kern_dbg = c->plits       ? plits_kernel_ptr(W, true)
+    const void* kern_dbg = c->plits       ? (c->ref_ties ? plits_ref_kernel_ptr(W, true) : plits_kernel_ptr(W, true))
                            : c->ref_ties  ? improve_ref_kernel_ptr(W, true)
                            : c->half_warp ? improve_hw_kernel_ptr(W, true)
                                           : improve_kernel_ptr(W, true);
     size_t graph_bytes = 0, warp_bytes = 0;
-    if (c->ref_ties) {
+    if (c->plits && c->ref_ties) {
+        const PlitsRefSmemLayout L = plits_ref_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+        graph_bytes = L.graph_bytes;
+        warp_bytes = L.warp_bytes;
+    } else if (c->ref_ties) {
         const RefSmemLayout L = improve_ref_smem_layout(n, nv, c->nvpad, c->lane_words, W);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
@@ -586,7 +588,9 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     }
     CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->ev0, c->st));
-    if (c->plits)
+    if (c->plits && c->ref_ties)
+        c->launched(launch_plits_ref(a, c->W, c->grid, c->threads, c->smem, c->st));
+    else if (c->plits)
         c->launched(launch_plits(a, c->W, c->grid, c->threads, c->smem, c->st));
     else if (c->ref_ties)
         c->launched(launch_improve_ref(a, c->W, c->grid, c->threads, c->smem, c->st));

@@ -194,6 +194,50 @@ __host__ __device__ inline PlitsSmemLayout plits_smem_layout(int n, int nv, int 
     return L;
 }
 
+// PLITS with the reference's tie-break (plits_ref.cu): colours, count planes, the two IndexSets,
+// possibly-tabu masks, a 32-vertex staging area and a neighbour scratch list per warp
+struct PlitsRefSmemLayout {
+    size_t graph_bytes, warp0, warp_bytes, w_col, w_rp, w_cp, w_un_el, w_un_pos, w_cf_el, w_cf_pos, w_T, w_stage,
+        w_stage_i, w_evl;
+};
+
+__host__ __device__ inline PlitsRefSmemLayout plits_ref_smem_layout(int n, int nv, int nvpad, int lane_words, int W) {
+    const ImproveSmemLayout G = improve_smem_layout(n, nv, nvpad, lane_words, W);
+    PlitsRefSmemLayout L;
+    L.graph_bytes = G.graph_bytes;
+    L.warp0 = G.warp0;
+    const size_t planes = (size_t)n * (5 + W) * W * 8, ids = align_up((size_t)nv * 2, 16);
+    size_t w = 0;
+    L.w_col = w;
+    w += (size_t)nvpad;
+    w = align_up(w, 16);
+    L.w_rp = w;
+    w += planes;
+    L.w_cp = w;
+    w += planes;
+    L.w_un_el = w;
+    w += ids;
+    L.w_un_pos = w;
+    w += ids;
+    L.w_cf_el = w;
+    w += ids;
+    L.w_cf_pos = w;
+    w += ids;
+    L.w_T = w;
+    w += (size_t)nv * W * 8;
+    L.w_stage = w;
+    w += (size_t)32 * (5 + W + 2) * W * 8;
+    L.w_stage_i = w;
+    w += 32 * 5 * 4;
+    L.w_evl = w;
+    w += align_up((size_t)2 * n * 2, 16);
+    L.warp_bytes = align_up(w, 16);
+    return L;
+}
+
+const void* plits_ref_kernel_ptr(int W, bool debug);
+cudaError_t launch_plits_ref(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
+
 const void* plits_kernel_ptr(int W, bool debug);
 cudaError_t launch_plits(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 

@@ -6,7 +6,7 @@
 // CSV, report JSON).  Everything goes through the C++ host API
 // (include/plse_b200.hpp) and the C ABI; run() executes on one B200.  Extra
 // device flags: --device N, --tie canon|ref (ref = the reference's own
-// tie-break, bit-exact with the reference; partial variant).
+// tie-break, bit-exact with the reference, both variants).
 //
 // The argument parser is a small stand-in for CLI11 (not available offline):
 // same option names and value forms; usage errors exit 106 like CLI11's.

@@ -8,7 +8,7 @@ p = int(os.environ.get("POP", "16384"))
 gens = int(os.environ.get("GENS", "4"))
 grid = P.generate_instance(60, 0.5, 12345)
 g = P.preprocess(grid)
-pop = P.DevicePopulation(g, P.SolverConfig(p=p, master_seed=1, variant=P.MPMA))
+pop = P.DevicePopulation(g, P.SolverConfig(p=p, master_seed=1, variant=P.MPMA, tie_mode=int(os.environ.get("TIE", "0"))))
 pop.initialize_population()
 pop.offspring = pop.members
 for gen in range(1, gens + 1):
