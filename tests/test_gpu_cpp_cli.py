@@ -68,3 +68,18 @@ def test_cpp_bench_equals_python_bench(plse, tmp_path):
     for x, y in zip(ra, rb):
         assert {k: v for k, v in x.items() if k != "elapsed_seconds"} == \
                {k: v for k, v in y.items() if k != "elapsed_seconds"}
+
+
+def test_cpp_solve_default_variant_ref_ties_equals_reference(plse, orc, ref, tmp_path):
+    """The reference CLI's defaults (variant mpma, p = 1024 scaled down here) with --tie ref: same JSON."""
+    if not ref.has_result_json():
+        pytest.skip("nlohmann/json not found when oracle/_ref was built")
+    grid = orc.generate_instance(12, 0.6, 88)
+    inst = tmp_path / "instance.txt"
+    inst.write_text(plse.serialize_instance(grid))
+    out = _run(CLI, "solve", inst, "--seed", 31337, "--pop", 16, "--gen-limit", 5, "--workers", 2, "--tie", "ref")
+    assert out.returncode in (0, 2), out.stderr
+    r = ref.run(grid, p=16, seed=31337, generation_limit=5, workers=2, variant=0)
+    want = ref.result_json("instance.txt", 12, r, r["stop_reason"], 16, 0.6, 10.0, 20.0, 0, 0, 0, 0, 0, 0, 31337, 2,
+                           0.0, 0, 5)
+    assert out.stdout == want + "\n"
