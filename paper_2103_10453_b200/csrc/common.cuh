@@ -69,7 +69,15 @@ struct Xoshiro {
         s3 = splitmix64(sm);
     }
     __host__ __device__ __forceinline__ static uint64_t rotl(uint64_t x, int k) {
+#ifdef __CUDA_ARCH__
+        // two funnel shifts (SHF.L.W) instead of the four shifts and an OR of the generic form
+        const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+        const uint32_t a = k < 32 ? lo : hi, b = k < 32 ? hi : lo;  // k >= 32: swap the halves first
+        const uint32_t nhi = __funnelshift_l(a, b, k & 31), nlo = __funnelshift_l(b, a, k & 31);
+        return ((uint64_t)nhi << 32) | nlo;
+#else
         return (x << k) | (x >> (64 - k));
+#endif
     }
     __host__ __device__ __forceinline__ uint64_t next() {
         const uint64_t result = rotl(s0 + s3, 23) + s0;

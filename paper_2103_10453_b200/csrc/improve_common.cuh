@@ -153,6 +153,29 @@ __device__ __forceinline__ int popc_w(const uint64_t (&m)[W]) {
     return c;
 }
 
+// lowest set bit of a W-word mask (64 W if empty)
+template <int W>
+__device__ __forceinline__ int first_bit_w(const uint64_t (&m)[W]) {
+    int k = 64 * W;
+#pragma unroll
+    for (int z = W - 1; z >= 0; --z)
+        if (m[z]) k = z * 64 + __ffsll((long long)m[z]) - 1;
+    return k;
+}
+
+// set bits of a W-word mask below bit position pos
+template <int W>
+__device__ __forceinline__ int popc_below_w(const uint64_t (&m)[W], int pos) {
+    int c = 0;
+#pragma unroll
+    for (int z = 0; z < W; ++z) {
+        const int lo = z * 64;
+        const uint64_t mk = pos >= lo + 64 ? ~0ULL : pos <= lo ? 0ULL : (1ULL << (pos - lo)) - 1;
+        c += __popcll(m[z] & mk);
+    }
+    return c;
+}
+
 // 0-based rr-th set bit of a W-word mask (rr < popc)
 template <int W>
 __device__ __forceinline__ int nth_bit_w(const uint64_t (&m)[W], int rr) {

@@ -15,6 +15,7 @@
 // fresh tabu table per phase, best tracking, the final repair, the byte model
 // -- is the canonical kernel's (plits.cu).
 #include "plits_common.cuh"
+#include "ref_draws.cuh"
 
 namespace plse_dev {
 
@@ -47,29 +48,6 @@ __device__ __forceinline__ void is_erase(uint16_t* el, uint16_t* pos, int& size,
     pos[last] = (uint16_t)p;
     --size;
     pos[x] = kNone;
-}
-
-// rng.hpp:43-49: next_below(bound) == 0, without a 64-bit division when the output is accepted
-__device__ __forceinline__ bool ref_draw_zero(Xoshiro& rng, uint64_t bound) {
-    for (;;) {
-        const uint64_t x = rng.next();
-        if (x < bound && x < (0 - bound) % bound) continue;  // rejected
-        const int sh = __ffsll((long long)bound) - 1;
-        if (x & ((1ULL << sh) - 1)) return false;
-        const uint64_t o = bound >> sh, y = x >> sh;
-        uint64_t inv = o;  // Newton: o * inv == 1 (mod 2^64)
-#pragma unroll
-        for (int it = 0; it < 5; ++it) inv *= 2 - o * inv;
-        return __umul64hi(y * inv, o) == 0;
-    }
-}
-
-template <class Rng>
-__device__ __forceinline__ uint64_t pr_below(Rng& rng, uint64_t bound) {
-    for (;;) {
-        const uint64_t x = rng.next();
-        if (x >= bound || x >= (0 - bound) % bound) return x % bound;
-    }
 }
 
 template <int W>
@@ -138,13 +116,15 @@ template <int W>
 __device__ __forceinline__ void ref_walk_vertex(RefChoice& ch, Xoshiro& rng, const uint64_t* S_, const uint64_t* M_,
                                                 int v, int cur, int dbase, int d0, bool conflicting, int wf, int wc,
                                                 const uint32_t* urow, uint64_t* Tv, uint32_t t, int64_t cur_scaled,
-                                                int64_t best_scaled) {
+                                                int64_t best_scaled, unsigned long long* pc) {
     constexpr int NB = PlitsK<W>::NB;
     const int gcur = cur ? (wf - d0) / wc : 0;
     auto consider = [&](int k, int delta, int dc, int df) {
         if (ch.found && delta > ch.delta) return;
+        if (pc) ++pc[6];
         const uint64_t bit = 1ULL << (k & 63);
         if (Tv[k >> 6] & bit) {
+            if (pc) ++pc[7];
             if (urow[k] > t) {
                 if (!(cur_scaled + delta < best_scaled)) return;  // tabu and not aspirating
             } else {
@@ -159,7 +139,7 @@ __device__ __forceinline__ void ref_walk_vertex(RefChoice& ch, Xoshiro& rng, con
             ch.k = k;
             ch.dc = dc;
             ch.df = df;
-        } else if (ref_draw_zero(rng, ++ch.ties)) {
+        } else if (ref_below_is_zero(rng, ++ch.ties)) {
             ch.v = v;
             ch.k = k;
             ch.dc = dc;
@@ -196,6 +176,235 @@ __device__ __forceinline__ void ref_walk_vertex(RefChoice& ch, Xoshiro& rng, con
     }
 }
 
+// ---- the same reservoir scan computed in parallel when the active sequence fits one warp (nseq <= 32).
+// Every quantity the serial walk branches on -- the candidate deltas, which candidates are tabu and not
+// aspirating -- is fixed before the walk starts, so its history is determined by the deltas alone: the
+// global minimum D, the prefix minimum of the per-vertex minima (where each vertex enters the walk), the
+// ties at levels above D before the first D-candidate (E early draws, whose values are irrelevant), and
+// the final segment -- every admissible candidate at D, the j-th of which (j >= 2) keeps the choice iff
+// next_below(j) == 0.  Lane p owns the p-th vertex of the sequence; lane 0 only generates the stream; the
+// lanes test their own final-segment draws.  Any output below 2^32 (a possible rejection, probability
+// 2^-32 per draw) or a final segment longer than the buffer falls back to the serial walk.
+template <int W>
+__device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRefWarp& s, int lane, int nseq, int nu,
+                                               int wf, int wc, uint32_t* until, int w1, uint32_t t,
+                                               int64_t cur_scaled, int64_t best_scaled, Xoshiro& rng,
+                                               RefChoice& ch, unsigned long long* tp) {
+    constexpr int NB = PlitsK<W>::NB;
+    constexpr int kInf = INT_MAX;
+    long long t0 = tp ? clock64() : 0;
+    auto stamp = [&](int z) {
+        if (tp) {
+            const long long x = clock64();
+            tp[z] += (unsigned long long)(x - t0);
+            t0 = x;
+        }
+    };
+    const bool mine = lane < nseq;
+    const bool conflicting = lane >= nu;
+    VertexMoves<W> m;
+    int v = 0;
+    uint64_t al[W];  // admissible colours k != 0
+#pragma unroll
+    for (int q = 0; q < W; ++q) al[q] = 0;
+    bool a0 = false;  // the move to 0 admissible (conflicting vertices only)
+    int vmin = kInf;
+    // tabu moves are admissible iff they aspirate: delta < best - cur
+    const int64_t asp64 = best_scaled - cur_scaled;
+    const int asp = (int)max((int64_t)INT_MIN / 4, min((int64_t)INT_MAX / 4, asp64));
+    if (mine) {
+        v = lane < nu ? s.un_el[lane] : s.cf_el[lane - nu];
+        vertex_moves<W>(g, s, v, wf, wc, m);
+        uint64_t live[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) live[q] = 0;
+        uint64_t* Tv = s.T + (size_t)v * W;
+        const uint32_t* urow = until + (size_t)v * w1;
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            uint64_t x = Tv[q] & (m.M[q] | ((q == 0 && conflicting) ? 1ULL : 0ULL));
+            uint64_t expired = 0;
+            while (x) {
+                const int b = __ffsll((long long)x) - 1;
+                x &= x - 1;
+                if (urow[q * 64 + b] > t)
+                    live[q] |= 1ULL << b;
+                else
+                    expired |= 1ULL << b;
+            }
+            if (expired) Tv[q] &= ~expired;  // the mask stays a superset of the live entries
+        }
+        a0 = conflicting && (!(live[0] & 1ULL) || m.d0 < asp);
+        live[0] &= ~1ULL;
+        // tabu colours admissible only with gamma <= floor((asp - 1 - dbase) / wc)
+        uint64_t hi[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) hi[q] = live[q];
+        sliced_ge<W, NB>(m.S, floor_div(asp - 1 - m.dbase, wc) + 1, hi);
+#pragma unroll
+        for (int q = 0; q < W; ++q) al[q] = m.M[q] & ~hi[q];
+        if (a0) vmin = m.d0;
+        if (popc_w<W>(al)) {
+            uint64_t sel[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) sel[q] = al[q];
+            vmin = min(vmin, m.dbase + wc * sliced_min<W, NB>(m.S, sel));
+        }
+    }
+    stamp(0);
+    const int D = __reduce_min_sync(kFull, vmin);
+    if (D == kInf) {  // every candidate tabu: nothing found, no draw
+        ch.found = 0;
+        return true;
+    }
+    int pm = vmin;  // inclusive prefix minimum of the per-vertex minima
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int x = __shfl_up_sync(kFull, pm, d);
+        if (lane >= d) pm = min(pm, x);
+    }
+    int rin = __shfl_up_sync(kFull, pm, 1);
+    if (lane == 0) rin = kInf;
+    const int istar = __ffs(__ballot_sync(kFull, vmin == D)) - 1;
+    // early draws: ties at levels above D before the first D-candidate, counted per level from the
+    // incoming running minimum -- a candidate at level L ties iff it precedes every candidate below L and
+    // the running minimum already is L (an earlier candidate at L, or the incoming one)
+    int early = 0;
+    if (mine && lane <= istar) {
+        int r = rin;
+        uint64_t G[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) G[q] = al[q];
+        if (a0) {  // k = 0 comes first
+            if (m.d0 < r)
+                r = m.d0;
+            else if (m.d0 == r)
+                ++early;
+        }
+        if (r == kInf && popc_w<W>(G)) {  // nothing before this vertex: its first colour resets
+            const int k1 = first_bit_w<W>(G);
+            r = m.dbase + wc * sliced_val<W, NB>(m.S, k1);
+#pragma unroll
+            for (int q = 0; q < W; ++q)
+                if ((k1 >> 6) == q) G[q] &= ~(1ULL << (k1 & 63));
+        }
+        if (r != kInf && r > D && popc_w<W>(G)) {
+            const int gr = floor_div(r - m.dbase, wc);
+            {
+                uint64_t hi[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) hi[q] = G[q];
+                sliced_ge<W, NB>(m.S, gr + 1, hi);
+#pragma unroll
+                for (int q = 0; q < W; ++q) G[q] &= ~hi[q];
+            }
+            if (popc_w<W>(G)) {
+                uint64_t sel[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) sel[q] = G[q];
+                const int gmin = sliced_min<W, NB>(m.S, sel);
+                for (int gl = gr; gl >= gmin; --gl) {
+                    const int L = m.dbase + wc * gl;
+                    if (L <= D) break;
+                    uint64_t eqg[W], lo[W];
+#pragma unroll
+                    for (int q = 0; q < W; ++q) eqg[q] = lo[q] = G[q];
+                    sliced_eq<W, NB>(m.S, gl, eqg);
+                    sliced_ge<W, NB>(m.S, gl, lo);  // lo = G minus the candidates below gl
+#pragma unroll
+                    for (int q = 0; q < W; ++q) lo[q] = G[q] & ~lo[q];
+                    const int cnt = popc_below_w<W>(eqg, first_bit_w<W>(lo));
+                    early += (L == r) ? cnt : max(cnt - 1, 0);
+                }
+            }
+        }
+    }
+    stamp(1);
+    // the final segment: admissible candidates at D, k = 0 first, then colours ascending
+    uint64_t aD[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) aD[q] = 0;
+    bool z0 = false;
+    if (mine && vmin == D) {
+        z0 = a0 && m.d0 == D;
+        const int num = D - m.dbase;
+        if (num >= 0 && num % wc == 0) {
+#pragma unroll
+            for (int q = 0; q < W; ++q) aD[q] = al[q];
+            sliced_eq<W, NB>(m.S, num / wc, aD);
+        }
+    }
+    const int cD = (int)z0 + popc_w<W>(aD);
+    const int E = (int)__reduce_add_sync(kFull, (unsigned)early);
+    int sD = cD;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int x = __shfl_up_sync(kFull, sD, d);
+        if (lane >= d) sD += x;
+    }
+    const int ND = __shfl_sync(kFull, sD, 31);
+    sD -= cD;
+    constexpr int cap = 32 * (NB + 1) * W;  // the staging buffer, reused for the final-segment outputs
+    uint64_t* out = s.stage;
+    if (ND - 1 > cap) return false;
+    const Xoshiro saved = rng;
+    bool ok = true;
+    stamp(2);
+    if (tp) tp[5] += (unsigned)(E + ND - 1);
+    if (lane == 0) {
+        uint32_t bad = 0;  // an output below 2^32: a rejection is possible, take the exact path
+#pragma unroll 4
+        for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
+#pragma unroll 4
+        for (int d = 0; d < ND - 1; ++d) {
+            const uint64_t x = rng.next();
+            bad |= (uint32_t)((x >> 32) == 0);
+            out[d] = x;
+        }
+        ok = bad == 0;
+    }
+    ok = __shfl_sync(kFull, (int)ok, 0) != 0;
+    __syncwarp();
+    stamp(3);
+    if (!ok) {
+        if (lane == 0) rng = saved;
+        return false;
+    }
+    // member j (1-based, in walk order) of the final segment keeps the choice iff next_below(j) == 0
+    // (j >= 2): draw E + j - 2 of the stream; the lanes test the members round-robin
+    int bestj = 0;
+    for (int j = 2 + lane; j <= ND; j += 32)
+        if (divides((uint64_t)j, out[j - 2])) bestj = j;
+    int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
+    if (J == 0) J = 1;
+    const bool own = sD < J && J <= sD + cD;
+    int kk = 0, dc = 0, df = 0;
+    if (own) {
+        const int li = J - sD - 1;
+        const int gcur = m.cur ? (wf - m.d0) / wc : 0;
+        if (z0 && li == 0) {
+            kk = 0;
+            dc = -gcur;
+            df = 1;
+        } else {
+            kk = nth_bit_w<W>(aD, li - (int)z0);
+            dc = (D - m.dbase) / wc - gcur;
+            df = m.cur ? 0 : -1;
+        }
+    }
+    const int wl = __ffs(__ballot_sync(kFull, own)) - 1;
+    ch.found = 1;
+    ch.delta = D;
+    ch.ties = (uint32_t)ND;
+    ch.v = __shfl_sync(kFull, v, wl);
+    ch.k = __shfl_sync(kFull, kk, wl);
+    ch.dc = __shfl_sync(kFull, dc, wl);
+    ch.df = __shfl_sync(kFull, df, wl);
+    __syncwarp();
+    stamp(4);
+    return true;
+}
+
 template <int W, bool kDebug>
 __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const PlitsRefWarp& s, uint32_t* until,
                               uint32_t* slot_clock, int i, int lane) {
@@ -205,6 +414,9 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
     uint8_t* col = s.col;
     uint8_t* best_row = a.improved + (size_t)i * g.nvpad;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
+    unsigned long long* prof = kDebug ? a.prof : nullptr;
+    unsigned long long pc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // steps, stage, walk, apply, sum nseq, walked vertices
+    long long tq = 0;
 
     uint32_t base = *slot_clock;
     if ((uint64_t)base + (uint64_t)a.budget + (uint64_t)a.budget2 + 2ull * (a.tenure_cap + 4) >= 0xFFFFFFFFull) {
@@ -263,7 +475,22 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
 
             // ---- the reservoir scan: uncoloured set, then conflicting set, in IndexSet order
             RefChoice ch{0, 0, -1, 0, 0, 0, 0};
-            for (int c0 = 0; c0 < nseq; c0 += 32) {
+            if (prof) {
+                tq = clock64();
+                ++pc[0];
+                pc[4] += (unsigned)nseq;
+            }
+            bool fast_done = false;
+            if (nseq <= 32) {
+                fast_done = plits_ref_fast<W>(g, s, lane, nseq, nu, wf, wc, until, w1, t, cur_scaled, best_scaled,
+                                              rng, ch, prof ? pc + 8 : nullptr);
+                if (prof) {
+                    const long long x = clock64();
+                    pc[3] += (unsigned long long)(x - tq);
+                    tq = x;
+                }
+            }
+            for (int c0 = 0; c0 < nseq && !fast_done; c0 += 32) {
                 const int p = c0 + lane;
                 if (p < nseq) {
                     const int v = p < nu ? s.un_el[p] : s.cf_el[p - nu];
@@ -290,18 +517,29 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
                     s.stage_i[lane * 5 + 4] = vm;
                 }
                 __syncwarp();
+                if (prof) {
+                    const long long x = clock64();
+                    pc[1] += (unsigned long long)(x - tq);
+                    tq = x;
+                }
                 if (lane == 0) {
                     const int mcount = min(32, nseq - c0);
                     for (int q = 0; q < mcount; ++q) {
                         if (ch.found && s.stage_i[q * 5 + 4] > ch.delta) continue;
+                        if (prof) ++pc[5];
                         const int v = s.stage_i[q * 5 + 0];
                         const uint64_t* st = s.stage + (size_t)q * (NB + 1) * W;
                         ref_walk_vertex<W>(ch, rng, st, st + NB * W, v, s.stage_i[q * 5 + 1], s.stage_i[q * 5 + 2],
                                            s.stage_i[q * 5 + 3], c0 + q >= nu, wf, wc, until + (size_t)v * w1,
-                                           s.T + (size_t)v * W, t, cur_scaled, best_scaled);
+                                           s.T + (size_t)v * W, t, cur_scaled, best_scaled, prof ? pc : nullptr);
                     }
                 }
                 __syncwarp();
+                if (prof) {
+                    const long long x = clock64();
+                    pc[2] += (unsigned long long)(x - tq);
+                    tq = x;
+                }
             }
             const int found = __shfl_sync(kFull, ch.found, 0);
             if (!found) {
@@ -376,7 +614,7 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
                     else
                         is_erase(s.cf_el, s.cf_pos, ncf, u);
                 }
-                tenure = (uint32_t)pr_below(rng, 10) + (uint32_t)(alpha * (double)(nu + ncf));
+                tenure = (uint32_t)ref_below(rng, 10) + (uint32_t)(alpha * (double)(nu + ncf));
                 until[(size_t)vs * w1 + from] = t + 1 + tenure;
                 s.T[(size_t)vs * W + (from >> 6)] |= 1ULL << (from & 63);
                 acc += 2ULL * (unsigned)w1 * (unsigned)active_before + 4ULL * g.deg[vs] + 2ULL;
@@ -400,6 +638,7 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
                     (int64_t)J, vs, ks, phase, from, nu + ncf, f, c, (int32_t)best_scaled, (int32_t)tenure,
                     (int32_t)ties, dl};
             __syncwarp();
+
             ++j;
             ++J;
         }
@@ -465,6 +704,10 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
         a.bytes[i] = acc;
         *slot_clock = base;
         if (race_flag && best_f <= a.race_f) atomicExch(const_cast<int*>(race_flag), 1);
+        if (prof) {
+#pragma unroll
+            for (int z = 0; z < 16; ++z) atomicAdd(prof + z, pc[z]);
+        }
     }
     __syncwarp();
 }
@@ -560,7 +803,7 @@ const void* plits_ref_kernel_ptr(int W, bool debug) {
 }
 
 cudaError_t launch_plits_ref(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    const bool debug = a.trace != nullptr;
+    const bool debug = a.trace != nullptr || a.prof != nullptr;
     if (W == 1) {
         if (debug)
             k_plits_ref<1, true><<<grid, threads, smem, st>>>(a);
