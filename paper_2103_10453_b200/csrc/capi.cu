@@ -631,9 +631,9 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         std::fprintf(stderr,
                      "[plse-prof plits-ref] steps %llu | cyc/step: stage %.0f walk %.0f fast %.0f | mean sequence "
                      "%.1f, walked vertices %.2f considered %.2f T-hits %.2f | fast: moves+tabu %.0f scan+early %.0f "
-                     "segment %.0f generate %.0f select %.0f outputs/step %.2f\n",
+                     "segment %.0f generate %.0f select %.0f outputs/step %.2f | long sequences %llu, long segments %llu\n",
                      pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st,
-                     pr[8] / st, pr[9] / st, pr[10] / st, pr[11] / st, pr[12] / st, pr[13] / st);
+                     pr[8] / st, pr[9] / st, pr[10] / st, pr[11] / st, pr[12] / st, pr[13] / st, pr[14], pr[15]);
     } else if (c->d_prof && std::getenv("PLSE_PROFILE") && c->ref_ties) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));

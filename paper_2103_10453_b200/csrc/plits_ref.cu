@@ -176,21 +176,168 @@ __device__ __forceinline__ void ref_walk_vertex(RefChoice& ch, Xoshiro& rng, con
     }
 }
 
-// ---- the same reservoir scan computed in parallel when the active sequence fits one warp (nseq <= 32).
+// ---- the same reservoir scan computed in parallel, 32 vertices of the sequence per round.
 // Every quantity the serial walk branches on -- the candidate deltas, which candidates are tabu and not
 // aspirating -- is fixed before the walk starts, so its history is determined by the deltas alone: the
 // global minimum D, the prefix minimum of the per-vertex minima (where each vertex enters the walk), the
 // ties at levels above D before the first D-candidate (E early draws, whose values are irrelevant), and
 // the final segment -- every admissible candidate at D, the j-th of which (j >= 2) keeps the choice iff
-// next_below(j) == 0.  Lane p owns the p-th vertex of the sequence; lane 0 only generates the stream; the
-// lanes test their own final-segment draws.  Any output below 2^32 (a possible rejection, probability
-// 2^-32 per draw) or a final segment longer than the buffer falls back to the serial walk.
+// next_below(j) == 0.  Lane p owns vertex 32 c + p of round c; lane 0 only generates the stream, 32
+// outputs at a time into shared memory, and the lanes test those draws.  A sequence of one round keeps
+// its vertex in registers; longer ones recompute it per pass (minimum, counts, owner) -- the until[][]
+// reads repeat only for the live entries of the possibly-tabu mask.  Any output below 2^32 (a possible
+// rejection, probability 2^-32 per draw) falls back to the serial walk.
+
+template <int W>
+struct LaneView {
+    VertexMoves<W> m;
+    int v;
+    uint64_t al[W];  // admissible colours k != 0
+    bool a0;         // the move to 0 admissible (conflicting vertices only)
+    int vmin;        // minimum delta over the admissible moves (INT_MAX: none)
+};
+
+template <int W>
+__device__ __forceinline__ void view_min(LaneView<W>& x, int wc) {
+    constexpr int NB = PlitsK<W>::NB;
+    x.vmin = x.a0 ? x.m.d0 : INT_MAX;
+    if (popc_w<W>(x.al)) {
+        uint64_t sel[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) sel[q] = x.al[q];
+        x.vmin = min(x.vmin, x.m.dbase + wc * sliced_min<W, NB>(x.m.S, sel));
+    }
+}
+
+// the admissible moves of sequence position p (tabu moves are admissible iff delta < asp = best - cur);
+// expired entries leave the possibly-tabu mask on the way
+template <int W>
+__device__ __forceinline__ void view_admissible(const Graph<W>& g, const PlitsRefWarp& s, int p, int nu, int wf,
+                                                int wc, const uint32_t* until, int w1, uint32_t t, int asp,
+                                                LaneView<W>& x) {
+    constexpr int NB = PlitsK<W>::NB;
+    const bool conflicting = p >= nu;
+    x.v = conflicting ? s.cf_el[p - nu] : s.un_el[p];
+    vertex_moves<W>(g, s, x.v, wf, wc, x.m);
+    uint64_t live[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) live[q] = 0;
+    uint64_t* Tv = s.T + (size_t)x.v * W;
+    const uint32_t* urow = until + (size_t)x.v * w1;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        uint64_t y = Tv[q] & (x.m.M[q] | ((q == 0 && conflicting) ? 1ULL : 0ULL));
+        uint64_t expired = 0;
+        while (y) {
+            const int b = __ffsll((long long)y) - 1;
+            y &= y - 1;
+            if (urow[q * 64 + b] > t)
+                live[q] |= 1ULL << b;
+            else
+                expired |= 1ULL << b;
+        }
+        if (expired) Tv[q] &= ~expired;  // the mask stays a superset of the live entries
+    }
+    x.a0 = conflicting && (!(live[0] & 1ULL) || x.m.d0 < asp);
+    live[0] &= ~1ULL;
+    // tabu colours admissible only with gamma <= floor((asp - 1 - dbase) / wc)
+    uint64_t hi[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) hi[q] = live[q];
+    sliced_ge<W, NB>(x.m.S, floor_div(asp - 1 - x.m.dbase, wc) + 1, hi);
+#pragma unroll
+    for (int q = 0; q < W; ++q) x.al[q] = x.m.M[q] & ~hi[q];
+    view_min<W>(x, wc);
+}
+
+// early draws of one vertex: ties at levels above D, counted per level from the incoming running
+// minimum rin -- a candidate at level L ties iff it precedes every candidate below L and the running
+// minimum already is L (an earlier candidate at L, or the incoming one)
+template <int W>
+__device__ __forceinline__ int view_early(const LaneView<W>& x, int rin, int D, int wc) {
+    constexpr int NB = PlitsK<W>::NB;
+    constexpr int kInf = INT_MAX;
+    int early = 0;
+    int r = rin;
+    uint64_t G[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) G[q] = x.al[q];
+    if (x.a0) {  // k = 0 comes first
+        if (x.m.d0 < r)
+            r = x.m.d0;
+        else if (x.m.d0 == r)
+            ++early;
+    }
+    if (r == kInf && popc_w<W>(G)) {  // nothing before this vertex: its first colour resets
+        const int k1 = first_bit_w<W>(G);
+        r = x.m.dbase + wc * sliced_val<W, NB>(x.m.S, k1);
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+            if ((k1 >> 6) == q) G[q] &= ~(1ULL << (k1 & 63));
+    }
+    if (r == kInf || r <= D || !popc_w<W>(G)) return early;
+    const int gr = floor_div(r - x.m.dbase, wc);
+    {
+        uint64_t hi[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) hi[q] = G[q];
+        sliced_ge<W, NB>(x.m.S, gr + 1, hi);
+#pragma unroll
+        for (int q = 0; q < W; ++q) G[q] &= ~hi[q];
+    }
+    if (!popc_w<W>(G)) return early;
+    uint64_t sel[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) sel[q] = G[q];
+    const int gmin = sliced_min<W, NB>(x.m.S, sel);
+    for (int gl = gr; gl >= gmin; --gl) {
+        const int L = x.m.dbase + wc * gl;
+        if (L <= D) break;
+        uint64_t eqg[W], lo[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) eqg[q] = lo[q] = G[q];
+        sliced_eq<W, NB>(x.m.S, gl, eqg);
+        sliced_ge<W, NB>(x.m.S, gl, lo);  // lo = G minus the candidates below gl
+#pragma unroll
+        for (int q = 0; q < W; ++q) lo[q] = G[q] & ~lo[q];
+        const int cnt = popc_below_w<W>(eqg, first_bit_w<W>(lo));
+        early += (L == r) ? cnt : max(cnt - 1, 0);
+    }
+    return early;
+}
+
+// the vertex's members of the final segment: k = 0 first (z0), then the colours aD ascending
+template <int W>
+__device__ __forceinline__ int view_final(const LaneView<W>& x, int D, int wc, uint64_t (&aD)[W], bool& z0) {
+    constexpr int NB = PlitsK<W>::NB;
+#pragma unroll
+    for (int q = 0; q < W; ++q) aD[q] = 0;
+    z0 = false;
+    if (x.vmin != D) return 0;
+    z0 = x.a0 && x.m.d0 == D;
+    const int num = D - x.m.dbase;
+    if (num >= 0 && num % wc == 0) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) aD[q] = x.al[q];
+        sliced_eq<W, NB>(x.m.S, num / wc, aD);
+    }
+    return (int)z0 + popc_w<W>(aD);
+}
+
+__device__ __forceinline__ int warp_incl_sum(int x, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x += y;
+    }
+    return x;
+}
+
 template <int W>
 __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRefWarp& s, int lane, int nseq, int nu,
                                                int wf, int wc, uint32_t* until, int w1, uint32_t t,
                                                int64_t cur_scaled, int64_t best_scaled, Xoshiro& rng,
                                                RefChoice& ch, unsigned long long* tp) {
-    constexpr int NB = PlitsK<W>::NB;
     constexpr int kInf = INT_MAX;
     long long t0 = tp ? clock64() : 0;
     auto stamp = [&](int z) {
@@ -200,206 +347,135 @@ __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRef
             t0 = x;
         }
     };
-    const bool mine = lane < nseq;
-    const bool conflicting = lane >= nu;
-    VertexMoves<W> m;
-    int v = 0;
-    uint64_t al[W];  // admissible colours k != 0
-#pragma unroll
-    for (int q = 0; q < W; ++q) al[q] = 0;
-    bool a0 = false;  // the move to 0 admissible (conflicting vertices only)
-    int vmin = kInf;
-    // tabu moves are admissible iff they aspirate: delta < best - cur
+    const int nch = (nseq + 31) >> 5;
+    uint64_t* out = s.stage;  // 32 outputs of the stream at a time
     const int64_t asp64 = best_scaled - cur_scaled;
     const int asp = (int)max((int64_t)INT_MIN / 4, min((int64_t)INT_MAX / 4, asp64));
-    if (mine) {
-        v = lane < nu ? s.un_el[lane] : s.cf_el[lane - nu];
-        vertex_moves<W>(g, s, v, wf, wc, m);
-        uint64_t live[W];
+    auto empty = [](LaneView<W>& x) {
 #pragma unroll
-        for (int q = 0; q < W; ++q) live[q] = 0;
-        uint64_t* Tv = s.T + (size_t)v * W;
-        const uint32_t* urow = until + (size_t)v * w1;
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-            uint64_t x = Tv[q] & (m.M[q] | ((q == 0 && conflicting) ? 1ULL : 0ULL));
-            uint64_t expired = 0;
-            while (x) {
-                const int b = __ffsll((long long)x) - 1;
-                x &= x - 1;
-                if (urow[q * 64 + b] > t)
-                    live[q] |= 1ULL << b;
-                else
-                    expired |= 1ULL << b;
-            }
-            if (expired) Tv[q] &= ~expired;  // the mask stays a superset of the live entries
-        }
-        a0 = conflicting && (!(live[0] & 1ULL) || m.d0 < asp);
-        live[0] &= ~1ULL;
-        // tabu colours admissible only with gamma <= floor((asp - 1 - dbase) / wc)
-        uint64_t hi[W];
-#pragma unroll
-        for (int q = 0; q < W; ++q) hi[q] = live[q];
-        sliced_ge<W, NB>(m.S, floor_div(asp - 1 - m.dbase, wc) + 1, hi);
-#pragma unroll
-        for (int q = 0; q < W; ++q) al[q] = m.M[q] & ~hi[q];
-        if (a0) vmin = m.d0;
-        if (popc_w<W>(al)) {
-            uint64_t sel[W];
-#pragma unroll
-            for (int q = 0; q < W; ++q) sel[q] = al[q];
-            vmin = min(vmin, m.dbase + wc * sliced_min<W, NB>(m.S, sel));
-        }
+        for (int q = 0; q < W; ++q) x.al[q] = 0;
+        x.a0 = false;
+        x.vmin = kInf;
+        x.v = 0;
+        x.m.cur = x.m.dbase = x.m.d0 = 0;
+    };
+    auto view_of = [&](int c, LaneView<W>& x) {
+        const int p = 32 * c + lane;
+        if (p < nseq)
+            view_admissible<W>(g, s, p, nu, wf, wc, until, w1, t, asp, x);
+        else
+            empty(x);
+    };
+
+    // ---- pass 1: admissible moves, their minimum
+    LaneView<W> x;
+    int D = kInf;
+    for (int c = 0; c < nch; ++c) {
+        view_of(c, x);
+        D = min(D, __reduce_min_sync(kFull, x.vmin));
     }
     stamp(0);
-    const int D = __reduce_min_sync(kFull, vmin);
     if (D == kInf) {  // every candidate tabu: nothing found, no draw
         ch.found = 0;
         return true;
     }
-    int pm = vmin;  // inclusive prefix minimum of the per-vertex minima
+    // ---- pass 2: early draws up to the first D-candidate, the size of the final segment
+    int E = 0, ND = 0, rcarry = kInf;
+    bool seen = false;
+    for (int c = 0; c < nch; ++c) {
+        if (nch > 1) view_of(c, x);
+        int pm = x.vmin;  // inclusive prefix minimum of the per-vertex minima
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int x = __shfl_up_sync(kFull, pm, d);
-        if (lane >= d) pm = min(pm, x);
-    }
-    int rin = __shfl_up_sync(kFull, pm, 1);
-    if (lane == 0) rin = kInf;
-    const int istar = __ffs(__ballot_sync(kFull, vmin == D)) - 1;
-    // early draws: ties at levels above D before the first D-candidate, counted per level from the
-    // incoming running minimum -- a candidate at level L ties iff it precedes every candidate below L and
-    // the running minimum already is L (an earlier candidate at L, or the incoming one)
-    int early = 0;
-    if (mine && lane <= istar) {
-        int r = rin;
-        uint64_t G[W];
-#pragma unroll
-        for (int q = 0; q < W; ++q) G[q] = al[q];
-        if (a0) {  // k = 0 comes first
-            if (m.d0 < r)
-                r = m.d0;
-            else if (m.d0 == r)
-                ++early;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, pm, d);
+            if (lane >= d) pm = min(pm, y);
         }
-        if (r == kInf && popc_w<W>(G)) {  // nothing before this vertex: its first colour resets
-            const int k1 = first_bit_w<W>(G);
-            r = m.dbase + wc * sliced_val<W, NB>(m.S, k1);
-#pragma unroll
-            for (int q = 0; q < W; ++q)
-                if ((k1 >> 6) == q) G[q] &= ~(1ULL << (k1 & 63));
+        if (!seen) {
+            int rin = __shfl_up_sync(kFull, pm, 1);
+            if (lane == 0) rin = kInf;
+            rin = min(rin, rcarry);
+            const unsigned bal = __ballot_sync(kFull, x.vmin == D);
+            const int istar = bal ? __ffs(bal) - 1 : 32;
+            const int early = (32 * c + lane < nseq && lane <= istar) ? view_early<W>(x, rin, D, wc) : 0;
+            E += (int)__reduce_add_sync(kFull, (unsigned)early);
+            seen = bal != 0;
         }
-        if (r != kInf && r > D && popc_w<W>(G)) {
-            const int gr = floor_div(r - m.dbase, wc);
-            {
-                uint64_t hi[W];
-#pragma unroll
-                for (int q = 0; q < W; ++q) hi[q] = G[q];
-                sliced_ge<W, NB>(m.S, gr + 1, hi);
-#pragma unroll
-                for (int q = 0; q < W; ++q) G[q] &= ~hi[q];
-            }
-            if (popc_w<W>(G)) {
-                uint64_t sel[W];
-#pragma unroll
-                for (int q = 0; q < W; ++q) sel[q] = G[q];
-                const int gmin = sliced_min<W, NB>(m.S, sel);
-                for (int gl = gr; gl >= gmin; --gl) {
-                    const int L = m.dbase + wc * gl;
-                    if (L <= D) break;
-                    uint64_t eqg[W], lo[W];
-#pragma unroll
-                    for (int q = 0; q < W; ++q) eqg[q] = lo[q] = G[q];
-                    sliced_eq<W, NB>(m.S, gl, eqg);
-                    sliced_ge<W, NB>(m.S, gl, lo);  // lo = G minus the candidates below gl
-#pragma unroll
-                    for (int q = 0; q < W; ++q) lo[q] = G[q] & ~lo[q];
-                    const int cnt = popc_below_w<W>(eqg, first_bit_w<W>(lo));
-                    early += (L == r) ? cnt : max(cnt - 1, 0);
-                }
-            }
-        }
+        uint64_t aD[W];
+        bool z0;
+        ND += (int)__reduce_add_sync(kFull, (unsigned)view_final<W>(x, D, wc, aD, z0));
+        rcarry = min(rcarry, __shfl_sync(kFull, pm, 31));
     }
     stamp(1);
-    // the final segment: admissible candidates at D, k = 0 first, then colours ascending
-    uint64_t aD[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) aD[q] = 0;
-    bool z0 = false;
-    if (mine && vmin == D) {
-        z0 = a0 && m.d0 == D;
-        const int num = D - m.dbase;
-        if (num >= 0 && num % wc == 0) {
-#pragma unroll
-            for (int q = 0; q < W; ++q) aD[q] = al[q];
-            sliced_eq<W, NB>(m.S, num / wc, aD);
-        }
-    }
-    const int cD = (int)z0 + popc_w<W>(aD);
-    const int E = (int)__reduce_add_sync(kFull, (unsigned)early);
-    int sD = cD;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int x = __shfl_up_sync(kFull, sD, d);
-        if (lane >= d) sD += x;
-    }
-    const int ND = __shfl_sync(kFull, sD, 31);
-    sD -= cD;
-    constexpr int cap = 32 * (NB + 1) * W;  // the staging buffer, reused for the final-segment outputs
-    uint64_t* out = s.stage;
-    if (ND - 1 > cap) return false;
-    const Xoshiro saved = rng;
-    bool ok = true;
-    stamp(2);
+    // member j (1-based, in walk order) of the final segment keeps the choice iff next_below(j) == 0
+    // (j >= 2): draw E + j - 2 of the stream
+    const Xoshiro before = rng;
+    uint32_t bad = 0;  // lane 0: an output below 2^32 -- a rejection is possible, take the exact path
     if (tp) tp[5] += (unsigned)(E + ND - 1);
     if (lane == 0) {
-        uint32_t bad = 0;  // an output below 2^32: a rejection is possible, take the exact path
 #pragma unroll 4
         for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
-#pragma unroll 4
-        for (int d = 0; d < ND - 1; ++d) {
-            const uint64_t x = rng.next();
-            bad |= (uint32_t)((x >> 32) == 0);
-            out[d] = x;
-        }
-        ok = bad == 0;
     }
-    ok = __shfl_sync(kFull, (int)ok, 0) != 0;
-    __syncwarp();
+    int bestj = 0;
+    for (int j0 = 2; j0 <= ND; j0 += 32) {
+        const int cnt = min(32, ND - j0 + 1);
+        if (lane == 0) {
+#pragma unroll 4
+            for (int d = 0; d < cnt; ++d) {
+                const uint64_t y = rng.next();
+                bad |= (uint32_t)((y >> 32) == 0);
+                out[d] = y;
+            }
+        }
+        __syncwarp();
+        if (lane < cnt && divides((uint64_t)(j0 + lane), out[lane])) bestj = j0 + lane;
+        __syncwarp();
+    }
     stamp(3);
-    if (!ok) {
-        if (lane == 0) rng = saved;
+    if (__shfl_sync(kFull, bad, 0)) {
+        if (lane == 0) rng = before;
         return false;
     }
-    // member j (1-based, in walk order) of the final segment keeps the choice iff next_below(j) == 0
-    // (j >= 2): draw E + j - 2 of the stream; the lanes test the members round-robin
-    int bestj = 0;
-    for (int j = 2 + lane; j <= ND; j += 32)
-        if (divides((uint64_t)j, out[j - 2])) bestj = j;
     int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
     if (J == 0) J = 1;
-    const bool own = sD < J && J <= sD + cD;
-    int kk = 0, dc = 0, df = 0;
-    if (own) {
-        const int li = J - sD - 1;
-        const int gcur = m.cur ? (wf - m.d0) / wc : 0;
-        if (z0 && li == 0) {
-            kk = 0;
-            dc = -gcur;
-            df = 1;
-        } else {
-            kk = nth_bit_w<W>(aD, li - (int)z0);
-            dc = (D - m.dbase) / wc - gcur;
-            df = m.cur ? 0 : -1;
+    // ---- pass 3: the owner of member J
+    int based = 0;
+    for (int c = 0; c < nch; ++c) {
+        if (nch > 1) view_of(c, x);
+        uint64_t aD[W];
+        bool z0;
+        const int cD = view_final<W>(x, D, wc, aD, z0);
+        const int incl = warp_incl_sum(cD, lane);
+        const int tot = __shfl_sync(kFull, incl, 31);
+        if (J > based + tot) {
+            based += tot;
+            continue;
         }
+        const int sD = based + incl - cD;
+        const bool own = sD < J && J <= sD + cD;
+        int kk = 0, dc = 0, df = 0;
+        if (own) {
+            const int li = J - sD - 1;
+            const int gcur = x.m.cur ? (wf - x.m.d0) / wc : 0;
+            if (z0 && li == 0) {
+                kk = 0;
+                dc = -gcur;
+                df = 1;
+            } else {
+                kk = nth_bit_w<W>(aD, li - (int)z0);
+                dc = (D - x.m.dbase) / wc - gcur;
+                df = x.m.cur ? 0 : -1;
+            }
+        }
+        const int wl = __ffs(__ballot_sync(kFull, own)) - 1;
+        ch.found = 1;
+        ch.delta = D;
+        ch.ties = (uint32_t)ND;
+        ch.v = __shfl_sync(kFull, x.v, wl);
+        ch.k = __shfl_sync(kFull, kk, wl);
+        ch.dc = __shfl_sync(kFull, dc, wl);
+        ch.df = __shfl_sync(kFull, df, wl);
+        break;
     }
-    const int wl = __ffs(__ballot_sync(kFull, own)) - 1;
-    ch.found = 1;
-    ch.delta = D;
-    ch.ties = (uint32_t)ND;
-    ch.v = __shfl_sync(kFull, v, wl);
-    ch.k = __shfl_sync(kFull, kk, wl);
-    ch.dc = __shfl_sync(kFull, dc, wl);
-    ch.df = __shfl_sync(kFull, df, wl);
     __syncwarp();
     stamp(4);
     return true;
@@ -481,7 +557,7 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
                 pc[4] += (unsigned)nseq;
             }
             bool fast_done = false;
-            if (nseq <= 32) {
+            {
                 fast_done = plits_ref_fast<W>(g, s, lane, nseq, nu, wf, wc, until, w1, t, cur_scaled, best_scaled,
                                               rng, ch, prof ? pc + 8 : nullptr);
                 if (prof) {
@@ -715,7 +791,7 @@ __device__ void plits_ref_one(const ImproveArgs& a, const Graph<W>& g, const Pli
 }  // namespace
 
 template <int W, bool kDebug>
-__global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits_ref(const ImproveArgs a) {
+__global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits_ref(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int n = a.n, nv = a.nv;
