@@ -83,3 +83,29 @@ def test_elite_and_victim_orders():
     c = np.array([0, 0, 0, 0, 2])
     assert islands.elite_order(f, c).tolist() == [1, 2, 0, 3, 4]
     assert islands.victim_order(f, c).tolist() == [4, 3, 0, 2, 1]
+
+
+def _reduce_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    from paper_2103_10453_b200 import islands
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # ranks 1 and 2 tie on the best f: the lowest rank owns it
+    best_f = [9, 4, 4][rank]
+    out = islands.reduce_generation(best_f, 100 * (rank + 1), 0.5 + rank, None, "cpu")
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array(out, dtype=np.float64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reduce_generation_over_gloo(tmp_path):
+    """The island run's per-generation collective: global best f, its lowest owning rank, summed
+    iterations, max elapsed -- identical on every rank."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_reduce_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True,
+                       start_method="spawn")
+    for r in range(3):
+        assert np.load(os.path.join(tmp_path, f"r{r}.npy")).tolist() == [4, 1, 600, 2.5]
