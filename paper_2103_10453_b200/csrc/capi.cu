@@ -648,8 +648,10 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         const double st = pr[0] ? (double)pr[0] : 1.0;
         std::fprintf(stderr,
                      "[plse-prof plits] indiv %llu steps %llu | cyc/step: list %.0f level %.0f select %.0f move %.0f "
-                     "total %.0f | extra level passes %.3f/step | mean active %.1f\n",
-                     pr[8], pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st);
+                     "total %.0f | extra level passes %.3f/step | mean active %.1f | move: select->membership %.0f "
+                     "membership %.0f tail %.0f\n",
+                     pr[8], pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st,
+                     pr[9] / st, pr[10] / st, pr[11] / st);
     } else if (c->d_prof && std::getenv("PLSE_PROFILE")) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));

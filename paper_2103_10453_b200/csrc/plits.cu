@@ -48,6 +48,9 @@ struct PlitsWarp {
     int32_t* vmin;    // [nv] per active vertex: tabu-blind minimum delta of its moves (refreshed when its
                       //      row or column changes)
     uint8_t* vcnt;    // [nv] per active vertex at the step's level: its admissible moves
+    uint64_t* T;      // [nv][W] GLOBAL (the slot's tabu-record area, L1-resident for a lone warp): colours
+                      //         possibly tabu -- a superset of the live until[][] entries, so only those
+                      //         colours read until[][]
 };
 
 // tabu-blind minimum delta over v's candidates (plits.hpp:135-176 without the tabu test)
@@ -152,12 +155,12 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int lane, int
 }
 
 // the admissible moves of one vertex at delta level dl (plits.hpp:146-147): adm = colours k != 0,
-// adm0 = the move to 0.  Tabu candidates read until[][] in independent batches of four.
+// adm0 = the move to 0.  Only colours in the possibly-tabu mask Tv read until[][] (independent batches
+// of four); expired ones leave the mask.
 template <int W>
 __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
-                                         uint32_t t, uint64_t (&adm)[W], bool& adm0) {
+                                         uint64_t* Tv, uint32_t t, uint64_t (&adm)[W], bool& adm0) {
     constexpr int NB = PlitsK<W>::NB;
-    adm0 = m.cur && m.d0 == dl && (asp_all || urow[0] <= t);
     const int qv = dl - m.dbase;
 #pragma unroll
     for (int q = 0; q < W; ++q) adm[q] = m.M[q];
@@ -167,10 +170,16 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
     } else {
         sliced_eq<W, NB>(m.S, qv / wc, adm);
     }
-    if (!asp_all) {
+    adm0 = m.cur && m.d0 == dl;
+    if (!asp_all && (adm0 || popc_w<W>(adm))) {
+        uint64_t tv[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) tv[q] = Tv[q];
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-            uint64_t x = adm[q];
+            uint64_t x = adm[q] & tv[q];
+            if (q == 0 && adm0) x |= tv[0] & 1ULL;
+            uint64_t expired = 0;
             while (x) {
                 int ks[4];
                 uint32_t us[4];
@@ -182,9 +191,19 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
 #pragma unroll
                 for (int z = 0; z < 4; ++z) us[z] = ks[z] >= 0 ? urow[q * 64 + ks[z]] : 0u;
 #pragma unroll
-                for (int z = 0; z < 4; ++z)
-                    if (ks[z] >= 0 && us[z] > t) adm[q] &= ~(1ULL << ks[z]);
+                for (int z = 0; z < 4; ++z) {
+                    if (ks[z] < 0) continue;
+                    if (us[z] > t) {
+                        if (q == 0 && ks[z] == 0)
+                            adm0 = false;
+                        else
+                            adm[q] &= ~(1ULL << ks[z]);
+                    } else {
+                        expired |= 1ULL << ks[z];
+                    }
+                }
             }
+            if (expired) Tv[q] = tv[q] & ~expired;
         }
     }
     return popc_w<W>(adm) + (adm0 ? 1 : 0);
@@ -201,7 +220,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     uint8_t* best_row = a.improved + (size_t)i * g.nvpad;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
-    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // steps, list, level, select, move, step, level iters, sum na
+    // steps, list, level, select, move, step, level iters, sum na | move: plane, membership, tail
+    unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tp0 = 0, tp1 = 0;
 
     // ---- tabu clock of this warp slot (two phases, each followed by a skip of tenure_cap + 2)
@@ -337,7 +357,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                         vertex_moves<W>(g, s, v, wf, wc, m);
                         uint64_t adm[W];
                         bool adm0;
-                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, t, adm, adm0);
+                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, s.T + (size_t)v * W, t, adm, adm0);
                         if (cnt && c_v < 0) {
                             c_v = v;
                             c_adm0 = adm0;
@@ -406,7 +426,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 } else {
                     VertexMoves<W> m;
                     vertex_moves<W>(g, s, sv, wf, wc, m);
-                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, t, adm, adm0);
+                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, s.T + (size_t)sv * W, t, adm, adm0);
                     d0 = m.d0;
                     dbase = m.dbase;
                 }
@@ -441,8 +461,15 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             }
             if (lane == 1) plane_move<W, NP>(s.cp + (size_t)cs_ * NP * W, from, ks);
             __syncwarp();
+            long long tm0 = prof ? clock64() : 0;
+            if (prof) pc[8] += (unsigned long long)(tm0 - tp1);
             plits_membership<W>(g, s, rs_, cs_, from, ks, wf, wc, lane);
             __syncwarp();
+            if (prof) {
+                const long long x = clock64();
+                pc[9] += (unsigned long long)(x - tm0);
+                tm0 = x;
+            }
             {
                 int al = 0;
                 for (int q = 0; q < g.lane_words; ++q) al += __popc(s.A[lane * g.lane_words + q]);
@@ -453,6 +480,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(alpha * (double)active);
             if (lane == 0) {
                 until[(size_t)vs * w1 + from] = t + 1 + tenure;
+                s.T[(size_t)vs * W + (from >> 6)] |= 1ULL << (from & 63);
                 acc += 2ULL * (unsigned)w1 * (unsigned)active_before + 4ULL * g.deg[vs] + 2ULL;
             }
             if (now < best_scaled) {
@@ -470,6 +498,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
+            if (prof) pc[10] += (unsigned long long)(clock64() - tm0);
             tick(4);
             if (prof) {
                 pc[5] += (unsigned long long)(clock64() - tp0);
@@ -544,6 +573,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 #pragma unroll
             for (int z = 0; z < 8; ++z) atomicAdd(prof + z, pc[z]);
             atomicAdd(prof + 8, 1ULL);
+            for (int z = 8; z < 11; ++z) atomicAdd(prof + z + 1, pc[z]);
         }
     }
     __syncwarp();
@@ -617,6 +647,9 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits(con
 
     const int slot = blockIdx.x * nwarps + warp;
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
+    // the possibly-tabu mask lives in the slot's tabu-record area (nv * 16 >= nv * 8 W bytes); any stale
+    // content is a harmless superset: every until[][] entry of an earlier individual is below its clock
+    s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
