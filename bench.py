@@ -302,6 +302,7 @@ def run_ours(a):
                 elite_buf.copy_(torch.cat(parts).to("cuda"))
             torch.cuda.synchronize()
             others = torch.cat([elite_buf[r * a.elites:(r + 1) * a.elites] for r in range(world) if r != rank])
+            torch.cuda.synchronize()  # the library reads `others` on its own stream
             pop.import_migrants(others.shape[0], others.data_ptr())
         pop.build_offspring(gen)
         c2 = pop.counters()

@@ -210,7 +210,9 @@ int plse_trace(plse_ctx* ctx, int32_t idx, uint64_t generation, int64_t max_step
 /* ---- island exchange (multi-GPU): the driver moves the bytes (NCCL all-gather) */
 /* copy the n_elite best members (ascending f, lowest index) as u8 rows [n_elite*|V|] into dev_out */
 int plse_export_elites(plse_ctx* ctx, int32_t n_elite, void* dev_out, int32_t* f_out);
-/* replace the n_in worst members by the given u8 rows [n_in*|V|] (device pointer) and refresh dist */
+/* replace the n_in worst members by the given u8 rows [n_in*|V|] (device pointer) and refresh dist;
+   the rows are read on the context's stream: the caller makes them complete first (e.g. synchronises
+   the stream that produced them) */
 int plse_import_migrants(plse_ctx* ctx, int32_t n_in, const void* dev_in);
 
 /* ---- the whole run() (engine.hpp:114-262) on one device */

@@ -63,6 +63,7 @@ class DeviceIsland:
         gathered = allgather_rows(self.mine, self.group)
         torch.cuda.synchronize()
         rest = others(gathered, self.rank, self.world).contiguous()
+        torch.cuda.synchronize()  # the library reads `rest` on its own stream
         self.pop.import_migrants(rest.shape[0], rest.data_ptr())
 
 
@@ -238,6 +239,7 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
                     gathered = allgather_rows(elites.cpu(), group).to("cuda")
                 torch.cuda.synchronize()
                 rest = others(gathered, rank, world).contiguous()
+                torch.cuda.synchronize()  # the library reads `rest` on its own stream
                 pop.import_migrants(rest.shape[0], rest.data_ptr())
             pop.build_offspring(gen)
             if on_generation:
