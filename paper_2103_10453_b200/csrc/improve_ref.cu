@@ -127,6 +127,152 @@ __device__ __forceinline__ void ref_walk(RefScan& st, Xoshiro& rng, const uint64
     }
 }
 
+// the same scan for |V0| > 32: 32 vertices per round, lane p owning vertex 32 c + p, the masks
+// recomputed per pass (minimum, counts, owner)
+template <int W>
+__device__ __forceinline__ bool partial_ref_fast(const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
+                                                 const uint32_t* until, const uint16_t* el, uint64_t* msk, int f,
+                                                 uint32_t t, bool asp, int lane, Xoshiro& rng, RefScan& st,
+                                                 unsigned long long* pc) {
+    long long tf = pc ? clock64() : 0;
+    auto fstamp = [&](int z) {
+        if (pc) {
+            const long long x = clock64();
+            pc[z] += (unsigned long long)(x - tf);
+            tf = x;
+        }
+    };
+    const int nch = (f + 31) >> 5;
+    uint64_t a0[W], a1[W], a2[W];
+    auto masks_of = [&](int c) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) a0[q] = a1[q] = a2[q] = 0;
+        const int p = 32 * c + lane;
+        if (p < f) dense_masks<W>(g, s, rec, until, el[p], t, asp, a0, a1, a2);
+    };
+    auto level_of = [&](int c) -> int {
+        return (32 * c + lane >= f) ? 3 : popc_w<W>(a0) ? 0 : popc_w<W>(a1) ? 1 : popc_w<W>(a2) ? 2 : 3;
+    };
+    // ---- pass 1: the global minimum level
+    int D = 3;
+    for (int c = 0; c < nch; ++c) {
+        masks_of(c);
+        D = min(D, (int)__reduce_min_sync(kFull, (unsigned)level_of(c)));
+    }
+    fstamp(6);
+    if (D == 3) return true;  // no admissible candidate: no draw at all
+    // ---- pass 2: early draws up to the first level-D candidate, the size of the final segment
+    int E = 0, ND = 0, Rc = 3, cD1 = 0, incl1 = 0;
+    bool seen = false;
+    for (int c = 0; c < nch; ++c) {
+        if (nch > 1) masks_of(c);
+        const int m = level_of(c);
+        int pm = m;  // inclusive prefix minimum of the per-vertex minimum level
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int x = __shfl_up_sync(kFull, pm, d);
+            if (lane >= d) pm = min(pm, x);
+        }
+        if (!seen) {
+            int R = __shfl_up_sync(kFull, pm, 1);
+            if (lane == 0) R = 3;
+            R = min(R, Rc);
+            const unsigned bal = __ballot_sync(kFull, m == D);
+            const int istar = bal ? __ffs(bal) - 1 : 32;
+            int early = 0;
+            if (lane <= istar && 32 * c + lane < f) early = vertex_draws<W>(a0, a1, a2, R, lane == istar ? D : 3);
+            E += (int)__reduce_add_sync(kFull, (unsigned)early);
+            seen = bal != 0;
+        }
+        uint64_t aD[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) aD[q] = D == 0 ? a0[q] : D == 1 ? a1[q] : a2[q];
+        cD1 = popc_w<W>(aD);
+        incl1 = cD1;  // inclusive prefix sum of the level-D counts (kept for a one-round set)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int x = __shfl_up_sync(kFull, incl1, d);
+            if (lane >= d) incl1 += x;
+        }
+        ND += __shfl_sync(kFull, incl1, 31);
+        Rc = min(Rc, __shfl_sync(kFull, pm, 31));
+    }
+    fstamp(7);
+    // ---- final-segment member j (1-based; the first is j = 1) keeps the choice iff next_below(j) == 0,
+    // draw E + j - 2 of the stream: lane 0 generates it 32 outputs at a time into msk, the lanes test the
+    // members round-robin
+    const Xoshiro saved = rng;
+    uint32_t bad = 0;  // lane 0: an output below 2^32, a rejection is possible
+    if (lane == 0) {
+#pragma unroll 4
+        for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
+    }
+    int bestj = 0;
+    for (int j0 = 2; j0 <= ND; j0 += 32) {
+        const int cnt = min(32, ND - j0 + 1);
+        if (lane == 0) {
+#pragma unroll 4
+            for (int d = 0; d < cnt; ++d) {
+                const uint64_t y = rng.next();
+                bad |= (uint32_t)((y >> 32) == 0);
+                msk[d] = y;
+            }
+        }
+        __syncwarp();
+        if (lane < cnt && divides((uint64_t)(j0 + lane), msk[lane])) bestj = j0 + lane;
+        __syncwarp();
+    }
+    fstamp(8);
+    if (__shfl_sync(kFull, bad, 0)) {
+        if (lane == 0) rng = saved;  // take the exact path
+        return false;
+    }
+    int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
+    if (J == 0) J = 1;
+    // ---- pass 3: the owner of member J
+    int based = 0;
+    for (int c = 0; c < nch; ++c) {
+        if (nch > 1) masks_of(c);
+        uint64_t aD[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) aD[q] = (32 * c + lane >= f) ? 0ULL : D == 0 ? a0[q] : D == 1 ? a1[q] : a2[q];
+        int cD = cD1, incl = incl1;
+        if (nch > 1) {
+            cD = popc_w<W>(aD);
+            incl = cD;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += x;
+            }
+        }
+        const int tot = nch > 1 ? __shfl_sync(kFull, incl, 31) : ND;
+        if (J > based + tot) {
+            based += tot;
+            continue;
+        }
+        const int sD = based + incl - cD;
+        const bool own = sD < J && J <= sD + cD;
+        int cv = 0, ck = 0, cpos = 0;
+        if (own) {
+            cpos = 32 * c + lane;
+            cv = el[cpos];
+            ck = nth_bit_w<W>(aD, J - sD - 1);
+        }
+        const int wl = __ffs(__ballot_sync(kFull, own)) - 1;
+        st.found = 1;
+        st.bd = D - 1;
+        st.ties = (uint32_t)ND;
+        st.cv = __shfl_sync(kFull, cv, wl);
+        st.ck = __shfl_sync(kFull, ck, wl);
+        st.cpos = __shfl_sync(kFull, cpos, wl);
+        break;
+    }
+    __syncwarp();
+    fstamp(9);
+    return true;
+}
+
 template <int W, bool kDebug>
 __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, uint16_t* el,
                                 uint64_t* msk, TabuRec* rec, uint32_t* until, uint32_t* slot_clock, uint8_t* conf, int i,
@@ -136,7 +282,9 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
     uint8_t* colT = s.colT;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
-    unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};  // steps, mask cycles, walk cycles, apply cycles, draws, sum f
+    // steps, mask cycles, walk cycles, apply cycles, draws, sum f | fast path: masks, scans, stream, owner
+    unsigned long long pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+
     long long tq = 0;
 
     uint32_t base = *slot_clock;
@@ -204,7 +352,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         }
         bool fast_done = false;
         if (f <= 32) {
-            // masks of position `lane` in registers
+            // one round: the masks of position `lane` stay in registers
             uint64_t a0[W], a1[W], a2[W];
 #pragma unroll
             for (int q = 0; q < W; ++q) a0[q] = a1[q] = a2[q] = 0;
@@ -238,39 +386,32 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 }
                 const int ND = __shfl_sync(kFull, sD, 31);
                 sD -= cD;  // exclusive: index (0-based) of this lane's first level-D candidate
-                const int cap = 32 * 3 * W;
-                bool ok = ND - 1 <= cap;
                 const Xoshiro saved = rng;
-                if (ok && lane == 0) {
-                    for (int d = 0; d < E + ND - 1; ++d) {
-                        const uint64_t x = rng.next();
-                        if (x < (1ULL << 32)) ok = false;  // a rejection is possible: take the exact path
-                        if (d >= E) msk[d - E] = x;
-                    }
+                uint32_t bad = 0;  // lane 0: an output below 2^32, a rejection is possible
+                if (lane == 0) {
+#pragma unroll 4
+                    for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
                 }
-                ok = __shfl_sync(kFull, (int)ok, 0) != 0;
-                __syncwarp();
-                if (ok) {
-                    // final-segment member j (1-based; c* is j = 1) keeps the choice iff next_below(j) == 0
-                    int bestj = 0, tloc = 0;
-                    uint64_t x[W];
-#pragma unroll
-                    for (int q = 0; q < W; ++q) x[q] = aD[q];
-                    for (int q = 0; q < W; ++q) {
-                        uint64_t y = word_sel<W>(x, q);
-                        while (y) {
-                            y &= y - 1;
-                            const int jj = sD + (++tloc);
-                            if (jj >= 2 && divides((uint64_t)jj, msk[jj - 2])) bestj = jj;
+                int bestj = 0;
+                for (int j0 = 2; j0 <= ND; j0 += 32) {
+                    const int cnt = min(32, ND - j0 + 1);
+                    if (lane == 0) {
+#pragma unroll 4
+                        for (int d = 0; d < cnt; ++d) {
+                            const uint64_t y = rng.next();
+                            bad |= (uint32_t)((y >> 32) == 0);
+                            msk[d] = y;
                         }
                     }
+                    __syncwarp();
+                    if (lane < cnt && divides((uint64_t)(j0 + lane), msk[lane])) bestj = j0 + lane;
+                    __syncwarp();
+                }
+                if (!__shfl_sync(kFull, bad, 0)) {
                     int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
                     if (J == 0) J = 1;
                     const bool own = sD < J && J <= sD + cD;
                     if (own) {
-                        st.found = 1;
-                        st.bd = D - 1;
-                        st.ties = (uint32_t)ND;
                         st.cv = el[lane];
                         st.ck = nth_bit_w<W>(aD, J - sD - 1);
                         st.cpos = lane;
@@ -284,15 +425,17 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                     st.cpos = __shfl_sync(kFull, st.cpos, wl);
                     fast_done = true;
                 } else if (lane == 0) {
-                    rng = saved;
+                    rng = saved;  // take the exact path
                 }
                 __syncwarp();
             }
-            if (prof) {
-                const long long x = clock64();
-                pc[2] += (unsigned long long)(x - tq);
-                tq = x;
-            }
+        } else {
+            fast_done = partial_ref_fast<W>(g, s, rec, until, el, msk, f, t, asp, lane, rng, st, prof ? pc : nullptr);
+        }
+        if (prof) {
+            const long long x = clock64();
+            pc[2] += (unsigned long long)(x - tq);
+            tq = x;
         }
         for (int c0 = 0; c0 < f && !fast_done; c0 += 32) {
             const int p = c0 + lane;
@@ -425,7 +568,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         *slot_clock = base + j + 2 + a.tenure_cap;
         if (prof) {
 #pragma unroll
-            for (int z = 0; z < 6; ++z) atomicAdd(prof + z, pc[z]);
+            for (int z = 0; z < 10; ++z) atomicAdd(prof + z, pc[z]);
         }
     }
     __syncwarp();
