@@ -640,9 +640,9 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         const double st = pr[0] ? (double)pr[0] : 1.0;
         std::fprintf(stderr,
                      "[plse-prof ref] steps %llu | cyc/step: masks %.0f walk %.0f apply %.0f | draws/step %.2f | "
-                     "mean f %.1f | fast path: masks %.0f scans %.0f stream %.0f owner %.0f\n",
+                     "mean f %.1f | fast path (|V0| > 32): masks %.0f scans %.0f stream %.0f owner %.0f | early draws/step %.2f\n",
                      pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st,
-                     pr[8] / st, pr[9] / st);
+                     pr[8] / st, pr[9] / st, pr[10] / st);
     } else if (c->d_prof && std::getenv("PLSE_PROFILE") && c->plits) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));

@@ -283,7 +283,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     // steps, mask cycles, walk cycles, apply cycles, draws, sum f | fast path: masks, scans, stream, owner
-    unsigned long long pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long pc[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
     long long tq = 0;
 
@@ -388,6 +388,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 sD -= cD;  // exclusive: index (0-based) of this lane's first level-D candidate
                 const Xoshiro saved = rng;
                 uint32_t bad = 0;  // lane 0: an output below 2^32, a rejection is possible
+                if (prof) pc[10] += (unsigned)E;
                 if (lane == 0) {
 #pragma unroll 4
                     for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
@@ -568,7 +569,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         *slot_clock = base + j + 2 + a.tenure_cap;
         if (prof) {
 #pragma unroll
-            for (int z = 0; z < 10; ++z) atomicAdd(prof + z, pc[z]);
+            for (int z = 0; z < 11; ++z) atomicAdd(prof + z, pc[z]);
         }
     }
     __syncwarp();
