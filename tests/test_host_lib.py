@@ -113,3 +113,40 @@ def test_lsc_instance_matches_reference_builder(plse):
     """config C5's LSC stand-in (builders.hpp:30-58)"""
     assert np.array_equal(plse.lsc_instance(20, 0.4, 7), G["lsc_20_0.4_7"])
     assert np.array_equal(plse.lsc_instance(70, 0.4, 7), G["lsc_70_0.4_7"])
+
+
+def test_raw_abi_rejects_null_and_bad_arguments(plse):
+    """Every context entry point rejects a NULL context with PLSE_ERR_INVALID (no crash, no device
+    work) and leaves a message in plse_last_error(NULL); host helpers reject NULL buffers."""
+    lib = ctypes.CDLL(plse.lib_path())
+    lib.plse_last_error.restype = ctypes.c_char_p
+    INVALID = 1
+    nul = ctypes.c_void_p()
+    buf = (ctypes.c_uint16 * 16)()
+    i32 = ctypes.c_int32()
+    i64 = ctypes.c_int64()
+    calls = {
+        "plse_init_population": (nul,),
+        "plse_full_distances": (nul,),
+        "plse_improve": (nul, ctypes.c_uint64(1), ctypes.byref(i64), ctypes.byref(i32), ctypes.byref(i32)),
+        "plse_distances": (nul,),
+        "plse_update": (nul, ctypes.byref(i32), ctypes.byref(i32), nul),
+        "plse_reset_exclusion": (nul,),
+        "plse_offspring": (nul, ctypes.c_uint64(1)),
+        "plse_export_elites": (nul, ctypes.c_int32(1), nul, nul),
+        "plse_import_migrants": (nul, ctypes.c_int32(1), nul),
+        "plse_get_stats": (nul, ctypes.c_int32(0), nul, nul, nul),
+        "plse_get_counters": (nul, nul),
+        "plse_timer_start": (nul,),
+        "plse_get_colors": (nul, ctypes.c_int32(0), buf),
+        "plse_to_grid": (nul, buf, buf),
+        "plse_solve_exact": (nul, ctypes.c_int64(10), ctypes.byref(i32), ctypes.byref(i32), ctypes.byref(i64), buf),
+        "plse_verify_certificate": (ctypes.c_int32(2), nul, ctypes.c_int32(2), nul, ctypes.byref(i32),
+                                    ctypes.byref(i32), nul, ctypes.c_int64(0), ctypes.byref(i64)),
+        "plse_preprocess": (ctypes.c_int32(2), nul, ctypes.byref(nul)),
+        "plse_solve": (ctypes.c_int32(2), nul, nul, nul, nul, nul, nul),
+    }
+    for name, args in calls.items():
+        rc = getattr(lib, name)(*args)
+        assert rc == INVALID, (name, rc)
+        assert lib.plse_last_error(None), name
