@@ -481,6 +481,23 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
         }
     }
     if (best_ind == 0) throw Unsupported("instance too large for the shared-memory resident search");
+    // a population that fits one warp per block everywhere runs one individual per block: the block
+    // scheduler then spreads the individuals evenly over the SMs (a latency-bound small population
+    // otherwise lands on whichever warps win the work counter)
+    if (!force_wpc && !c->half_warp && c->wpc != 1) {
+        const size_t smem1 = graph_bytes + warp_bytes;
+        if (smem1 <= (size_t)max_optin) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+            int bps1 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps1, kern, 32, smem1));
+            if (bps1 > 0 && c->prm.p <= bps1 * c->nsm) {
+                best_ind = bps1;
+                c->wpc = 1;
+                c->smem = smem1;
+                c->grid = bps1 * c->nsm;
+            }
+        }
+    }
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     CK(cudaFuncSetAttribute(kern_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     c->threads = 32 * c->wpc;
@@ -588,16 +605,19 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     }
     CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
     CK(cudaEventRecord(c->ev0, c->st));
+    // one individual per block when the blocks are single warps (see create): the first blocks, spread
+    // round-robin over the SMs by the block scheduler, take the individuals
+    const int grid = c->wpc == 1 ? std::max(1, std::min(c->grid, p_eff - first)) : c->grid;
     if (c->plits && c->ref_ties)
-        c->launched(launch_plits_ref(a, c->W, c->grid, c->threads, c->smem, c->st));
+        c->launched(launch_plits_ref(a, c->W, grid, c->threads, c->smem, c->st));
     else if (c->plits)
-        c->launched(launch_plits(a, c->W, c->grid, c->threads, c->smem, c->st));
+        c->launched(launch_plits(a, c->W, grid, c->threads, c->smem, c->st));
     else if (c->ref_ties)
-        c->launched(launch_improve_ref(a, c->W, c->grid, c->threads, c->smem, c->st));
+        c->launched(launch_improve_ref(a, c->W, grid, c->threads, c->smem, c->st));
     else if (c->half_warp)
-        c->launched(launch_improve_hw(a, c->W, c->grid, c->threads, c->smem, c->st));
+        c->launched(launch_improve_hw(a, c->W, grid, c->threads, c->smem, c->st));
     else
-        c->launched(launch_improve(a, c->W, c->grid, c->threads, c->smem, c->st));
+        c->launched(launch_improve(a, c->W, grid, c->threads, c->smem, c->st));
     CK(cudaEventRecord(c->ev1, c->st));
 }
 
