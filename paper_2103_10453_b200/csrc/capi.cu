@@ -670,9 +670,9 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         std::fprintf(stderr,
                      "[plse-prof plits] indiv %llu steps %llu | cyc/step: list %.0f level %.0f select %.0f move %.0f "
                      "total %.0f | extra level passes %.3f/step | mean active %.1f | move: select->membership %.0f "
-                     "membership %.0f tail %.0f\n",
+                     "membership %.0f tail %.0f | level: minimum %.0f admissible %.0f extra passes %.0f\n",
                      pr[8], pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st,
-                     pr[9] / st, pr[10] / st, pr[11] / st);
+                     pr[9] / st, pr[10] / st, pr[11] / st, pr[12] / st, pr[13] / st, pr[14] / st);
     } else if (c->d_prof && std::getenv("PLSE_PROFILE")) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));

@@ -155,11 +155,13 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int lane, int
 }
 
 // the admissible moves of one vertex at delta level dl (plits.hpp:146-147): adm = colours k != 0,
-// adm0 = the move to 0.  Only colours in the possibly-tabu mask Tv read until[][] (independent batches
-// of four); expired ones leave the mask.
+// adm0 = the move to 0.  Only colours in the possibly-tabu mask (tv, loaded by the caller ahead of the
+// move classes so the load overlaps them) read until[][] (independent batches of four); expired ones
+// leave the mask Tv.
 template <int W>
 __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
-                                         uint64_t* Tv, uint32_t t, uint64_t (&adm)[W], bool& adm0) {
+                                         uint64_t* Tv, const uint64_t (&tv)[W], uint32_t t, uint64_t (&adm)[W],
+                                         bool& adm0) {
     constexpr int NB = PlitsK<W>::NB;
     const int qv = dl - m.dbase;
 #pragma unroll
@@ -172,9 +174,6 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
     }
     adm0 = m.cur && m.d0 == dl;
     if (!asp_all && (adm0 || popc_w<W>(adm))) {
-        uint64_t tv[W];
-#pragma unroll
-        for (int q = 0; q < W; ++q) tv[q] = Tv[q];
 #pragma unroll
         for (int q = 0; q < W; ++q) {
             uint64_t x = adm[q] & tv[q];
@@ -221,7 +220,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     // steps, list, level, select, move, step, level iters, sum na | move: plane, membership, tail
-    unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long pc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tp0 = 0, tp1 = 0;
 
     // ---- tabu clock of this warp slot (two phases, each followed by a skip of tenure_cap + 2)
@@ -345,6 +344,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                     }
                 }
                 dl = __reduce_min_sync(kFull, lmin);
+                long long tl0 = prof ? clock64() : 0;
+                if (prof) pc[has_prev ? 13 : 11] += (unsigned long long)(tl0 - tp1);
                 if (dl == INT_MAX) break;  // every candidate tabu
                 asp_all = dl < thr;
                 lc = 0;
@@ -353,11 +354,15 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                     {
                         const int v = s.list[idx];
                         if (!has_prev && s.vmin[v] > dl) continue;
+                        uint64_t tv[W];
+#pragma unroll
+                        for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)v * W + q];
                         VertexMoves<W> m;
                         vertex_moves<W>(g, s, v, wf, wc, m);
                         uint64_t adm[W];
                         bool adm0;
-                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, s.T + (size_t)v * W, t, adm, adm0);
+                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, s.T + (size_t)v * W,
+                                                     tv, t, adm, adm0);
                         if (cnt && c_v < 0) {
                             c_v = v;
                             c_adm0 = adm0;
@@ -371,6 +376,11 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                     }
                 }
                 N = (int)__reduce_add_sync(kFull, (unsigned)lc);
+                if (prof) {
+                    const long long x = clock64();
+                    pc[has_prev ? 13 : 12] += (unsigned long long)(x - tl0);
+                    tp1 = x;
+                }
                 if (N > 0) break;
                 has_prev = true;
                 prev = dl;
@@ -426,7 +436,10 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 } else {
                     VertexMoves<W> m;
                     vertex_moves<W>(g, s, sv, wf, wc, m);
-                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, s.T + (size_t)sv * W, t, adm, adm0);
+                    uint64_t tv[W];
+#pragma unroll
+                    for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)sv * W + q];
+                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, s.T + (size_t)sv * W, tv, t, adm, adm0);
                     d0 = m.d0;
                     dbase = m.dbase;
                 }
@@ -573,7 +586,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 #pragma unroll
             for (int z = 0; z < 8; ++z) atomicAdd(prof + z, pc[z]);
             atomicAdd(prof + 8, 1ULL);
-            for (int z = 8; z < 11; ++z) atomicAdd(prof + z + 1, pc[z]);
+            for (int z = 8; z < 14; ++z) atomicAdd(prof + z + 1, pc[z]);
         }
     }
     __syncwarp();
