@@ -285,23 +285,24 @@ __device__ __forceinline__ int view_early(const LaneView<W>& x, int rin, int D, 
 #pragma unroll
         for (int q = 0; q < W; ++q) G[q] &= ~hi[q];
     }
-    if (!popc_w<W>(G)) return early;
-    uint64_t sel[W];
+    // the levels present, lowest first (each one's count only depends on the candidates below it)
+    uint64_t lower[W];
 #pragma unroll
-    for (int q = 0; q < W; ++q) sel[q] = G[q];
-    const int gmin = sliced_min<W, NB>(x.m.S, sel);
-    for (int gl = gr; gl >= gmin; --gl) {
-        const int L = x.m.dbase + wc * gl;
-        if (L <= D) break;
-        uint64_t eqg[W], lo[W];
+    for (int q = 0; q < W; ++q) lower[q] = 0;
+    while (popc_w<W>(G)) {
+        uint64_t sel[W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) eqg[q] = lo[q] = G[q];
-        sliced_eq<W, NB>(x.m.S, gl, eqg);
-        sliced_ge<W, NB>(x.m.S, gl, lo);  // lo = G minus the candidates below gl
+        for (int q = 0; q < W; ++q) sel[q] = G[q];
+        const int L = x.m.dbase + wc * sliced_min<W, NB>(x.m.S, sel);  // sel: the candidates at L
+        if (L > D) {
+            const int cnt = popc_below_w<W>(sel, first_bit_w<W>(lower));
+            early += (L == r) ? cnt : max(cnt - 1, 0);
+        }
 #pragma unroll
-        for (int q = 0; q < W; ++q) lo[q] = G[q] & ~lo[q];
-        const int cnt = popc_below_w<W>(eqg, first_bit_w<W>(lo));
-        early += (L == r) ? cnt : max(cnt - 1, 0);
+        for (int q = 0; q < W; ++q) {
+            lower[q] |= sel[q];
+            G[q] &= ~sel[q];
+        }
     }
     return early;
 }
