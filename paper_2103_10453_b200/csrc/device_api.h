@@ -223,8 +223,7 @@ __host__ __device__ inline PlitsRefSmemLayout plits_ref_smem_layout(int n, int n
     w += ids;
     L.w_cf_pos = w;
     w += ids;
-    L.w_T = w;
-    w += (size_t)nv * W * 8;
+    L.w_T = 0;  // the possibly-tabu mask lives in global memory (plits_ref.cu)
     L.w_stage = w;
     w += (size_t)32 * (5 + W + 2) * W * 8;
     L.w_stage_i = w;

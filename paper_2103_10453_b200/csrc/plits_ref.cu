@@ -28,7 +28,7 @@ struct PlitsRefWarp {
     uint64_t* rp;
     uint64_t* cp;
     uint16_t *un_el, *un_pos, *cf_el, *cf_pos;  // IndexSets (plits.hpp:74-75)
-    uint64_t* T;                                // [nv][W] colours possibly tabu
+    uint64_t* T;                                // [nv][W] colours possibly tabu (GLOBAL, per warp slot)
     uint64_t* stage;                            // 32 staged vertices: S planes and candidate mask
     int32_t* stage_i;                           // 32 staged vertices: v, cur, dbase, d0
     uint16_t* evl;                              // neighbours whose membership is re-decided, CSR order
@@ -218,15 +218,18 @@ __device__ __forceinline__ void view_admissible(const Graph<W>& g, const PlitsRe
     constexpr int NB = PlitsK<W>::NB;
     const bool conflicting = p >= nu;
     x.v = conflicting ? s.cf_el[p - nu] : s.un_el[p];
+    uint64_t* Tv = s.T + (size_t)x.v * W;
+    uint64_t tv[W];  // global: issued ahead of the move classes so the load overlaps them
+#pragma unroll
+    for (int q = 0; q < W; ++q) tv[q] = Tv[q];
     vertex_moves<W>(g, s, x.v, wf, wc, x.m);
     uint64_t live[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) live[q] = 0;
-    uint64_t* Tv = s.T + (size_t)x.v * W;
     const uint32_t* urow = until + (size_t)x.v * w1;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-        uint64_t y = Tv[q] & (x.m.M[q] | ((q == 0 && conflicting) ? 1ULL : 0ULL));
+        uint64_t y = tv[q] & (x.m.M[q] | ((q == 0 && conflicting) ? 1ULL : 0ULL));
         uint64_t expired = 0;
         while (y) {
             const int b = __ffsll((long long)y) - 1;
@@ -236,7 +239,7 @@ __device__ __forceinline__ void view_admissible(const Graph<W>& g, const PlitsRe
             else
                 expired |= 1ULL << b;
         }
-        if (expired) Tv[q] &= ~expired;  // the mask stays a superset of the live entries
+        if (expired) Tv[q] = tv[q] & ~expired;  // the mask stays a superset of the live entries
     }
     x.a0 = conflicting && (!(live[0] & 1ULL) || x.m.d0 < asp);
     live[0] &= ~1ULL;
@@ -856,13 +859,16 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits_ref(const Improve
     s.un_pos = reinterpret_cast<uint16_t*>(wbase + L.w_un_pos);
     s.cf_el = reinterpret_cast<uint16_t*>(wbase + L.w_cf_el);
     s.cf_pos = reinterpret_cast<uint16_t*>(wbase + L.w_cf_pos);
-    s.T = reinterpret_cast<uint64_t*>(wbase + L.w_T);
     s.stage = reinterpret_cast<uint64_t*>(wbase + L.w_stage);
     s.stage_i = reinterpret_cast<int32_t*>(wbase + L.w_stage_i);
     s.evl = reinterpret_cast<uint16_t*>(wbase + L.w_evl);
 
     const int slot = blockIdx.x * nwarps + warp;
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
+    // the possibly-tabu mask lives in the slot's tabu-record area in global memory (nv * 16 >= nv * 8 W
+    // bytes): shared memory stays for the colouring, the count planes and the IndexSets, which doubles
+    // the resident warps
+    s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(a.work_counter, 1);
