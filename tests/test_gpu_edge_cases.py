@@ -78,3 +78,31 @@ def test_iteration_limit_and_spacing_params(plse, orc):
 def test_lsc_instance_run(plse, orc):
     grid = orc.lsc_instance(20, 0.4, 7)
     _same_run(plse, orc, grid, p=16, master_seed=8, generation_limit=2, phase1_iters=5000)
+
+
+@pytest.mark.parametrize("variant,tie", [("partial", 0), ("partial", 1), ("mpma", 0), ("mpma", 1)])
+def test_results_do_not_depend_on_launch_geometry(plse, orc, monkeypatch, variant, tie):
+    """Warp slots keep tabu state across individuals (monotone clocks, possibly-tabu masks) and the
+    block shape follows the population size: the same population improved under different block
+    shapes (and so different individual -> slot assignments, each slot reused several times) must
+    give identical colourings and iteration counts."""
+    grid = orc.generate_instance(20, 0.5, 9)
+    g = plse.preprocess(grid)
+    outs = []
+    for wpc in ("1", "8", "0"):
+        monkeypatch.setenv("PLSE_IMPROVE_WPC", wpc)
+        dp = plse.DevicePopulation(g, plse.SolverConfig(
+            p=600, master_seed=4, phase1_iters=3000, tie_mode=tie,
+            variant=plse.MPMA if variant == "mpma" else plse.PARTIAL))
+        dp.initialize_population()
+        dp.offspring = dp.members
+        res = []
+        for gen in (1, 2, 3):  # slots are reused across launches too
+            dp.improve(gen)
+            f, c, it = dp.stats(plse.IMPROVED)
+            res.append((dp.improved.copy(), f.copy(), it.copy()))
+        outs.append(res)
+        dp.close()
+    for other in outs[1:]:
+        for (a_col, a_f, a_it), (b_col, b_f, b_it) in zip(outs[0], other):
+            assert np.array_equal(a_col, b_col) and np.array_equal(a_f, b_f) and np.array_equal(a_it, b_it)
