@@ -325,8 +325,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint32_t rnk = __umulhi(g1, (uint32_t)N);
             const int excl = incl - cnt;
             const int wl = __ffs(__ballot_sync(kFull, (uint32_t)excl <= rnk && rnk < (uint32_t)incl)) - 1;
-            const int kmine = nth_bit_w<W>(m, min(max((int)rnk - excl, 0), max(cnt - 1, 0)));
-            const int ks = __shfl_sync(kFull, kmine, wl);
+            const int ks = warp_nth_bit<W>(m, (int)rnk - __shfl_sync(kFull, excl, wl), wl, lane);
             const uint32_t vcs = __shfl_sync(kFull, svc, wl);
             const int vs = (int)(vcs & 0xFFFFu), rs_ = (vcs >> 16) & 0xFF, cs_ = vcs >> 24;
             const int lvl = lc - 1;
@@ -348,35 +347,39 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint32_t tenure = __umulhi(g2, 10u) + (uint32_t)(alpha * (double)f_new);
             const uint32_t ut = ts + 1 + tenure;
             const bool improved = f_new < bestf;
-            const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
-            TabuRec nr{0, 0, 0, 0};
-            if (my_u >= 0) nr = rec[my_u];  // issued early, consumed after the updates
-            __syncwarp();
-            // ---- predicated five-lane update:
+            // ---- predicated five-lane update, straight-line (no reconvergence blocks):
             //   lanes 0-2: colour byte (row- and column-major) and U bit of v*, ur, uc
-            //   lanes 1/2 also clear k* from the evictee's other line
+            //   lane 1: C[col ur] loses k*; lane 2: R[row uc] loses k*
             //   lane 3: R[row v*] gains k* unless ur held it; lane 4: C[col v*] likewise unless uc did
+            const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
+            const int u = lane == 0 ? vs : my_u;
+            const bool act = u >= 0;  // lanes 0-2 with a vertex
+            const int uu = act ? u : 0;
+            TabuRec nr = rec[uu];  // issued early, consumed after the updates (lanes 1/2 only)
+            const uint16_t cu = g.cell[uu];
+            const int cpos = g.colpos[uu];
+            const uint32_t dg = g.deg[uu];
+            __syncwarp();
             {
-                const int u = lane == 0 ? vs : my_u;
-                if (lane < 3 && u >= 0) {
-                    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
-                    col[u] = nc;
-                    colT[g.colpos[u]] = nc;
-                    atomicXor(&s.U[u >> 5], 1u << (u & 31));
-                    const uint16_t cu = g.cell[u];
-                    uint64_t* line = lane == 1 ? &s.C[(cu & 0xFF) * W + kw] : &s.R[(cu >> 8) * W + kw];
-                    if (lane > 0) *line ^= bitk;
-                    acc += lane == 0 ? 2ULL * (unsigned)w1 * (unsigned)fb + 4ULL * g.deg[u] + 2ULL +
-                                           (improved ? 2ULL * (unsigned)nv : 0ULL)
-                                     : 4ULL * g.deg[u] + 2ULL;
+                const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+                if (act) {
+                    col[uu] = nc;
+                    colT[cpos] = nc;
+                    atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
                 }
-                if (lane == 3 && !inR) s.R[rs_ * W + kw] ^= bitk;
-                if (lane == 4 && !inC) s.C[cs_ * W + kw] ^= bitk;
+                const bool on_c = lane == 1 || lane == 4;
+                const int line_no = lane == 1 ? (cu & 0xFF) : lane == 2 ? (cu >> 8) : lane == 3 ? rs_ : cs_;
+                const bool lx = (lane == 1 || lane == 2) ? act : lane == 3 ? !inR : lane == 4 && !inC;
+                uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
+                if (lx) *line ^= bitk;
+                const uint32_t add = (act ? 4u * dg + 2u : 0u) +
+                                     (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)fb + (improved ? 2u * (uint32_t)nv : 0u) : 0u);
+                acc += add;
             }
-            if (my_u >= 0) {
-                until[(size_t)my_u * w1 + ks] = ut;
-                cache_forbid(nr, ks, ut, ts);
-                rec[my_u] = nr;
+            if (act && lane > 0) {
+                until[(size_t)uu * w1 + ks] = ut;
+                cache_forbid_nb(nr, ks, ut, ts);
+                rec[uu] = nr;
             }
             f = f_new;
             if (improved) {

@@ -114,6 +114,40 @@ __device__ __forceinline__ void cache_forbid(TabuRec& r, int k, uint32_t ut, uin
     r.kk = (uint32_t)n1 | ((uint32_t)n2 << 8) | ovf;
 }
 
+// cache_forbid as straight-line selects (the sparse loop's evictee lanes run it every step)
+__device__ __forceinline__ void cache_forbid_nb(TabuRec& r, int k, uint32_t ut, uint32_t t) {
+    const int k1 = r.kk & 0xFF, k2 = (r.kk >> 8) & 0xFF;
+    const bool A = k1 == k && r.u1 != 0;  // k already cached in pair 1
+    const bool B = k2 == k && r.u2 != 0;  // ... in pair 2
+    const bool l1 = r.u1 > t, l2 = r.u2 > t;
+    const bool ov = !A && !B && l1 && l2;  // both pairs live: the dense table becomes authoritative
+    const bool s1 = A || (!B && (!l1 || (l2 && r.u1 <= r.u2)));
+    const uint32_t n1 = s1 ? (uint32_t)k : (uint32_t)k1, n2 = s1 ? (uint32_t)k2 : (uint32_t)k;
+    r.u1 = s1 ? ut : r.u1;
+    r.u2 = s1 ? r.u2 : ut;
+    r.kk = n1 | (n2 << 8) | (ov ? (1u << 16) : (r.kk & 0xFF0000u));
+}
+
+// rr-th set bit (0-based) of lane src's W-word mask, found by the whole warp: lane src's words are
+// broadcast and lane l tests bit l of the word holding the answer (warp-uniform result)
+template <int W>
+__device__ __forceinline__ int warp_nth_bit(const uint64_t (&m)[W], int rr, int src, int lane) {
+    uint32_t word = 0;
+    int wbase = 0, r2 = 0;
+#pragma unroll
+    for (int z = 0; z < 2 * W; ++z) {
+        const uint32_t x = __shfl_sync(kFull, (uint32_t)(m[z >> 1] >> (32 * (z & 1))), src);
+        const int pc = __popc(x);
+        const bool here = rr >= 0 && rr < pc;
+        word = here ? x : word;
+        wbase = here ? 32 * z : wbase;
+        r2 = here ? rr : r2;
+        rr -= pc;
+    }
+    const bool hit = ((word >> lane) & 1u) && __popc(word & ((1u << lane) - 1u)) == r2;
+    return wbase + __ffs(__ballot_sync(kFull, hit)) - 1;
+}
+
 // admissible candidate masks of an uncoloured vertex at the three delta levels
 template <int W>
 __device__ __forceinline__ void level_masks(const WarpSmem& s, int r, int c, const uint64_t (&dom)[W],
