@@ -200,32 +200,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(alpha * (double)f_new);
             const uint32_t ut = t + 1 + tenure;
             const bool improved = f_new < bestf;
-            __syncwarp();
-            if (lane < 3) {
-                const int u = lane == 0 ? vs : lane == 1 ? ur : uc;
-                if (u >= 0) {
-                    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
-                    col[u] = nc;
-                    colT[g.colpos[u]] = nc;
-                    atomicXor(&s.U[u >> 5], 1u << (u & 31));
-                    acc += lane == 0 ? 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
-                                           (improved ? 2ULL * (unsigned)nv : 0ULL)
-                                     : 4ULL * g.deg[u] + 2ULL;
-                    if (lane > 0) {
-                        until[(size_t)u * w1 + ks] = ut;
-                        TabuRec nr = rec[u];
-                        cache_forbid(nr, ks, ut, t);
-                        rec[u] = nr;
-                        if (lane == 1)
-                            s.C[(g.cell[u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
-                        else
-                            s.R[(g.cell[u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
-                    } else {
-                        s.R[rs_ * W + kw] |= bitk;
-                        s.C[cs_ * W + kw] |= bitk;
-                    }
-                }
-            }
+            apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, f_before, improved, ut, t, lane,
+                                acc);
             f = f_new;
             if (improved) {
                 bestf = f;
@@ -347,40 +323,9 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint32_t tenure = __umulhi(g2, 10u) + (uint32_t)(alpha * (double)f_new);
             const uint32_t ut = ts + 1 + tenure;
             const bool improved = f_new < bestf;
-            // ---- predicated five-lane update, straight-line (no reconvergence blocks):
-            //   lanes 0-2: colour byte (row- and column-major) and U bit of v*, ur, uc
-            //   lane 1: C[col ur] loses k*; lane 2: R[row uc] loses k*
-            //   lane 3: R[row v*] gains k* unless ur held it; lane 4: C[col v*] likewise unless uc did
-            const int my_u = lane == 1 ? ur : lane == 2 ? uc : -1;
-            const int u = lane == 0 ? vs : my_u;
-            const bool act = u >= 0;  // lanes 0-2 with a vertex
-            const int uu = act ? u : 0;
-            TabuRec nr = rec[uu];  // issued early, consumed after the updates (lanes 1/2 only)
-            const uint16_t cu = g.cell[uu];
-            const int cpos = g.colpos[uu];
-            const uint32_t dg = g.deg[uu];
-            __syncwarp();
-            {
-                const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
-                if (act) {
-                    col[uu] = nc;
-                    colT[cpos] = nc;
-                    atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
-                }
-                const bool on_c = lane == 1 || lane == 4;
-                const int line_no = lane == 1 ? (cu & 0xFF) : lane == 2 ? (cu >> 8) : lane == 3 ? rs_ : cs_;
-                const bool lx = (lane == 1 || lane == 2) ? act : lane == 3 ? !inR : lane == 4 && !inC;
-                uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
-                if (lx) *line ^= bitk;
-                const uint32_t add = (act ? 4u * dg + 2u : 0u) +
-                                     (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)fb + (improved ? 2u * (uint32_t)nv : 0u) : 0u);
-                acc += add;
-            }
-            if (act && lane > 0) {
-                until[(size_t)uu * w1 + ks] = ut;
-                cache_forbid_nb(nr, ks, ut, ts);
-                rec[uu] = nr;
-            }
+            // ---- the move: predicated five-lane update (improve_common.cuh apply_move_lanes)
+            const TabuRec nr = apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, fb, improved,
+                                                   ut, ts, lane, acc);
             f = f_new;
             if (improved) {
                 bestf = f;

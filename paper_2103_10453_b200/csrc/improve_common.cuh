@@ -128,6 +128,47 @@ __device__ __forceinline__ void cache_forbid_nb(TabuRec& r, int k, uint32_t ut, 
     r.kk = n1 | (n2 << 8) | (ov ? (1u << 16) : (r.kk & 0xFF0000u));
 }
 
+// The move of partial.hpp:124-141 on the occupancy state, as one straight-line predicated pass (no
+// reconvergence blocks): lanes 0-2 write the colour byte (row- and column-major) and the U bit of v*, ur,
+// uc; lane 1 clears k* from C[col ur], lane 2 from R[row uc]; lane 3 sets it in R[row v*] unless ur held
+// it, lane 4 in C[col v*] unless uc did; lanes 1/2 forbid (evictee, k*) until ut (search_util.hpp:73-75)
+// and return the evictee's updated tabu cache.  Adds the SURVEY 8(d) bytes of the step to acc (lanes 0-2).
+template <int W>
+__device__ __forceinline__ TabuRec apply_move_lanes(const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
+                                                    uint32_t* until, int vs, int ur, int uc, int ks, int rs_,
+                                                    int cs_, bool inR, bool inC, int f_before, bool improved,
+                                                    uint32_t ut, uint32_t t, int lane, unsigned long long& acc) {
+    const int w1 = g.n + 1, kw = ks >> 6;
+    const uint64_t bitk = 1ULL << (ks & 63);
+    const int u = lane == 0 ? vs : lane == 1 ? ur : lane == 2 ? uc : -1;
+    const bool act = u >= 0;
+    const int uu = act ? u : 0;
+    TabuRec nr = rec[uu];  // issued early, consumed after the updates (lanes 1/2 only)
+    const uint16_t cu = g.cell[uu];
+    const int cpos = g.colpos[uu];
+    const uint32_t dg = g.deg[uu];
+    __syncwarp();
+    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+    if (act) {
+        s.col[uu] = nc;
+        s.colT[cpos] = nc;
+        atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
+    }
+    const bool on_c = lane == 1 || lane == 4;
+    const int line_no = lane == 1 ? (cu & 0xFF) : lane == 2 ? (cu >> 8) : lane == 3 ? rs_ : cs_;
+    const bool lx = (lane == 1 || lane == 2) ? act : lane == 3 ? !inR : lane == 4 && !inC;
+    uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
+    if (lx) *line ^= bitk;
+    acc += (act ? 4u * dg + 2u : 0u) +
+           (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)f_before + (improved ? 2u * (uint32_t)g.nv : 0u) : 0u);
+    if (act && lane > 0) {
+        until[(size_t)uu * w1 + ks] = ut;
+        cache_forbid_nb(nr, ks, ut, t);
+        rec[uu] = nr;
+    }
+    return nr;
+}
+
 // rr-th set bit (0-based) of lane src's W-word mask, found by the whole warp: lane src's words are
 // broadcast and lane l tests bit l of the word holding the answer (warp-uniform result)
 template <int W>

@@ -518,31 +518,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         const uint32_t ut = t + 1 + tenure;
         const bool improved = f_new < bestf;
         __syncwarp();
-        if (lane < 3) {
-            const int u = lane == 0 ? vs : lane == 1 ? ur : uc;
-            if (u >= 0) {
-                const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
-                col[u] = nc;
-                colT[g.colpos[u]] = nc;
-                atomicXor(&s.U[u >> 5], 1u << (u & 31));
-                acc += lane == 0 ? 2ULL * (unsigned)w1 * (unsigned)f_before + 4ULL * g.deg[vs] + 2ULL +
-                                       (improved ? 2ULL * (unsigned)nv : 0ULL)
-                                 : 4ULL * g.deg[u] + 2ULL;
-                if (lane > 0) {
-                    until[(size_t)u * w1 + ks] = ut;
-                    TabuRec nr = rec[u];
-                    cache_forbid(nr, ks, ut, t);
-                    rec[u] = nr;
-                    if (lane == 1)
-                        s.C[(g.cell[u] & 0xFF) * W + kw] &= ~bitk;  // row holder leaves its column
-                    else
-                        s.R[(g.cell[u] >> 8) * W + kw] &= ~bitk;    // column holder leaves its row
-                } else {
-                    s.R[rs_ * W + kw] |= bitk;
-                    s.C[cs_ * W + kw] |= bitk;
-                }
-            }
-        }
+        apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, f_before, improved, ut, t, lane, acc);
         f = f_new;
         if (improved) {
             bestf = f;
