@@ -11,10 +11,6 @@ import subprocess
 import sys
 
 KERNEL = "_ZN8plse_dev9k_improveILi1ELb0EEEvNS_11ImproveArgsE"
-IMPROVE_BLOCKS = [(0, 245, "dense step / prologue"), (246, 279, "sparse entry"), (280, 306, "score"),
-                  (307, 313, "scan"), (314, 324, "all-tabu step"), (325, 335, "select"),
-                  (336, 345, "holder search setup"), (346, 350, "tenure"), (351, 389, "update"),
-                  (390, 427, "slot re-sort"), (428, 440, "loop control")]
 CSRC = __import__("os").environ.get("CSRC_DIR") or __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)),
                                   "..", "..", "paper_2103_10453_b200", "csrc")
 _FUNCS = {}
@@ -57,12 +53,28 @@ def line_map(cubin):
     return out
 
 
+_SECTIONS = {}
+
+
+def section(f, l):
+    """the last `// ----` / `// ====` section comment of csrc/<f> at or before line l"""
+    if f not in _SECTIONS:
+        marks = []
+        for i, t in enumerate(open(__import__("os").path.join(CSRC, f)), 1):
+            m = re.match(r"\s*// [-=]{4,}\s*(.*)", t)
+            if m:
+                marks.append((i, m.group(1).strip()[:60]))
+        _SECTIONS[f] = marks
+    name = None
+    for i, n in _SECTIONS[f]:
+        if i <= l:
+            name = n
+    return name
+
+
 def block(f, l):
     if f == "improve.cu":
-        for lo, hi, name in IMPROVE_BLOCKS:
-            if lo <= l <= hi:
-                return name
-        return "other (improve.cu)"
+        return "improve.cu: " + (section(f, l) or "other")
     fn = enclosing_function(f, l) if f.endswith((".cuh", ".h")) else None
     return f + ":" + fn if fn else "other (" + f + ")"
 
