@@ -262,11 +262,13 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const uint32_t g2 = fmix32(g1 + 0x632BE5ABu);
             // ---- score this lane's slot
             const int r = (svc >> 16) & 0xFF, c = svc >> 24;
+            const bool mine = lane < f;
             uint64_t dom[W], T[W], m0[W], m1[W], m2[W];
             dom_mask<W>(g, r, c, dom);
+#pragma unroll
+            for (int z = 0; z < W; ++z) dom[z] = mine ? dom[z] : 0ULL;  // an empty slot has no candidates
             tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
             level_masks<W>(s, r, c, dom, T, asp_s, m0, m1, m2);
-            const bool mine = lane < f;
             uint64_t o0 = 0, o1 = 0, o2 = 0;
 #pragma unroll
             for (int z = 0; z < W; ++z) {
@@ -274,11 +276,11 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 o1 |= m1[z];
                 o2 |= m2[z];
             }
-            const unsigned lv = !mine ? 3u : o0 ? 0u : o1 ? 1u : o2 ? 2u : 3u;
+            const unsigned lv = o0 ? 0u : o1 ? 1u : o2 ? 2u : 3u;
             const int lc = (int)__reduce_min_sync(kFull, lv);
             uint64_t m[W];
 #pragma unroll
-            for (int z = 0; z < W; ++z) m[z] = !mine ? 0ULL : lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z];
+            for (int z = 0; z < W; ++z) m[z] = lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z];
             const int cnt = popc_w<W>(m);
             int incl = cnt;
 #pragma unroll
@@ -349,9 +351,10 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 const bool old_ok = mine && lane != wl;
                 const unsigned br = __ballot_sync(kFull, old_ok && vl < ur);
                 const unsigned bc = __ballot_sync(kFull, old_ok && vl < uc);
-                const int pr_ = ur >= 0 ? __popc(br) + (uc >= 0 && uc < ur) : -1;
-                const int pc_ = uc >= 0 ? __popc(bc) + (ur >= 0 && ur < uc) : -1;
-                const int y = lane - (pr_ >= 0 && pr_ < lane) - (pc_ >= 0 && pc_ < lane);
+                // new lanes of ur / uc (64 = absent; -1 compares as the largest unsigned id)
+                const int pr_ = ur >= 0 ? __popc(br) + ((unsigned)uc < (unsigned)ur) : 64;
+                const int pc_ = uc >= 0 ? __popc(bc) + ((unsigned)ur < (unsigned)uc) : 64;
+                const int y = lane - (pr_ < lane) - (pc_ < lane);
                 const int src = (y >= wl ? y + 1 : y) & 31;
                 const uint32_t mvc = __shfl_sync(kFull, svc, src);
                 const uint32_t mu1 = __shfl_sync(kFull, su1, src);

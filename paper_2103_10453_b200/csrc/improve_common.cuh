@@ -140,9 +140,13 @@ __device__ __forceinline__ TabuRec apply_move_lanes(const Graph<W>& g, const War
                                                     uint32_t ut, uint32_t t, int lane, unsigned long long& acc) {
     const int w1 = g.n + 1, kw = ks >> 6;
     const uint64_t bitk = 1ULL << (ks & 63);
-    const int u = lane == 0 ? vs : lane == 1 ? ur : lane == 2 ? uc : -1;
-    const bool act = u >= 0;
-    const int uu = act ? u : 0;
+    (void)rs_;
+    (void)cs_;
+    // lane 1 addresses ur, lane 2 uc, every other lane v* (lanes 3/4 take v*'s row / column from its cell)
+    const bool l1 = lane == 1, l2 = lane == 2;
+    const int u = l1 ? ur : l2 ? uc : vs;
+    const bool act = lane < 3 && u >= 0;
+    const int uu = max(u, 0);
     TabuRec nr = rec[uu];  // issued early, consumed after the updates (lanes 1/2 only)
     const uint16_t cu = g.cell[uu];
     const int cpos = g.colpos[uu];
@@ -154,9 +158,9 @@ __device__ __forceinline__ TabuRec apply_move_lanes(const Graph<W>& g, const War
         s.colT[cpos] = nc;
         atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
     }
-    const bool on_c = lane == 1 || lane == 4;
-    const int line_no = lane == 1 ? (cu & 0xFF) : lane == 2 ? (cu >> 8) : lane == 3 ? rs_ : cs_;
-    const bool lx = (lane == 1 || lane == 2) ? act : lane == 3 ? !inR : lane == 4 && !inC;
+    const bool on_c = l1 || lane == 4;
+    const int line_no = on_c ? (cu & 0xFF) : (cu >> 8);
+    const bool lx = lane == 3 ? !inR : lane == 4 ? !inC : (l1 || l2) && act;
     uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
     if (lx) *line ^= bitk;
     acc += (act ? 4u * dg + 2u : 0u) +
