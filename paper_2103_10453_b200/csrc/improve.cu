@@ -141,12 +141,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const unsigned b2 = __ballot_sync(kFull, c2 > 0);
             const int lvl = b0 ? -1 : b1 ? 0 : b2 ? 1 : 2;
             const int cnt = lvl == -1 ? c0 : lvl == 0 ? c1 : lvl == 1 ? c2 : 0;
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += x;
-            }
+            int incl = warp_incl_sum(cnt);
             const int N = __shfl_sync(kFull, incl, 31);
             if (N == 0) {
                 if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
@@ -227,12 +222,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         {
             int cnt = 0;
             for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += x;
-            }
+            int incl = warp_incl_sum(cnt);
             int at = incl - cnt;
             for (int q = 0; q < g.lane_words; ++q) {
                 uint32_t bits = s.U[lane * g.lane_words + q];
@@ -282,12 +272,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 #pragma unroll
             for (int z = 0; z < W; ++z) m[z] = lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z];
             const int cnt = popc_w<W>(m);
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                incl += lane >= d ? x : 0;
-            }
+            int incl = warp_incl_sum(cnt);
             const int N = __shfl_sync(kFull, incl, 31);
             if (N == 0) {
                 // every candidate tabu: no move, the clock still advances (partial.hpp:121-122)
