@@ -186,6 +186,18 @@ __device__ __forceinline__ int warp_incl_sum(int x) {
     return x;
 }
 
+// inclusive warp prefix minimum, same scheme
+__device__ __forceinline__ int warp_incl_min(int x) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+        asm("{\n\t.reg .s32 r0;\n\t.reg .pred p;\n\t"
+            "shfl.sync.up.b32 r0|p, %0, %1, 0x0, 0xffffffff;\n\t"
+            "@p min.s32 %0, r0, %0;\n\t}"
+            : "+r"(x)
+            : "r"(d));
+    return x;
+}
+
 // rr-th set bit (0-based) of lane src's W-word mask, found by the whole warp: lane src's words are
 // broadcast and lane l tests bit l of the word holding the answer (warp-uniform result)
 template <int W>

@@ -167,12 +167,7 @@ __device__ __forceinline__ bool partial_ref_fast(const Graph<W>& g, const WarpSm
     for (int c = 0; c < nch; ++c) {
         if (nch > 1) masks_of(c);
         const int m = level_of(c);
-        int pm = m;  // inclusive prefix minimum of the per-vertex minimum level
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int x = __shfl_up_sync(kFull, pm, d);
-            if (lane >= d) pm = min(pm, x);
-        }
+        const int pm = warp_incl_min(m);  // inclusive prefix minimum of the per-vertex minimum level
         if (!seen) {
             int R = __shfl_up_sync(kFull, pm, 1);
             if (lane == 0) R = 3;
@@ -188,12 +183,7 @@ __device__ __forceinline__ bool partial_ref_fast(const Graph<W>& g, const WarpSm
 #pragma unroll
         for (int q = 0; q < W; ++q) aD[q] = D == 0 ? a0[q] : D == 1 ? a1[q] : a2[q];
         cD1 = popc_w<W>(aD);
-        incl1 = cD1;  // inclusive prefix sum of the level-D counts (kept for a one-round set)
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int x = __shfl_up_sync(kFull, incl1, d);
-            if (lane >= d) incl1 += x;
-        }
+        incl1 = warp_incl_sum(cD1);  // inclusive prefix sum of the level-D counts (kept for a one-round set)
         ND += __shfl_sync(kFull, incl1, 31);
         Rc = min(Rc, __shfl_sync(kFull, pm, 31));
     }
@@ -239,12 +229,7 @@ __device__ __forceinline__ bool partial_ref_fast(const Graph<W>& g, const WarpSm
         int cD = cD1, incl = incl1;
         if (nch > 1) {
             cD = popc_w<W>(aD);
-            incl = cD;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += x;
-            }
+            incl = warp_incl_sum(cD);
         }
         const int tot = nch > 1 ? __shfl_sync(kFull, incl, 31) : ND;
         if (J > based + tot) {
