@@ -284,12 +284,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
     {
         int cnt = 0;
         for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
-        int incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int x = __shfl_up_sync(kFull, incl, d);
-            incl += lane >= d ? x : 0;
-        }
+        const int incl = warp_incl_sum(cnt);
         int at = incl - cnt;
         const int v_lo = lane * 32 * g.lane_words;
         for (int q = 0; q < g.lane_words; ++q) {
@@ -347,12 +342,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
             if (D == 3) {
                 fast_done = true;  // no admissible candidate: no draw at all
             } else {
-                int pm = m;  // inclusive prefix minimum of the per-vertex minimum level
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int x = __shfl_up_sync(kFull, pm, d);
-                    if (lane >= d) pm = min(pm, x);
-                }
+                const int pm = warp_incl_min(m);  // inclusive prefix minimum of the per-vertex minimum level
                 int R = __shfl_up_sync(kFull, pm, 1);
                 if (lane == 0) R = 3;
                 const int istar = __ffs(__ballot_sync(kFull, m == D)) - 1;
@@ -363,12 +353,7 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 for (int q = 0; q < W; ++q) aD[q] = D == 0 ? a0[q] : D == 1 ? a1[q] : a2[q];
                 const int cD = popc_w<W>(aD);
                 const int E = (int)__reduce_add_sync(kFull, (unsigned)early);
-                int sD = cD;  // inclusive prefix sum of the level-D counts
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int x = __shfl_up_sync(kFull, sD, d);
-                    if (lane >= d) sD += x;
-                }
+                int sD = warp_incl_sum(cD);  // inclusive prefix sum of the level-D counts
                 const int ND = __shfl_sync(kFull, sD, 31);
                 sD -= cD;  // exclusive: index (0-based) of this lane's first level-D candidate
                 const Xoshiro saved = rng;

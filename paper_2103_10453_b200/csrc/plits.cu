@@ -297,12 +297,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             {
                 int my = 0;
                 for (int q = 0; q < g.lane_words; ++q) my += __popc(s.A[lane * g.lane_words + q]);
-                int incl = my;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int x = __shfl_up_sync(kFull, incl, d);
-                    incl += lane >= d ? x : 0;
-                }
+                const int incl = warp_incl_sum(my);
                 na = __shfl_sync(kFull, incl, 31);
                 int pos = incl - my;
                 for (int q = 0; q < g.lane_words; ++q) {
@@ -402,12 +397,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 
             // ---- the r-th admissible candidate in ascending (v, k)
             const uint32_t rnk = __umulhi(h1, (uint32_t)N);
-            int incl = lc;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int x = __shfl_up_sync(kFull, incl, d);
-                incl += lane >= d ? x : 0;
-            }
+            const int incl = warp_incl_sum(lc);
             const bool owner = (uint32_t)(incl - lc) <= rnk && rnk < (uint32_t)incl;
             int sv = -1, sk = 0, sdc = 0;
             if (owner) {

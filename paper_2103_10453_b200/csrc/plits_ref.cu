@@ -78,15 +78,7 @@ __device__ void plits_ref_build(const Graph<W>& g, const PlitsRefWarp& s, int la
             cc += gv > 0;
         }
     }
-    int iu = cu, ic = cc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int x = __shfl_up_sync(kFull, iu, d), y = __shfl_up_sync(kFull, ic, d);
-        if (lane >= d) {
-            iu += x;
-            ic += y;
-        }
-    }
+    const int iu = warp_incl_sum(cu), ic = warp_incl_sum(cc);
     nu = __shfl_sync(kFull, iu, 31);
     ncf = __shfl_sync(kFull, ic, 31);
     int pu = iu - cu, pc = ic - cc;
@@ -328,15 +320,6 @@ __device__ __forceinline__ int view_final(const LaneView<W>& x, int D, int wc, u
     return (int)z0 + popc_w<W>(aD);
 }
 
-__device__ __forceinline__ int warp_incl_sum(int x, int lane) {
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(kFull, x, d);
-        if (lane >= d) x += y;
-    }
-    return x;
-}
-
 template <int W>
 __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRefWarp& s, int lane, int nseq, int nu,
                                                int wf, int wc, uint32_t* until, int w1, uint32_t t,
@@ -388,12 +371,7 @@ __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRef
     bool seen = false;
     for (int c = 0; c < nch; ++c) {
         if (nch > 1) view_of(c, x);
-        int pm = x.vmin;  // inclusive prefix minimum of the per-vertex minima
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(kFull, pm, d);
-            if (lane >= d) pm = min(pm, y);
-        }
+        const int pm = warp_incl_min(x.vmin);  // inclusive prefix minimum of the per-vertex minima
         if (!seen) {
             int rin = __shfl_up_sync(kFull, pm, 1);
             if (lane == 0) rin = kInf;
@@ -448,7 +426,7 @@ __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRef
         uint64_t aD[W];
         bool z0;
         const int cD = view_final<W>(x, D, wc, aD, z0);
-        const int incl = warp_incl_sum(cD, lane);
+        const int incl = warp_incl_sum(cD);
         const int tot = __shfl_sync(kFull, incl, 31);
         if (J > based + tot) {
             based += tot;
