@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libplse_b200.so")
-SOURCES = ["capi.cu", "improve.cu", "improve_hw.cu", "population.cu", "distance.cu", "similarity_tc.cu", "host_graph.cu", "plits.cu", "improve_ref.cu", "plits_ref.cu"]
+SOURCES = ["capi.cu", "improve.cu", "population.cu", "distance.cu", "similarity_tc.cu", "host_graph.cu", "plits.cu", "improve_ref.cu", "plits_ref.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -52,18 +52,44 @@ def build_cli(force: bool = False) -> str:
     return CLI
 
 
+def _compile(src: str, obj: str) -> subprocess.CompletedProcess:
+    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3",
+           "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc -c per translation unit (in parallel; only the sources newer than their object unless
+    forced), then one shared-library link."""
     if not force and not needs_build():
         build_cli()
         return LIB
-    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(ROOT, "include", "plse_b200.h"))
+    newest_header = max(os.path.getmtime(h) for h in headers if os.path.exists(h))
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_header)
+        jobs.append((src, obj, stale))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        results = {src: ex.submit(_compile, src, obj) for src, obj, stale in jobs if stale}
+        log = []
+        for src, fut in results.items():
+            out = fut.result()
+            if out.returncode != 0:
+                raise RuntimeError("nvcc failed on " + src + ":\n" + out.stdout + out.stderr)
+            log.append(out.stderr)
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[obj for _, obj, _ in jobs]]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out.stdout + out.stderr)
+        raise RuntimeError("nvcc link failed:\n" + " ".join(cmd) + "\n" + out.stdout + out.stderr)
     os.replace(LIB + ".tmp", LIB)
     if verbose:
-        sys.stderr.write(out.stderr)
+        sys.stderr.write("".join(log))
     build_cli(force=True)
     return LIB
 

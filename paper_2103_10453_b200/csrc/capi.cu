@@ -101,7 +101,6 @@ struct plse_ctx {
     uint32_t tenure_cap = 0;
     size_t rec_stride = 0, until_stride = 0;
     int grid = 0, threads = 0, wpc = 0, slots = 0, warps_per_sm = 0;
-    bool half_warp = false;  // k_improve (one individual per warp) vs k_improve_hw (PLSE_IMPROVE_KERNEL=hw)
     bool plits = false;      // variant MPMA: k_plits (plits.cu) is the improve kernel
     bool ref_ties = false;   // tie_mode REF: k_improve_ref (improve_ref.cu)
     int64_t budget2 = 0;     // PLITS phase-2 budget
@@ -356,6 +355,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     for (int v = 0; v < nv; ++v)
         for (int a = gr->dom_offsets[v]; a < gr->dom_offsets[v + 1]; ++a) colvert[a] = (uint16_t)v;
     if (const char* env = std::getenv("PLSE_TC")) c->use_tc = env[0] != '0';
+    if (c->use_tc) CK(prepare_similarity_tc());
     std::vector<uint64_t> below(n + 1, 0);
     for (int b = 1; b <= n; ++b) below[b] = (0 - (uint64_t)b) % (uint64_t)b;
 
@@ -427,16 +427,12 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_work = dalloc<int>(1);
 
     // ---- improve launch shape: maximise resident individuals per SM
-    if (const char* env = std::getenv("PLSE_IMPROVE_KERNEL"))
-        c->half_warp = std::string(env) == "hw" && !c->plits && !c->ref_ties;
     c->lane_words16 = (nwords + 15) / 16;
     const void* kern = c->plits       ? (c->ref_ties ? plits_ref_kernel_ptr(W, false) : plits_kernel_ptr(W, false))
                        : c->ref_ties  ? improve_ref_kernel_ptr(W, false)
-                       : c->half_warp ? improve_hw_kernel_ptr(W, false)
                                       : improve_kernel_ptr(W, false);
     const void* kern_dbg = c->plits       ? (c->ref_ties ? plits_ref_kernel_ptr(W, true) : plits_kernel_ptr(W, true))
                            : c->ref_ties  ? improve_ref_kernel_ptr(W, true)
-                           : c->half_warp ? improve_hw_kernel_ptr(W, true)
                                           : improve_kernel_ptr(W, true);
     size_t graph_bytes = 0, warp_bytes = 0;
     if (c->plits && c->ref_ties) {
@@ -451,16 +447,12 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
         const PlitsSmemLayout L = plits_smem_layout(n, nv, c->nvpad, c->lane_words, W);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
-    } else if (c->half_warp) {
-        const HwSmemLayout L = improve_hw_smem_layout(n, nv, c->nvpad, c->lane_words16, W);
-        graph_bytes = L.graph_bytes;
-        warp_bytes = L.warp_bytes;
     } else {
         const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
     }
-    const int per_warp = c->half_warp ? 2 : 1;
+    const int per_warp = 1;
     int best_ind = 0;
     int force_wpc = 0;
     if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
@@ -484,7 +476,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     // a population that fits one warp per block everywhere runs one individual per block: the block
     // scheduler then spreads the individuals evenly over the SMs (a latency-bound small population
     // otherwise lands on whichever warps win the work counter)
-    if (!force_wpc && !c->half_warp && c->wpc != 1) {
+    if (!force_wpc && c->wpc != 1) {
         const size_t smem1 = graph_bytes + warp_bytes;
         if (smem1 <= (size_t)max_optin) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
@@ -614,8 +606,6 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
         c->launched(launch_plits(a, c->W, grid, c->threads, c->smem, c->st));
     else if (c->ref_ties)
         c->launched(launch_improve_ref(a, c->W, grid, c->threads, c->smem, c->st));
-    else if (c->half_warp)
-        c->launched(launch_improve_hw(a, c->W, grid, c->threads, c->smem, c->st));
     else
         c->launched(launch_improve(a, c->W, grid, c->threads, c->smem, c->st));
     CK(cudaEventRecord(c->ev1, c->st));

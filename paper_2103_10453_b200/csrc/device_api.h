@@ -107,57 +107,6 @@ __host__ __device__ inline ImproveSmemLayout improve_smem_layout(int n, int nv, 
     return L;
 }
 
-// two individuals per warp (improve_hw.cu): graph part + per-warp block of two half blocks
-constexpr int kHwMaxThreads = 256;
-constexpr int kHwMinBlocks = 2;  // 16 warps (32 individuals) per SM -> <= 128 registers
-
-struct HwSmemLayout {
-    size_t cell, rs, cs, cl, colpos, deg, pr, pc, graph_bytes;
-    size_t warp0, warp_bytes, half_bytes, h_col, h_colT, h_R, h_C, h_U, h_list;
-};
-
-__host__ __device__ inline HwSmemLayout improve_hw_smem_layout(int n, int nv, int nvpad, int lane_words16, int W) {
-    HwSmemLayout L;
-    size_t o = 0;
-    L.cell = o;
-    o += (size_t)nv * 2;
-    L.rs = o;
-    o += (size_t)(n + 1) * 2;
-    L.cs = o;
-    o += (size_t)(n + 1) * 2;
-    L.cl = o;
-    o += (size_t)nv * 2;
-    L.colpos = o;
-    o += (size_t)nv * 2;
-    L.deg = o;
-    o += (size_t)nv;
-    o = align_up(o, 16);
-    L.pr = o;
-    o += (size_t)n * W * 8;
-    L.pc = o;
-    o += (size_t)n * W * 8;
-    o = align_up(o, 16);
-    L.graph_bytes = o;
-    L.warp0 = o;
-    size_t h = 0;
-    L.h_col = h;
-    h += (size_t)nvpad;
-    L.h_colT = h;  // the repair's conflict counters live here until the column-major copy is built
-    h += (size_t)nvpad;
-    h = align_up(h, 16);
-    L.h_R = h;
-    h += (size_t)n * W * 8;
-    L.h_C = h;
-    h += (size_t)n * W * 8;
-    L.h_U = h;
-    h += (size_t)16 * lane_words16 * 4;
-    L.h_list = h;
-    h += 64;
-    L.half_bytes = align_up(h, 16);
-    L.warp_bytes = 2 * L.half_bytes;
-    return L;
-}
-
 // PLITS (plits.cu): graph part as improve_smem_layout, per warp: colours, bit-sliced row /
 // column colour counts ((5 + W) planes of W words per line), the active-vertex bitmask, the
 // compacted active list and a per-listed-vertex scratch word
@@ -275,9 +224,6 @@ __host__ __device__ inline RefSmemLayout improve_ref_smem_layout(int n, int nv, 
 const void* improve_ref_kernel_ptr(int W, bool debug);
 cudaError_t launch_improve_ref(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
 
-const void* improve_hw_kernel_ptr(int W, bool debug);
-cudaError_t launch_improve_hw(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
-
 size_t tabu_rec_bytes(int W);
 const void* improve_kernel_ptr(int W, bool debug);
 cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st);
@@ -290,6 +236,7 @@ cudaError_t launch_hamming(const uint8_t* A, int na, const uint8_t* B, int nb, i
 // K3 on tcgen05 (similarity_tc.cu): one-hot expansion + i8 UMMA GEMM, D = |V| - A.B^T
 cudaError_t launch_onehot(const uint8_t* X, int rows, int nvpad, const uint16_t* col_vert, const uint8_t* col_color,
                           int K, int Kpad, uint8_t* H, cudaStream_t st);
+cudaError_t prepare_similarity_tc();
 cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, int N, int Kpad, int nv, uint16_t* D,
                                  int ldd, cudaStream_t st);
 

@@ -1,5 +1,5 @@
 // improve_common.cuh -- device helpers shared by the improve kernels
-// (improve.cu: one individual per warp; improve_hw.cu: one per half-warp).
+// (improve.cu and improve_ref.cu: one individual per warp).
 #pragma once
 #include "common.cuh"
 #include "device_api.h"
@@ -15,7 +15,7 @@ struct alignas(16) TabuRec {
 
 struct WarpSmem {
     uint8_t* col;    // colour of vertex v
-    uint8_t* conf;   // improve_hw: repair counters / column-major copy
+    uint8_t* conf;   // repair counters
     uint64_t* R;
     uint64_t* C;
     uint32_t* U;
@@ -31,7 +31,7 @@ struct Graph {
     const uint16_t* rs;
     const uint16_t* cs;
     const uint16_t* cl;
-    const uint16_t* colpos;  // position of v in the column-major list cl (improve_hw only)
+    const uint16_t* colpos;  // position of v in the column-major list cl
     const uint64_t* pr;
     const uint64_t* pc;
     uint64_t full[W];
@@ -178,7 +178,7 @@ __device__ __forceinline__ TabuRec apply_move_lanes(const Graph<W>& g, const War
 __device__ __forceinline__ int warp_incl_sum(int x) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1)
-        asm("{\n\t.reg .s32 r0;\n\t.reg .pred p;\n\t"
+        asm volatile("{\n\t.reg .s32 r0;\n\t.reg .pred p;\n\t"
             "shfl.sync.up.b32 r0|p, %0, %1, 0x0, 0xffffffff;\n\t"
             "@p add.s32 %0, r0, %0;\n\t}"
             : "+r"(x)
@@ -190,7 +190,7 @@ __device__ __forceinline__ int warp_incl_sum(int x) {
 __device__ __forceinline__ int warp_incl_min(int x) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1)
-        asm("{\n\t.reg .s32 r0;\n\t.reg .pred p;\n\t"
+        asm volatile("{\n\t.reg .s32 r0;\n\t.reg .pred p;\n\t"
             "shfl.sync.up.b32 r0|p, %0, %1, 0x0, 0xffffffff;\n\t"
             "@p min.s32 %0, r0, %0;\n\t}"
             : "+r"(x)

@@ -251,14 +251,13 @@ cudaError_t launch_onehot(const uint8_t* X, int rows, int nvpad, const uint16_t*
     return cudaGetLastError();
 }
 
+// the shared-memory opt-in is a per-device function attribute: called by plse_create after cudaSetDevice
+cudaError_t prepare_similarity_tc() {
+    return cudaFuncSetAttribute(k_sim_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+}
+
 cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, int N, int Kpad, int nv, uint16_t* D,
                                  int ldd, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_sim_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
     CUtensorMap ma, mb;
     if (!make_map(&ma, HA, M, Kpad, kTcBM) || !make_map(&mb, HB, N, Kpad, kTcBN)) return cudaErrorInvalidValue;
     const int tiles = ((N + kTcBN - 1) / kTcBN) * ((M + kTcBM - 1) / kTcBM);
