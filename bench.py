@@ -15,9 +15,12 @@ counted exactly as the reference counts SearchStats.iterations
 working set (1.5 GB of distance blocks, GBs of tabu scratch) is far larger
 than the 126 MB L2, so no explicit flush is needed.
 
-N > 1 (torchrun): island model -- every rank evolves its own 16384-individual
-island (weak scaling), stream index space gen*p_total + rank*p + i, and the
-ranks all-gather 32 elites each over NCCL every 2 generations.
+N > 1 (torchrun): island model -- the population of 16384 is
+sharded into N islands of 16384/N individuals (strong scaling, BASELINE C3:
+"population 16384 sharded over 2/4/8 B200"; --weak keeps 16384 per GPU), stream
+index space gen*p_total + rank*p + i, and every 2 generations the ranks
+all-gather 32 elites each over NCCL (on the population's CUDA stream) and stage
+the other ranks' elites as extra candidates of their next pool update.
 
 --impl reference: the reference's own CPU improve phase (oracle/_ref =
 /root/reference compiled in place; parallel_for over all host threads,
@@ -55,7 +58,8 @@ def args_():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pop", type=int, default=16384)
+    ap.add_argument("--pop", type=int, default=16384, help="total population (sharded over the GPUs)")
+    ap.add_argument("--weak", action="store_true", help="--pop individuals per GPU instead of in total")
     ap.add_argument("--n", type=int, default=60)
     ap.add_argument("--r", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=12345)
@@ -143,17 +147,34 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config_key: str):
-    """dram bytes per improve launch from the committed ncu --set full summary, if it matches this config."""
-    path = os.path.join(ROOT, "profiles", "improve_ncu_summary.json")
+def kernel_src_hash(kernel: str) -> str:
+    """sha256 (16 hex) of the sources the named improve kernel is compiled from: an ncu capture counts
+    for a bench line only if it was taken of the same kernel source."""
+    import hashlib
+    csrc = os.path.join(ROOT, "paper_2103_10453_b200", "csrc")
+    files = {"k_improve": ["improve.cu", "improve_common.cuh", "common.cuh", "device_api.h"],
+             "k_plits": ["plits.cu", "plits_common.cuh", "improve_common.cuh", "common.cuh", "device_api.h"]}[kernel]
+    h = hashlib.sha256()
+    for name in files:
+        with open(os.path.join(csrc, name), "rb") as f:
+            h.update(name.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_profile(kernel: str, config_key: str):
+    """The committed ncu --set full summary of this kernel (profiles/<kernel>_ncu_summary.json) if it was
+    captured from the same kernel source and config; else None (the line then says why)."""
+    path = os.path.join(ROOT, "profiles", f"{kernel}_ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        if d.get("config_key") == config_key:
-            return d.get("dram_bytes_per_launch")
     except (OSError, ValueError):
-        pass
-    return None
+        return None, "no committed ncu summary"
+    if d.get("src_hash") != kernel_src_hash(kernel):
+        return None, f"{os.path.relpath(path, ROOT)} was captured from another kernel source"
+    if d.get("config_key") != config_key:
+        return None, f"{os.path.relpath(path, ROOT)} was captured at another config"
+    return d, os.path.relpath(path, ROOT)
 
 
 def lsc_grid(a):
@@ -163,22 +184,33 @@ def lsc_grid(a):
     return lsc_instance(a.n, a.r, a.seed)
 
 
+def i8_peak():
+    """dense i8 tensor peak: measured on a B200 of this pool by tools/probes/i8_peak.py
+    (profiles/i8_peak.json: cuBLASLt int8 GEMM via torch._int_mm, best of 10), else 2x the measured
+    bf16 burst (the sm_100 dense i8 rate is twice bf16)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "i8_peak.json")) as f:
+            d = json.load(f)
+        return float(d["i8_tops_burst"]), "measured: profiles/i8_peak.json (" + d.get("how", "") + ")"
+    except (OSError, KeyError, ValueError):
+        pass
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return 2 * float(json.load(f)["bf16_tflops"]), "2 x measured bf16 burst (i8 peak not measured)"
+    except (OSError, KeyError, ValueError):
+        return 2 * 1590.0, "2 x fallback bf16 (B200_PROFILING.md)"
+
+
 def k3_roofline(ph, tensor_cores):
-    """similarity GEMM (one-hot i8 tcgen05): algorithmic ops 2*M*N*Kpad per GEMM over the phase time."""
+    """similarity GEMM (one-hot i8 tcgen05): algorithmic ops (2*K_pad per pair: p^2 cross pairs + p(p-1)/2
+    fresh pairs) over the distance phase's time, which includes the one-hot expansion of both operands."""
     if ph["distances"] <= 0 or ph["k3_ops"] <= 0:
         return None
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(path) as f:
-            bf16 = float(json.load(f)["bf16_tflops"])
-        src = "2 x measured bf16 burst (i8 dense rate = 2x bf16 on sm_100; i8 not measured by the driver)"
-    except (OSError, KeyError, ValueError):
-        bf16, src = 1590.0, "2 x fallback bf16 (B200_PROFILING.md)"
+    peak, src = i8_peak()
     achieved = ph["k3_ops"] / (ph["distances"] / 1e3) / 1e12
-    peak = 2 * bf16
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
             "kernel": "k_onehot + k_sim_tc" if tensor_cores else "k_hamming (CUDA cores)", "peak_source": src,
-            "includes": "one-hot expansion of both operands"}
+            "includes": "one-hot expansion (members, improved once) + cross GEMM + fresh upper-triangle GEMM"}
 
 
 def cpu_threads():
@@ -259,23 +291,28 @@ def run_ours(a):
             dist.init_process_group(backend)
     coll = "cuda" if backend == "nccl" else "cpu"
     import paper_2103_10453_b200 as P
+    from paper_2103_10453_b200.islands import DeviceIsland
 
     grid = lsc_grid(a) if a.lsc else P.generate_instance(a.n, a.r, a.seed)
     graph = P.preprocess(grid)
     nv = graph.vertex_count
     budget = a.budget if a.budget > 0 else 100 * nv
     mpma = a.variant == "mpma"
-    cfg = P.SolverConfig(p=a.pop, master_seed=a.master_seed, phase1_iters=a.budget, device=local,
-                         p_total=a.pop * world, offset=a.pop * rank, variant=P.MPMA if mpma else P.PARTIAL,
+    if a.weak:
+        p_rank = a.pop
+    else:
+        if a.pop % world:
+            raise SystemExit(f"--pop {a.pop} does not split over {world} GPUs")
+        p_rank = a.pop // world
+    p_total = p_rank * world
+    cfg = P.SolverConfig(p=p_rank, master_seed=a.master_seed, phase1_iters=a.budget, device=local,
+                         p_total=p_total, offset=p_rank * rank, variant=P.MPMA if mpma else P.PARTIAL,
                          phase2_iters=a.budget2, tie_mode=P.TIE_REF if a.tie == "ref" else P.TIE_CANON)
     pop = P.DevicePopulation(graph, cfg)
     pop.initialize_population()
     pop.offspring = pop.members  # generation-0 offspring are the initial individuals (engine.hpp:163)
     gen = 0
-    elite_buf = None
-    if world > 1:
-        elite_buf = torch.empty((world * a.elites, pop.row_bytes), dtype=torch.uint8, device="cuda")
-        my_elites = torch.empty((a.elites, pop.row_bytes), dtype=torch.uint8, device="cuda")
+    isl = DeviceIsland(pop, a.elites, rank, world) if world > 1 else None
 
     def barrier():
         torch.cuda.synchronize()
@@ -283,34 +320,30 @@ def run_ours(a):
             dist.barrier()
 
     phase = {"improve": 0.0, "distances": 0.0, "update": 0.0, "offspring": 0.0, "k3_ops": 0.0}
+    state = {"pending": False}  # the previous generation's population phases are not yet accounted
+
+    def add_phases(c):
+        phase["distances"] += c.distances_ms
+        phase["update"] += c.update_ms
+        phase["offspring"] += c.offspring_ms
+        phase["k3_ops"] += c.k3_ops
 
     def generation():
+        """one Partial-MPMA generation; the only host synchronisation is the improve phase's summary
+        (iterations, best f).  The population phases' timers of the PREVIOUS generation are read there."""
         nonlocal gen
         gen += 1
         it, bf, bi = pop.improve(gen)
         ctr = pop.counters()
-        pop.compute_cross_distances()
-        pop.update_population()
-        if world > 1 and gen % a.migrate_every == 0:
-            pop.export_elites(a.elites, my_elites.data_ptr())
-            torch.cuda.synchronize()
-            if coll == "cuda":
-                dist.all_gather_into_tensor(elite_buf, my_elites)
-            else:
-                parts = [torch.empty_like(my_elites, device="cpu") for _ in range(world)]
-                dist.all_gather(parts, my_elites.cpu())
-                elite_buf.copy_(torch.cat(parts).to("cuda"))
-            torch.cuda.synchronize()
-            others = torch.cat([elite_buf[r * a.elites:(r + 1) * a.elites] for r in range(world) if r != rank])
-            torch.cuda.synchronize()  # the library reads `others` on its own stream
-            pop.import_migrants(others.shape[0], others.data_ptr())
-        pop.build_offspring(gen)
-        c2 = pop.counters()
+        if state["pending"]:
+            add_phases(ctr)
         phase["improve"] += ctr.improve_ms
-        phase["distances"] += c2.distances_ms
-        phase["update"] += c2.update_ms
-        phase["offspring"] += c2.offspring_ms
-        phase["k3_ops"] += c2.k3_ops
+        if isl is not None and gen % a.migrate_every == 0:
+            isl.migrate()
+        pop.compute_cross_distances()
+        pop.update_population(info=False)
+        pop.build_offspring(gen)
+        state["pending"] = True
         return it, bf, ctr.improve_ms, ctr.alg_bytes
 
     # gen-1 improve rate (for the CPU-baseline comparison, same generation as the reference sample)
@@ -323,6 +356,7 @@ def run_ours(a):
     launches0 = pop.counters().kernel_launches
     for k in phase:
         phase[k] = 0.0
+    state["pending"] = False  # the last warm-up generation's phases stay out of the timed totals
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -340,9 +374,11 @@ def run_ours(a):
     ms = pop.timer_stop()
     barrier()
     clk = clocks.stop()
-    launches = pop.counters().kernel_launches - launches0
-
+    last = pop.counters()
+    add_phases(last)
+    launches = last.kernel_launches - launches0
     timed_phase = dict(phase)
+
     # e2e through the public API with host buffers: H2D offspring, generation, D2H next offspring + stats
     host_off = pop.offspring
     e2e_moves = 0
@@ -356,8 +392,8 @@ def run_ours(a):
         f, c, iters = pop.stats(P.IMPROVED)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    h2d = a.pop * nv * 2
-    d2h = a.pop * nv * 2 + a.pop * (4 + 4 + 8)
+    h2d = p_rank * nv * 2
+    d2h = p_rank * nv * 2 + p_rank * (4 + 4 + 8)
 
     tot_moves, tot_e2e = moves, e2e_moves
     t_max, e2e_max = ms, e2e_s
@@ -372,39 +408,58 @@ def run_ours(a):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = alg_bytes / (imp_ms / 1e3) / 1e9
-        key = f"n{a.n}_r{a.r}_s{a.seed}_p{a.pop}_b{budget}"
+        kernel = "k_plits" if mpma else "k_improve"
+        key = f"n{a.n}_r{a.r}_s{a.seed}_p{p_rank}_b{budget}" + ("_lsc" if a.lsc else "")
+        prof, prof_src = ncu_profile(kernel, key)
         ctr = pop.counters()
+        improve_rate = moves / (imp_ms / 1e3)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+                "kernel": kernel, "peak_source": peak_src, "config_key": key,
+                "src_hash": kernel_src_hash(kernel), "profile": prof_src,
+                "bytes_def": ("DESIGN.md PLITS byte model summed over every step of the launch" if mpma
+                              else "SURVEY 8(d) B_t summed over every step of the launch (int16 gamma rows the "
+                                   "reference's step reads; this kernel derives gamma from occupancy masks)"),
+                "kernel_share_of_step": imp_ms / ms,
+                "binding_limit": "instruction issue (the gamma table is never materialised: measured DRAM "
+                                 "traffic is a few % of the algorithmic bytes)"}
+        if prof and prof.get("inst_per_move") and clk.get("sm_mhz"):
+            peak_inst = 148 * 4 * clk["sm_mhz"] * 1e6
+            ach_inst = prof["inst_per_move"] * improve_rate
+            roof["issue"] = {"inst_per_move": prof["inst_per_move"], "achieved_warp_inst_per_s": ach_inst,
+                             "peak_warp_inst_per_s": peak_inst, "frac": ach_inst / peak_inst,
+                             "peak_def": "148 SMs x 4 schedulers x median SM clock under load",
+                             "inst_source": prof_src}
+        if prof and prof.get("dram_bytes_per_launch") and prof.get("launch_ms"):
+            roof["dram_measured"] = {"gbs": prof["dram_bytes_per_launch"] / (prof["launch_ms"] / 1e3) / 1e9,
+                                     "frac": prof["dram_bytes_per_launch"] / (prof["launch_ms"] / 1e3) / 1e9 / peak,
+                                     "source": prof_src}
         line = {
             "metric": METRIC, "value": tot_moves / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": t_max / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32",
+            "warmup": a.warmup, "ms_per_step": t_max / a.steps, "higher_is_better": True,
+            "scaling": "weak" if a.weak else "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (generate_instance(60,0.5,12345); random initial population, seeds fixed)",
-            "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}, "
+            "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}" + (" (LSC builder)" if a.lsc else "") + ", "
                                    + ("MPMA (PLITS) generation" if mpma else "Partial-MPMA generation")
-                                   + f" (improve+distances+update+offspring), pop {a.pop}/GPU, budget {budget}"
-                                   + (" + 2|V|" if mpma else ""),
+                                   + f" (improve+distances+update+offspring), pop {p_total} = {world} x {p_rank}, "
+                                   f"budget {budget}" + (" + 2|V|" if mpma else ""),
                        "variant": a.variant, "tie_break": a.tie,
-                       "global_batch": a.pop * world, "vertices": nv, "budget": budget,
+                       "global_batch": p_total, "per_gpu": p_rank, "vertices": nv, "budget": budget,
                        "parallelism": f"islands x{world}" + (f", {a.elites} elites all-gathered every "
-                                                             f"{a.migrate_every} gens" if world > 1 else ""),
-                       "l2": "inputs larger than L2 (1.5 GB distance blocks + tabu scratch per step)",
+                                                             f"{a.migrate_every} gens as pool candidates"
+                                                             if world > 1 else ""),
+                       "l2": "inputs larger than L2 (distance blocks + tabu scratch per step)",
                        "improve_launch": {"grid": ctr.grid, "threads": ctr.threads, "warps_per_sm": ctr.warps_per_sm,
                                           "smem_bytes": ctr.smem_bytes}},
             "gpu_launches": launches,
             "clocks": clk,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None if mpma else ncu_traffic(key),
-                         "kernel": "k_plits" if mpma else "k_improve",
-                         "peak_source": peak_src, "config_key": key,
-                         "bytes_def": ("DESIGN.md PLITS byte model summed over every step of the launch" if mpma
-                                       else "SURVEY 8(d) B_t summed over every step of the launch"),
-                         "kernel_share_of_step": imp_ms / ms},
-            "improve_moves_per_s": moves / (imp_ms / 1e3),
+            "roofline": roof,
+            "improve_moves_per_s": improve_rate,
             "phase_ms_per_step": {k: v / a.steps for k, v in timed_phase.items() if k != "k3_ops"},
             "k3_roofline": k3_roofline(timed_phase, pop.counters().k3_tensor_cores),
             "best_f_seen": best,
-            "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": a.e2e_steps},
+            "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": a.e2e_steps},
             "gen1": gen1,
         }
         if world > 1 and (one_gpu or backend != "nccl"):

@@ -201,19 +201,24 @@ int plse_init_population(plse_ctx* ctx);
 int plse_full_distances(plse_ctx* ctx); /* dist <- D(members, members) */
 int plse_improve(plse_ctx* ctx, uint64_t generation, int64_t* iters_total, int32_t* best_f, int32_t* best_idx);
 int plse_distances(plse_ctx* ctx);
+/* the whole update runs on the device; the outputs (each optional, NULL = not read back, no host
+   synchronisation) are UpdateInfo's fields */
 int plse_update(plse_ctx* ctx, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* shortfall_slots /* cap p */);
 int plse_reset_exclusion(plse_ctx* ctx);
 int plse_offspring(plse_ctx* ctx, uint64_t generation);
 /* run individual idx of OFFSPRING through improve with a per-step trace (parity probe) */
 int plse_trace(plse_ctx* ctx, int32_t idx, uint64_t generation, int64_t max_steps, plse_step* out, int64_t* n_out);
 
-/* ---- island exchange (multi-GPU): the driver moves the bytes (NCCL all-gather) */
-/* copy the n_elite best members (ascending f, lowest index) as u8 rows [n_elite*|V|] into dev_out */
+/* ---- island exchange (multi-GPU, SURVEY 8(e)): the driver moves the bytes (NCCL all-gather) */
+/* the n_elite best members ((illegal, f, slot) ascending) as u8 rows [n_elite * row_stride] into dev_out,
+   written on the context's stream (plse_stream); f_out (host, optional) synchronises */
 int plse_export_elites(plse_ctx* ctx, int32_t n_elite, void* dev_out, int32_t* f_out);
-/* replace the n_in worst members by the given u8 rows [n_in*|V|] (device pointer) and refresh dist;
-   the rows are read on the context's stream: the caller makes them complete first (e.g. synchronises
-   the stream that produced them) */
+/* stage n_in u8 rows [n_in * row_stride] (device pointer, read on the context's stream) as extra
+   candidates -- pool ids 2p..2p+n_in-1 -- of the next plse_update (update_population with a 2p+n_in
+   pool, population.hpp:103-183); call between plse_improve and plse_update */
 int plse_import_migrants(plse_ctx* ctx, int32_t n_in, const void* dev_in);
+/* the cudaStream_t every phase of this context is enqueued on (for event / collective ordering) */
+int plse_stream(plse_ctx* ctx, void** stream_out);
 
 /* ---- the whole run() (engine.hpp:114-262) on one device */
 int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, plse_run_result* res,

@@ -159,6 +159,8 @@ class Oracle:
         L.or_full_distances.argtypes = [C.c_int, C.c_int, u16p, i32p]
         L.or_update.argtypes = [C.c_void_p, C.c_int, C.c_double, u16p, i32p, u16p, i32p, i32p,
                                 C.POINTER(C.c_int32), i32p, C.POINTER(C.c_int32), i32p]
+        L.or_update_ex.argtypes = [C.c_void_p, C.c_int, C.c_double, u16p, i32p, u16p, i32p, i32p, C.c_int,
+                                   C.c_void_p, C.POINTER(C.c_int32), i32p, C.POINTER(C.c_int32), i32p]
         L.or_offspring.argtypes = [C.c_void_p, C.c_int, u16p, i32p, C.c_int, C.c_double, C.c_int, C.c_int,
                                    u8p, C.c_uint64, C.c_uint64, u16p, i32p]
         L.or_init_population.argtypes = [C.c_void_p, C.c_int, C.c_uint64, u16p]
@@ -276,16 +278,19 @@ class Oracle:
         self.lib.or_full_distances(nv, p, np.ascontiguousarray(members, np.uint16).reshape(-1), d)
         return d.reshape(p, p)
 
-    def update(self, grid, members, dist, improved, cross, fresh, gamma=10.0):
+    def update(self, grid, members, dist, improved, cross, fresh, gamma=10.0, migrants=None):
+        """population.hpp:103-183; `migrants` (k x |V|) join the pool as ids 2p..2p+k-1 (island exchange)"""
         p, nv = members.shape
         m = np.array(members, np.uint16).reshape(-1)
         d = np.array(dist, np.int32).reshape(-1)
         pbf, nsf = C.c_int32(), C.c_int32()
         sfs = np.zeros(p, np.int32)
         sel = np.zeros(p, np.int32)
-        self.lib.or_update(self._h(grid), p, gamma, m, d, np.ascontiguousarray(improved, np.uint16).reshape(-1),
-                           np.ascontiguousarray(cross, np.int32).reshape(-1),
-                           np.ascontiguousarray(fresh, np.int32).reshape(-1), C.byref(pbf), sfs, C.byref(nsf), sel)
+        mig = np.ascontiguousarray(migrants if migrants is not None else np.zeros((0, nv)), np.uint16)
+        self.lib.or_update_ex(self._h(grid), p, gamma, m, d, np.ascontiguousarray(improved, np.uint16).reshape(-1),
+                              np.ascontiguousarray(cross, np.int32).reshape(-1),
+                              np.ascontiguousarray(fresh, np.int32).reshape(-1), mig.shape[0],
+                              mig.ctypes.data_as(C.c_void_p), C.byref(pbf), sfs, C.byref(nsf), sel)
         return dict(members=m.reshape(p, nv), dist=d.reshape(p, p), pool_best_f=pbf.value,
                     shortfall_slots=sfs[:nsf.value].tolist(), selected=sel)
 

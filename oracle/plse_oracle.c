@@ -1023,21 +1023,26 @@ static int cmp_key(const void* a, const void* b) {
     return x->id - y->id;
 }
 
-/* population.hpp:103-183 */
-int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members, int32_t* dist,
-              const uint16_t* improved, const int32_t* cross, const int32_t* fresh,
-              int32_t* pool_best_f, int32_t* shortfall_slots, int32_t* n_shortfall,
-              int32_t* selected_ids) {
+/* population.hpp:103-183, with the island exchange's migrants as extra pool candidates:
+   pool ids 0..p-1 members, p..2p-1 improved, 2p..2p+m-1 migrants; a migrant's distances are Hamming
+   distances computed here (coloring.hpp:159-167).  m = 0 is the reference's update exactly. */
+int or_update_ex(const or_graph* g, int p, double spacing_gamma, uint16_t* members, int32_t* dist,
+                 const uint16_t* improved, const int32_t* cross, const int32_t* fresh, int m,
+                 const uint16_t* migrants, int32_t* pool_best_f, int32_t* shortfall_slots,
+                 int32_t* n_shortfall, int32_t* selected_ids) {
     const int nv = g->nv;
     const double threshold = nv / spacing_gamma;
-    const int pool = 2 * p;
+    const int pool = 2 * p + m;
     pool_key* keys = (pool_key*)malloc(sizeof(pool_key) * pool);
     int* legal = (int*)malloc(sizeof(int) * pool);
     int* fval = (int*)calloc(pool, sizeof(int));
+#define ROW(id)                                                   \
+    ((id) < p       ? members + (size_t)(id) * nv                 \
+     : (id) < 2 * p ? improved + (size_t)((id) - p) * nv          \
+                    : migrants + (size_t)((id) - 2 * p) * nv)
     for (int id = 0; id < pool; ++id) {
-        const uint16_t* c = id < p ? members + (size_t)id * nv : improved + (size_t)(id - p) * nv;
         int f, cc;
-        or_eval(g, c, &f, &cc);
+        or_eval(g, ROW(id), &f, &cc);
         legal[id] = cc == 0;
         fval[id] = f;
         keys[id].illegal = cc == 0 ? 0 : 1;
@@ -1047,6 +1052,7 @@ int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members,
     qsort(keys, pool, sizeof(pool_key), cmp_key);
 #define PD(a, b)                                                                          \
     ((a) == (b) ? 0                                                                       \
+     : ((a) >= 2 * p || (b) >= 2 * p) ? or_hamming(nv, ROW(a), ROW(b))                    \
      : ((a) < p && (b) < p)   ? dist[(size_t)(a) * p + (b)]                               \
      : ((a) >= p && (b) >= p) ? fresh[(size_t)((a) - p) * p + ((b) - p)]                  \
      : ((a) < p)              ? cross[(size_t)(a) * p + ((b) - p)]                        \
@@ -1091,10 +1097,10 @@ int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members,
     uint16_t* nm = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)p * nv);
     for (int i = 0; i < p; ++i) {
         const int id = sel[i];
-        const uint16_t* c = id < p ? members + (size_t)id * nv : improved + (size_t)(id - p) * nv;
-        memcpy(nm + (size_t)i * nv, c, sizeof(uint16_t) * nv);
+        memcpy(nm + (size_t)i * nv, ROW(id), sizeof(uint16_t) * nv);
         if (selected_ids) selected_ids[i] = id;
     }
+#undef ROW
     memcpy(members, nm, sizeof(uint16_t) * (size_t)p * nv);
     memcpy(dist, nd, sizeof(int32_t) * (size_t)p * p);
     free(nm);
@@ -1105,6 +1111,15 @@ int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members,
     free(legal);
     free(fval);
     return 0;
+}
+
+/* population.hpp:103-183 */
+int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members, int32_t* dist,
+              const uint16_t* improved, const int32_t* cross, const int32_t* fresh,
+              int32_t* pool_best_f, int32_t* shortfall_slots, int32_t* n_shortfall,
+              int32_t* selected_ids) {
+    return or_update_ex(g, p, spacing_gamma, members, dist, improved, cross, fresh, 0, NULL, pool_best_f,
+                        shortfall_slots, n_shortfall, selected_ids);
 }
 
 /* population.hpp:209-228 (excl: p*p bytes, slot-keyed; NULL = no exclusion) */

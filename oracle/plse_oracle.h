@@ -160,6 +160,11 @@ int or_enumerate_exact(const or_graph* g, or_exact_result* res, uint16_t* certif
 void or_cross_distances(int nv, int p, const uint16_t* members, const uint16_t* improved,
                         int32_t* cross, int32_t* fresh);
 void or_full_distances(int nv, int p, const uint16_t* members, int32_t* dist);
+/* or_update with m migrant rows as extra pool candidates (ids 2p..2p+m-1; island exchange) */
+int or_update_ex(const or_graph* g, int p, double spacing_gamma, uint16_t* members, int32_t* dist,
+                 const uint16_t* improved, const int32_t* cross, const int32_t* fresh, int m,
+                 const uint16_t* migrants, int32_t* pool_best_f, int32_t* shortfall_slots,
+                 int32_t* n_shortfall, int32_t* selected_ids);
 int or_update(const or_graph* g, int p, double spacing_gamma, uint16_t* members, int32_t* dist,
               const uint16_t* improved, const int32_t* cross, const int32_t* fresh,
               int32_t* pool_best_f, int32_t* shortfall_slots, int32_t* n_shortfall,

@@ -164,12 +164,13 @@ def _load() -> C.CDLL:
         "plse_improve": ([ctx, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
                          C.c_int),
         "plse_distances": ([ctx], C.c_int),
-        "plse_update": ([ctx, C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32p], C.c_int),
+        "plse_update": ([ctx, vp, vp, vp], C.c_int),
         "plse_reset_exclusion": ([ctx], C.c_int),
         "plse_offspring": ([ctx, C.c_uint64], C.c_int),
         "plse_trace": ([ctx, C.c_int32, C.c_uint64, C.c_int64, vp, C.POINTER(C.c_int64)], C.c_int),
         "plse_export_elites": ([ctx, C.c_int32, vp, vp], C.c_int),
         "plse_import_migrants": ([ctx, C.c_int32, vp], C.c_int),
+        "plse_stream": ([ctx, C.POINTER(vp)], C.c_int),
         "plse_solve": ([C.c_int32, u16p, C.POINTER(_SolverConfig), C.POINTER(_RunResult), u16p, _GEN_CB, vp],
                        C.c_int),
     }
@@ -599,10 +600,15 @@ class DevicePopulation:
     def compute_cross_distances(self) -> None:
         _check(_lib.plse_distances(self._ctx), self._ctx)
 
-    def update_population(self) -> UpdateInfo:
+    def update_population(self, info: bool = True) -> Optional[UpdateInfo]:
+        """population.hpp:103-183 on the device.  With info=False nothing is read back (no host
+        synchronisation); the UpdateInfo is returned only when asked for."""
+        if not info:
+            _check(_lib.plse_update(self._ctx, None, None, None), self._ctx)
+            return None
         pbf, nsf = C.c_int32(), C.c_int32()
         slots = np.zeros(self.p, np.int32)
-        _check(_lib.plse_update(self._ctx, C.byref(pbf), C.byref(nsf), slots), self._ctx)
+        _check(_lib.plse_update(self._ctx, C.byref(pbf), C.byref(nsf), slots.ctypes.data_as(C.c_void_p)), self._ctx)
         return UpdateInfo(pbf.value, slots[:nsf.value].tolist())
 
     def reset_exclusion(self) -> None:
@@ -620,14 +626,25 @@ class DevicePopulation:
         m = min(n.value, max_steps)
         return [{k: getattr(buf[i], k) for k, _ in Step._fields_} for i in range(m)], n.value
 
-    def export_elites(self, n_elite: int, dev_ptr: int):
+    def export_elites(self, n_elite: int, dev_ptr: int, with_f: bool = False):
+        """The n_elite best members ((illegal, f, slot) order) as u8 rows into dev_ptr, written on this
+        population's stream (see `stream`); with_f also returns their f (synchronises)."""
         f = np.zeros(max(n_elite, 1), np.int32)
-        _check(_lib.plse_export_elites(self._ctx, n_elite, C.c_void_p(dev_ptr), f.ctypes.data_as(C.c_void_p)),
-               self._ctx)
-        return f[:n_elite]
+        _check(_lib.plse_export_elites(self._ctx, n_elite, C.c_void_p(dev_ptr),
+                                       f.ctypes.data_as(C.c_void_p) if with_f else None), self._ctx)
+        return f[:n_elite] if with_f else None
 
     def import_migrants(self, n_in: int, dev_ptr: int) -> None:
+        """Stage n_in u8 rows (device pointer, read on this population's stream) as extra candidates of
+        the next update_population; call between improve() and update_population()."""
         _check(_lib.plse_import_migrants(self._ctx, n_in, C.c_void_p(dev_ptr)), self._ctx)
+
+    @property
+    def stream(self) -> int:
+        """The cudaStream_t (as an int) every phase of this population runs on."""
+        s = C.c_void_p()
+        _check(_lib.plse_stream(self._ctx, C.byref(s)), self._ctx)
+        return s.value or 0
 
     @property
     def row_bytes(self) -> int:

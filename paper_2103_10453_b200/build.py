@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libplse_b200.so")
-SOURCES = ["capi.cu", "improve.cu", "population.cu", "distance.cu", "similarity_tc.cu", "host_graph.cu", "plits.cu", "improve_ref.cu", "plits_ref.cu"]
+SOURCES = ["capi.cu", "improve.cu", "population.cu", "pool.cu", "distance.cu", "similarity_tc.cu", "host_graph.cu", "plits.cu", "improve_ref.cu", "plits_ref.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -83,8 +83,8 @@ struct plse_ctx {
             *d_tmpc = nullptr;
     int64_t* d_iters = nullptr;
     unsigned long long* d_bytes = nullptr;
-    std::vector<int32_t> h_mf, h_mc, h_if, h_ic;
-    std::vector<int64_t> h_iters;
+    int32_t* d_imc = nullptr;  // c of the improved individuals (0 after improve; set by plse_set_colors)
+    int32_t *d_nf = nullptr, *d_nc = nullptr;  // next members' f / c (gathered by the update)
     uint32_t* d_excl = nullptr;
     int excl_words = 0;
     // K3 on tcgen05: one-hot operands (p x Kpad u8) and the column tables of the domain CSR
@@ -112,10 +112,22 @@ struct plse_ctx {
     int race_f = -1;
     unsigned long long* d_deadline = nullptr;  // %globaltimer deadline of plse_solve's time limit
     unsigned long long* d_dsum = nullptr;      // GenerationStats::mean_distance reduction
-    // pool update scratch
-    int32_t *d_order = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_mts = nullptr;
-    uint32_t* d_conf = nullptr;
-    uint8_t *d_legal = nullptr, *d_admitted = nullptr;
+    // pool update scratch (pool.cu)
+    PoolScratch ps{};
+    int pool_cap = 0;  // pool positions the scratch holds (2p + migrant capacity)
+    // island exchange: migrants staged as extra pool candidates of the next update
+    uint8_t* d_migr = nullptr;
+    int32_t *d_gf = nullptr, *d_gc = nullptr;
+    uint16_t* d_migd = nullptr;  // n_mig x (2p + n_mig)
+    uint8_t* d_hM = nullptr;     // one-hot rows of the migrants
+    int mig_cap = 0, n_mig = 0;
+    bool onehot_valid = false;  // d_hA / d_hB hold onehot(members) / onehot(improved) of this generation
+    ImproveSummary* d_sum = nullptr;
+    ImproveSummary* h_sum = nullptr;  // pinned
+    int32_t* h_info = nullptr;        // pinned: pool_best_f, shortfall count
+    // phase timers: events recorded on the stream, resolved when the counters are read
+    cudaEvent_t ph_ev[3][2] = {};
+    bool ph_pending[3] = {false, false, false};
     // host staging (pinned, so host<->device copies run at full PCIe rate)
     uint8_t* stage = nullptr;
     size_t stage_bytes = 0;
@@ -127,11 +139,18 @@ struct plse_ctx {
         if (device >= 0) cudaSetDevice(device);
         void* bufs[] = {d_cell, d_rs, d_cs, d_cl, d_pr, d_pc, d_below, d_dom_off, d_dom, d_members, d_offspring,
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
-                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock, d_conf_scratch, d_work, d_prof, d_race, d_deadline, d_dsum, d_colvert, d_hA, d_hB, d_order,
-                        d_sel, d_nsel, d_mts, d_conf, d_legal, d_admitted};
+                        d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock,
+                        d_conf_scratch, d_work, d_prof, d_race, d_deadline, d_dsum, d_colvert, d_hA, d_hB, d_imc,
+                        d_nf, d_nc, ps.keys0, ps.keys1, ps.order, ps.sel, ps.nsel, ps.slots, ps.info, ps.legal,
+                        ps.admitted, ps.ok, ps.conf, d_migr, d_gf, d_gc, d_migd, d_hM, d_sum};
         for (void* b : bufs)
             if (b) cudaFree(b);
         if (stage) cudaFreeHost(stage);
+        if (h_sum) cudaFreeHost(h_sum);
+        if (h_info) cudaFreeHost(h_info);
+        for (auto& pr : ph_ev)
+            for (cudaEvent_t e : pr)
+                if (e) cudaEventDestroy(e);
         if (tm0) cudaEventDestroy(tm0);
         if (tm1) cudaEventDestroy(tm1);
         if (ev0) cudaEventDestroy(ev0);
@@ -222,44 +241,102 @@ void validate_params(const plse_params& p) {
     if (p.p_total < 0 || p.offset < 0) throw std::invalid_argument("negative island coordinates");
 }
 
-void eval_into(plse_ctx* c, const uint8_t* colors, std::vector<int32_t>& f, std::vector<int32_t>& cc, int32_t* df,
-               int32_t* dc) {
-    c->launched(launch_eval_fc(c->pop_graph(), c->prm.p, colors, df, dc, c->st));
-    f.resize(c->prm.p);
-    cc.resize(c->prm.p);
-    CK(cudaMemcpyAsync(f.data(), df, sizeof(int32_t) * c->prm.p, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(cc.data(), dc, sizeof(int32_t) * c->prm.p, cudaMemcpyDeviceToHost, c->st));
+// f / c of p colour rows into device arrays (coloring.hpp:59-73)
+void eval_into(plse_ctx* c, const uint8_t* colors, int32_t* df, int32_t* dc, int rows = -1) {
+    c->launched(launch_eval_fc(c->pop_graph(), rows < 0 ? c->prm.p : rows, colors, df, dc, c->st));
+}
+
+// K3: D = hamming(A rows, B rows) -- tcgen05 one-hot GEMM over precomputed one-hot operands, or the
+// CUDA-core kernel (PLSE_TC=0) over the colour rows.  upper: A == B, only tiles on or above the diagonal.
+void sim_block(plse_ctx* c, const uint8_t* hA, const uint8_t* A, int na, const uint8_t* hB, const uint8_t* B, int nb,
+               uint16_t* D, int ldd, int upper) {
+    if (!c->use_tc) {
+        c->launched(launch_hamming(A, na, B, nb, c->nv, c->nvpad, D, ldd, c->st, upper));
+        return;
+    }
+    c->launched(launch_similarity_tc(hA, na, hB, nb, c->kpad, c->nv, D, ldd, c->st, upper));
+    c->ctr.k3_ops += upper ? (double)na * (na - 1) * c->kpad : 2.0 * na * (double)nb * c->kpad;
+}
+
+void onehot(plse_ctx* c, const uint8_t* X, int rows, uint8_t* H) {
+    if (c->use_tc) c->launched(launch_onehot(X, rows, c->nvpad, c->d_colvert, c->d_dom, c->kdom, c->kpad, H, c->st));
+}
+
+// the full members x members matrix (population.hpp:76-87)
+void full_distances(plse_ctx* c) {
+    const int p = c->prm.p;
+    onehot(c, c->d_members, p, c->d_hA);
+    sim_block(c, c->d_hA, c->d_members, p, c->d_hA, c->d_members, p, c->d_dist, p, 0);
+    c->onehot_valid = false;  // d_hB does not hold onehot(improved)
+}
+
+// migrant rows vs members | improved | migrants (the extra candidates of the next pool); needs the
+// one-hot operands of this generation's members and improved in d_hA / d_hB
+void migrant_distances(plse_ctx* c) {
+    const int p = c->prm.p, m = c->n_mig, ld = 2 * p + m;
+    if (!m) return;
+    onehot(c, c->d_migr, m, c->d_hM);
+    sim_block(c, c->d_hM, c->d_migr, m, c->d_hA, c->d_members, p, c->d_migd, ld, 0);
+    sim_block(c, c->d_hM, c->d_migr, m, c->d_hB, c->d_improved, p, c->d_migd + p, ld, 0);
+    sim_block(c, c->d_hM, c->d_migr, m, c->d_hM, c->d_migr, m, c->d_migd + 2 * p, ld, 0);
+}
+
+// population.hpp:41-61: cross = D(members, improved); fresh = D(improved, improved), upper triangle only
+// (the pool update reads fresh[min][max]); onehot(improved) is expanded once for both
+void cross_distances(plse_ctx* c) {
+    const int p = c->prm.p;
+    onehot(c, c->d_members, p, c->d_hA);
+    onehot(c, c->d_improved, p, c->d_hB);
+    sim_block(c, c->d_hA, c->d_members, p, c->d_hB, c->d_improved, p, c->d_cross, p, 0);
+    sim_block(c, c->d_hB, c->d_improved, p, c->d_hB, c->d_improved, p, c->d_fresh, p, 1);
+    c->onehot_valid = true;
+    migrant_distances(c);
+}
+
+// pool-position scratch for 2p + m candidates (m = staged migrants)
+void ensure_pool_scratch(plse_ctx* c, int m) {
+    const int P = 2 * c->prm.p + m;
+    if (P <= c->pool_cap) return;
+    for (void* b : {(void*)c->ps.keys0, (void*)c->ps.keys1, (void*)c->ps.order, (void*)c->ps.legal,
+                    (void*)c->ps.admitted})
+        if (b) CK(cudaFree(b));
+    c->ps.keys0 = dalloc<uint64_t>(P);
+    c->ps.keys1 = dalloc<uint64_t>(P);
+    c->ps.order = dalloc<int32_t>(P);
+    c->ps.legal = dalloc<uint8_t>(P);
+    c->ps.admitted = dalloc<uint8_t>(P);
+    c->pool_cap = P;
+}
+
+// the f / c of a population buffer, read back from the device
+void fetch_fc(plse_ctx* c, int which, std::vector<int32_t>& f, std::vector<int32_t>& cc) {
+    const int p = c->prm.p;
+    f.resize(p);
+    cc.resize(p);
+    const int32_t* df = which == PLSE_MEMBERS ? c->d_mf : c->d_best_f;
+    const int32_t* dc = which == PLSE_MEMBERS ? c->d_mc : c->d_imc;
+    CK(cudaMemcpyAsync(f.data(), df, 4 * p, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(cc.data(), dc, 4 * p, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
 }
 
-// K3: D = hamming(A rows, B rows) -- tcgen05 one-hot GEMM, or the CUDA-core kernel (PLSE_TC=0)
-struct PhaseTimer {
-    plse_ctx* c;
-    double* out;
-    PhaseTimer(plse_ctx* c_, double* o) : c(c_), out(o) { CK(cudaEventRecord(c->ev0, c->st)); }
-    void stop() {
-        CK(cudaEventRecord(c->ev1, c->st));
-        CK(cudaEventSynchronize(c->ev1));
+// phase timers: PH_DIST, PH_UPDATE, PH_OFFSPRING
+enum { PH_DIST = 0, PH_UPDATE = 1, PH_OFFSPRING = 2 };
+void phase_begin(plse_ctx* c, int ph) { CK(cudaEventRecord(c->ph_ev[ph][0], c->st)); }
+void phase_end(plse_ctx* c, int ph) {
+    CK(cudaEventRecord(c->ph_ev[ph][1], c->st));
+    c->ph_pending[ph] = true;
+}
+void resolve_phase_timers(plse_ctx* c) {
+    double* out[3] = {&c->ctr.distances_ms, &c->ctr.update_ms, &c->ctr.offspring_ms};
+    for (int ph = 0; ph < 3; ++ph) {
+        if (!c->ph_pending[ph]) continue;
+        CK(cudaEventSynchronize(c->ph_ev[ph][1]));
         float ms = 0;
-        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-        *out = ms;
+        CK(cudaEventElapsedTime(&ms, c->ph_ev[ph][0], c->ph_ev[ph][1]));
+        *out[ph] = ms;
+        c->ph_pending[ph] = false;
     }
-};
-
-void hamming(plse_ctx* c, const uint8_t* A, const uint8_t* B, uint16_t* D) {
-    const int p = c->prm.p;
-    if (!c->use_tc) {
-        c->launched(launch_hamming(A, p, B, p, c->nv, c->nvpad, D, p, c->st));
-        return;
-    }
-    c->launched(launch_onehot(A, p, c->nvpad, c->d_colvert, c->d_dom, c->kdom, c->kpad, c->d_hA, c->st));
-    const uint8_t* hb = c->d_hA;
-    if (B != A) {
-        c->launched(launch_onehot(B, p, c->nvpad, c->d_colvert, c->d_dom, c->kdom, c->kpad, c->d_hB, c->st));
-        hb = c->d_hB;
-    }
-    c->launched(launch_similarity_tc(c->d_hA, p, hb, p, c->kpad, c->nv, D, p, c->st));
-    c->ctr.k3_ops += 2.0 * p * (double)p * c->kpad;
 }
 
 void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_ctx** out) {
@@ -408,22 +485,34 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->d_tmpc = dalloc<int32_t>(p);
     c->d_iters = dalloc<int64_t>(p);
     c->d_bytes = dalloc<unsigned long long>(p);
-    c->h_mf.assign(p, nv);
-    c->h_mc.assign(p, 0);
-    c->h_if.assign(p, nv);
-    c->h_ic.assign(p, 0);
-    c->h_iters.assign(p, 0);
+    c->d_imc = dalloc<int32_t>(p);
+    c->d_nf = dalloc<int32_t>(p);
+    c->d_nc = dalloc<int32_t>(p);
+    {  // members start uncoloured (f = |V|, c = 0) until initialised or uploaded
+        std::vector<int32_t> fv(p, nv);
+        CK(cudaMemcpy(c->d_mf, fv.data(), 4 * p, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_best_f, fv.data(), 4 * p, cudaMemcpyHostToDevice));
+        CK(cudaMemset(c->d_mc, 0, 4 * p));
+        CK(cudaMemset(c->d_imc, 0, 4 * p));
+        CK(cudaMemset(c->d_iters, 0, 8 * p));
+    }
     c->excl_words = (int)((p + 31) / 32);
     c->d_excl = dalloc<uint32_t>(p * c->excl_words);
     CK(cudaMemset(c->d_excl, 0, 4 * p * c->excl_words));
     c->d_partner = dalloc<int32_t>(p);
-    c->d_order = dalloc<int32_t>(2 * p);
-    c->d_sel = dalloc<int32_t>(p);
-    c->d_nsel = dalloc<int32_t>(1);
-    c->d_mts = dalloc<int32_t>(1024);
-    c->d_conf = dalloc<uint32_t>(1024 * 32);
-    c->d_legal = dalloc<uint8_t>(2 * p);
-    c->d_admitted = dalloc<uint8_t>(2 * p);
+    ensure_pool_scratch(c, 0);
+    c->ps.sel = dalloc<int32_t>(p);
+    c->ps.nsel = dalloc<int32_t>(1);
+    c->ps.slots = dalloc<int32_t>(p);
+    c->ps.info = dalloc<int32_t>(2);
+    c->ps.ok = dalloc<uint8_t>(1024);
+    c->ps.conf = dalloc<uint32_t>(1024 * 32);
+    CK(prepare_pool_update());
+    c->d_sum = dalloc<ImproveSummary>(1);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_sum), sizeof(ImproveSummary), cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_info), 2 * sizeof(int32_t), cudaHostAllocDefault));
+    for (auto& pr : c->ph_ev)
+        for (cudaEvent_t& e : pr) CK(cudaEventCreate(&e));
     c->d_work = dalloc<int>(1);
 
     // ---- improve launch shape: maximise resident individuals per SM
@@ -528,8 +617,9 @@ void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) 
     }
     uint8_t* dst = c->colors(which);
     CK(cudaMemcpyAsync(dst, stage, (size_t)p * nvpad, cudaMemcpyHostToDevice, c->st));
-    if (which == PLSE_MEMBERS) eval_into(c, dst, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
-    if (which == PLSE_IMPROVED) eval_into(c, dst, c->h_if, c->h_ic, c->d_tmpf, c->d_tmpc);
+    if (which == PLSE_MEMBERS) eval_into(c, dst, c->d_mf, c->d_mc);
+    if (which == PLSE_IMPROVED) eval_into(c, dst, c->d_best_f, c->d_imc);
+    c->onehot_valid = false;
     CK(cudaStreamSynchronize(c->st));
 }
 
@@ -613,27 +703,18 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
 
 void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t* best_idx) {
     const int p = c->prm.p;
-    std::vector<unsigned long long> bytes(p);
-    c->h_if.resize(p);
-    c->h_iters.resize(p);
-    CK(cudaMemcpyAsync(c->h_if.data(), c->d_best_f, 4 * p, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(c->h_iters.data(), c->d_iters, 8 * p, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(bytes.data(), c->d_bytes, 8 * p, cudaMemcpyDeviceToHost, c->st));
+    // engine.hpp:207-217 on the device: total iterations, lowest-index argmin of f (strict <); the
+    // improved individuals are legal (repair / PLITS' final repair), so their c is 0
+    CK(cudaMemsetAsync(c->d_imc, 0, 4 * p, c->st));
+    c->launched(launch_improve_reduce(c->d_best_f, c->d_iters, c->d_bytes, p, c->d_sum, c->st));
+    CK(cudaMemcpyAsync(c->h_sum, c->d_sum, sizeof(ImproveSummary), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    c->h_ic.assign(p, 0);
-    int64_t tot = 0;
-    double by = 0;
-    int bf = c->nv + 1, bi = -1;
-    for (int i = 0; i < p; ++i) {
-        tot += c->h_iters[i];
-        by += (double)bytes[i];
-        if (c->h_if[i] < bf) {  // engine.hpp:212-217: strict <, lowest index wins
-            bf = c->h_if[i];
-            bi = i;
-        }
-    }
+    c->onehot_valid = false;
+    const int64_t tot = c->h_sum->iters;
+    const double by = (double)c->h_sum->bytes;
+    const int bf = c->h_sum->best_f, bi = c->h_sum->best_idx;
     if (c->d_prof && std::getenv("PLSE_PROFILE") && c->ref_ties && c->plits) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));
@@ -682,80 +763,36 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
     if (best_idx) *best_idx = bi;
 }
 
-// population.hpp:103-183 on the device: host sorts the 2p pool keys, the
-// admission chain runs in blocks of 1024 candidates (k_pool_check/resolve),
-// then next_dist and the next members are gathered on the device.
+// population.hpp:103-183 on the device (pool.cu): key sort, admission chain, shortfall fill and the
+// gathers are enqueued on the stream with no host round trip; the UpdateInfo outputs are read back only
+// when the caller asks for them.  Staged migrants (island exchange) join the pool as ids 2p..2p+m-1.
 void update_impl(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* slots_out) {
-    const int p = c->prm.p, P2 = 2 * p;
-    const double thr = c->nv / c->prm.gamma;
-    std::vector<int> f(P2), legal(P2);
-    for (int i = 0; i < p; ++i) {
-        f[i] = c->h_mf[i];
-        legal[i] = c->h_mc[i] == 0;
-        f[p + i] = c->h_if[i];
-        legal[p + i] = c->h_ic[i] == 0;
-    }
-    std::vector<int32_t> order(P2);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int a, int b) {
-        return std::make_tuple(legal[a] ? 0 : 1, f[a], a) < std::make_tuple(legal[b] ? 0 : 1, f[b], b);
-    });
-    std::vector<uint8_t> leg8(P2);
-    for (int i = 0; i < P2; ++i) leg8[i] = (uint8_t)legal[i];
-    CK(cudaMemcpyAsync(c->d_order, order.data(), 4 * P2, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_legal, leg8.data(), P2, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemsetAsync(c->d_admitted, 0, P2, c->st));
-    const int one = 1;
-    const uint8_t yes = 1;
-    CK(cudaMemcpyAsync(c->d_sel, &order[0], 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_nsel, &one, 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_admitted, &yes, 1, cudaMemcpyHostToDevice, c->st));
-    PoolView pv{p, c->d_dist, c->d_cross, c->d_fresh};
-    int ns = 1;
-    const int BLK = 1024;
-    for (int lo = 1; lo < P2 && ns < p; lo += BLK) {
-        const int bn = std::min(BLK, P2 - lo);
-        const int cw = (bn + 31) / 32;
-        c->launched(launch_pool_block_check(pv, c->d_order, lo, bn, c->d_sel, ns, thr, c->d_legal, c->d_mts,
-                                            c->d_conf, cw, c->st));
-        c->launched(launch_pool_block_resolve(c->d_order, lo, bn, c->d_mts, c->d_conf, cw, thr, c->d_legal, c->d_sel,
-                                              c->d_nsel, p, c->d_admitted, c->st));
-        CK(cudaMemcpyAsync(&ns, c->d_nsel, 4, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-    }
-    std::vector<int32_t> sel(p);
-    CK(cudaMemcpyAsync(sel.data(), c->d_sel, 4 * ns, cudaMemcpyDeviceToHost, c->st));
-    std::vector<uint8_t> adm(P2);
-    CK(cudaMemcpyAsync(adm.data(), c->d_admitted, P2, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    int nsf = 0;
-    if (ns < p) {
-        // shortfall rule (population.hpp:157-160): skipped candidates in pool order
-        for (int pos = 1; pos < P2 && ns < p; ++pos) {
-            if (adm[pos]) continue;
-            if (slots_out) slots_out[nsf] = ns;
-            ++nsf;
-            sel[ns++] = order[pos];
-        }
-        CK(cudaMemcpyAsync(c->d_sel, sel.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
-    }
-    c->launched(launch_pool_gather(pv, c->d_sel, c->d_dnext, c->d_members, c->d_improved, c->d_next, c->nvpad, c->st),
-                2);
+    const int p = c->prm.p, m = c->n_mig;
+    ensure_pool_scratch(c, m);
+    const double thr = c->nv / c->prm.gamma;  // population.hpp:74 spacing threshold, compared as double
+    const int dthr = (int)std::floor(thr);    // integer d > thr  <=>  d > floor(thr)
+    PoolView pv{p, m, c->d_dist, c->d_cross, c->d_fresh, c->d_migd};
+    PoolFC fc{p, m, c->d_mf, c->d_mc, c->d_best_f, c->d_imc, c->d_gf, c->d_gc};
+    int64_t nl = 0;
+    CK(launch_pool_update(pv, fc, c->ps, c->nv, dthr, c->d_members, c->d_improved, c->d_migr, c->d_next, c->d_dnext,
+                          c->d_nf, c->d_nc, c->nvpad, c->st, &nl));
+    c->ctr.kernel_launches += nl;
     std::swap(c->d_members, c->d_next);
     std::swap(c->d_dist, c->d_dnext);
-    std::vector<int32_t> nf(p), nc(p);
-    for (int i = 0; i < p; ++i) {
-        const int id = sel[i];
-        nf[i] = f[id];
-        nc[i] = id < p ? c->h_mc[id] : c->h_ic[id - p];
+    std::swap(c->d_mf, c->d_nf);
+    std::swap(c->d_mc, c->d_nc);
+    c->n_mig = 0;
+    c->onehot_valid = false;
+    if (pool_best_f || n_shortfall || slots_out) {
+        CK(cudaMemcpyAsync(c->h_info, c->ps.info, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (pool_best_f) *pool_best_f = c->h_info[0];
+        if (n_shortfall) *n_shortfall = c->h_info[1];
+        if (slots_out && c->h_info[1] > 0) {
+            CK(cudaMemcpyAsync(slots_out, c->ps.slots, 4 * (size_t)c->h_info[1], cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        }
     }
-    c->h_mf = nf;
-    c->h_mc = nc;
-    CK(cudaMemcpyAsync(c->d_mf, c->h_mf.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_mc, c->h_mc.data(), 4 * p, cudaMemcpyHostToDevice, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    if (pool_best_f) *pool_best_f = f[order[0]];
-    if (n_shortfall) *n_shortfall = nsf;
 }
 
 void offspring_impl(plse_ctx* c, uint64_t gen) {
@@ -768,14 +805,13 @@ void offspring_impl(plse_ctx* c, uint64_t gen) {
         c->launched(launch_crossover(c->d_members, c->d_dist, c->d_partner, p, c->nv, c->nvpad, c->prm.crossover,
                                      c->prm.beta, c->prm.master_seed, c->stream_base(gen), c->d_offspring, c->st));
     }
-    CK(cudaStreamSynchronize(c->st));
 }
 
 void init_impl(plse_ctx* c) {
     c->launched(launch_init_population(c->pop_graph(), c->prm.p, c->prm.master_seed, (uint64_t)c->prm.offset,
                                        c->d_members, c->st));
-    eval_into(c, c->d_members, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
-    hamming(c, c->d_members, c->d_members, c->d_dist);
+    eval_into(c, c->d_members, c->d_mf, c->d_mc);
+    full_distances(c);
     CK(cudaStreamSynchronize(c->st));
 }
 
@@ -907,6 +943,11 @@ int plse_get_dist(plse_ctx* c, int32_t which, int32_t* host) {
         std::vector<uint16_t> tmp(pp);
         CK(cudaMemcpyAsync(tmp.data(), c->distbuf(which), 2 * pp, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
+        const int p = c->prm.p;
+        if (which == PLSE_FRESH) {  // the device keeps fresh's upper triangle; mirror it (population.hpp:84-86)
+            for (int i = 0; i < p; ++i)
+                for (int j = 0; j < i; ++j) tmp[(size_t)i * p + j] = tmp[(size_t)j * p + i];
+        }
         for (size_t q = 0; q < pp; ++q) host[q] = tmp[q];
     });
 }
@@ -933,18 +974,23 @@ int plse_get_stats(plse_ctx* c, int32_t which, int32_t* f, int32_t* cc, int64_t*
         CK(cudaSetDevice(c->device));
         const int p = c->prm.p;
         std::vector<int32_t> ff, cv;
-        if (which == PLSE_MEMBERS) {
-            ff = c->h_mf;
-            cv = c->h_mc;
-        } else if (which == PLSE_IMPROVED) {
-            ff = c->h_if;
-            cv = c->h_ic;
+        if (which == PLSE_MEMBERS || which == PLSE_IMPROVED) {
+            fetch_fc(c, which, ff, cv);
         } else {
-            eval_into(c, c->colors(which), ff, cv, c->d_tmpf, c->d_tmpc);
+            c->colors(which);  // validates `which`
+            eval_into(c, c->colors(which), c->d_tmpf, c->d_tmpc);
+            ff.resize(p);
+            cv.resize(p);
+            CK(cudaMemcpyAsync(ff.data(), c->d_tmpf, 4 * p, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaMemcpyAsync(cv.data(), c->d_tmpc, 4 * p, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
         }
         if (f) std::memcpy(f, ff.data(), 4 * p);
         if (cc) std::memcpy(cc, cv.data(), 4 * p);
-        if (iters) std::memcpy(iters, c->h_iters.data(), 8 * p);
+        if (iters) {
+            CK(cudaMemcpyAsync(iters, c->d_iters, 8 * p, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        }
     });
 }
 
@@ -959,8 +1005,11 @@ int plse_get_partners(plse_ctx* c, int32_t* host) {
 
 int plse_get_counters(plse_ctx* c, plse_counters* out) {
     if (!c || !out) return finish(c, PLSE_ERR_INVALID, "null argument");
-    *out = c->ctr;
-    return PLSE_OK;
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        resolve_phase_timers(c);
+        *out = c->ctr;
+    });
 }
 
 int plse_timer_start(plse_ctx* c) {
@@ -1006,7 +1055,7 @@ int plse_full_distances(plse_ctx* c) {
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
-        hamming(c, c->d_members, c->d_members, c->d_dist);
+        full_distances(c);
         CK(cudaStreamSynchronize(c->st));
     });
 }
@@ -1026,10 +1075,9 @@ int plse_distances(plse_ctx* c) {
         CK(cudaSetDevice(c->device));
         c->ctr.k3_ops = 0;
         c->ctr.k3_tensor_cores = c->use_tc ? 1 : 0;
-        PhaseTimer t(c, &c->ctr.distances_ms);
-        hamming(c, c->d_members, c->d_improved, c->d_cross);
-        hamming(c, c->d_improved, c->d_improved, c->d_fresh);
-        t.stop();
+        phase_begin(c, PH_DIST);
+        cross_distances(c);
+        phase_end(c, PH_DIST);
     });
 }
 
@@ -1037,9 +1085,9 @@ int plse_update(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
-        PhaseTimer t(c, &c->ctr.update_ms);
+        phase_begin(c, PH_UPDATE);
         update_impl(c, pool_best_f, n_shortfall, shortfall_slots);
-        t.stop();
+        phase_end(c, PH_UPDATE);
     });
 }
 
@@ -1056,9 +1104,9 @@ int plse_offspring(plse_ctx* c, uint64_t generation) {
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
-        PhaseTimer t(c, &c->ctr.offspring_ms);
+        phase_begin(c, PH_OFFSPRING);
         offspring_impl(c, generation);
-        t.stop();
+        phase_end(c, PH_OFFSPRING);
     });
 }
 
@@ -1092,17 +1140,16 @@ int plse_export_elites(plse_ctx* c, int32_t n_elite, void* dev_out, int32_t* f_o
         CK(cudaSetDevice(c->device));
         const int p = c->prm.p;
         if (n_elite < 0 || n_elite > p || (n_elite && !dev_out)) throw std::invalid_argument("bad elite count");
-        std::vector<int> idx(p);
-        std::iota(idx.begin(), idx.end(), 0);
-        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
-            return std::make_tuple(c->h_mc[a] ? 1 : 0, c->h_mf[a]) < std::make_tuple(c->h_mc[b] ? 1 : 0, c->h_mf[b]);
-        });
-        for (int e = 0; e < n_elite; ++e) {
-            CK(cudaMemcpyAsync(static_cast<uint8_t*>(dev_out) + (size_t)e * c->nvpad,
-                               c->d_members + (size_t)idx[e] * c->nvpad, c->nvpad, cudaMemcpyDeviceToDevice, c->st));
-            if (f_out) f_out[e] = c->h_mf[idx[e]];
+        // members in (illegal, f, slot) order on the device; the rows are written on the context's stream
+        int32_t* d_f = nullptr;
+        if (f_out && n_elite) d_f = c->d_tmpf;
+        CK(launch_export_elites(c->d_mf, c->d_mc, c->nv, p, n_elite, c->d_members, c->nvpad, c->ps,
+                                static_cast<uint8_t*>(dev_out), d_f, c->st));
+        c->ctr.kernel_launches += 2 + (n_elite > 0);
+        if (d_f) {
+            CK(cudaMemcpyAsync(f_out, d_f, 4 * (size_t)n_elite, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
         }
-        CK(cudaStreamSynchronize(c->st));
     });
 }
 
@@ -1111,21 +1158,31 @@ int plse_import_migrants(plse_ctx* c, int32_t n_in, const void* dev_in) {
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         const int p = c->prm.p;
-        if (n_in < 0 || n_in > p || (n_in && !dev_in)) throw std::invalid_argument("bad migrant count");
-        std::vector<int> idx(p);
-        std::iota(idx.begin(), idx.end(), 0);
-        // worst first: illegal, then highest f, then highest index
-        std::sort(idx.begin(), idx.end(), [&](int a, int b) {
-            return std::make_tuple(c->h_mc[a] ? 1 : 0, c->h_mf[a], a) > std::make_tuple(c->h_mc[b] ? 1 : 0, c->h_mf[b], b);
-        });
-        for (int e = 0; e < n_in; ++e)
-            CK(cudaMemcpyAsync(c->d_members + (size_t)idx[e] * c->nvpad,
-                               static_cast<const uint8_t*>(dev_in) + (size_t)e * c->nvpad, c->nvpad,
-                               cudaMemcpyDeviceToDevice, c->st));
-        eval_into(c, c->d_members, c->h_mf, c->h_mc, c->d_mf, c->d_mc);
-        hamming(c, c->d_members, c->d_members, c->d_dist);
-        CK(cudaStreamSynchronize(c->st));
+        if (n_in < 0 || n_in > 4 * p || (n_in && !dev_in)) throw std::invalid_argument("bad migrant count");
+        if (n_in > c->mig_cap) {
+            for (void* b : {(void*)c->d_migr, (void*)c->d_gf, (void*)c->d_gc, (void*)c->d_migd, (void*)c->d_hM})
+                if (b) CK(cudaFree(b));
+            c->d_migr = dalloc<uint8_t>((size_t)n_in * c->nvpad);
+            c->d_gf = dalloc<int32_t>(n_in);
+            c->d_gc = dalloc<int32_t>(n_in);
+            c->d_migd = dalloc<uint16_t>((size_t)n_in * (2 * p + n_in));
+            if (c->use_tc) c->d_hM = dalloc<uint8_t>((size_t)n_in * c->kpad);
+            c->mig_cap = n_in;
+        }
+        c->n_mig = n_in;
+        if (!n_in) return;
+        CK(cudaMemcpyAsync(c->d_migr, dev_in, (size_t)n_in * c->nvpad, cudaMemcpyDeviceToDevice, c->st));
+        eval_into(c, c->d_migr, c->d_gf, c->d_gc, n_in);
+        // after this generation's plse_distances the one-hot operands are still in place: the migrant
+        // block is computed now; otherwise plse_distances computes it
+        if (c->onehot_valid || !c->use_tc) migrant_distances(c);
     });
+}
+
+int plse_stream(plse_ctx* c, void** stream_out) {
+    if (!c || !stream_out) return finish(c, PLSE_ERR_INVALID, "null argument");
+    *stream_out = c->st;
+    return PLSE_OK;
 }
 
 // engine.hpp:114-262 (Partial-MPMA) on one device.
@@ -1181,12 +1238,16 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
             for (int v = 0; v < g.nv; ++v) best[v] = row[v];
         };
         init_impl(c);
-        for (int i = 0; i < p; ++i)
-            if (c->h_mc[i] == 0 && c->h_mf[i] < res->best_f) {
-                res->best_f = c->h_mf[i];
-                fetch_row(c->d_members, i);
-                ttb = elapsed();
-            }
+        {
+            std::vector<int32_t> mf, mc;
+            fetch_fc(c, PLSE_MEMBERS, mf, mc);
+            for (int i = 0; i < p; ++i)
+                if (mc[i] == 0 && mf[i] < res->best_f) {
+                    res->best_f = mf[i];
+                    fetch_row(c->d_members, i);
+                    ttb = elapsed();
+                }
+        }
         if (opt_stop && is_opt(res->best_f)) {
             finalize(PLSE_STOP_OPTIMAL);
             return;
@@ -1210,8 +1271,10 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
             plse_generation_stats st{};
             st.generation = gen;
             st.best_f = res->best_f;
+            std::vector<int32_t> mf, mc;
+            fetch_fc(c, PLSE_MEMBERS, mf, mc);
             double fs = 0;
-            for (int i = 0; i < p; ++i) fs += c->h_mf[i];
+            for (int i = 0; i < p; ++i) fs += mf[i];
             st.mean_f = fs / p;
             if (!c->d_dsum) c->d_dsum = dalloc<unsigned long long>(1);
             CK(cudaMemsetAsync(c->d_dsum, 0, 8, c->st));
@@ -1252,10 +1315,9 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
                                    : PLSE_STOP_TARGET);
                 return;
             }
-            hamming(c, c->d_members, c->d_improved, c->d_cross);
-            hamming(c, c->d_improved, c->d_improved, c->d_fresh);
-            int32_t pbf = 0, nsf = 0;
-            update_impl(c, &pbf, &nsf, nullptr);
+            cross_distances(c);
+            int32_t nsf = 0;
+            update_impl(c, nullptr, cb ? &nsf : nullptr, nullptr);
             if (c->prm.exclusion == PLSE_E_GENERATION) CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
             offspring_impl(c, (uint64_t)gen);
             emit_stats(gen, nsf);

@@ -230,15 +230,16 @@ cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, s
 
 // ---- distances (K3)
 // D[i][j] = #{v : A_i[v] != B_j[v]} for u8 rows with stride nvpad (pad bytes equal)
+// upper != 0 (A == B, square): tiles strictly below the diagonal are skipped (the consumer reads [min][max])
 cudaError_t launch_hamming(const uint8_t* A, int na, const uint8_t* B, int nb, int nv, int nvpad, uint16_t* D,
-                           int ldd, cudaStream_t st);
+                           int ldd, cudaStream_t st, int upper = 0);
 
 // K3 on tcgen05 (similarity_tc.cu): one-hot expansion + i8 UMMA GEMM, D = |V| - A.B^T
 cudaError_t launch_onehot(const uint8_t* X, int rows, int nvpad, const uint16_t* col_vert, const uint8_t* col_color,
                           int K, int Kpad, uint8_t* H, cudaStream_t st);
 cudaError_t prepare_similarity_tc();
 cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, int N, int Kpad, int nv, uint16_t* D,
-                                 int ldd, cudaStream_t st);
+                                 int ldd, cudaStream_t st, int upper = 0);
 
 // ---- population kernels (population.cu)
 struct PopGraph {
@@ -260,23 +261,39 @@ cudaError_t launch_match(const uint16_t* dist, int p, int matching, int exclusio
 cudaError_t launch_crossover(const uint8_t* members, const uint16_t* dist, const int32_t* partner, int p, int nv,
                              int nvpad, int mode, double beta, uint64_t master, uint64_t stream_base,
                              uint8_t* offspring, cudaStream_t st);
-// pool update helpers
+// ---- pool update (pool.cu): population.hpp:103-183 on the device
 struct PoolView {
-    int p;
-    const uint16_t* dist;   // members x members
+    int p, m;               // members = improved count, migrant count
+    const uint16_t* dist;   // members x members (full)
     const uint16_t* cross;  // members x improved
-    const uint16_t* fresh;  // improved x improved
+    const uint16_t* fresh;  // improved x improved, upper triangle (i <= j) valid
+    const uint16_t* migd;   // m x (2p + m): migrant vs members | improved | migrants
 };
-cudaError_t launch_pool_block_check(const PoolView& pv, const int32_t* order, int blk_lo, int blk_n,
-                                    const int32_t* selected, int n_selected, double thr, const uint8_t* legal,
-                                    int32_t* min_to_sel, uint32_t* conflict, int cwords, cudaStream_t st);
-cudaError_t launch_pool_block_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
-                                      const uint32_t* conflict, int cwords, double thr, const uint8_t* legal,
-                                      int32_t* selected, int32_t* n_selected, int p, uint8_t* admitted,
-                                      cudaStream_t st);
-cudaError_t launch_pool_gather(const PoolView& pv, const int32_t* sel, uint16_t* next_dist,
-                               const uint8_t* members, const uint8_t* improved, uint8_t* next_members, int nvpad,
-                               cudaStream_t st);
+struct PoolFC {             // f and c of every pool id
+    int p, m;
+    const int32_t *mf, *mc, *imf, *imc, *gf, *gc;
+};
+struct PoolScratch {
+    uint64_t *keys0, *keys1;
+    int32_t *order, *sel, *nsel, *slots, *info;  // info[0] = pool_best_f, info[1] = shortfall count
+    uint8_t *legal, *admitted, *ok;
+    uint32_t* conf;
+};
+struct ImproveSummary {
+    int64_t iters;
+    unsigned long long bytes;
+    int32_t best_f, best_idx;
+};
+cudaError_t prepare_pool_update();
+cudaError_t launch_pool_update(const PoolView& pv, const PoolFC& fc, const PoolScratch& w, int nv, int dthr,
+                               const uint8_t* members, const uint8_t* improved, const uint8_t* migrants,
+                               uint8_t* next_members, uint16_t* next_dist, int32_t* next_f, int32_t* next_c,
+                               int nvpad, cudaStream_t st, int64_t* launches);
+cudaError_t launch_improve_reduce(const int32_t* best_f, const int64_t* iters, const unsigned long long* bytes,
+                                  int p, ImproveSummary* out, cudaStream_t st);
+cudaError_t launch_export_elites(const int32_t* mf, const int32_t* mc, int nv, int p, int n_elite,
+                                 const uint8_t* members, int nvpad, const PoolScratch& w, uint8_t* out,
+                                 int32_t* fout, cudaStream_t st);
 cudaError_t launch_u16_to_i32(const uint16_t* in, int32_t* out, size_t count, cudaStream_t st);
 cudaError_t launch_i32_to_u16(const int32_t* in, uint16_t* out, size_t count, cudaStream_t st);
 cudaError_t launch_colors_u16_to_u8(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, cudaStream_t st);

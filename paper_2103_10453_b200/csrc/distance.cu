@@ -23,11 +23,13 @@ __device__ __forceinline__ uint32_t ndiff4(uint32_t a, uint32_t b) {
 }
 
 __global__ void __launch_bounds__(256) k_hamming(const uint8_t* __restrict__ A, int na, const uint8_t* __restrict__ B,
-                                                 int nb, int nwords, int nvpad, uint16_t* __restrict__ D, int ldd) {
+                                                 int nb, int nwords, int nvpad, uint16_t* __restrict__ D, int ldd,
+                                                 int upper) {
     __shared__ uint32_t As[kKw][kTile + 4];
     __shared__ uint32_t Bs[kKw][kTile + 4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int i0 = blockIdx.y * kTile, j0 = blockIdx.x * kTile;
+    if (upper && j0 + kTile <= i0) return;  // strictly below the diagonal: the consumer reads [min][max]
     uint32_t acc[8][8];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -78,10 +80,10 @@ __global__ void __launch_bounds__(256) k_hamming(const uint8_t* __restrict__ A, 
 }
 
 cudaError_t launch_hamming(const uint8_t* A, int na, const uint8_t* B, int nb, int nv, int nvpad, uint16_t* D,
-                           int ldd, cudaStream_t st) {
+                           int ldd, cudaStream_t st, int upper) {
     (void)nv;
     dim3 grid((nb + kTile - 1) / kTile, (na + kTile - 1) / kTile);
-    k_hamming<<<grid, 256, 0, st>>>(A, na, B, nb, nvpad / 4, nvpad, D, ldd);
+    k_hamming<<<grid, 256, 0, st>>>(A, na, B, nb, nvpad / 4, nvpad, D, ldd, upper);
     return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
-// population.cu -- K0 init, f/c evaluation, K4a pool update, K4b matching,
-// K4c crossover on sm_100a.  All integer / byte work (HBM-bound); the
+// population.cu -- K0 init, f/c evaluation, K4b matching, K4c crossover on
+// sm_100a (K4a pool update: pool.cu).  All integer / byte work (HBM-bound); the
 // sequential xoshiro streams of the reference are replayed exactly, one
 // thread per individual, so these phases are bit-exact with the reference.
 #include "common.cuh"
@@ -187,122 +187,6 @@ cudaError_t launch_crossover(const uint8_t* members, const uint16_t* dist, const
                              uint8_t* offspring, cudaStream_t st) {
     k_crossover<<<(p + 63) / 64, 64, 0, st>>>(members, dist, partner, p, nv, nvpad, mode, beta, master, stream_base,
                                              offspring);
-    return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------- K4a pool update
-// population.hpp:103-183.  Pool ids 0..p-1 are members, p..2p-1 improved.
-__device__ __forceinline__ uint32_t pool_dist(const PoolView& v, int a, int b) {
-    const int p = v.p;
-    if (a == b) return 0;
-    if (a < p && b < p) return v.dist[(size_t)a * p + b];
-    if (a >= p && b >= p) return v.fresh[(size_t)(a - p) * p + (b - p)];
-    return a < p ? v.cross[(size_t)a * p + (b - p)] : v.cross[(size_t)b * p + (a - p)];
-}
-
-// One CTA per block candidate: min distance to the already selected set, and the
-// candidate's conflict row (d <= |V|/gamma) against the later candidates of the block.
-__global__ void k_pool_check(const PoolView pv, const int32_t* order, int blk_lo, int blk_n, const int32_t* sel,
-                             int n_sel, double thr, const uint8_t* legal, int32_t* min_to_sel, uint32_t* conflict,
-                             int cwords) {
-    const int t = blockIdx.x;
-    const int c = order[blk_lo + t];
-    __shared__ uint32_t red[32];
-    if (!legal[c]) {
-        if (threadIdx.x == 0) min_to_sel[t] = 0;
-        for (int w = threadIdx.x; w < cwords; w += blockDim.x) conflict[(size_t)t * cwords + w] = 0;
-        return;
-    }
-    uint32_t md = 0xFFFFFFFFu;
-    for (int q = threadIdx.x; q < n_sel; q += blockDim.x) md = min(md, pool_dist(pv, c, sel[q]));
-    md = __reduce_min_sync(kFull, md);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = md;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        uint32_t x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0xFFFFFFFFu;
-        x = __reduce_min_sync(kFull, x);
-        if (threadIdx.x == 0) min_to_sel[t] = (int32_t)min(x, 0x7FFFFFFFu);
-    }
-    for (int base = 0; base < cwords * 32; base += blockDim.x) {
-        const int u = base + threadIdx.x;
-        bool hit = false;
-        if (u > t && u < blk_n) {
-            const int cu = order[blk_lo + u];
-            hit = legal[cu] && !((double)pool_dist(pv, c, cu) > thr);
-        }
-        const unsigned bal = __ballot_sync(kFull, hit);
-        if ((threadIdx.x & 31) == 0 && (u >> 5) < cwords) conflict[(size_t)t * cwords + (u >> 5)] = bal;
-    }
-}
-
-cudaError_t launch_pool_block_check(const PoolView& pv, const int32_t* order, int blk_lo, int blk_n,
-                                    const int32_t* selected, int n_selected, double thr, const uint8_t* legal,
-                                    int32_t* min_to_sel, uint32_t* conflict, int cwords, cudaStream_t st) {
-    if (blk_n <= 0) return cudaSuccess;
-    k_pool_check<<<blk_n, 256, 0, st>>>(pv, order, blk_lo, blk_n, selected, n_selected, thr, legal, min_to_sel,
-                                         conflict, cwords);
-    return cudaGetLastError();
-}
-
-// One warp walks the block in pool order (the reference's greedy, population.hpp:144-156).
-// Lane l keeps word l of the "blocked by an admitted in-block candidate" bitmask.
-__global__ void k_pool_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
-                               const uint32_t* conflict, int cwords, double thr, const uint8_t* legal, int32_t* sel,
-                               int32_t* n_sel_io, int p, uint8_t* admitted) {
-    const int lane = threadIdx.x;
-    int ns = *n_sel_io;
-    uint32_t blocked = 0;  // lane's word(s); cwords <= 32
-    for (int t = 0; t < blk_n && ns < p; ++t) {
-        const int c = order[blk_lo + t];
-        const uint32_t wbits = __shfl_sync(kFull, blocked, t >> 5);
-        const bool is_blocked = (wbits >> (t & 31)) & 1;
-        const bool ok = legal[c] && !is_blocked && ((double)min_to_sel[t] > thr);
-        if (ok) {
-            if (lane == 0) {
-                sel[ns] = c;
-                admitted[blk_lo + t] = 1;
-            }
-            ++ns;
-            if (lane < cwords) blocked |= conflict[(size_t)t * cwords + lane];
-        }
-    }
-    if (lane == 0) *n_sel_io = ns;
-}
-
-cudaError_t launch_pool_block_resolve(const int32_t* order, int blk_lo, int blk_n, const int32_t* min_to_sel,
-                                      const uint32_t* conflict, int cwords, double thr, const uint8_t* legal,
-                                      int32_t* selected, int32_t* n_selected, int p, uint8_t* admitted,
-                                      cudaStream_t st) {
-    if (blk_n <= 0) return cudaSuccess;
-    k_pool_resolve<<<1, 32, 0, st>>>(order, blk_lo, blk_n, min_to_sel, conflict, cwords, thr, legal, selected,
-                                     n_selected, p, admitted);
-    return cudaGetLastError();
-}
-
-// next_dist[i][j] = pool_dist(sel[i], sel[j]); next_members[i] = pool row sel[i]
-__global__ void k_pool_gather_dist(const PoolView pv, const int32_t* sel, uint16_t* next_dist) {
-    const int p = pv.p;
-    const int i = blockIdx.y;
-    const int a = sel[i];
-    for (int jj = blockIdx.x * blockDim.x + threadIdx.x; jj < p; jj += gridDim.x * blockDim.x)
-        next_dist[(size_t)i * p + jj] = (uint16_t)pool_dist(pv, a, sel[jj]);
-}
-
-__global__ void k_pool_gather_rows(const int32_t* sel, int p, const uint8_t* members, const uint8_t* improved,
-                                   uint8_t* next_members, int nvpad) {
-    const int i = blockIdx.x;
-    const int a = sel[i];
-    const uint4* src = reinterpret_cast<const uint4*>(a < p ? members + (size_t)a * nvpad
-                                                            : improved + (size_t)(a - p) * nvpad);
-    uint4* dst = reinterpret_cast<uint4*>(next_members + (size_t)i * nvpad);
-    for (int t = threadIdx.x; t < nvpad / 16; t += blockDim.x) dst[t] = src[t];
-}
-
-cudaError_t launch_pool_gather(const PoolView& pv, const int32_t* sel, uint16_t* next_dist, const uint8_t* members,
-                               const uint8_t* improved, uint8_t* next_members, int nvpad, cudaStream_t st) {
-    dim3 grid((pv.p + 255) / 256 < 8 ? (pv.p + 255) / 256 : 8, pv.p);
-    k_pool_gather_dist<<<grid, 256, 0, st>>>(pv, sel, next_dist);
-    k_pool_gather_rows<<<pv.p, 128, 0, st>>>(sel, pv.p, members, improved, next_members, nvpad);
     return cudaGetLastError();
 }
 

@@ -113,7 +113,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 // ---------------------------------------------------------------- GEMM
 __global__ void __launch_bounds__(128, 1)
     k_sim_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-             int num_kb, int nv, uint16_t* __restrict__ D, int ldd) {
+             int num_kb, int nv, uint16_t* __restrict__ D, int ldd, int upper) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(128, 1)
     const int lin = blockIdx.x, per_group = kTcGroupM * nt_n;
     const int first_m = (lin / per_group) * kTcGroupM, gm = min(nt_m - first_m, kTcGroupM);
     const int tile_m = first_m + (lin % per_group) % gm, tile_n = (lin % per_group) / gm;
+    // symmetric block (A == B): tiles strictly below the diagonal are skipped, the consumer reads [min][max]
+    if (upper && (tile_n + 1) * kTcBN <= tile_m * kTcBM) return;
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcStages), done = smem_u32(bars + 2 * kTcStages);
 
     if (threadIdx.x == 0) {
@@ -257,11 +259,11 @@ cudaError_t prepare_similarity_tc() {
 }
 
 cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, int N, int Kpad, int nv, uint16_t* D,
-                                 int ldd, cudaStream_t st) {
+                                 int ldd, cudaStream_t st, int upper) {
     CUtensorMap ma, mb;
     if (!make_map(&ma, HA, M, Kpad, kTcBM) || !make_map(&mb, HB, N, Kpad, kTcBN)) return cudaErrorInvalidValue;
     const int tiles = ((N + kTcBN - 1) / kTcBN) * ((M + kTcBM - 1) / kTcBM);
-    k_sim_tc<<<tiles, 128, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd);
+    k_sim_tc<<<tiles, 128, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd, upper);
     return cudaGetLastError();
 }
 

@@ -4,13 +4,16 @@ of the elite or migrant individuals over NVLink every generation block").
 
 One process per GPU.  Rank r of N evolves an island of p individuals with
 stream keys gen*p_total + r*p + i (p_total = N*p), so N = 1 is exactly the
-reference's single population.  Every `every` generations each rank exports
-its `n_elite` best members (ascending (illegal, f), lowest slot first), the
-ranks all-gather them (NCCL for CUDA tensors, gloo for CPU tensors), and each
-rank replaces its worst (N-1)*n_elite members -- descending (illegal, f, slot)
--- by the other ranks' elites in rank order, then recomputes its distance
-matrix.  The exchange is the only collective on the path; the improve phase
-and the population phases run locally.
+reference's single population.  Every `every` generations, after the improve
+phase, each rank exports its `n_elite` best members (ascending (illegal, f),
+lowest slot first), the ranks all-gather them (NCCL for CUDA tensors, gloo for
+CPU tensors), and each rank stages the other ranks' elites, in rank order, as
+extra candidates of its next pool: its update_population then
+ranks 2p + (N-1)*n_elite candidates (population.hpp:103-183 with pool ids
+2p.. for the migrants), so a migrant enters only if it is good and spaced
+like any other candidate.  The exchange is the only collective on the data
+path; it runs on the population's own CUDA stream (no host synchronisation
+for NCCL), and the improve phase and the population phases run locally.
 """
 from __future__ import annotations
 
@@ -24,11 +27,6 @@ import numpy as np
 def elite_order(f: np.ndarray, c: np.ndarray) -> np.ndarray:
     """Slots sorted best-first: (illegal, f) ascending, ties by slot (stable)."""
     return np.lexsort((np.arange(len(f)), f, (c != 0).astype(np.int64)))
-
-
-def victim_order(f: np.ndarray, c: np.ndarray) -> np.ndarray:
-    """Slots sorted worst-first: (illegal, f, slot) descending."""
-    return np.lexsort((np.arange(len(f)), f, (c != 0).astype(np.int64)))[::-1]
 
 
 def allgather_rows(mine, group=None):
@@ -49,42 +47,53 @@ def others(gathered, rank: int, world: int):
 
 
 class DeviceIsland:
-    """A DevicePopulation shard plus the NCCL elite exchange (used by bench.py)."""
+    """A DevicePopulation shard plus the elite exchange (used by bench.py and run_islands).
+
+    `migrate()` is called between the improve phase and update_population: export (device sort of the
+    members) -> all-gather -> stage the other ranks' elites as pool candidates.  Everything is ordered on
+    the population's CUDA stream: for NCCL the collective is issued with that stream current, so no host
+    synchronisation happens; for gloo the rows cross host memory."""
 
     def __init__(self, pop, n_elite: int, rank: int, world: int, group=None):
         import torch
+        import torch.distributed as dist
         self.pop, self.n_elite, self.rank, self.world, self.group = pop, n_elite, rank, world, group
         self.mine = torch.empty((n_elite, pop.row_bytes), dtype=torch.uint8, device="cuda")
+        self.gathered = torch.empty((world * n_elite, pop.row_bytes), dtype=torch.uint8, device="cuda")
+        self.rest = torch.empty(((world - 1) * n_elite, pop.row_bytes), dtype=torch.uint8, device="cuda")
+        self.nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
+        self.stream = torch.cuda.ExternalStream(pop.stream)
 
     def migrate(self) -> None:
         import torch
-        self.pop.export_elites(self.n_elite, self.mine.data_ptr())
-        torch.cuda.synchronize()
-        gathered = allgather_rows(self.mine, self.group)
-        torch.cuda.synchronize()
-        rest = others(gathered, self.rank, self.world).contiguous()
-        torch.cuda.synchronize()  # the library reads `rest` on its own stream
-        self.pop.import_migrants(rest.shape[0], rest.data_ptr())
-
-
-def migrate_host(members: np.ndarray, f: np.ndarray, c: np.ndarray, incoming: np.ndarray) -> np.ndarray:
-    """Host restatement of plse_import_migrants: the worst len(incoming) slots take the migrants."""
-    out = members.copy()
-    victims = victim_order(f, c)[:len(incoming)]
-    for k, slot in enumerate(victims):
-        out[slot] = incoming[k]
-    return out
+        import torch.distributed as dist
+        if self.world < 2:
+            return
+        per = self.n_elite
+        with torch.cuda.stream(self.stream):
+            self.pop.export_elites(per, self.mine.data_ptr())
+            if self.nccl:
+                dist.all_gather_into_tensor(self.gathered, self.mine, group=self.group)
+            else:
+                host = torch.empty((self.world * per, self.mine.shape[1]), dtype=torch.uint8)
+                dist.all_gather_into_tensor(host, self.mine.cpu(), group=self.group)
+                self.gathered.copy_(host)
+            k = 0
+            for r in range(self.world):
+                if r != self.rank:
+                    self.rest[k * per:(k + 1) * per].copy_(self.gathered[r * per:(r + 1) * per])
+                    k += 1
+            self.pop.import_migrants(self.rest.shape[0], self.rest.data_ptr())
 
 
 def exchange_host(islands_members, islands_f, islands_c, n_elite: int):
-    """Sequential restatement of one exchange over all islands (the reference for the N>1 tests)."""
+    """Sequential restatement of one exchange over all islands (the reference for the N>1 tests): for
+    every rank, the other ranks' n_elite best members in rank order -- the extra pool candidates of its
+    next update."""
     world = len(islands_members)
     elites = [m[elite_order(f, c)[:n_elite]] for m, f, c in zip(islands_members, islands_f, islands_c)]
-    out = []
-    for r in range(world):
-        incoming = np.concatenate([elites[q] for q in range(world) if q != r]) if world > 1 else elites[0][:0]
-        out.append(migrate_host(islands_members[r], islands_f[r], islands_c[r], incoming))
-    return out
+    return [np.concatenate([elites[q] for q in range(world) if q != r]) if world > 1 else elites[0][:0]
+            for r in range(world)]
 
 
 def stream_coords(rank: int, world: int, p: int, total: Optional[int] = None):
@@ -125,8 +134,9 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
                 on_generation: Optional[Callable[[GenerationReport], None]] = None, keep_members: bool = False):
     """The north star's island model as a run: one process per GPU, each evolving a p-individual island
     of the Partial-MPMA generation (engine.hpp:114-262) with stream keys gen*p_total + rank*p + i; every
-    `migrate_every` generations the ranks all-gather their `n_elite` best members (NCCL for the nccl
-    backend, host tensors for gloo) and each replaces its worst by the others' elites; every generation
+    `migrate_every` generations, after the improve phase, the ranks all-gather their `n_elite` best
+    members (NCCL for the nccl backend, host tensors for gloo) and each ranks the others' elites as extra
+    candidates of its pool update (DeviceIsland); every generation
     the best f, the iteration count and the elapsed time are all-reduced so that every rank takes the
     same stop decision (optimal / time / iterations / generations / target, engine.hpp:215-236), and
     the rank holding a new global best broadcasts its colouring.  With torch.distributed not
@@ -202,9 +212,7 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
             return result(best_f, best, "optimal", 0, 0, ttb, members())
         pop.offspring = pop.members
         pop.reset_exclusion()
-        elites = gathered = None
-        if world > 1:
-            elites = torch.empty((n_elite, pop.row_bytes), dtype=torch.uint8, device="cuda")
+        isl = DeviceIsland(pop, n_elite, rank, world, group) if world > 1 else None
         total = 0
         gen = 0
         while True:
@@ -225,22 +233,13 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
                 if on_generation:
                     on_generation(GenerationReport(gen, best_f, git, total, el, False))
                 return result(best_f, best, reason, gen, total, ttb, members())
-            pop.compute_cross_distances()
-            pop.update_population()
-            if cfg.exclusion == P.GENERATION:
-                pop.reset_exclusion()
             migrated = world > 1 and migrate_every > 0 and gen % migrate_every == 0
             if migrated:
-                pop.export_elites(n_elite, elites.data_ptr())
-                torch.cuda.synchronize()
-                if coll == "cuda":
-                    gathered = allgather_rows(elites, group)
-                else:
-                    gathered = allgather_rows(elites.cpu(), group).to("cuda")
-                torch.cuda.synchronize()
-                rest = others(gathered, rank, world).contiguous()
-                torch.cuda.synchronize()  # the library reads `rest` on its own stream
-                pop.import_migrants(rest.shape[0], rest.data_ptr())
+                isl.migrate()
+            pop.compute_cross_distances()
+            pop.update_population(info=False)
+            if cfg.exclusion == P.GENERATION:
+                pop.reset_exclusion()
             pop.build_offspring(gen)
             if on_generation:
                 on_generation(GenerationReport(gen, best_f, git, total, el, migrated))

@@ -14,16 +14,20 @@ def island_init(orc, grid, p, seed, rank, world):
             "excl": np.zeros((p, p), np.uint8), "rank": rank, "world": world, "p": p}
 
 
-def island_improve_update(orc, grid, st, seed, gen, budget):
+def island_improve(orc, grid, st, seed, gen, budget):
     p, world, rank = st["p"], st["world"], st["rank"]
     g = orc.preprocess(grid)
     stop_f = 1 if g.l == 1 else 0
-    imp = np.stack([orc.improve(grid, st["offspring"][i], orc.derive_seed(seed, 2, gen * p * world + rank * p + i),
-                                budget, stop_f=stop_f, tie=oracle.TIE_CANON)["best"] for i in range(p)])
+    return np.stack([orc.improve(grid, st["offspring"][i], orc.derive_seed(seed, 2, gen * p * world + rank * p + i),
+                                 budget, stop_f=stop_f, tie=oracle.TIE_CANON)["best"] for i in range(p)])
+
+
+def island_update(orc, grid, st, imp, migrants=None):
+    """population.hpp:103-183 with the migrants as extra pool candidates (ids 2p..)"""
     cr, fr = orc.cross_distances(st["members"], imp)
-    u = orc.update(grid, st["members"], st["dist"], imp, cr, fr)
+    u = orc.update(grid, st["members"], st["dist"], imp, cr, fr, migrants=migrants)
     st["members"], st["dist"] = u["members"], u["dist"]
-    return imp
+    return u
 
 
 def fc(orc, grid, members):
@@ -36,17 +40,19 @@ def island_offspring(orc, grid, st, seed, gen):
     st["offspring"], _ = orc.offspring_ex(grid, st["members"], st["dist"], st["excl"], seed, gen * p * world + rank * p)
 
 
-def simulate(orc, grid, p, world, seed, gens, budget, n_elite):
-    """all islands sequentially in one process"""
+def simulate(orc, grid, p, world, seed, gens, budget, n_elite, every=1):
+    """all islands sequentially in one process: improve, then (every `every` generations) the elite
+    exchange staged as pool candidates, then update and offspring"""
     sts = [island_init(orc, grid, p, seed, r, world) for r in range(world)]
     for gen in range(1, gens + 1):
-        for st in sts:
-            island_improve_update(orc, grid, st, seed, gen, budget)
-        fcs = [fc(orc, grid, st["members"]) for st in sts]
-        new = islands.exchange_host([st["members"] for st in sts], [x[0] for x in fcs], [x[1] for x in fcs], n_elite)
-        for st, m in zip(sts, new):
-            st["members"] = m
-            st["dist"] = orc.full_distances(m)
+        imps = [island_improve(orc, grid, st, seed, gen, budget) for st in sts]
+        incoming = [None] * world
+        if world > 1 and every > 0 and gen % every == 0:
+            fcs = [fc(orc, grid, st["members"]) for st in sts]
+            incoming = islands.exchange_host([st["members"] for st in sts], [x[0] for x in fcs],
+                                             [x[1] for x in fcs], n_elite)
+        for st, imp, inc in zip(sts, imps, incoming):
+            island_update(orc, grid, st, imp, inc)
         for st in sts:
             island_offspring(orc, grid, st, seed, gen)
     return [st["members"] for st in sts]

@@ -176,15 +176,22 @@ def test_two_device_islands_match_island_restatement(plse, orc):
     for gen in range(1, gens + 1):
         for pop in pops:
             pop.improve(gen)
-            pop.compute_cross_distances()
-            pop.update_population()
+        # the exchange after the improve phase: each island's best members become extra pool candidates
+        # of the other island's update (in the order distances-before / distances-after the import)
         bufs = [torch.empty((elites, rb), dtype=torch.uint8, device="cuda") for _ in pops]
         for pop, b in zip(pops, bufs):
             pop.export_elites(elites, b.data_ptr())
         torch.cuda.synchronize()
-        pops[0].import_migrants(elites, bufs[1].data_ptr())
-        pops[1].import_migrants(elites, bufs[0].data_ptr())
+        if gen % 2:
+            pops[0].import_migrants(elites, bufs[1].data_ptr())
+            pops[1].import_migrants(elites, bufs[0].data_ptr())
         for pop in pops:
+            pop.compute_cross_distances()
+        if not gen % 2:
+            pops[0].import_migrants(elites, bufs[1].data_ptr())
+            pops[1].import_migrants(elites, bufs[0].data_ptr())
+        for pop in pops:
+            pop.update_population()
             pop.build_offspring(gen)
     want = S.simulate(orc, grid, p, 2, seed, gens, budget, elites)
     for pop, w in zip(pops, want):

@@ -37,13 +37,14 @@ def _worker(rank, world, port, out_dir, cfg):
     grid = orc.generate_instance(cfg["n"], cfg["r"], cfg["s"])
     st = S.island_init(orc, grid, cfg["p"], cfg["seed"], rank, world)
     for gen in range(1, cfg["gens"] + 1):
-        S.island_improve_update(orc, grid, st, cfg["seed"], gen, cfg["budget"])
+        imp = S.island_improve(orc, grid, st, cfg["seed"], gen, cfg["budget"])
+        # the exchange: this island's best members (before its update) all-gathered; the others' elites
+        # become extra candidates of this island's pool
         f, c = S.fc(orc, grid, st["members"])
         mine = torch.from_numpy(st["members"][islands.elite_order(f, c)[:cfg["elites"]]].astype(np.int32))
         gathered = islands.allgather_rows(mine)
         incoming = islands.others(gathered, rank, world).numpy().astype(np.uint16)
-        st["members"] = islands.migrate_host(st["members"], f, c, incoming)
-        st["dist"] = orc.full_distances(st["members"])
+        S.island_update(orc, grid, st, imp, incoming)
         S.island_offspring(orc, grid, st, cfg["seed"], gen)
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), st["members"])
     dist.barrier()
@@ -77,12 +78,36 @@ def test_single_island_is_the_reference_population(orc):
     assert np.array_equal(a, b)
 
 
-def test_elite_and_victim_orders():
+def test_elite_order_and_exchange():
     from paper_2103_10453_b200 import islands
     f = np.array([5, 3, 3, 9, 1])
     c = np.array([0, 0, 0, 0, 2])
     assert islands.elite_order(f, c).tolist() == [1, 2, 0, 3, 4]
-    assert islands.victim_order(f, c).tolist() == [4, 3, 0, 2, 1]
+    m = [np.arange(10).reshape(5, 2) + 100 * r for r in range(3)]
+    inc = islands.exchange_host(m, [f] * 3, [c] * 3, 2)
+    assert [x[:, 0].tolist() for x in inc] == [[102, 104, 202, 204], [2, 4, 202, 204], [2, 4, 102, 104]]
+
+
+def test_update_with_migrants_extends_the_pool(orc):
+    """A migrant better than every pool member enters first; with none the update is the reference's."""
+    grid = orc.generate_instance(10, 0.5, 3)
+    p = 8
+    mem = orc.init_population(grid, p, 5)
+    dist = orc.full_distances(mem)
+    imp = np.stack([orc.improve(grid, mem[i], orc.derive_seed(5, 2, p + i), 300, tie=0)["best"] for i in range(p)])
+    cr, fr = orc.cross_distances(mem, imp)
+    base = orc.update(grid, mem, dist, imp, cr, fr)
+    same = orc.update(grid, mem, dist, imp, cr, fr, migrants=np.zeros((0, mem.shape[1]), np.uint16))
+    assert np.array_equal(base["members"], same["members"]) and np.array_equal(base["dist"], same["dist"])
+    best = orc.improve(grid, imp[0], orc.derive_seed(9, 2, 0), 5000, tie=0)["best"]
+    fb, _ = orc.eval(grid, best)
+    if fb < base["pool_best_f"]:
+        u = orc.update(grid, mem, dist, imp, cr, fr, migrants=best[None, :])
+        assert u["selected"][0] == 2 * p and np.array_equal(u["members"][0], best)
+        assert u["pool_best_f"] == fb
+    # distances of the new population stay consistent with its rows
+    u = orc.update(grid, mem, dist, imp, cr, fr, migrants=imp[:3][::-1].copy())
+    assert np.array_equal(u["dist"], orc.full_distances(u["members"]))
 
 
 def _reduce_worker(rank, world, port, out_dir):
