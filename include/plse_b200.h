@@ -209,6 +209,16 @@ int plse_offspring(plse_ctx* ctx, uint64_t generation);
 /* run individual idx of OFFSPRING through improve with a per-step trace (parity probe) */
 int plse_trace(plse_ctx* ctx, int32_t idx, uint64_t generation, int64_t max_steps, plse_step* out, int64_t* n_out);
 
+/* per-step state probe (the north star's "gamma tables ... tabu lists bit-exact per step"): run
+   individual idx of OFFSPRING through improve and, before each listed step j (ascending; j = 0 is the
+   post-repair state), dump gamma[v][k] (coloring.hpp:105-116; n_steps x |V| x (order+1)) and the live
+   tabu entries (v, k, until) on the reference's iteration clock (search_util.hpp:54-81; n_steps x tabu_cap
+   x 3, count per step in n_tabu_out).  n_dumped = probe points the search reached; cache_mismatch =
+   vertices whose tabu cache disagreed with the dense table (0 on a correct kernel).  Canonical PartialCol. */
+int plse_probe(plse_ctx* ctx, int32_t idx, uint64_t generation, int32_t n_steps, const int64_t* steps,
+               int32_t* gamma_out, int32_t tabu_cap, int32_t* tabu_out, int32_t* n_tabu_out, int32_t* n_dumped,
+               int32_t* cache_mismatch);
+
 /* ---- island exchange (multi-GPU): the driver moves the bytes (NCCL all-gather) */
 /* the n_elite best members ((illegal, f, slot) ascending) as u8 rows [n_elite * row_stride] into dev_out,
    written on the context's stream (plse_stream); f_out (host, optional) synchronises */

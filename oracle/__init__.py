@@ -53,6 +53,11 @@ class OrImproveStats(C.Structure):
                 ("alg_bytes", C.c_double)]
 
 
+class OrProbe(C.Structure):
+    _fields_ = [("n", C.c_int), ("steps", C.c_void_p), ("gamma", C.c_void_p), ("tabu", C.c_void_p),
+                ("n_tabu", C.c_void_p), ("dumped", C.c_void_p), ("cap", C.c_int)]
+
+
 class OrConfig(C.Structure):
     _fields_ = [("p", C.c_int32), ("alpha", C.c_double), ("gamma", C.c_double), ("beta", C.c_double),
                 ("phase1_iters", C.c_int64), ("crossover", C.c_int32), ("matching", C.c_int32),
@@ -143,7 +148,7 @@ class Oracle:
         L.or_preprocess.restype = C.c_void_p
         L.or_preprocess.argtypes = [C.c_int, u16p]
         L.or_graph_free.argtypes = [C.c_void_p]
-        for f in ("or_graph_nv", "or_graph_l", "or_graph_adj_len", "or_graph_dom_len"):
+        for f in ("or_graph_nv", "or_graph_l", "or_graph_adj_len", "or_graph_dom_len", "or_graph_order"):
             getattr(L, f).argtypes = [C.c_void_p]
         L.or_graph_export.argtypes = [C.c_void_p, i32p, i32p, i32p, i32p, i32p, u16p]
         L.or_eval.argtypes = [C.c_void_p, u16p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -153,6 +158,8 @@ class Oracle:
         L.or_enumerate_exact.argtypes = [C.c_void_p, C.POINTER(OrExact), u16p]
         L.or_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                C.c_int, C.POINTER(OrPlitsStats), C.c_void_p, C.c_int64]
+        L.or_improve_probe.argtypes = [C.c_void_p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int, C.c_int,
+                                       C.c_void_p]
         L.or_improve.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int,
                                  C.c_int, C.POINTER(OrImproveStats), C.c_void_p, C.c_int64]
         L.or_cross_distances.argtypes = [C.c_int, C.c_int, u16p, u16p, i32p, i32p]
@@ -233,6 +240,24 @@ class Oracle:
             m = min(trace_cap, st.iterations)
             res["trace"] = [{k: getattr(tr[i], k) for k, _ in OrStep._fields_} for i in range(m)]
         return res
+
+    def improve_probe(self, grid, colors, stream_seed, budget, steps, tabu_cap=4096, alpha=0.6, stop_f=0,
+                      tie=TIE_CANON):
+        """the gamma table and the live tabu entries (v, k, until) before each listed step of or_improve"""
+        h = self._h(grid)
+        nv, w = len(colors), self.lib.or_graph_order(h) + 1
+        steps = np.ascontiguousarray(steps, np.int64)
+        n = len(steps)
+        gam = np.zeros((max(n, 1), nv, w), np.int32)
+        tabu = np.zeros((max(n, 1), max(tabu_cap, 1), 3), np.int32)
+        nt = np.zeros(max(n, 1), np.int32)
+        dumped = np.zeros(1, np.int32)
+        pr = OrProbe(n, steps.ctypes.data, gam.ctypes.data, tabu.ctypes.data, nt.ctypes.data, dumped.ctypes.data,
+                     tabu_cap)
+        self.lib.or_improve_probe(h, np.ascontiguousarray(colors, np.uint16), stream_seed, budget, alpha, stop_f,
+                                  tie, C.byref(pr))
+        return [dict(step=int(steps[q]), gamma=gam[q], tabu=tabu[q, :min(nt[q], tabu_cap)].copy(),
+                     n_tabu=int(nt[q])) for q in range(int(dumped[0]))]
 
     def solve_exact(self, grid, node_budget=50_000_000, enumerate=False):
         """oracle.hpp:134 solve_exact / 141 enumerate_exact -> (f, exact, nodes, certificate)"""

@@ -298,6 +298,7 @@ int or_graph_nv(const or_graph* g) { return g->nv; }
 int or_graph_l(const or_graph* g) { return g->l; }
 int or_graph_adj_len(const or_graph* g) { return g->adj_off[g->nv]; }
 int or_graph_dom_len(const or_graph* g) { return g->dom_off[g->nv]; }
+int or_graph_order(const or_graph* g) { return g->n; }
 
 void or_graph_export(const or_graph* g, int32_t* cell_row, int32_t* cell_col, int32_t* adj_off,
                      int32_t* adj, int32_t* dom_off, uint16_t* dom) {
@@ -438,10 +439,13 @@ static void is_erase(indexset* x, int v) {
 }
 
 /* partial.hpp:76-169 + 8(d) byte counter.  Tabu state is fresh per call,
- * which equals the reference's skip_past reuse (partial.hpp:60) for alpha <= 1. */
-int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uint64_t stream_seed,
-               int64_t budget, double alpha, int stop_f, int tie_mode, or_improve_stats* st,
-               or_step* trace, int64_t trace_cap) {
+ * which equals the reference's skip_past reuse (partial.hpp:60) for alpha <= 1.
+ * probe (optional): before each listed step j, the incremental gamma table
+ * (coloring.hpp:139-156) and the live tabu entries until > j in (v, k) order
+ * (search_util.hpp:69-75). */
+static int improve_core(const or_graph* g, const uint16_t* input, uint16_t* out_best, uint64_t stream_seed,
+                        int64_t budget, double alpha, int stop_f, int tie_mode, or_improve_stats* st,
+                        or_step* trace, int64_t trace_cap, const or_probe* probe) {
     const int nv = g->nv;
     state s;
     state_init(&s, g, input);
@@ -464,9 +468,28 @@ int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uin
     double bytes = 0.0;
 
     int64_t it = 0;
+    int probe_next = 0;
+    if (probe) *probe->dumped = 0;
     while (it < budget && bestf > stop_f) {
         if (s.f == 0) break; /* step() returns false: not counted (partial.hpp:93, 163) */
         const int64_t j = it; /* tabu clock of this step's scan */
+        if (probe && probe_next < probe->n && probe->steps[probe_next] == j) {
+            memcpy(probe->gamma + (size_t)probe_next * nv * w, s.gamma, sizeof(int32_t) * (size_t)nv * w);
+            int cnt = 0;
+            int32_t* tb = probe->tabu + (size_t)probe_next * probe->cap * 3;
+            for (int v = 0; v < nv; ++v)
+                for (int k = 1; k < w; ++k)
+                    if (until[(size_t)v * w + k] > j) {
+                        if (cnt < probe->cap) {
+                            tb[3 * cnt] = v;
+                            tb[3 * cnt + 1] = k;
+                            tb[3 * cnt + 2] = (int32_t)until[(size_t)v * w + k];
+                        }
+                        ++cnt;
+                    }
+            probe->n_tabu[probe_next] = cnt;
+            *probe->dumped = ++probe_next;
+        }
         const int f_before = s.f;
         int bv = -1, bk = 0, level = 2, nadm = 0;
         uint64_t x = 0;
@@ -607,6 +630,18 @@ int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uin
     free(best);
     state_free(&s);
     return 0;
+}
+
+int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uint64_t stream_seed,
+               int64_t budget, double alpha, int stop_f, int tie_mode, or_improve_stats* st,
+               or_step* trace, int64_t trace_cap) {
+    return improve_core(g, input, out_best, stream_seed, budget, alpha, stop_f, tie_mode, st, trace, trace_cap,
+                        NULL);
+}
+
+int or_improve_probe(const or_graph* g, const uint16_t* input, uint64_t stream_seed, int64_t budget, double alpha,
+                     int stop_f, int tie_mode, const or_probe* probe) {
+    return improve_core(g, input, NULL, stream_seed, budget, alpha, stop_f, tie_mode, NULL, NULL, 0, probe);
 }
 
 

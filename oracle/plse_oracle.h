@@ -75,6 +75,7 @@ int or_graph_nv(const or_graph* g);
 int or_graph_l(const or_graph* g);
 int or_graph_adj_len(const or_graph* g);
 int or_graph_dom_len(const or_graph* g);
+int or_graph_order(const or_graph* g);
 /* copies the CSR arrays out (caller-sized buffers, any may be NULL) */
 void or_graph_export(const or_graph* g, int32_t* cell_row, int32_t* cell_col, int32_t* adj_off,
                      int32_t* adj, int32_t* dom_off, uint16_t* dom);
@@ -107,6 +108,18 @@ typedef struct {
 
 /* partial_mpma_improve(scratch, input, Rng(stream_seed), budget, ..., alpha, stop_f)
  * out_best receives best(); trace (optional) receives up to trace_cap steps. */
+/* state probe of or_improve (the per-step parity contract): before each listed step */
+typedef struct {
+    int n;                 /* probe points, ascending steps */
+    const int64_t* steps;
+    int32_t* gamma;        /* n x nv x (order+1) */
+    int32_t* tabu;         /* n x cap x 3: v, k, until */
+    int32_t* n_tabu;       /* n */
+    int32_t* dumped;       /* [1] */
+    int cap;
+} or_probe;
+int or_improve_probe(const or_graph* g, const uint16_t* input, uint64_t stream_seed, int64_t budget, double alpha,
+                     int stop_f, int tie_mode, const or_probe* probe);
 int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uint64_t stream_seed,
                int64_t budget, double alpha, int stop_f, int tie_mode, or_improve_stats* st,
                or_step* trace, int64_t trace_cap);

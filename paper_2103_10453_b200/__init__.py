@@ -171,6 +171,8 @@ def _load() -> C.CDLL:
         "plse_export_elites": ([ctx, C.c_int32, vp, vp], C.c_int),
         "plse_import_migrants": ([ctx, C.c_int32, vp], C.c_int),
         "plse_stream": ([ctx, C.POINTER(vp)], C.c_int),
+        "plse_probe": ([ctx, C.c_int32, C.c_uint64, C.c_int32, vp, vp, C.c_int32, vp, vp, C.POINTER(C.c_int32),
+                        C.POINTER(C.c_int32)], C.c_int),
         "plse_solve": ([C.c_int32, u16p, C.POINTER(_SolverConfig), C.POINTER(_RunResult), u16p, _GEN_CB, vp],
                        C.c_int),
     }
@@ -625,6 +627,25 @@ class DevicePopulation:
                self._ctx)
         m = min(n.value, max_steps)
         return [{k: getattr(buf[i], k) for k, _ in Step._fields_} for i in range(m)], n.value
+
+    def probe(self, idx: int, generation: int, steps, tabu_cap: int = 4096):
+        """Per-step state probe (canonical PartialCol): runs OFFSPRING[idx] through improve and returns,
+        for every listed step the search reaches, the gamma table (|V| x (order+1), coloring.hpp:105-116)
+        and the live tabu entries (v, k, until) on the reference's iteration clock (search_util.hpp:54-81);
+        plus the number of vertices whose tabu cache disagreed with the dense table."""
+        steps = np.ascontiguousarray(steps, np.int64)
+        n = len(steps)
+        w = self.graph.order + 1
+        gam = np.zeros((max(n, 1), self.nv, w), np.int32)
+        tabu = np.zeros((max(n, 1), max(tabu_cap, 1), 3), np.int32)
+        nt = np.zeros(max(n, 1), np.int32)
+        dumped, mism = C.c_int32(), C.c_int32()
+        _check(_lib.plse_probe(self._ctx, idx, generation, n, steps.ctypes.data_as(C.c_void_p),
+                               gam.ctypes.data_as(C.c_void_p), tabu_cap, tabu.ctypes.data_as(C.c_void_p),
+                               nt.ctypes.data_as(C.c_void_p), C.byref(dumped), C.byref(mism)), self._ctx)
+        out = [dict(step=int(steps[q]), gamma=gam[q], tabu=tabu[q, :min(nt[q], tabu_cap)].copy(), n_tabu=int(nt[q]))
+               for q in range(dumped.value)]
+        return out, mism.value
 
     def export_elites(self, n_elite: int, dev_ptr: int, with_f: bool = False):
         """The n_elite best members ((illegal, f, slot) order) as u8 rows into dev_ptr, written on this

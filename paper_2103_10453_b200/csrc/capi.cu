@@ -634,8 +634,9 @@ void download_colors(plse_ctx* c, int which, uint16_t* host) {
 }
 
 void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, plse_step* d_trace, int p_eff,
-                  int first) {
+                  int first, const StateProbe* probe = nullptr) {
     ImproveArgs a{};
+    if (probe) a.probe = *probe;
     a.n = c->n;
     a.nv = c->nv;
     a.nvpad = c->nvpad;
@@ -1131,6 +1132,60 @@ int plse_trace(plse_ctx* c, int32_t idx, uint64_t generation, int64_t max_steps,
             throw;
         }
         if (d_tr) cudaFree(d_tr);
+    });
+}
+
+int plse_probe(plse_ctx* c, int32_t idx, uint64_t generation, int32_t n_steps, const int64_t* steps,
+               int32_t* gamma_out, int32_t tabu_cap, int32_t* tabu_out, int32_t* n_tabu_out, int32_t* n_dumped,
+               int32_t* cache_mismatch) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (c->plits || c->ref_ties) throw Unsupported("the state probe covers the canonical PartialCol kernel");
+        if (idx < 0 || idx >= c->prm.p) throw std::invalid_argument("individual out of range");
+        if (n_steps < 0 || tabu_cap < 0 || (n_steps && (!steps || !gamma_out || !n_tabu_out)) ||
+            (tabu_cap && !tabu_out))
+            throw std::invalid_argument("bad probe buffers");
+        for (int q = 1; q < n_steps; ++q)
+            if (steps[q] <= steps[q - 1]) throw std::invalid_argument("probe steps must ascend");
+        const size_t gsz = (size_t)n_steps * c->nv * (c->n + 1);
+        StateProbe pr{};
+        pr.n = n_steps;
+        pr.cap = tabu_cap;
+        int64_t* d_steps = dalloc<int64_t>(std::max(n_steps, 1));
+        int32_t* d_gamma = dalloc<int32_t>(std::max<size_t>(gsz, 1));
+        int32_t* d_tabu = dalloc<int32_t>(std::max<size_t>((size_t)n_steps * tabu_cap * 3, 1));
+        int32_t* d_small = dalloc<int32_t>(n_steps + 2);
+        auto cleanup = [&] {
+            cudaFree(d_steps);
+            cudaFree(d_gamma);
+            cudaFree(d_tabu);
+            cudaFree(d_small);
+        };
+        try {
+            if (n_steps) CK(cudaMemcpy(d_steps, steps, 8 * n_steps, cudaMemcpyHostToDevice));
+            CK(cudaMemset(d_small, 0, 4 * (n_steps + 2)));
+            pr.steps = d_steps;
+            pr.gamma = d_gamma;
+            pr.tabu = d_tabu;
+            pr.n_tabu = d_small + 2;
+            pr.dumped = d_small;
+            pr.mismatch = d_small + 1;
+            improve_impl(c, generation, idx, 0, nullptr, idx + 1, idx, &pr);
+            CK(cudaStreamSynchronize(c->st));
+            std::vector<int32_t> small(n_steps + 2);
+            CK(cudaMemcpy(small.data(), d_small, 4 * (n_steps + 2), cudaMemcpyDeviceToHost));
+            if (gsz) CK(cudaMemcpy(gamma_out, d_gamma, 4 * gsz, cudaMemcpyDeviceToHost));
+            if (n_steps && tabu_cap)
+                CK(cudaMemcpy(tabu_out, d_tabu, 12ull * n_steps * tabu_cap, cudaMemcpyDeviceToHost));
+            if (n_steps) std::memcpy(n_tabu_out, small.data() + 2, 4 * n_steps);
+            if (n_dumped) *n_dumped = small[0];
+            if (cache_mismatch) *cache_mismatch = small[1];
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
     });
 }
 

@@ -12,6 +12,19 @@ namespace plse_dev {
 constexpr int kImproveMaxThreads = 256;
 constexpr int kImproveMinBlocks = 4;  // 32 resident warps per SM -> <= 64 registers
 
+// state probe of the per-step parity contract (plse_probe): gamma table and live tabu entries of the
+// traced individual at chosen steps
+struct StateProbe {
+    int n;                 // probe points (0 = off)
+    const int64_t* steps;  // ascending step indices (the state before step j; j = 0 is the post-repair state)
+    int32_t* gamma;        // n x nv x (order+1)
+    int32_t* tabu;         // n x cap x 3: (v, k, until on the reference's iteration clock)
+    int32_t* n_tabu;       // n: live entries (may exceed cap)
+    int32_t* dumped;       // [1] probe points reached
+    int32_t* mismatch;     // [1] vertices whose tabu cache disagrees with the dense table
+    int cap;
+};
+
 struct ImproveArgs {
     // graph (global copies; the kernel stages them in shared memory)
     int n, nv, nvpad, lane_words, lane_words16;
@@ -57,6 +70,7 @@ struct ImproveArgs {
     int trace_idx;
     int64_t trace_cap;
     void* trace;
+    StateProbe probe;
 };
 
 struct ImproveSmemLayout {

@@ -76,6 +76,16 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
     const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
+    const bool probing = kDebug && (i == a.trace_idx) && a.probe.n > 0;
+    int probe_next = 0;
+    // the state before step jj, at the probe points (plse_probe)
+    auto probe_at = [&](uint32_t jj) {
+        if (probing && probe_next < a.probe.n && (int64_t)jj == a.probe.steps[probe_next]) {
+            __syncwarp();
+            probe_dump<W>(a, g, s, rec, until, base, base + jj, probe_next, lane);
+            ++probe_next;
+        }
+    };
     const int64_t budget = a.budget;
     const int stop_f = a.stop_f;
     const double alpha = a.alpha;
@@ -115,6 +125,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     for (;;) {
         if (!((int64_t)j < budget && bestf > stop_f && f > 0)) break;
         if ((j & 63) == 0 && poll_stop(j)) break;
+        if (kDebug) probe_at(j);
         const int f_before = f;
         const bool asp = (f == bestf);
         const uint32_t t = base + j;
@@ -245,6 +256,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         }
         for (;;) {
             if (prof) t_step = clock64();
+            if (kDebug) probe_at(j);
             const int fb = f;
             const bool asp_s = (f == bestf);
             const uint32_t ts = base + j;
@@ -488,7 +500,7 @@ const void* improve_kernel_ptr(int W, bool debug) {
 }
 
 cudaError_t launch_improve(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    const bool debug = a.trace != nullptr || a.prof != nullptr;
+    const bool debug = a.trace != nullptr || a.prof != nullptr || a.probe.n > 0;
     if (W == 1) {
         if (debug)
             k_improve<1, true><<<grid, threads, smem, st>>>(a);

@@ -324,6 +324,89 @@ __device__ __forceinline__ int warp_find_byte(const uint8_t* buf, int a, int b, 
     return -1;
 }
 
+// plse_probe: materialise the state the step reads, as the reference holds it (coloring.hpp:105-116,
+// search_util.hpp:54-81).  gamma[v][k]: 0 for k = 0; for k = col(v) the conflict count (same-coloured
+// neighbours, what the repair counters hold); otherwise [k in R[row v]] + [k in C[col v]] from the
+// occupancy masks the kernel decides with.  Tabu: every dense-table entry live at clock t, in (v, k) order,
+// reported on the reference's iteration clock (until - base); the per-vertex caches are checked against it.
+template <int W>
+__device__ void probe_dump(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, const TabuRec* rec,
+                           const uint32_t* until, uint32_t base, uint32_t t, int q, int lane) {
+    const int nv = g.nv, w1 = g.n + 1;
+    int32_t* gam = a.probe.gamma + (size_t)q * nv * w1;
+    for (int v = lane; v < nv; v += 32) {
+        const uint16_t rc = g.cell[v];
+        const int r = rc >> 8, c = rc & 0xFF;
+        const int kv = s.col[v];
+        int same = 0;
+        if (kv) {
+            for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) same += u != v && s.col[u] == kv;
+            for (int x = g.cs[c]; x < g.cs[c + 1]; ++x) same += g.cl[x] != v && s.col[g.cl[x]] == kv;
+        }
+        gam[(size_t)v * w1] = 0;
+        for (int k = 1; k <= g.n; ++k) {
+            const int inr = (int)((s.R[r * W + (k >> 6)] >> (k & 63)) & 1);
+            const int inc = (int)((s.C[c * W + (k >> 6)] >> (k & 63)) & 1);
+            gam[(size_t)v * w1 + k] = k == kv ? same : inr + inc;
+        }
+    }
+    int32_t* tb = a.probe.tabu + (size_t)q * a.probe.cap * 3;
+    int total = 0, mism = 0;
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        const int v = v0 + lane;
+        int nl = 0;
+        uint64_t live[W];
+#pragma unroll
+        for (int z = 0; z < W; ++z) live[z] = 0;
+        if (v < nv)
+            for (int k = 1; k <= g.n; ++k)
+                if (until[(size_t)v * w1 + k] > t) {
+                    live[k >> 6] |= 1ULL << (k & 63);
+                    ++nl;
+                }
+        const int incl = warp_incl_sum(nl);
+        int at = total + incl - nl;
+        if (v < nv) {
+            for (int k = 1; k <= g.n; ++k)
+                if ((live[k >> 6] >> (k & 63)) & 1) {
+                    if (at < a.probe.cap) {
+                        tb[3 * at] = v;
+                        tb[3 * at + 1] = k;
+                        tb[3 * at + 2] = (int32_t)(until[(size_t)v * w1 + k] - base);
+                    }
+                    ++at;
+                }
+            const TabuRec tr = rec[v];
+            if (!(tr.kk >> 16)) {  // exact cache: its live pairs must be the dense table's live set
+                uint64_t cm[W];
+#pragma unroll
+                for (int z = 0; z < W; ++z) cm[z] = 0;
+                const int k1 = tr.kk & 0xFF, k2 = (tr.kk >> 8) & 0xFF;
+                bool bad = false;
+                if (tr.u1 > t) {
+                    cm[k1 >> 6] |= 1ULL << (k1 & 63);
+                    bad |= until[(size_t)v * w1 + k1] != tr.u1;
+                }
+                if (tr.u2 > t) {
+                    cm[k2 >> 6] |= 1ULL << (k2 & 63);
+                    bad |= until[(size_t)v * w1 + k2] != tr.u2;
+                }
+#pragma unroll
+                for (int z = 0; z < W; ++z) bad |= cm[z] != live[z];
+                mism += bad;
+            }
+        }
+        total += __shfl_sync(kFull, incl, 31);
+    }
+    mism = (int)__reduce_add_sync(kFull, (unsigned)mism);
+    if (lane == 0) {
+        a.probe.n_tabu[q] = total;
+        *a.probe.dumped = q + 1;
+        *a.probe.mismatch += mism;
+    }
+    __syncwarp();
+}
+
 // Shared by the PartialCol kernels (improve.cu canonical policy, improve_ref.cu reference policy):
 // load offspring i, reset the slot's tabu caches, K1 conflict counts (coloring.hpp:105-116), K1b greedy
 // repair (partial.hpp:22-39), occupancy masks R/C, uncoloured bitmask U and the column-major copy.

@@ -6,9 +6,12 @@ import paper_2103_10453_b200 as P
 
 p = int(os.environ.get("POP", "16384"))
 gens = int(os.environ.get("GENS", "3"))
-grid = P.generate_instance(60, 0.5, 12345)
+n, r, s = int(os.environ.get("N", "60")), float(os.environ.get("R", "0.5")), int(os.environ.get("S", "12345"))
+grid = P.generate_instance(n, r, s)
 g = P.preprocess(grid)
-pop = P.DevicePopulation(g, P.SolverConfig(p=p, master_seed=1, tie_mode=int(os.environ.get("TIE", "0"))))
+variant = P.MPMA if os.environ.get("VARIANT") == "mpma" else P.PARTIAL
+pop = P.DevicePopulation(g, P.SolverConfig(p=p, master_seed=1, tie_mode=int(os.environ.get("TIE", "0")),
+                                           variant=variant))
 pop.initialize_population()
 pop.offspring = pop.members
 for gen in range(1, gens + 1):
