@@ -343,7 +343,7 @@ cudaError_t prepare_pool_update() {
 
 // ---------------------------------------------------------------- best tracking (engine.hpp:211-217)
 // sum of iterations and algorithmic bytes, lowest-index argmin of the improved f (strict <)
-__global__ void __launch_bounds__(1024) k_improve_reduce(const int32_t* best_f, const int64_t* iters,
+__global__ void __launch_bounds__(1024) k_best_reduce(const int32_t* best_f, const int64_t* iters,
                                                          const unsigned long long* bytes, int p,
                                                          ImproveSummary* out) {
     __shared__ unsigned long long s_it[32], s_by[32];
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(1024) k_improve_reduce(const int32_t* best_f, 
 
 cudaError_t launch_improve_reduce(const int32_t* best_f, const int64_t* iters, const unsigned long long* bytes,
                                   int p, ImproveSummary* out, cudaStream_t st) {
-    k_improve_reduce<<<1, 1024, 0, st>>>(best_f, iters, bytes, p, out);
+    k_best_reduce<<<1, 1024, 0, st>>>(best_f, iters, bytes, p, out);
     return cudaGetLastError();
 }
 
