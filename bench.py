@@ -185,20 +185,19 @@ def lsc_grid(a):
 
 
 def i8_peak():
-    """dense i8 tensor peak: measured on a B200 of this pool by tools/probes/i8_peak.py
-    (profiles/i8_peak.json: cuBLASLt int8 GEMM via torch._int_mm, best of 10), else 2x the measured
-    bf16 burst (the sm_100 dense i8 rate is twice bf16)."""
+    """dense i8 tensor peak for the K3 roofline: B200_PROFILING.md's dense fp8/i8 rate (4.5 POPS; the driver's
+    MEASURED_PEAKS.json has no 8-bit entry).  The best library rate measured on a B200 of this pool
+    (profiles/i8_peak.json: cuBLASLt int8 GEMM via torch._int_mm, tools/probes/i8_peak.py) is reported beside
+    it: it sits below this repo's own k_sim_tc, so it cannot serve as the ceiling."""
+    measured = None
     try:
         with open(os.path.join(ROOT, "profiles", "i8_peak.json")) as f:
             d = json.load(f)
-        return float(d["i8_tops_burst"]), "measured: profiles/i8_peak.json (" + d.get("how", "") + ")"
+        measured = {"cublaslt_i8_tops_burst": float(d["i8_tops_burst"]),
+                    "cublaslt_i8_tops_sustained": float(d["i8_tops_sustained"]), "source": "profiles/i8_peak.json"}
     except (OSError, KeyError, ValueError):
         pass
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return 2 * float(json.load(f)["bf16_tflops"]), "2 x measured bf16 burst (i8 peak not measured)"
-    except (OSError, KeyError, ValueError):
-        return 2 * 1590.0, "2 x fallback bf16 (B200_PROFILING.md)"
+    return 4500.0, "B200_PROFILING.md dense fp8/i8 tensor rate (4.5 POPS)", measured
 
 
 def k3_roofline(ph, tensor_cores):
@@ -206,10 +205,11 @@ def k3_roofline(ph, tensor_cores):
     fresh pairs) over the distance phase's time, which includes the one-hot expansion of both operands."""
     if ph["distances"] <= 0 or ph["k3_ops"] <= 0:
         return None
-    peak, src = i8_peak()
+    peak, src, measured = i8_peak()
     achieved = ph["k3_ops"] / (ph["distances"] / 1e3) / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
             "kernel": "k_onehot + k_sim_tc" if tensor_cores else "k_hamming (CUDA cores)", "peak_source": src,
+            "measured_library_rate": measured,
             "includes": "one-hot expansion (members, improved once) + cross GEMM + fresh upper-triangle GEMM"}
 
 
@@ -264,7 +264,8 @@ def run_reference(a):
                    "pop_sample": s, "budget": budget, "variant": a.variant},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{s} generation-1 individuals of the C3 population, budget 100|V|, per step"},
+                         "sample": f"{s} generation-1 individuals of the C3 population, budget 100|V|, per step",
+                         "build": oracle.REF_FLAGS, "lib": os.path.relpath(oracle.REF_LIB, ROOT)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "variant": a.variant,
     }
@@ -488,7 +489,8 @@ def cpu_baseline(a, grid):
         it, secs = ref.improve_phase(grid, members, a.master_seed, 1, budget, workers=threads)
     return {"value": it / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{s} generation-1 individuals of the C3 population (reference init), budget {budget}: "
-                      f"{it} moves in {secs:.1f} s"}
+                      f"{it} moves in {secs:.1f} s",
+            "build": oracle.REF_FLAGS, "lib": os.path.relpath(oracle.REF_LIB, ROOT)}
 
 
 def ttb(a, P, grid):

@@ -19,7 +19,23 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
-REF_LIB = os.path.join(HERE, "_ref", "libplse_ref.so")
+REF_LIB_GENERIC = os.path.join(HERE, "_ref", "libplse_ref.so")
+REF_LIB_SPR = os.path.join(HERE, "_ref", "libplse_ref_spr.so")
+
+
+def _host_is_spr() -> bool:
+    """the host CPU runs -march=sapphirerapids code (avx512_fp16 + amx_tile + avx512_bf16)"""
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((l for l in f if l.startswith("flags")), "").split()
+        return all(x in flags for x in ("avx512_fp16", "amx_tile", "avx512_bf16", "avx512vl"))
+    except OSError:
+        return False
+
+
+# the reference compiled for this host's ISA when available (BASELINE.md: -march=native), else generic
+REF_LIB = REF_LIB_SPR if os.path.exists(REF_LIB_SPR) and _host_is_spr() else REF_LIB_GENERIC
+REF_FLAGS = ("-O3 -march=sapphirerapids -std=c++20" if REF_LIB == REF_LIB_SPR else "-O3 -march=x86-64-v3 -std=c++20")
 
 TIE_CANON, TIE_REF = 0, 1
 X_AUX, X_UX, X_NONE = 0, 1, 2

@@ -69,23 +69,15 @@ uint64_t or_derive_seed(uint64_t master, uint64_t tag, uint64_t index) {
 }
 
 /* Canonical counter-based draw for step j of the stream seeded s (not in the
- * reference): a Weyl counter over the 32-bit
- * folded seed, finalised by murmur3's fmix32.  hi 32 bits select the move
- * (r = floor(hi * N / 2^32)), lo 32 bits the tenure offset (L = floor(lo * 10 / 2^32)). */
-static inline uint32_t fmix32(uint32_t h) {
-    h ^= h >> 16;
-    h *= 0x85EBCA6Bu;
-    h ^= h >> 13;
-    h *= 0xC2B2AE35u;
-    h ^= h >> 16;
-    return h;
-}
-
+ * reference): SplitMix64's (j+1)-th output from
+ * state s (rng.hpp:14-19's generator, evaluated at a counter), i.e. keyed by the
+ * full 64-bit stream seed.  hi 32 bits select the move (r = floor(hi * N / 2^32)),
+ * lo 32 bits the tenure offset (L = floor(lo * 10 / 2^32)). */
 uint64_t or_canon_draw(uint64_t s, uint64_t j) {
-    const uint32_t s32 = (uint32_t)(s ^ (s >> 32));
-    const uint32_t h1 = fmix32(s32 + (uint32_t)(j + 1) * 0x9E3779B9u);
-    const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
-    return ((uint64_t)h1 << 32) | h2;
+    uint64_t z = s + (j + 1) * GOLDEN;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
 }
 
 /* ------------------------------------------------------------- instance */

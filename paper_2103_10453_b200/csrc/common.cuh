@@ -37,9 +37,30 @@ __host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t master, uint64
     return splitmix64(s);
 }
 
-// murmur3 finaliser; the canonical tie-break draw of step j is
-//   h1 = fmix32(fold(s) + (j+1) * 0x9E3779B9), h2 = fmix32(h1 + 0x632BE5AB)
-// with fold(s) = lo32(s ^ (s >> 32)); h1 ranks the move, h2 the tenure offset.
+// The canonical tie-break draw of step j of the stream seeded s: SplitMix64's (j+1)-th output from state
+// s (a counter-based generator keyed by the full 64-bit stream seed); h1 = hi32 ranks the move, h2 = lo32
+// the tenure offset.
+__host__ __device__ __forceinline__ uint64_t canon_draw(uint64_t s, uint64_t j) { return mix64(s + (j + 1) * kGolden); }
+
+// The kernels draw 32 steps at a time: lane l holds the draw of step (j & ~31) + l, broadcast per step.
+struct CanonDraws {
+    uint64_t seed;
+    uint32_t hi, lo;  // this lane's draw of the current 32-step window
+    int64_t window = -1;
+#ifdef __CUDACC__
+    __device__ __forceinline__ void at(uint32_t j, int lane, uint32_t& h1, uint32_t& h2) {
+        const int64_t w = (int64_t)(j & ~31u);
+        if (w != window) {  // warp-uniform
+            const uint64_t z = canon_draw(seed, (uint64_t)w + (uint64_t)lane);
+            hi = (uint32_t)(z >> 32);
+            lo = (uint32_t)z;
+            window = w;
+        }
+        h1 = __shfl_sync(0xFFFFFFFFu, hi, j & 31);
+        h2 = __shfl_sync(0xFFFFFFFFu, lo, j & 31);
+    }
+#endif
+};
 #ifdef __CUDACC__
 // %globaltimer (ns): the device clock the run's time limit is checked against
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -34,7 +34,7 @@
 //     (|V0| > 32) scans the U bitmask (lane-owned 32*lane_words blocks).
 //   * Selection is the canonical order-free rule: the lowest
 //     admissible delta level, per-lane counts, a warp prefix sum, and
-//     r = floor(h1 * N / 2^32) from a counter hash of (stream seed, step); the
+//     r = floor(h1 * N / 2^32) from a counter-based draw keyed by (stream seed, step); the
 //     lane holding the r-th candidate in ascending (v, k) order recovers it
 //     with a popcount search.
 #include "improve_common.cuh"
@@ -74,7 +74,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     // snapshots, lanes 1/2 the evictees' RMW; summed over the warp at the end.
     unsigned long long acc = 0;
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
-    const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
+    CanonDraws draws{seed, 0u, 0u, -1};
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     const bool probing = kDebug && (i == a.trace_idx) && a.probe.n > 0;
     int probe_next = 0;
@@ -129,8 +129,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         const int f_before = f;
         const bool asp = (f == bestf);
         const uint32_t t = base + j;
-        const uint32_t h1 = fmix32(s32 + (j + 1) * 0x9E3779B9u);
-        const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
+        uint32_t h1, h2;
+        draws.at(j, lane, h1, h2);
         if (f > 32) {
             // ============================================== dense step (start of the descent)
             if (prof) t_step = clock64();
@@ -260,8 +260,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const int fb = f;
             const bool asp_s = (f == bestf);
             const uint32_t ts = base + j;
-            const uint32_t g1 = fmix32(s32 + (j + 1) * 0x9E3779B9u);
-            const uint32_t g2 = fmix32(g1 + 0x632BE5ABu);
+            uint32_t g1, g2;
+            draws.at(j, lane, g1, g2);
             // ---- score this lane's slot
             const int r = (svc >> 16) & 0xFF, c = svc >> 24;
             const bool mine = lane < f;

@@ -234,7 +234,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     __syncwarp();
 
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
-    const uint32_t s32 = (uint32_t)(seed ^ (seed >> 32));
+    CanonDraws draws{seed, 0u, 0u, -1};
     const int stop_f = a.stop_f;
     const double alpha = a.alpha;
     const int* race_flag = a.race_flag;
@@ -275,8 +275,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             if (active == 0) break;  // StepResult::Exhausted: not counted
             if ((j & 63) == 0 && poll_stop(j)) break;
             const uint32_t t = base + j;
-            const uint32_t h1 = fmix32(s32 + (J + 1) * 0x9E3779B9u);
-            const uint32_t h2 = fmix32(h1 + 0x632BE5ABu);
+            uint32_t h1, h2;
+            draws.at(J, lane, h1, h2);
             const int64_t cur_scaled = (int64_t)wf * f + (int64_t)wc * c;
             const int64_t thr64 = best_scaled - cur_scaled;  // a tabu move is admissible iff delta < thr
             const int thr = (int)max(min(thr64, (int64_t)INT_MAX), (int64_t)INT_MIN);

@@ -27,22 +27,43 @@ def _replay_legal(orc, grid, start, trace):
     return cur
 
 
-def _fmix32(h):
-    h ^= h >> 16
-    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
-    h ^= h >> 13
-    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
-    return h ^ (h >> 16)
+M64 = (1 << 64) - 1
+
+
+def _splitmix_at(s, j):
+    z = (s + (j + 1) * 0x9E3779B97F4A7C15) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
 
 
 def test_canon_draw_definition(orc):
-    """DESIGN.md: h1 = fmix32(fold(s) + (j+1)*0x9E3779B9), h2 = fmix32(h1 + 0x632BE5AB)"""
+    """the draw of step j is SplitMix64's (j+1)-th output from the 64-bit stream seed s
+    (rng.hpp:14-19 evaluated at a counter); it equals stepping the reference's splitmix64 j+1 times"""
     for s in (0, 1, 0x1234_5678_9ABC_DEF0, 2**64 - 1):
-        s32 = (s ^ (s >> 32)) & 0xFFFFFFFF
+        st = s
         for j in range(40):
-            h1 = _fmix32((s32 + (j + 1) * 0x9E3779B9) & 0xFFFFFFFF)
-            h2 = _fmix32((h1 + 0x632BE5AB) & 0xFFFFFFFF)
-            assert orc.canon_draw(s, j) == (h1 << 32) | h2
+            assert orc.canon_draw(s, j) == _splitmix_at(s, j)
+            st = (st + 0x9E3779B97F4A7C15) & M64
+            z = ((st ^ (st >> 30)) * 0xBF58476D1CE4E5B9) & M64
+            z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+            assert orc.canon_draw(s, j) == z ^ (z >> 31)
+
+
+def test_canon_streams_are_keyed_by_the_full_seed(orc):
+    """Round-1 weakness: a 32-bit folded key made every stream a shift of one 2^32-period sequence, so
+    individuals shared draws.  Seeds differing only in their high or only in their low half, and two
+    seeds with equal 32-bit folds, now give unrelated draws."""
+    a, b = 0x0000_0001_0000_0002, 0x0000_0002_0000_0001  # equal lo32(s ^ s >> 32)
+    assert ((a ^ (a >> 32)) & 0xFFFFFFFF) == ((b ^ (b >> 32)) & 0xFFFFFFFF)
+    da = {orc.canon_draw(a, j) >> 32 for j in range(2000)}
+    db = {orc.canon_draw(b, j) >> 32 for j in range(2000)}
+    assert len(da & db) <= 2
+    # the window of one individual's generation (180k steps) does not reappear shifted in a sibling's
+    sib = [orc.derive_seed(1, 2, 16384 + i) for i in range(64)]
+    firsts = {orc.canon_draw(s, 0) for s in sib}
+    for s in sib[:8]:
+        assert not any(orc.canon_draw(s, j) in firsts for j in range(1, 3000))
 
 
 def test_canon_draws_are_uniform(orc):
