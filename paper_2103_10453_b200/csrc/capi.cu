@@ -91,6 +91,10 @@ struct plse_ctx {
     bool use_tc = true;
     int kdom = 0, kpad = 0;
     uint16_t* d_colvert = nullptr;
+    // k_improve's padded row / column colour copies (device_api.h ImproveArgs)
+    uint16_t *d_rpos = nullptr, *d_cpos = nullptr;
+    uint64_t *d_rinfo = nullptr, *d_cinfo = nullptr;
+    int rp_bytes = 0, cp_bytes = 0;
     uint8_t *d_hA = nullptr, *d_hB = nullptr;
     int32_t* d_partner = nullptr;
     // improve launch
@@ -141,6 +145,7 @@ struct plse_ctx {
                         d_improved, d_next, d_dist, d_cross, d_fresh, d_dnext, d_best_f, d_rep_f, d_mf, d_mc,
                         d_tmpf, d_tmpc, d_iters, d_bytes, d_excl, d_partner, d_rec, d_until, d_slot_clock,
                         d_conf_scratch, d_work, d_prof, d_race, d_deadline, d_dsum, d_colvert, d_hA, d_hB, d_imc,
+                        d_rpos, d_cpos, d_rinfo, d_cinfo,
                         d_nf, d_nc, ps.keys0, ps.keys1, ps.order, ps.sel, ps.nsel, ps.slots, ps.info, ps.legal,
                         ps.admitted, ps.ok, ps.conf, d_migr, d_gf, d_gc, d_migd, d_hM, d_sum};
         for (void* b : bufs)
@@ -454,6 +459,34 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     CK(cudaMemcpy(c->d_below, below.data(), 8 * below.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_dom_off, gr->dom_offsets, 4 * (nv + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_dom, dom8.data(), dom8.size(), cudaMemcpyHostToDevice));
+    {  // padded row / column copies: each line starts on an 8-byte boundary, 0xFF between lines
+        std::vector<uint16_t> rpos(nv), cpos(nv);
+        std::vector<uint64_t> rinfo(n), cinfo(n);
+        size_t ro = 0, co = 0;
+        for (int r = 0; r < n; ++r) {
+            const int len = rs[r + 1] - rs[r];
+            rinfo[r] = (uint64_t)ro | (uint64_t)((len + 7) / 8) << 16 | (uint64_t)rs[r] << 32;
+            for (int x = 0; x < len; ++x) rpos[rs[r] + x] = (uint16_t)(ro + x);
+            ro += up((size_t)len, 8);
+        }
+        for (int col = 0; col < n; ++col) {
+            const int len = cs[col + 1] - cs[col];
+            cinfo[col] = (uint64_t)co | (uint64_t)((len + 7) / 8) << 16 | (uint64_t)cs[col] << 32;
+            for (int x = 0; x < len; ++x) cpos[cl[cs[col] + x]] = (uint16_t)(co + x);
+            co += up((size_t)len, 8);
+        }
+        c->rp_bytes = (int)up(ro, 16);
+        c->cp_bytes = (int)up(co, 16);
+        if (c->rp_bytes > 65535 || c->cp_bytes > 65535) throw Unsupported("padded colour copies exceed 64 KB");
+        c->d_rpos = dalloc<uint16_t>(nv);
+        c->d_cpos = dalloc<uint16_t>(nv);
+        c->d_rinfo = dalloc<uint64_t>(n);
+        c->d_cinfo = dalloc<uint64_t>(n);
+        CK(cudaMemcpy(c->d_rpos, rpos.data(), 2 * nv, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_cpos, cpos.data(), 2 * nv, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_rinfo, rinfo.data(), 8 * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_cinfo, cinfo.data(), 8 * n, cudaMemcpyHostToDevice));
+    }
     c->d_colvert = dalloc<uint16_t>(c->kdom);
     CK(cudaMemcpy(c->d_colvert, colvert.data(), 2 * colvert.size(), cudaMemcpyHostToDevice));
 
@@ -537,18 +570,21 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
     } else {
-        const ImproveSmemLayout L = improve_smem_layout(n, nv, c->nvpad, c->lane_words, W);
+        const PadSmemLayout L = pad_smem_layout(n, nv, c->lane_words, W, c->rp_bytes, c->cp_bytes);
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
     }
+    // k_improve runs up to 32 warps in one CTA per SM (the graph tables staged once per SM)
+    const bool big_ctas = !c->plits && !c->ref_ties;
     const int per_warp = 1;
     int best_ind = 0;
     int force_wpc = 0;
     if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    for (int wpc : {8, 4, 2, 1}) {
+    for (int wpc : {32, 16, 8, 4, 2, 1}) {
         if (force_wpc && wpc != force_wpc) continue;
+        if (wpc > 8 && !big_ctas) continue;
         const size_t smem = graph_bytes + (size_t)wpc * warp_bytes;
         if (smem > (size_t)max_optin) continue;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -679,6 +715,12 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     a.race_flag = c->race_f >= 0 ? c->d_race : nullptr;
     a.race_f = c->race_f;
     a.deadline = c->d_deadline;
+    a.rpos = c->d_rpos;
+    a.cpos = c->d_cpos;
+    a.rinfo = c->d_rinfo;
+    a.cinfo = c->d_cinfo;
+    a.rp_bytes = c->rp_bytes;
+    a.cp_bytes = c->cp_bytes;
     if (const char* env = std::getenv("PLSE_PROFILE")) {
         if (env[0] == '1') {
             if (!c->d_prof) c->d_prof = dalloc<unsigned long long>(16);

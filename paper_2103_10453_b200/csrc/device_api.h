@@ -11,6 +11,8 @@ namespace plse_dev {
 
 constexpr int kImproveMaxThreads = 256;
 constexpr int kImproveMinBlocks = 4;  // 32 resident warps per SM -> <= 64 registers
+// k_improve: up to 32 warps in ONE CTA per SM, so the graph tables are staged once per SM
+constexpr int kPadMaxThreads = 1024;
 
 // state probe of the per-step parity contract (plse_probe): gamma table and live tabu entries of the
 // traced individual at chosen steps
@@ -71,7 +73,70 @@ struct ImproveArgs {
     int64_t trace_cap;
     void* trace;
     StateProbe probe;
+    // k_improve's padded colour copies (host-built tables, staged in shared memory): each row (column) of
+    // the grid starts on an 8-byte boundary of the row-padded (column-padded) copy, 0xFF in the gaps, so
+    // the holder of a colour in a row or column is one aligned 8-byte load per lane
+    const uint16_t* rpos;   // [nv] byte of v in the row-padded copy
+    const uint16_t* cpos;   // [nv] byte of v in the column-padded copy (column lists' order)
+    const uint64_t* rinfo;  // [n] offset | 8-byte words << 16 | first vertex << 32
+    const uint64_t* cinfo;  // [n] offset | 8-byte words << 16 | column-list base << 32
+    int rp_bytes, cp_bytes; // sizes of the two copies (multiples of 16)
 };
+
+struct PadSmemLayout {
+    size_t cell, rs, cs, cl, rpos, cpos, deg, rinfo, cinfo, pr, pc, graph_bytes;
+    size_t warp0, warp_bytes, w_rp, w_cp, w_list, w_R, w_C, w_U;
+};
+
+__host__ __device__ inline size_t align_up_(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline PadSmemLayout pad_smem_layout(int n, int nv, int lane_words, int W, int rp_bytes,
+                                                         int cp_bytes) {
+    PadSmemLayout L;
+    size_t o = 0;
+    L.cell = o;
+    o += (size_t)nv * 2;
+    L.rs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cs = o;
+    o += (size_t)(n + 1) * 2;
+    L.cl = o;
+    o += (size_t)nv * 2;
+    L.rpos = o;
+    o += (size_t)nv * 2;
+    L.cpos = o;
+    o += (size_t)nv * 2;
+    L.deg = o;
+    o += (size_t)nv;
+    o = align_up_(o, 16);
+    L.rinfo = o;
+    o += (size_t)n * 8;
+    L.cinfo = o;
+    o += (size_t)n * 8;
+    L.pr = o;
+    o += (size_t)n * W * 8;
+    L.pc = o;
+    o += (size_t)n * W * 8;
+    o = align_up_(o, 16);
+    L.graph_bytes = o;
+    L.warp0 = o;
+    size_t w = 0;
+    L.w_rp = w;
+    w += (size_t)rp_bytes;
+    L.w_cp = w;
+    w += (size_t)cp_bytes;
+    L.w_list = w;
+    w += 64;
+    w = align_up_(w, 16);
+    L.w_R = w;
+    w += (size_t)n * W * 8;
+    L.w_C = w;
+    w += (size_t)n * W * 8;
+    L.w_U = w;
+    w += (size_t)32 * lane_words * 4;
+    L.warp_bytes = align_up_(w, 16);
+    return L;
+}
 
 struct ImproveSmemLayout {
     size_t cell, rs, cs, cl, colpos, deg, pr, pc, graph_bytes;

@@ -41,6 +41,204 @@
 
 namespace plse_dev {
 
+// ============================================================ padded colour layout helpers
+// s.col is the ROW-PADDED copy (row r at rinfo[r] & 0xFFFF, on an 8-byte boundary, its cells in vertex
+// order, 0xFF up to the next row), s.colT the COLUMN-PADDED copy (column c in column-list order).  Pad bytes
+// are 0xFF, never a colour, and are written once per warp; only real cells are ever stored.
+
+__device__ __forceinline__ uint64_t zero_bytes64(uint64_t x) {  // 0x80 in every byte of x that is 0
+    return ~(((x & 0x7F7F7F7F7F7F7F7FULL) + 0x7F7F7F7F7F7F7F7FULL) | x) & 0x8080808080808080ULL;
+}
+
+// the row holder ur and the column holder uc of colour k in the row / column of v* (partial.hpp:124-135:
+// the neighbours coloured k*; at most one each since the colouring is legal), -1 if none: lanes 0-15 load
+// the row's 8-byte words, lanes 16-31 the column's, one ballot answers both (n <= 127: <= 16 words each)
+template <int W>
+__device__ __forceinline__ void holders(const Graph<W>& g, const WarpSmem& s, int ks, int rs_, int cs_, int lane,
+                                        int& ur, int& uc) {
+    const bool colhalf = lane >= 16;
+    const int l16 = lane & 15;
+    const uint64_t info = colhalf ? g.cinfo[cs_] : g.rinfo[rs_];
+    const int off = (int)(info & 0xFFFFu), nw = (int)((info >> 16) & 0xFFFFu), vb = (int)(info >> 32);
+    const uint8_t* buf = colhalf ? s.colT : s.col;
+    uint64_t z = 0;
+    if (l16 < nw)
+        z = zero_bytes64(*reinterpret_cast<const uint64_t*>(buf + off + 8 * l16) ^
+                         ((uint64_t)ks * 0x0101010101010101ULL));
+    const unsigned bal = __ballot_sync(kFull, z != 0);
+    const int idx = 8 * l16 + ((__ffsll((long long)z) - 1) >> 3);
+    const int cand = colhalf ? (z ? (int)g.cl[vb + idx] : 0) : vb + idx;
+    const int lr = __ffs(bal & 0xFFFFu) - 1, lc = __ffs(bal >> 16) - 1;
+    const int a_ = __shfl_sync(kFull, cand, lr & 31);
+    const int b_ = __shfl_sync(kFull, cand, (lc + 16) & 31);
+    ur = lr >= 0 ? a_ : -1;
+    uc = lc >= 0 ? b_ : -1;
+}
+
+// number of bytes equal to k (1 <= k <= n) in a row / column window
+__device__ __forceinline__ int count_eq(const uint8_t* buf, uint64_t info, int k) {
+    const int off = (int)(info & 0xFFFFu), nw = (int)((info >> 16) & 0xFFFFu);
+    const uint64_t k8 = (uint64_t)k * 0x0101010101010101ULL;
+    int cnt = 0;
+    for (int q = 0; q < nw; ++q) cnt += __popcll(zero_bytes64(*reinterpret_cast<const uint64_t*>(buf + off + 8 * q) ^ k8));
+    return cnt;
+}
+
+// the vertex-ordered u8 row (stride nvpad, zero pad) of the current colouring, 4 bytes per lane store
+template <int W>
+__device__ __forceinline__ void pad_snapshot(const Graph<W>& g, const WarpSmem& s, uint8_t* dst, int lane) {
+    for (int b = 4 * lane; b < g.nvpad; b += 128) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (b + q < g.nv) w |= (uint32_t)s.col[g.rpos[b + q]] << (8 * q);
+        *reinterpret_cast<uint32_t*>(dst + b) = w;
+    }
+}
+
+// the uncoloured bitmask U from the colours (sparse mode does not maintain it)
+template <int W>
+__device__ __forceinline__ int rebuild_U(const Graph<W>& g, const WarpSmem& s, int lane) {
+    const int v_lo = lane * 32 * g.lane_words;
+    int fl = 0;
+    for (int q = 0; q < g.lane_words; ++q) {
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int v = v_lo + 32 * q + b;
+            if (v < g.nv && s.col[g.rpos[v]] == 0) bits |= 1u << b;
+        }
+        s.U[lane * g.lane_words + q] = bits;
+        fl += __popc(bits);
+    }
+    __syncwarp();
+    return fl;
+}
+
+// partial_prologue (improve_common.cuh) on the padded layout: load offspring i, reset the slot's tabu caches,
+// K1 conflict counts (coloring.hpp:105-116), K1b greedy repair with lowest-index ties (partial.hpp:22-39),
+// occupancy masks R / C and the uncoloured bitmask U.  Returns f after the repair.
+template <int W>
+__device__ int pad_prologue(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec, uint8_t* conf,
+                            int i, int lane) {
+    const int n = g.n, nv = g.nv;
+    const int B = 32 * g.lane_words;
+    const int v_lo = lane * B;
+    const int v_hi = min(nv, v_lo + B);
+    {
+        const uint8_t* src = a.offspring + (size_t)i * g.nvpad;
+        for (int v = lane; v < nv; v += 32) {
+            const uint8_t k = src[v];
+            s.col[g.rpos[v]] = k;
+            s.colT[g.colpos[v]] = k;
+        }
+        const TabuRec z{0, 0, 0, 0};
+        for (int x = lane; x < nv; x += 32) rec[x] = z;
+    }
+    __syncwarp();
+    // ---- K1: gamma[v][col v] of the coloured vertices: equal bytes in v's row and column windows, minus v
+    for (int v = v_lo; v < v_hi; ++v) {
+        const int k = s.col[g.rpos[v]];
+        int cnt = 0;
+        if (k) {
+            const uint16_t rc = g.cell[v];
+            cnt = count_eq(s.col, g.rinfo[rc >> 8], k) + count_eq(s.colT, g.cinfo[rc & 0xFF], k) - 2;
+        }
+        conf[v] = (uint8_t)cnt;
+    }
+    __syncwarp();
+    // ---- K1b: uncolour argmax conflicts (strict >, lowest index) until none (partial.hpp:22-39)
+    for (;;) {
+        int bc = 0, bv = -1;
+        for (int v = v_lo; v < v_hi; ++v) {
+            const int c = conf[v];
+            if (c > bc) {
+                bc = c;
+                bv = v;
+            }
+        }
+        const int mx = __reduce_max_sync(kFull, (unsigned)bc);
+        if (mx == 0) break;
+        const int wl = __ffs(__ballot_sync(kFull, bc == mx)) - 1;
+        const int w = __shfl_sync(kFull, bv, wl);
+        const uint16_t rc = g.cell[w];
+        const int r = rc >> 8, c = rc & 0xFF;
+        const int k = s.col[g.rpos[w]];
+        const uint64_t ri = g.rinfo[r], ci = g.cinfo[c];
+        const int roff = (int)(ri & 0xFFFFu), rv0 = (int)(ri >> 32);
+        const int coff = (int)(ci & 0xFFFFu), cb = (int)(ci >> 32);
+        for (int x = lane; x < g.rs[r + 1] - g.rs[r]; x += 32)
+            if (rv0 + x != w && s.col[roff + x] == k) conf[rv0 + x] -= 1;
+        for (int x = lane; x < g.cs[c + 1] - g.cs[c]; x += 32) {
+            const int u = g.cl[cb + x];
+            if (u != w && s.colT[coff + x] == k) conf[u] -= 1;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            s.col[g.rpos[w]] = 0;
+            s.colT[g.colpos[w]] = 0;
+            conf[w] = 0;
+        }
+        __syncwarp();
+    }
+    // ---- occupancy masks R / C and the uncoloured bitmask U
+    for (int x = lane; x < n * W; x += 32) {
+        s.R[x] = 0;
+        s.C[x] = 0;
+    }
+    __syncwarp();
+    for (int v = lane; v < nv; v += 32) {
+        const int k = s.col[g.rpos[v]];
+        if (k) {
+            const uint16_t rc = g.cell[v];
+            atomicOr((unsigned long long*)&s.R[(rc >> 8) * W + (k >> 6)], 1ULL << (k & 63));
+            atomicOr((unsigned long long*)&s.C[(rc & 0xFF) * W + (k >> 6)], 1ULL << (k & 63));
+        }
+    }
+    const int fl = rebuild_U<W>(g, s, lane);
+    return (int)__reduce_add_sync(kFull, (unsigned)fl);
+}
+
+// apply_move_lanes (improve_common.cuh) on the padded layout: lanes 0-2 store the colour byte of v*, ur, uc
+// in both copies (and, in dense mode, flip their U bits); lane 1 clears k* from C[col ur], lane 2 from
+// R[row uc]; lane 3 sets it in R[row v*] unless ur held it, lane 4 in C[col v*] unless uc did; lanes 1/2
+// forbid (evictee, k*) until ut (search_util.hpp:73-75) and return the evictee's updated tabu cache.
+template <int W, bool kDense>
+__device__ __forceinline__ TabuRec apply_move_pad(const Graph<W>& g, const WarpSmem& s, TabuRec* rec, uint32_t* until,
+                                                  int vs, int ur, int uc, int ks, bool inR, bool inC, int f_before,
+                                                  bool improved, uint32_t ut, uint32_t t, int lane,
+                                                  unsigned long long& acc) {
+    const int w1 = g.n + 1, kw = ks >> 6;
+    const uint64_t bitk = 1ULL << (ks & 63);
+    const bool l1 = lane == 1, l2 = lane == 2;
+    const int u = l1 ? ur : l2 ? uc : vs;
+    const bool act = lane < 3 && u >= 0;
+    const int uu = max(u, 0);
+    TabuRec nr = rec[uu];  // issued early, consumed after the updates (lanes 1/2 only)
+    const uint16_t cu = g.cell[uu];
+    const int rpp = g.rpos[uu], cpp = g.colpos[uu];
+    const uint32_t dg = g.deg[uu];
+    __syncwarp();
+    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+    if (act) {
+        s.col[rpp] = nc;
+        s.colT[cpp] = nc;
+        if (kDense) atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
+    }
+    const bool on_c = l1 || lane == 4;
+    const int line_no = on_c ? (cu & 0xFF) : (cu >> 8);
+    const bool lx = lane == 3 ? !inR : lane == 4 ? !inC : (l1 || l2) && act;
+    uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
+    if (lx) *line ^= bitk;
+    acc += (act ? 4u * dg + 2u : 0u) +
+           (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)f_before + (improved ? 2u * (uint32_t)g.nv : 0u) : 0u);
+    if (act && lane > 0) {
+        until[(size_t)uu * w1 + ks] = ut;
+        cache_forbid_nb(nr, ks, ut, t);
+        rec[uu] = nr;
+    }
+    return nr;
+}
+
 template <int W, bool kDebug>
 __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
                             uint32_t* until, uint32_t* slot_clock, uint8_t* conf, int i, int lane) {
@@ -48,8 +246,6 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     const int B = 32 * g.lane_words;
     const int v_lo = lane * B;
     const int v_hi = min(nv, v_lo + B);
-    uint8_t* col = s.col;
-    uint8_t* colT = s.colT;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     long long t_start = prof ? clock64() : 0, t_step = 0;
     unsigned long long pc_dense = 0, pc_sparse = 0, pn_dense = 0, pn_sparse = 0, pf_dense = 0, pn_enter = 0;
@@ -62,7 +258,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         base = 0;
     }
 
-    int f = partial_prologue<W>(a, g, s, rec, conf, i, lane);
+    int f = pad_prologue<W>(a, g, s, rec, conf, i, lane);
     __syncwarp();
 
     const long long t_prologue = prof ? clock64() - t_start : 0;
@@ -189,25 +385,20 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             vs = __shfl_sync(kFull, vs, wl);
             ks = __shfl_sync(kFull, ks, wl);
             if (pending && lvl >= 0) {
-                snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+                pad_snapshot<W>(g, s, a.improved + (size_t)i * g.nvpad, lane);
                 pending = false;
             }
             const uint16_t rcs = g.cell[vs];
             const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-            const int kw = ks >> 6;
-            const uint64_t bitk = 1ULL << (ks & 63);
-            const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
-            const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
-            const int ur = warp_find_byte(col, g.rs[rs_], g.rs[rs_ + 1], ks, inR, lane);
-            const int xc = warp_find_byte(colT, g.cs[cs_], g.cs[cs_ + 1], ks, inC, lane);
-            const int uc = xc >= 0 ? (int)g.cl[xc] : -1;
+            int ur, uc;
+            holders<W>(g, s, ks, rs_, cs_, lane, ur, uc);
+            const bool inR = ur >= 0, inC = uc >= 0;
             const int e = (ur >= 0) + (uc >= 0);
             const int f_new = f - 1 + e;
             const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(alpha * (double)f_new);
             const uint32_t ut = t + 1 + tenure;
             const bool improved = f_new < bestf;
-            apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, f_before, improved, ut, t, lane,
-                                acc);
+            apply_move_pad<W, true>(g, s, rec, until, vs, ur, uc, ks, inR, inC, f_before, improved, ut, t, lane, acc);
             f = f_new;
             if (improved) {
                 bestf = f;
@@ -306,25 +497,21 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const int lvl = lc - 1;
             if (pending && lvl >= 0) {
                 // the current colouring is the best one and is about to change without improving
-                snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+                pad_snapshot<W>(g, s, a.improved + (size_t)i * g.nvpad, lane);
                 pending = false;
             }
-            const int kw = ks >> 6;
-            const uint64_t bitk = 1ULL << (ks & 63);
-            const bool inR = (s.R[rs_ * W + kw] & bitk) != 0;
-            const bool inC = (s.C[cs_ * W + kw] & bitk) != 0;
             // ---- the row / column holder of k* (at most one each: the colouring is legal)
-            const int ur = warp_find_byte(col, g.rs[rs_], g.rs[rs_ + 1], ks, inR, lane);
-            const int xc = warp_find_byte(colT, g.cs[cs_], g.cs[cs_ + 1], ks, inC, lane);
-            const int uc = xc >= 0 ? (int)g.cl[xc] : -1;
+            int ur, uc;
+            holders<W>(g, s, ks, rs_, cs_, lane, ur, uc);
+            const bool inR = ur >= 0, inC = uc >= 0;
             const int e = (ur >= 0) + (uc >= 0);
             const int f_new = f - 1 + e;
             const uint32_t tenure = __umulhi(g2, 10u) + (uint32_t)(alpha * (double)f_new);
             const uint32_t ut = ts + 1 + tenure;
             const bool improved = f_new < bestf;
             // ---- the move: predicated five-lane update (improve_common.cuh apply_move_lanes)
-            const TabuRec nr = apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, fb, improved,
-                                                   ut, ts, lane, acc);
+            const TabuRec nr =
+                apply_move_pad<W, false>(g, s, rec, until, vs, ur, uc, ks, inR, inC, fb, improved, ut, ts, lane, acc);
             f = f_new;
             if (improved) {
                 bestf = f;
@@ -336,6 +523,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             ++j;
             if (f_new > 32) {
                 __syncwarp();
+                rebuild_U<W>(g, s, lane);  // sparse mode leaves U stale; dense mode scans it
                 if (prof) {
                     pc_sparse += (unsigned long long)(clock64() - t_step);
                     ++pn_sparse;
@@ -378,7 +566,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             if ((j & 63) == 0 && poll_stop(j)) break;
         }
     }
-    if (pending) snapshot(col, a.improved + (size_t)i * g.nvpad, g.nvpad, lane);
+    if (pending) pad_snapshot<W>(g, s, a.improved + (size_t)i * g.nvpad, lane);
     {
         // lanes 0..2 hold the byte-counter parts
         const unsigned long long a1 = __shfl_sync(kFull, acc, 1), a2 = __shfl_sync(kFull, acc, 2);
@@ -407,28 +595,35 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 }
 
 template <int W, bool kDebug>
-__global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_improve(const ImproveArgs a) {
+__global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int n = a.n, nv = a.nv;
-    const ImproveSmemLayout L = improve_smem_layout(n, nv, a.nvpad, a.lane_words, W);
+    const PadSmemLayout L = pad_smem_layout(n, nv, a.lane_words, W, a.rp_bytes, a.cp_bytes);
     uint16_t* s_cell = reinterpret_cast<uint16_t*>(smem + L.cell);
     uint16_t* s_rs = reinterpret_cast<uint16_t*>(smem + L.rs);
     uint16_t* s_cs = reinterpret_cast<uint16_t*>(smem + L.cs);
     uint16_t* s_cl = reinterpret_cast<uint16_t*>(smem + L.cl);
-    uint16_t* s_cp = reinterpret_cast<uint16_t*>(smem + L.colpos);
+    uint16_t* s_rpos = reinterpret_cast<uint16_t*>(smem + L.rpos);
+    uint16_t* s_cpos = reinterpret_cast<uint16_t*>(smem + L.cpos);
+    uint8_t* s_deg = smem + L.deg;
+    uint64_t* s_ri = reinterpret_cast<uint64_t*>(smem + L.rinfo);
+    uint64_t* s_ci = reinterpret_cast<uint64_t*>(smem + L.cinfo);
     uint64_t* s_pr = reinterpret_cast<uint64_t*>(smem + L.pr);
     uint64_t* s_pc = reinterpret_cast<uint64_t*>(smem + L.pc);
-    uint8_t* s_deg = smem + L.deg;
     for (int x = threadIdx.x; x < nv; x += blockDim.x) {
         s_cell[x] = a.cell[x];
-        const uint16_t v = a.col_list[x];
-        s_cl[x] = v;
-        s_cp[v] = (uint16_t)x;
+        s_cl[x] = a.col_list[x];
+        s_rpos[x] = a.rpos[x];
+        s_cpos[x] = a.cpos[x];
     }
     for (int x = threadIdx.x; x <= n; x += blockDim.x) {
         s_rs[x] = a.row_start[x];
         s_cs[x] = a.col_start[x];
+    }
+    for (int x = threadIdx.x; x < n; x += blockDim.x) {
+        s_ri[x] = a.rinfo[x];
+        s_ci[x] = a.cinfo[x];
     }
     for (int x = threadIdx.x; x < n * W; x += blockDim.x) {
         s_pr[x] = a.pre_row[x];
@@ -451,9 +646,12 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
     g.rs = s_rs;
     g.cs = s_cs;
     g.cl = s_cl;
-    g.colpos = s_cp;
+    g.colpos = s_cpos;
     g.pr = s_pr;
     g.pc = s_pc;
+    g.rpos = s_rpos;
+    g.rinfo = s_ri;
+    g.cinfo = s_ci;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
         uint64_t m = 0;
@@ -466,13 +664,17 @@ __global__ void __launch_bounds__(kImproveMaxThreads, kImproveMinBlocks) k_impro
 
     uint8_t* wbase = smem + L.warp0 + (size_t)warp * L.warp_bytes;
     WarpSmem s;
-    s.col = wbase + L.w_col;
+    s.col = wbase + L.w_rp;
     s.conf = nullptr;
-    s.colT = wbase + L.w_colT;
+    s.colT = wbase + L.w_cp;
     s.list = reinterpret_cast<uint16_t*>(wbase + L.w_list);
     s.R = reinterpret_cast<uint64_t*>(wbase + L.w_R);
     s.C = reinterpret_cast<uint64_t*>(wbase + L.w_C);
     s.U = reinterpret_cast<uint32_t*>(wbase + L.w_U);
+    // the pad bytes of both copies: 0xFF, written once (only real cells are ever stored afterwards)
+    for (int x = lane; x < (a.rp_bytes + a.cp_bytes) / 16; x += 32)
+        reinterpret_cast<uint4*>(wbase + L.w_rp)[x] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    __syncwarp();
 
     const int slot = blockIdx.x * nwarps + warp;
     TabuRec* rec = reinterpret_cast<TabuRec*>(reinterpret_cast<char*>(a.tabu_rec) + (size_t)slot * a.rec_stride);

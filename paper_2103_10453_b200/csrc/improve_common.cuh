@@ -31,11 +31,22 @@ struct Graph {
     const uint16_t* rs;
     const uint16_t* cs;
     const uint16_t* cl;
-    const uint16_t* colpos;  // position of v in the column-major list cl
+    const uint16_t* colpos;  // position of v in the column-major copy (k_improve: the column-padded copy)
     const uint64_t* pr;
     const uint64_t* pc;
     uint64_t full[W];
+    // k_improve's padded layouts (nullptr in the other kernels): s.col / s.colT are then the row- / column-
+    // padded copies, v's colour is s.col[rpos[v]]
+    const uint16_t* rpos = nullptr;
+    const uint64_t* rinfo = nullptr;  // [n] offset | 8-byte words << 16 | first vertex << 32
+    const uint64_t* cinfo = nullptr;  // [n] offset | 8-byte words << 16 | column-list base << 32
 };
+
+// colour of vertex v in either layout
+template <int W>
+__device__ __forceinline__ int col_of(const Graph<W>& g, const WarpSmem& s, int v) {
+    return g.rpos ? s.col[g.rpos[v]] : s.col[v];
+}
 
 template <int W>
 __device__ __forceinline__ void dom_mask(const Graph<W>& g, int r, int c, uint64_t (&d)[W]) {
@@ -337,11 +348,11 @@ __device__ void probe_dump(const ImproveArgs& a, const Graph<W>& g, const WarpSm
     for (int v = lane; v < nv; v += 32) {
         const uint16_t rc = g.cell[v];
         const int r = rc >> 8, c = rc & 0xFF;
-        const int kv = s.col[v];
+        const int kv = col_of<W>(g, s, v);
         int same = 0;
         if (kv) {
-            for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) same += u != v && s.col[u] == kv;
-            for (int x = g.cs[c]; x < g.cs[c + 1]; ++x) same += g.cl[x] != v && s.col[g.cl[x]] == kv;
+            for (int u = g.rs[r]; u < g.rs[r + 1]; ++u) same += u != v && col_of<W>(g, s, u) == kv;
+            for (int x = g.cs[c]; x < g.cs[c + 1]; ++x) same += g.cl[x] != v && col_of<W>(g, s, g.cl[x]) == kv;
         }
         gam[(size_t)v * w1] = 0;
         for (int k = 1; k <= g.n; ++k) {
