@@ -214,7 +214,9 @@ int plse_trace(plse_ctx* ctx, int32_t idx, uint64_t generation, int64_t max_step
    post-repair state), dump gamma[v][k] (coloring.hpp:105-116; n_steps x |V| x (order+1)) and the live
    tabu entries (v, k, until) on the reference's iteration clock (search_util.hpp:54-81; n_steps x tabu_cap
    x 3, count per step in n_tabu_out).  n_dumped = probe points the search reached; cache_mismatch =
-   vertices whose tabu cache disagreed with the dense table (0 on a correct kernel).  Canonical PartialCol. */
+   vertices whose tabu cache disagreed with the dense table (0 on a correct kernel).  Canonical policy;
+   with variant MPMA (PLITS) the steps are counted over both phases, colour 0 can be tabu, and until is on
+   the phase's own clock (plits.hpp:81). */
 int plse_probe(plse_ctx* ctx, int32_t idx, uint64_t generation, int32_t n_steps, const int64_t* steps,
                int32_t* gamma_out, int32_t tabu_cap, int32_t* tabu_out, int32_t* n_tabu_out, int32_t* n_dumped,
                int32_t* cache_mismatch);

@@ -174,6 +174,8 @@ class Oracle:
         L.or_enumerate_exact.argtypes = [C.c_void_p, C.POINTER(OrExact), u16p]
         L.or_plits.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                C.c_int, C.POINTER(OrPlitsStats), C.c_void_p, C.c_int64]
+        L.or_plits_probe.argtypes = [C.c_void_p, u16p, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                     C.c_int, C.c_void_p]
         L.or_improve_probe.argtypes = [C.c_void_p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int, C.c_int,
                                        C.c_void_p]
         L.or_improve.argtypes = [C.c_void_p, u16p, u16p, C.c_uint64, C.c_int64, C.c_double, C.c_int,
@@ -258,8 +260,9 @@ class Oracle:
         return res
 
     def improve_probe(self, grid, colors, stream_seed, budget, steps, tabu_cap=4096, alpha=0.6, stop_f=0,
-                      tie=TIE_CANON):
-        """the gamma table and the live tabu entries (v, k, until) before each listed step of or_improve"""
+                      tie=TIE_CANON, plits_budget2=None):
+        """the gamma table and the live tabu entries (v, k, until) before each listed step of or_improve
+        (or of or_plits when plits_budget2 is given: steps counted over both phases, until on the phase clock)"""
         h = self._h(grid)
         nv, w = len(colors), self.lib.or_graph_order(h) + 1
         steps = np.ascontiguousarray(steps, np.int64)
@@ -270,8 +273,12 @@ class Oracle:
         dumped = np.zeros(1, np.int32)
         pr = OrProbe(n, steps.ctypes.data, gam.ctypes.data, tabu.ctypes.data, nt.ctypes.data, dumped.ctypes.data,
                      tabu_cap)
-        self.lib.or_improve_probe(h, np.ascontiguousarray(colors, np.uint16), stream_seed, budget, alpha, stop_f,
-                                  tie, C.byref(pr))
+        if plits_budget2 is None:
+            self.lib.or_improve_probe(h, np.ascontiguousarray(colors, np.uint16), stream_seed, budget, alpha, stop_f,
+                                      tie, C.byref(pr))
+        else:
+            self.lib.or_plits_probe(h, np.ascontiguousarray(colors, np.uint16), stream_seed, budget, plits_budget2,
+                                    alpha, stop_f, tie, C.byref(pr))
         return [dict(step=int(steps[q]), gamma=gam[q], tabu=tabu[q, :min(nt[q], tabu_cap)].copy(),
                      n_tabu=int(nt[q])) for q in range(int(dumped[0]))]
 

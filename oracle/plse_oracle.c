@@ -430,6 +430,27 @@ static void is_erase(indexset* x, int v) {
     x->pos[v] = -1;
 }
 
+/* the state probe of the per-step parity contract: gamma (|V| x (n+1)) and the live tabu entries
+   (until > j, colours kmin..n, (v, k) order) into probe point q */
+static void probe_dump_state(const or_probe* probe, int q, const int32_t* gamma, const int64_t* until, int nv, int w,
+                             int64_t j, int kmin) {
+    memcpy(probe->gamma + (size_t)q * nv * w, gamma, sizeof(int32_t) * (size_t)nv * w);
+    int cnt = 0;
+    int32_t* tb = probe->tabu + (size_t)q * probe->cap * 3;
+    for (int v = 0; v < nv; ++v)
+        for (int k = kmin; k < w; ++k)
+            if (until[(size_t)v * w + k] > j) {
+                if (cnt < probe->cap) {
+                    tb[3 * cnt] = v;
+                    tb[3 * cnt + 1] = k;
+                    tb[3 * cnt + 2] = (int32_t)until[(size_t)v * w + k];
+                }
+                ++cnt;
+            }
+    probe->n_tabu[q] = cnt;
+    *probe->dumped = q + 1;
+}
+
 /* partial.hpp:76-169 + 8(d) byte counter.  Tabu state is fresh per call,
  * which equals the reference's skip_past reuse (partial.hpp:60) for alpha <= 1.
  * probe (optional): before each listed step j, the incremental gamma table
@@ -465,23 +486,8 @@ static int improve_core(const or_graph* g, const uint16_t* input, uint16_t* out_
     while (it < budget && bestf > stop_f) {
         if (s.f == 0) break; /* step() returns false: not counted (partial.hpp:93, 163) */
         const int64_t j = it; /* tabu clock of this step's scan */
-        if (probe && probe_next < probe->n && probe->steps[probe_next] == j) {
-            memcpy(probe->gamma + (size_t)probe_next * nv * w, s.gamma, sizeof(int32_t) * (size_t)nv * w);
-            int cnt = 0;
-            int32_t* tb = probe->tabu + (size_t)probe_next * probe->cap * 3;
-            for (int v = 0; v < nv; ++v)
-                for (int k = 1; k < w; ++k)
-                    if (until[(size_t)v * w + k] > j) {
-                        if (cnt < probe->cap) {
-                            tb[3 * cnt] = v;
-                            tb[3 * cnt + 1] = k;
-                            tb[3 * cnt + 2] = (int32_t)until[(size_t)v * w + k];
-                        }
-                        ++cnt;
-                    }
-            probe->n_tabu[probe_next] = cnt;
-            *probe->dumped = ++probe_next;
-        }
+        if (probe && probe_next < probe->n && probe->steps[probe_next] == j)
+            probe_dump_state(probe, probe_next++, s.gamma, until, nv, w, j, 1);
         const int f_before = s.f;
         int bv = -1, bk = 0, level = 2, nadm = 0;
         uint64_t x = 0;
@@ -675,7 +681,8 @@ static void plits_membership(plits_phase_state* ps, int v, int from, int to) {
  * col is the phase input and receives search.best(). Returns hit_target. */
 static int plits_phase(const or_graph* g, uint16_t* col, int phase, int64_t wf, int64_t wc, int64_t budget,
                        double alpha, int stop_f, int tie_mode, or_rng* rng, uint64_t seed, int64_t* J,
-                       int64_t* iters, double* bytes, or_plits_step* trace, int64_t trace_cap) {
+                       int64_t* iters, double* bytes, or_plits_step* trace, int64_t trace_cap,
+                       const or_probe* probe, int* probe_next) {
     const int nv = g->nv;
     plits_phase_state ps;
     ps.g = g;
@@ -713,6 +720,9 @@ static int plits_phase(const or_graph* g, uint16_t* col, int phase, int64_t wf, 
         }
         if (ps.un.size == 0 && ps.cf.size == 0) break; /* StepResult::Exhausted, not counted */
         const int64_t j = it;                           /* tabu clock of this step's scan */
+        /* probe points are keyed by the step index over both phases; tabu entries on the phase clock */
+        if (probe && *probe_next < probe->n && probe->steps[*probe_next] == *J)
+            probe_dump_state(probe, (*probe_next)++, ps.s.gamma, ps.until, nv, w, j, 0);
         const int64_t cur_scaled = wf * ps.s.f + wc * ps.s.c;
         int bv = -1, bk = 0, bdf = 0, bdc = 0;
         int64_t bd = 0;
@@ -842,9 +852,11 @@ static int plits_phase(const or_graph* g, uint16_t* col, int phase, int64_t wf, 
 }
 
 /* plits.hpp:276-292 plits_run */
-int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
-             int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
-             or_plits_step* trace, int64_t trace_cap) {
+static int plits_core(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
+                      int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
+                      or_plits_step* trace, int64_t trace_cap, const or_probe* probe) {
+    int probe_next = 0;
+    if (probe) *probe->dumped = 0;
     const int nv = g->nv;
     or_plits_stats z;
     memset(&z, 0, sizeof(z));
@@ -861,12 +873,12 @@ int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t s
     int64_t J = 0, iters = 0;
     double bytes = 0;
     const int done = plits_phase(g, col, 1, 2, 1, iters1, alpha, stop_f, tie_mode, &rng, stream_seed, &J, &iters,
-                                 &bytes, trace, trace_cap);
+                                 &bytes, trace, trace_cap, probe, &probe_next);
     z.phase1_iterations = iters;
     z.hit_target = done;
     if (!done)
         plits_phase(g, col, 2, 2, 2LL * nv, iters2, alpha, stop_f, tie_mode, &rng, stream_seed, &J, &iters, &bytes,
-                    trace, trace_cap);
+                    trace, trace_cap, probe, &probe_next);
     int f, c;
     or_eval(g, col, &f, &c);
     if (c > 0) {
@@ -875,13 +887,27 @@ int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t s
         z.repaired = 1;
         bytes += 2.0 * nv;
     }
-    memcpy(out, col, sizeof(uint16_t) * nv);
+    if (out) memcpy(out, col, sizeof(uint16_t) * nv);
     z.iterations = iters;
     z.final_f = f;
     z.alg_bytes = bytes;
     if (st) *st = z;
     free(col);
     return 0;
+}
+
+int or_plits(const or_graph* g, const uint16_t* input, uint16_t* out, uint64_t stream_seed, int64_t iters1,
+             int64_t iters2, double alpha, int stop_f, int tie_mode, or_plits_stats* st,
+             or_plits_step* trace, int64_t trace_cap) {
+    return plits_core(g, input, out, stream_seed, iters1, iters2, alpha, stop_f, tie_mode, st, trace, trace_cap,
+                      NULL);
+}
+
+/* the state probe of or_plits: before each listed step J (counted over both phases) the gamma table and
+   the live tabu entries (v, k >= 0, until) on the phase's own clock (plits.hpp:81: a fresh table per phase) */
+int or_plits_probe(const or_graph* g, const uint16_t* input, uint64_t stream_seed, int64_t iters1, int64_t iters2,
+                   double alpha, int stop_f, int tie_mode, const or_probe* probe) {
+    return plits_core(g, input, NULL, stream_seed, iters1, iters2, alpha, stop_f, tie_mode, NULL, NULL, 0, probe);
 }
 
 

@@ -118,6 +118,8 @@ typedef struct {
     int32_t* dumped;       /* [1] */
     int cap;
 } or_probe;
+int or_plits_probe(const or_graph* g, const uint16_t* input, uint64_t stream_seed, int64_t iters1, int64_t iters2,
+                   double alpha, int stop_f, int tie_mode, const or_probe* probe);
 int or_improve_probe(const or_graph* g, const uint16_t* input, uint64_t stream_seed, int64_t budget, double alpha,
                      int stop_f, int tie_mode, const or_probe* probe);
 int or_improve(const or_graph* g, const uint16_t* input, uint16_t* out_best, uint64_t stream_seed,

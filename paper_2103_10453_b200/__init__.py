@@ -629,7 +629,7 @@ class DevicePopulation:
         return [{k: getattr(buf[i], k) for k, _ in Step._fields_} for i in range(m)], n.value
 
     def probe(self, idx: int, generation: int, steps, tabu_cap: int = 4096):
-        """Per-step state probe (canonical PartialCol): runs OFFSPRING[idx] through improve and returns,
+        """Per-step state probe (canonical PartialCol or PLITS): runs OFFSPRING[idx] through improve and returns,
         for every listed step the search reaches, the gamma table (|V| x (order+1), coloring.hpp:105-116)
         and the live tabu entries (v, k, until) on the reference's iteration clock (search_util.hpp:54-81);
         plus the number of vertices whose tabu cache disagreed with the dense table."""

@@ -1183,7 +1183,7 @@ int plse_probe(plse_ctx* c, int32_t idx, uint64_t generation, int32_t n_steps, c
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
-        if (c->plits || c->ref_ties) throw Unsupported("the state probe covers the canonical PartialCol kernel");
+        if (c->ref_ties) throw Unsupported("the state probe covers the canonical kernels (PartialCol, PLITS)");
         if (idx < 0 || idx >= c->prm.p) throw std::invalid_argument("individual out of range");
         if (n_steps < 0 || tabu_cap < 0 || (n_steps && (!steps || !gamma_out || !n_tabu_out)) ||
             (tabu_cap && !tabu_out))

@@ -208,6 +208,51 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
     return popc_w<W>(adm) + (adm0 ? 1 : 0);
 }
 
+// plse_probe on PLITS: gamma[v][k] = cnt_row[r][k] + cnt_col[c][k] - 2 [k = col v] for k >= 1 (the
+// incremental table of coloring.hpp:139-156, here from the bit-sliced counts), column 0 zero; the live tabu
+// entries (v, k >= 0, until) of the dense table on the phase's own clock (plits.hpp:81)
+template <int W>
+__device__ void plits_probe_dump(const ImproveArgs& a, const Graph<W>& g, const PlitsWarp& s, const uint32_t* until,
+                                 uint32_t base, uint32_t t, int q, int lane) {
+    constexpr int NP = PlitsK<W>::NP;
+    const int nv = g.nv, w1 = g.n + 1;
+    int32_t* gam = a.probe.gamma + (size_t)q * nv * w1;
+    for (int v = lane; v < nv; v += 32) {
+        const uint16_t rc = g.cell[v];
+        const int kv = s.col[v];
+        gam[(size_t)v * w1] = 0;
+        for (int k = 1; k <= g.n; ++k)
+            gam[(size_t)v * w1 + k] = plane_val<W, NP>(s.rp + (size_t)(rc >> 8) * NP * W, k) +
+                                      plane_val<W, NP>(s.cp + (size_t)(rc & 0xFF) * NP * W, k) - 2 * (k == kv);
+    }
+    int32_t* tb = a.probe.tabu + (size_t)q * a.probe.cap * 3;
+    int total = 0;
+    for (int v0 = 0; v0 < nv; v0 += 32) {
+        const int v = v0 + lane;
+        int nl = 0;
+        if (v < nv)
+            for (int k = 0; k <= g.n; ++k) nl += until[(size_t)v * w1 + k] > t;
+        const int incl = warp_incl_sum(nl);
+        int at = total + incl - nl;
+        if (v < nv)
+            for (int k = 0; k <= g.n; ++k)
+                if (until[(size_t)v * w1 + k] > t) {
+                    if (at < a.probe.cap) {
+                        tb[3 * at] = v;
+                        tb[3 * at + 1] = k;
+                        tb[3 * at + 2] = (int32_t)(until[(size_t)v * w1 + k] - base);
+                    }
+                    ++at;
+                }
+        total += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) {
+        a.probe.n_tabu[q] = total;
+        *a.probe.dumped = q + 1;
+    }
+    __syncwarp();
+}
+
 template <int W, bool kDebug>
 __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWarp& s, uint32_t* until,
                           uint32_t* slot_clock, int i, int lane) {
@@ -218,6 +263,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     uint8_t* col = s.col;
     uint8_t* best_row = a.improved + (size_t)i * g.nvpad;
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
+    const bool probing = kDebug && (i == a.trace_idx) && a.probe.n > 0;
+    int probe_next = 0;
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     // steps, list, level, select, move, step, level iters, sum na | move: plane, membership, tail
     unsigned long long pc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -274,6 +321,10 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             if (!((int64_t)j < budget)) break;
             if (active == 0) break;  // StepResult::Exhausted: not counted
             if ((j & 63) == 0 && poll_stop(j)) break;
+            if (kDebug && probing && probe_next < a.probe.n && (int64_t)J == a.probe.steps[probe_next]) {
+                __syncwarp();
+                plits_probe_dump<W>(a, g, s, until, base, base + j, probe_next++, lane);
+            }
             const uint32_t t = base + j;
             uint32_t h1, h2;
             draws.at(J, lane, h1, h2);
@@ -670,7 +721,7 @@ const void* plits_kernel_ptr(int W, bool debug) {
 }
 
 cudaError_t launch_plits(const ImproveArgs& a, int W, int grid, int threads, size_t smem, cudaStream_t st) {
-    const bool debug = a.trace != nullptr || a.prof != nullptr;
+    const bool debug = a.trace != nullptr || a.prof != nullptr || a.probe.n > 0;
     if (W == 1) {
         if (debug)
             k_plits<1, true><<<grid, threads, smem, st>>>(a);
