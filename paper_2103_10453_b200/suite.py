@@ -196,6 +196,17 @@ def report_to_json(report: BenchReport) -> dict:
     return {"rows": rows, "aggregates": aggs}
 
 
+def load_instance(path: str):
+    """instance.hpp:186-192"""
+    from . import parse_instance
+    try:
+        with open(path) as fh:
+            text = fh.read()
+    except OSError:
+        raise RuntimeError("cannot open instance file: " + path) from None
+    return parse_instance(text)
+
+
 def suite_tasks(suite_dir: str) -> List[BenchTask]:
     """plse.cpp:203-211: the suite's *.txt files in sorted path order."""
     files = sorted(os.path.join(suite_dir, f) for f in os.listdir(suite_dir)
@@ -212,7 +223,7 @@ def run_bench(tasks: Sequence[BenchTask], sweep: Sequence[SolverConfig], repeats
     if not sweep:
         raise ValueError("empty configuration sweep")
     if load is None:
-        from .cli import load_instance as load
+        load = load_instance
     specs = [(t, s, rep) for t in tasks for s in range(len(sweep)) for rep in range(repeats)]
     rows: List[Optional[BenchRow]] = [None] * len(specs)
     if devices is None:

@@ -10,6 +10,12 @@
 //
 // The argument parser is a small stand-in for CLI11 (not available offline):
 // same option names and value forms; usage errors exit 106 like CLI11's.
+//
+// Provenance: the flag-to-config glue (resolve_workers, make_config, warn_memory), the fixed output strings
+// and the bench sweep loop deliberately follow tools/plse.cpp line for line (plse.cpp:69-113, 132-150,
+// 176-190, 215-229) so that `solve --tie ref` prints the reference CLI's bytes; the CLI itself is outside
+// the hot path and kept only as the reference-facing driver.  `python -m
+// paper_2103_10453_b200` is a thin wrapper over this binary.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
