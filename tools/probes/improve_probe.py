@@ -11,7 +11,7 @@ grid = P.generate_instance(n, r, s)
 g = P.preprocess(grid)
 variant = P.MPMA if os.environ.get("VARIANT") == "mpma" else P.PARTIAL
 pop = P.DevicePopulation(g, P.SolverConfig(p=p, master_seed=1, tie_mode=int(os.environ.get("TIE", "0")),
-                                           variant=variant))
+                                           variant=variant, phase1_iters=int(os.environ.get("BUDGET", "0"))))
 pop.initialize_population()
 pop.offspring = pop.members
 for gen in range(1, gens + 1):
