@@ -213,6 +213,24 @@ def k3_roofline(ph, tensor_cores):
             "includes": "one-hot expansion (members, improved once) + cross GEMM + fresh upper-triangle GEMM"}
 
 
+def population_rooflines(ph, p, nvpad, steps, peak):
+    """HBM-bound population phases ('K0, K1, K4 ... report them, but they are small'): the
+    algorithmic bytes each phase must move per generation over its measured time.
+    K4a update: gather of the next p x p u16 distance matrix (read + write) and of the next member rows;
+    K4b+c offspring: k_match scans its p x p u16 distance rows and exclusion bits, k_crossover reads two
+    parent rows and writes one child row per individual."""
+    out = {}
+    for name, ms, by in (
+            ("k4a_update (k_pool_*)", ph["update"] / steps, 4.0 * p * p + 2.0 * p * nvpad),
+            ("k4bc_offspring (k_match + k_crossover)", ph["offspring"] / steps,
+             2.0 * p * p + p * p / 8.0 + 3.0 * p * nvpad)):
+        if ms > 0:
+            gbs = by / (ms / 1e3) / 1e9
+            out[name] = {"bound": "hbm", "alg_bytes": by, "ms": ms, "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak}
+    return out
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -458,6 +476,8 @@ def run_ours(a):
             "improve_moves_per_s": improve_rate,
             "phase_ms_per_step": {k: v / a.steps for k, v in timed_phase.items() if k != "k3_ops"},
             "k3_roofline": k3_roofline(timed_phase, pop.counters().k3_tensor_cores),
+            "population_rooflines": population_rooflines(timed_phase, p_rank, (nv + 15) // 16 * 16, a.steps,
+                                                         peak),
             "best_f_seen": best,
             "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": a.e2e_steps},
