@@ -477,7 +477,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
         }
         c->rp_bytes = (int)up(ro, 16);
         c->cp_bytes = (int)up(co, 16);
-        if (c->rp_bytes > 65535 || c->cp_bytes > 65535) throw Unsupported("padded colour copies exceed 64 KB");
+        if (c->rp_bytes + c->cp_bytes > 65535) throw Unsupported("padded colour copies exceed 64 KB");
         c->d_rpos = dalloc<uint16_t>(nv);
         c->d_cpos = dalloc<uint16_t>(nv);
         c->d_rinfo = dalloc<uint64_t>(n);

@@ -58,16 +58,24 @@ __device__ __forceinline__ void holders(const Graph<W>& g, const WarpSmem& s, in
                                         int& ur, int& uc) {
     const bool colhalf = lane >= 16;
     const int l16 = lane & 15;
-    const uint64_t info = colhalf ? g.cinfo[cs_] : g.rinfo[rs_];
+    // one table for both halves: rinfo[0, n) rows, rinfo[n, 2n) columns (their offsets already include the
+    // row-padded copy's size, so both halves address s.col)
+    const uint64_t info = g.rinfo[colhalf ? g.n + cs_ : rs_];
     const int off = (int)(info & 0xFFFFu), nw = (int)((info >> 16) & 0xFFFFu), vb = (int)(info >> 32);
-    const uint8_t* buf = colhalf ? s.colT : s.col;
-    uint64_t z = 0;
-    if (l16 < nw)
-        z = zero_bytes64(*reinterpret_cast<const uint64_t*>(buf + off + 8 * l16) ^
-                         ((uint64_t)ks * 0x0101010101010101ULL));
-    const unsigned bal = __ballot_sync(kFull, z != 0);
-    const int idx = 8 * l16 + ((__ffsll((long long)z) - 1) >> 3);
-    const int cand = colhalf ? (z ? (int)g.cl[vb + idx] : 0) : vb + idx;
+    // every lane loads a word of its line (clamped into it) and drops the hit if past the end; the line holds k
+    // at most once (legal colouring), so a lane sees at most one zero byte
+    const uint2 w = *reinterpret_cast<const uint2*>(s.col + off + 8 * min(l16, nw - 1));
+    const uint32_t k4 = (uint32_t)ks * 0x01010101u;
+    const uint32_t live = l16 < nw ? 0x80808080u : 0u;
+    const uint32_t xl = w.x ^ k4, xh = w.y ^ k4;
+    const uint32_t zl = ~(((xl & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | xl) & live;
+    const uint32_t zh = ~(((xh & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | xh) & live;
+    const unsigned bal = __ballot_sync(kFull, (zl | zh) != 0);
+    // byte of the single hit: the leading one of its half sits at bit 8b + 7
+    const uint32_t zz = zl ? zl : zh;
+    const int idx = 8 * l16 + (zl ? 0 : 4) + ((31 - __clz(zz)) >> 3);
+    int cand = vb + idx;
+    if (colhalf) cand = g.cl[cand];
     const int lr = __ffs(bal & 0xFFFFu) - 1, lc = __ffs(bal >> 16) - 1;
     const int a_ = __shfl_sync(kFull, cand, lr & 31);
     const int b_ = __shfl_sync(kFull, cand, (lc + 16) & 31);
@@ -141,7 +149,7 @@ __device__ int pad_prologue(const ImproveArgs& a, const Graph<W>& g, const WarpS
         int cnt = 0;
         if (k) {
             const uint16_t rc = g.cell[v];
-            cnt = count_eq(s.col, g.rinfo[rc >> 8], k) + count_eq(s.colT, g.cinfo[rc & 0xFF], k) - 2;
+            cnt = count_eq(s.col, g.rinfo[rc >> 8], k) + count_eq(s.col, g.cinfo[rc & 0xFF], k) - 2;
         }
         conf[v] = (uint8_t)cnt;
     }
@@ -170,7 +178,7 @@ __device__ int pad_prologue(const ImproveArgs& a, const Graph<W>& g, const WarpS
             if (rv0 + x != w && s.col[roff + x] == k) conf[rv0 + x] -= 1;
         for (int x = lane; x < g.cs[c + 1] - g.cs[c]; x += 32) {
             const int u = g.cl[cb + x];
-            if (u != w && s.colT[coff + x] == k) conf[u] -= 1;
+            if (u != w && s.col[coff + x] == k) conf[u] -= 1;
         }
         __syncwarp();
         if (lane == 0) {
@@ -623,7 +631,7 @@ __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs
     }
     for (int x = threadIdx.x; x < n; x += blockDim.x) {
         s_ri[x] = a.rinfo[x];
-        s_ci[x] = a.cinfo[x];
+        s_ci[x] = a.cinfo[x] + (uint64_t)a.rp_bytes;  // column offsets relative to s.col (the copies are adjacent)
     }
     for (int x = threadIdx.x; x < n * W; x += blockDim.x) {
         s_pr[x] = a.pre_row[x];
