@@ -728,7 +728,8 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
             a.prof = c->d_prof;
         }
     }
-    CK(cudaMemcpyAsync(c->d_work, &first, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    a.first = first;
+    CK(cudaMemsetAsync(c->d_work, 0, sizeof(int), c->st));
     CK(cudaEventRecord(c->ev0, c->st));
     // one individual per block when the blocks are single warps (see create): the first blocks, spread
     // round-robin over the SMs by the block scheduler, take the individuals

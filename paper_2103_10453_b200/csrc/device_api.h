@@ -51,7 +51,8 @@ struct ImproveArgs {
     size_t until_stride;        // u32 per slot (multiple of 4)
     uint32_t* slot_clock;       // per slot: tabu clock base of its next individual
     uint32_t tenure_cap;        // 10 + floor(alpha*|V|) > any tenure
-    int* work_counter;
+    int* work_counter;          // zeroed per launch; individuals past the first per slot are pulled from it
+    int first;                  // individuals [first, p) are searched
     // streams (engine.hpp:189-191): seed = derive(master, 2, gen*p_total + offset + i)
     uint64_t master, generation, p_total, offset;
     int64_t budget;

@@ -689,13 +689,8 @@ __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
     uint8_t* conf = a.conf_scratch + (size_t)slot * a.conf_stride;
 
-    for (;;) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(a.work_counter, 1);
-        i = __shfl_sync(kFull, i, 0);
-        if (i >= a.p) break;
+    for (int i = first_individual(a.first, warp); i < a.p; i = next_individual(a.first, a.work_counter, nwarps, lane))
         improve_one<W, kDebug>(a, g, s, rec, until, a.slot_clock + slot, conf, i, lane);
-    }
 }
 
 // W = 64-bit words per colour mask: 1 for n <= 63, 2 for n <= 127 (the u8 conflict

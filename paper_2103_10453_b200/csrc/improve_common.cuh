@@ -42,6 +42,19 @@ struct Graph {
     const uint64_t* cinfo = nullptr;  // [n] offset | 8-byte words << 16 | column-list base << 32
 };
 
+// Work distribution of the persistent improve kernels: the first individual of every warp slot is static --
+// slot (CTA b, warp w) takes first + b + gridDim.x * w, so a population smaller than the slot count is spread
+// evenly over the SMs and their schedulers -- and the rest are pulled from the work counter (load balance for
+// the very different per-individual step counts).
+__device__ __forceinline__ int first_individual(int first, int warp) {
+    return first + (int)blockIdx.x + (int)gridDim.x * warp;
+}
+__device__ __forceinline__ int next_individual(int first, int* counter, int nwarps, int lane) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1);
+    return first + (int)gridDim.x * nwarps + __shfl_sync(0xFFFFFFFFu, k, 0);
+}
+
 // colour of vertex v in either layout
 template <int W>
 __device__ __forceinline__ int col_of(const Graph<W>& g, const WarpSmem& s, int v) {
