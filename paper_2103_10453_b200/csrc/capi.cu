@@ -729,6 +729,12 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
         }
     }
     a.first = first;
+    {  // balanced rounds: every active slot searches the same number of individuals
+        const int todo = std::max(1, p_eff - first);
+        const int resident = c->wpc == 1 ? std::min(c->grid, todo) : c->slots;
+        const int rounds = (todo + resident - 1) / resident;
+        a.nslots = (todo + rounds - 1) / rounds;
+    }
     CK(cudaMemsetAsync(c->d_work, 0, sizeof(int), c->st));
     CK(cudaEventRecord(c->ev0, c->st));
     // one individual per block when the blocks are single warps (see create): the first blocks, spread

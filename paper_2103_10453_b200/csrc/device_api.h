@@ -53,6 +53,7 @@ struct ImproveArgs {
     uint32_t tenure_cap;        // 10 + floor(alpha*|V|) > any tenure
     int* work_counter;          // zeroed per launch; individuals past the first per slot are pulled from it
     int first;                  // individuals [first, p) are searched
+    int nslots;                 // warp slots that search (<= resident slots; balanced rounds)
     // streams (engine.hpp:189-191): seed = derive(master, 2, gen*p_total + offset + i)
     uint64_t master, generation, p_total, offset;
     int64_t budget;

@@ -689,7 +689,8 @@ __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
     uint8_t* conf = a.conf_scratch + (size_t)slot * a.conf_stride;
 
-    for (int i = first_individual(a.first, warp); i < a.p; i = next_individual(a.first, a.work_counter, nwarps, lane))
+    for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
+         i = next_individual(a.first, a.nslots, a.work_counter, lane))
         improve_one<W, kDebug>(a, g, s, rec, until, a.slot_clock + slot, conf, i, lane);
 }
 

@@ -42,17 +42,20 @@ struct Graph {
     const uint64_t* cinfo = nullptr;  // [n] offset | 8-byte words << 16 | column-list base << 32
 };
 
-// Work distribution of the persistent improve kernels: the first individual of every warp slot is static --
-// slot (CTA b, warp w) takes first + b + gridDim.x * w, so a population smaller than the slot count is spread
-// evenly over the SMs and their schedulers -- and the rest are pulled from the work counter (load balance for
-// the very different per-individual step counts).
-__device__ __forceinline__ int first_individual(int first, int warp) {
-    return first + (int)blockIdx.x + (int)gridDim.x * warp;
+// Work distribution of the persistent improve kernels.  Only `nslots` warp slots search (the host picks
+// nslots = ceil(p / rounds) with rounds = ceil(p / resident warps), so every slot gets the same number of
+// individuals and no round runs half empty); slot (CTA b, warp w) is number b + gridDim.x * w, so the active
+// slots are spread evenly over the SMs and their schedulers.  A slot's first individual is first + its
+// number, the rest are pulled from the work counter (load balance for the very different per-individual
+// step counts).
+__device__ __forceinline__ int first_individual(int first, int nslots, int p, int warp) {
+    const int s = (int)blockIdx.x + (int)gridDim.x * warp;
+    return s < nslots ? first + s : p;
 }
-__device__ __forceinline__ int next_individual(int first, int* counter, int nwarps, int lane) {
+__device__ __forceinline__ int next_individual(int first, int nslots, int* counter, int lane) {
     int k = 0;
     if (lane == 0) k = atomicAdd(counter, 1);
-    return first + (int)gridDim.x * nwarps + __shfl_sync(0xFFFFFFFFu, k, 0);
+    return first + nslots + __shfl_sync(0xFFFFFFFFu, k, 0);
 }
 
 // colour of vertex v in either layout

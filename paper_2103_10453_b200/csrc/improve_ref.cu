@@ -596,7 +596,8 @@ __global__ void __launch_bounds__(kImproveMaxThreads, 2) k_improve_ref(const Imp
     TabuRec* rec = reinterpret_cast<TabuRec*>(reinterpret_cast<char*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
     uint8_t* conf = a.conf_scratch + (size_t)slot * a.conf_stride;
-    for (int i = first_individual(a.first, warp); i < a.p; i = next_individual(a.first, a.work_counter, nwarps, lane))
+    for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
+         i = next_individual(a.first, a.nslots, a.work_counter, lane))
         improve_ref_one<W, kDebug>(a, g, s, el, msk, rec, until, a.slot_clock + slot, conf, i, lane);
 }
 

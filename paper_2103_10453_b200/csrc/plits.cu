@@ -704,7 +704,8 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits(con
     // the possibly-tabu mask lives in the slot's tabu-record area (nv * 16 >= nv * 8 W bytes); any stale
     // content is a harmless superset: every until[][] entry of an earlier individual is below its clock
     s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
-    for (int i = first_individual(a.first, warp); i < a.p; i = next_individual(a.first, a.work_counter, nwarps, lane))
+    for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
+         i = next_individual(a.first, a.nslots, a.work_counter, lane))
         plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane);
 }
 

@@ -847,7 +847,8 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits_ref(const Improve
     // bytes): shared memory stays for the colouring, the count planes and the IndexSets, which doubles
     // the resident warps
     s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
-    for (int i = first_individual(a.first, warp); i < a.p; i = next_individual(a.first, a.work_counter, nwarps, lane))
+    for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
+         i = next_individual(a.first, a.nslots, a.work_counter, lane))
         plits_ref_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane);
 }
 
