@@ -226,22 +226,24 @@ __device__ __forceinline__ TabuRec apply_move_pad(const Graph<W>& g, const WarpS
     const int rpp = g.rpos[uu], cpp = g.colpos[uu];
     const uint32_t dg = g.deg[uu];
     __syncwarp();
-    // branch-free: every lane computes, only the stores are predicated (no reconvergence blocks on the path)
-    const uint32_t nc = lane == 0 ? (uint32_t)ks : 0u;
-    pst_s8(act, s.col + rpp, nc);
-    pst_s8(act, s.colT + cpp, nc);
-    if (kDense && act) atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
-    const bool on_c = l1 | (lane == 4);
+    const uint8_t nc = lane == 0 ? (uint8_t)ks : (uint8_t)0;
+    if (act) {
+        s.col[rpp] = nc;
+        s.colT[cpp] = nc;
+        if (kDense) atomicXor(&s.U[uu >> 5], 1u << (uu & 31));
+    }
+    const bool on_c = l1 || lane == 4;
     const int line_no = on_c ? (cu & 0xFF) : (cu >> 8);
-    const bool lx = ((lane == 3) & !inR) | ((lane == 4) & !inC) | ((l1 | l2) & act);
+    const bool lx = lane == 3 ? !inR : lane == 4 ? !inC : (l1 || l2) && act;
     uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
-    pst_s64(lx, line, *line ^ bitk);  // the four lx lanes address four different words
+    if (lx) *line ^= bitk;
     acc += (act ? 4u * dg + 2u : 0u) +
            (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)f_before + (improved ? 2u * (uint32_t)g.nv : 0u) : 0u);
-    const bool ev = act & (lane > 0);
-    cache_forbid_nb(nr, ks, ut, t);
-    pst_g32(ev, until + (size_t)uu * w1 + ks, ut);
-    pst_g128(ev, rec + uu, nr.u1, nr.u2, nr.kk, nr.pad);
+    if (act && lane > 0) {
+        until[(size_t)uu * w1 + ks] = ut;
+        cache_forbid_nb(nr, ks, ut, t);
+        rec[uu] = nr;
+    }
     return nr;
 }
 
@@ -519,9 +521,11 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const TabuRec nr =
                 apply_move_pad<W, false>(g, s, rec, until, vs, ur, uc, ks, inR, inC, fb, improved, ut, ts, lane, acc);
             f = f_new;
-            bestf = improved ? f : bestf;
-            pending = pending || improved;
-            if (race_flag && improved && f <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
+            if (improved) {
+                bestf = f;
+                pending = true;
+                if (race_flag && bestf <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
+            }
             if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                 trace_step(j, vs, ks, ur, uc, rs_, cs_, fb, f, bestf, (int)tenure, N, lvl);
             ++j;

@@ -58,30 +58,6 @@ __device__ __forceinline__ int next_individual(int first, int nslots, int* count
     return first + nslots + __shfl_sync(0xFFFFFFFFu, k, 0);
 }
 
-// Predicated stores that stay predicated (the compiler otherwise wraps guarded stores in branch regions whose
-// reconvergence costs instructions and branch-resolution stalls on the step's critical path).
-__device__ __forceinline__ void pst_s8(bool p, uint8_t* ptr, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}" ::"r"((int)p),
-                 "r"((uint32_t)__cvta_generic_to_shared(ptr)), "r"(v)
-                 : "memory");
-}
-__device__ __forceinline__ void pst_s64(bool p, uint64_t* ptr, uint64_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.shared.u64 [%1], %2;\n\t}" ::"r"((int)p),
-                 "r"((uint32_t)__cvta_generic_to_shared(ptr)), "l"(v)
-                 : "memory");
-}
-__device__ __forceinline__ void pst_g32(bool p, uint32_t* ptr, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.u32 [%1], %2;\n\t}" ::"r"((int)p),
-                 "l"(ptr), "r"(v)
-                 : "memory");
-}
-__device__ __forceinline__ void pst_g128(bool p, void* ptr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.v4.u32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"((int)p),
-        "l"(ptr), "r"(x), "r"(y), "r"(z), "r"(w)
-        : "memory");
-}
-
 // colour of vertex v in either layout
 template <int W>
 __device__ __forceinline__ int col_of(const Graph<W>& g, const WarpSmem& s, int v) {
