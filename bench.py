@@ -78,6 +78,8 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttb", action="store_true")
     ap.add_argument("--ttb-ref-pop", type=int, default=1024)
+    ap.add_argument("--ttb-hard", action="store_true",
+                    help="also chase the reference's best on n=60 r=0.7 and C4 live (~15 min; tools/ttb_hard.py)")
     return ap.parse_args()
 
 
@@ -490,6 +492,7 @@ def run_ours(a):
             line["cpu_baseline"] = cpu_baseline(a, grid)
         if world == 1 and not a.no_ttb:
             line["time_to_best"] = ttb(a, P, grid)
+            line["time_to_best_multi_generation"] = ttb_hard(a)
         print(json.dumps(line))
     pop.close()
     if dist is not None:
@@ -556,6 +559,34 @@ def ttb(a, P, grid):
         out["target_score"] = target
         out["ours_reached_target"] = res.best_score >= target
     return out
+
+
+def ttb_hard(a):
+    """time to the reference's best where the generational loop matters (n=60 r=0.7: the reference improves
+    for 129 generations in 600 s; C4: optimum in generation 13): live with --ttb-hard, otherwise the committed
+    run of tools/ttb_hard.py on a B200 of this pool (profiles/r02_ttb_hard.json), summarised."""
+    if a.ttb_hard:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ttb_hard.py"), "--configs", "hard,c4",
+                              "--pops", "16384", "--limit", "600"], capture_output=True, text=True, timeout=3600)
+        src, d = "live (tools/ttb_hard.py)", json.loads(out.stdout)
+    else:
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_ttb_hard.json")) as f:
+                d = json.load(f)
+            src = "profiles/r02_ttb_hard.json (tools/ttb_hard.py on a B200 of this pool)"
+        except (OSError, ValueError):
+            return None
+    rows = []
+    for r in d.get("runs", []):
+        ref = r.get("reference", {})
+        row = {"instance": r["instance"], "target_score": r["target_score"],
+               "reference": {k: ref.get(k) for k in ("pop", "best_score", "seconds_to_best", "generations", "cores")}}
+        for k, v in r.items():
+            if k.startswith("ours_"):
+                row[k] = {x: v.get(x) for x in ("pop", "best_score", "seconds_to_best", "generations", "mode",
+                                                 "speedup_vs_reference")}
+        rows.append(row)
+    return {"source": src, "host_threads": d.get("host_threads"), "runs": rows}
 
 
 def main():
