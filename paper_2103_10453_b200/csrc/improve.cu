@@ -234,7 +234,7 @@ __device__ __forceinline__ TabuRec apply_move_pad(const Graph<W>& g, const WarpS
     }
     const bool on_c = l1 || lane == 4;
     const int line_no = on_c ? (cu & 0xFF) : (cu >> 8);
-    const bool lx = lane == 3 ? !inR : lane == 4 ? !inC : (l1 || l2) && act;
+    const bool lx = ((lane == 3) & !inR) | ((lane == 4) & !inC) | ((l1 | l2) & act);
     uint64_t* line = (on_c ? s.C : s.R) + line_no * W + kw;
     if (lx) *line ^= bitk;
     acc += (act ? 4u * dg + 2u : 0u) +
@@ -469,19 +469,34 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 #pragma unroll
             for (int z = 0; z < W; ++z) dom[z] = mine ? dom[z] : 0ULL;  // an empty slot has no candidates
             tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
-            level_masks<W>(s, r, c, dom, T, asp_s, m0, m1, m2);
-            uint64_t o0 = 0, o1 = 0, o2 = 0;
+            // delta -1 / 0 masks first; the +1 class (2% of the steps at C3) only when no lane has a move at or
+            // below 0 (warp-uniform branch)
+            uint64_t o0 = 0, o1 = 0;
 #pragma unroll
             for (int z = 0; z < W; ++z) {
+                const uint64_t Rr = s.R[r * W + z], Cc = s.C[c * W + z];
+                const uint64_t fr = dom[z] & ~Rr & ~Cc;
+                m0[z] = asp_s ? fr : (fr & ~T[z]);
+                m1[z] = dom[z] & (Rr ^ Cc) & ~T[z];
                 o0 |= m0[z];
                 o1 |= m1[z];
-                o2 |= m2[z];
             }
-            const unsigned lv = o0 ? 0u : o1 ? 1u : o2 ? 2u : 3u;
-            const int lc = (int)__reduce_min_sync(kFull, lv);
+            int lc = (int)__reduce_min_sync(kFull, o0 ? 0u : o1 ? 1u : 2u);
             uint64_t m[W];
+            if (lc == 2) {
+                uint64_t o2 = 0;
 #pragma unroll
-            for (int z = 0; z < W; ++z) m[z] = lc == 0 ? m0[z] : lc == 1 ? m1[z] : m2[z];
+                for (int z = 0; z < W; ++z) {
+                    m2[z] = dom[z] & s.R[r * W + z] & s.C[c * W + z] & ~T[z];
+                    o2 |= m2[z];
+                }
+                lc = (int)__reduce_min_sync(kFull, o2 ? 2u : 3u);
+#pragma unroll
+                for (int z = 0; z < W; ++z) m[z] = m2[z];
+            } else {
+#pragma unroll
+                for (int z = 0; z < W; ++z) m[z] = lc == 0 ? m0[z] : m1[z];
+            }
             const int cnt = popc_w<W>(m);
             int incl = warp_incl_sum(cnt);
             const int N = __shfl_sync(kFull, incl, 31);
@@ -521,11 +536,9 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const TabuRec nr =
                 apply_move_pad<W, false>(g, s, rec, until, vs, ur, uc, ks, inR, inC, fb, improved, ut, ts, lane, acc);
             f = f_new;
-            if (improved) {
-                bestf = f;
-                pending = true;
-                if (race_flag && bestf <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
-            }
+            bestf = improved ? f : bestf;
+            pending = pending || improved;
+            if (race_flag && improved && f <= race_f && lane == 0) atomicExch(const_cast<int*>(race_flag), 1);
             if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                 trace_step(j, vs, ks, ur, uc, rs_, cs_, fb, f, bestf, (int)tenure, N, lvl);
             ++j;
