@@ -10,4 +10,5 @@ POP=2048 GENS=2 BUDGET=40000 timeout 900 ncu --set full --import-source on --clo
   -o gpurun_out/imp2k_$TAG -f python tools/probes/improve_probe.py > gpurun_out/imp2k_$TAG.log 2>&1
 ncu -i gpurun_out/imp2k_$TAG.ncu-rep --page source --csv --print-source sass > gpurun_out/imp2k_${TAG}_src.csv 2>&1
 ncu -i gpurun_out/imp2k_$TAG.ncu-rep --page raw --csv > gpurun_out/imp2k_${TAG}_raw.csv 2>&1
+[ -n "$TTB" ] && timeout 1500 python tools/ttb_hard.py --configs hard,c4 --pops $TTB --race-only --reference-from profiles/r02_ttb_hard.json > gpurun_out/ttb_$TAG.json 2> gpurun_out/ttb_$TAG.err
 tail -2 gpurun_out/t_$TAG.log

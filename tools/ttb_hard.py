@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--limit", type=float, default=600.0)
     ap.add_argument("--ref-pop", type=int, default=1024)
     ap.add_argument("--pops", default="16384,4096")
+    ap.add_argument("--reference-from", default="",
+                    help="reuse the reference runs of an earlier output (same host) instead of re-running them")
+    ap.add_argument("--race-only", action="store_true")
     a = ap.parse_args()
     import oracle
     import paper_2103_10453_b200 as P
@@ -40,7 +43,14 @@ def main():
         n, r, s, what = CONFIGS[name]
         grid = P.generate_instance(n, r, s)
         rec = {"config": name, "instance": f"generate_instance({n},{r},{s})", "what": what}
-        if oracle.Reference.available():
+        prev = None
+        if a.reference_from:
+            with open(a.reference_from) as fh:
+                prev = next((x for x in json.load(fh)["runs"] if x["config"] == name), None)
+        if prev is not None:
+            rec["reference"] = dict(prev["reference"], reused_from=a.reference_from)
+            target = prev["target_score"]
+        elif oracle.Reference.available():
             ref = oracle.Reference()
             t0 = time.time()
             rr = ref.run(grid, p=a.ref_pop, seed=1, workers=threads, time_limit=a.limit, variant=1, log_cap=4096)
@@ -56,7 +66,7 @@ def main():
             target = None
         rec["target_score"] = target
         for pop in (int(x) for x in a.pops.split(",")):
-            for race in (True, False):
+            for race in ((True,) if a.race_only else (True, False)):
                 traj = []
                 t0 = time.time()
                 cfg = P.SolverConfig(p=pop, master_seed=1, time_limit=a.limit, target_score=float(target or 0),
