@@ -135,3 +135,24 @@ def test_cli_bench_suite_rows_match_oracle(plse, orc, tmp_path):
     j = json.loads((tmp_path / "a.json").read_text())
     assert [x["seed"] for x in j["rows"]] == [int(x["seed"]) for x in rows]
     assert len(j["aggregates"]) == 2
+
+
+def test_c1_twenty_generations_match_oracle(plse, orc):
+    """BASELINE configs[0] (C1): generate_instance(30, 0.5, 12345), population 64, 20 generations with the
+    default 100|V| budget; the instance is solved in generation 1, so the optimality stop (engine.hpp:237-249)
+    is disabled in both runs to reach 20 generations.  Every generation's stats, the final best and the
+    total iteration count equal the oracle's."""
+    grid = orc.generate_instance(30, 0.5, 12345)
+    seen = []
+    res = plse.run(grid, plse.SolverConfig(p=64, master_seed=1, generation_limit=20, disable_optimal_stop=True),
+                   seen.append)
+    o = orc.run(grid, p=64, seed=1, generation_limit=20, tie=oracle.TIE_CANON, disable_optimal_stop=True,
+                log_cap=32)
+    assert res.generations == o["generations"] == 20 and len(seen) == len(o["log"]) == 20
+    for st, e in zip(seen, o["log"]):
+        assert (st.generation, st.best_f, st.shortfall, st.iterations) == \
+            (e["generation"], e["best_f"], e["shortfall"], e["iterations"])
+        assert st.mean_f == e["mean_f"] and st.mean_distance == e["mean_distance"]
+    assert (res.best_f, res.total_iterations, res.stop_reason) == (o["best_f"], o["total_iterations"],
+                                                                   "generation_limit")
+    assert np.array_equal(res.best_solution, o["best_colors"])
