@@ -87,7 +87,7 @@ struct ImproveArgs {
 
 struct PadSmemLayout {
     size_t cell, rs, cs, cl, rpos, cpos, deg, rinfo, cinfo, pr, pc, graph_bytes;
-    size_t warp0, warp_bytes, w_rp, w_cp, w_list, w_R, w_C, w_U;
+    size_t warp0, warp_bytes, w_rp, w_cp, w_list, w_seed, w_R, w_C, w_U;
 };
 
 __host__ __device__ inline size_t align_up_(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -129,6 +129,8 @@ __host__ __device__ inline PadSmemLayout pad_smem_layout(int n, int nv, int lane
     w += (size_t)cp_bytes;
     L.w_list = w;
     w += 64;
+    L.w_seed = w;  // the individual's 64-bit stream seed (read when a 32-step draw window is refilled)
+    w += 16;
     w = align_up_(w, 16);
     L.w_R = w;
     w += (size_t)n * W * 8;

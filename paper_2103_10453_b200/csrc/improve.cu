@@ -214,7 +214,7 @@ template <int W, bool kDense>
 __device__ __forceinline__ TabuRec apply_move_pad(const Graph<W>& g, const WarpSmem& s, TabuRec* rec, uint32_t* until,
                                                   int vs, int ur, int uc, int ks, bool inR, bool inC, int f_before,
                                                   bool improved, uint32_t ut, uint32_t t, int lane,
-                                                  unsigned long long& acc) {
+                                                  uint32_t& acc) {
     const int w1 = g.n + 1, kw = ks >> 6;
     const uint64_t bitk = 1ULL << (ks & 63);
     const bool l1 = lane == 1, l2 = lane == 2;
@@ -276,9 +276,30 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     uint32_t j = 0;
     // SURVEY 8(d) algorithmic bytes: lane 0 accounts the scan, v*'s RMW and the
     // snapshots, lanes 1/2 the evictees' RMW; summed over the warp at the end.
-    unsigned long long acc = 0;
-    const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
-    CanonDraws draws{seed, 0u, 0u, -1};
+    // 32-bit partial byte counts (lanes 0-2), flushed into a.bytes[i] every 64 steps
+    uint32_t acc = 0;
+    if (lane == 0) a.bytes[i] = 0;
+    __syncwarp();
+    auto flush_bytes = [&]() {
+        if (lane < 3 && acc) atomicAdd(a.bytes + i, (unsigned long long)acc);
+        acc = 0;
+    };
+    // canonical draws, 32 steps per refill (CanonDraws in common.cuh, with the seed parked in shared memory
+    // and a 32-bit window to spare registers)
+    if (lane == 0) *s.seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
+    __syncwarp();
+    uint32_t dwin = 1u, dhi = 0, dlo = 0;  // window 1: no 32-step window yet
+    auto draw = [&](uint32_t jj, uint32_t& h1, uint32_t& h2) {
+        const uint32_t w = jj & ~31u;
+        if (w != dwin) {  // warp-uniform
+            const uint64_t z = canon_draw(*s.seed, (uint64_t)w + (uint64_t)lane);
+            dhi = (uint32_t)(z >> 32);
+            dlo = (uint32_t)z;
+            dwin = w;
+        }
+        h1 = __shfl_sync(kFull, dhi, jj & 31);
+        h2 = __shfl_sync(kFull, dlo, jj & 31);
+    };
     const bool tracing = kDebug && (i == a.trace_idx) && a.trace != nullptr;
     const bool probing = kDebug && (i == a.trace_idx) && a.probe.n > 0;
     int probe_next = 0;
@@ -290,7 +311,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             ++probe_next;
         }
     };
-    const int64_t budget = a.budget;
+    const int budget = (int)a.budget;  // < 2^30 (plse_create)
     const int stop_f = a.stop_f;
     const double alpha = a.alpha;
     const int* race_flag = a.race_flag;
@@ -303,6 +324,12 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         if (race_flag && *reinterpret_cast<const volatile int*>(race_flag)) return true;
         if (!deadline || jj == 0 || (jj & 0xFFFu)) return false;
         return __shfl_sync(kFull, globaltimer_ns() >= *deadline ? 1 : 0, 0) != 0;
+    };
+
+    // every 64 steps: flush the byte counts, poll the race flag / deadline
+    auto poll64 = [&](uint32_t jj) -> bool {
+        flush_bytes();
+        return poll_stop(jj);
     };
 
     // step record of the parity probe
@@ -327,14 +354,14 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
     };
 
     for (;;) {
-        if (!((int64_t)j < budget && bestf > stop_f && f > 0)) break;
-        if ((j & 63) == 0 && poll_stop(j)) break;
+        if (!((int)j < budget && bestf > stop_f && f > 0)) break;
+        if ((j & 63) == 0 && poll64(j)) break;
         if (kDebug) probe_at(j);
         const int f_before = f;
         const bool asp = (f == bestf);
         const uint32_t t = base + j;
         uint32_t h1, h2;
-        draws.at(j, lane, h1, h2);
+        draw(j, h1, h2);
         if (f > 32) {
             // ============================================== dense step (start of the descent)
             if (prof) t_step = clock64();
@@ -359,7 +386,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             int incl = warp_incl_sum(cnt);
             const int N = __shfl_sync(kFull, incl, 31);
             if (N == 0) {
-                if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
+                if (lane == 0) acc += 2u * (unsigned)w1 * (unsigned)f;
                 if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                     trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
                 ++j;
@@ -460,7 +487,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const bool asp_s = (f == bestf);
             const uint32_t ts = base + j;
             uint32_t g1, g2;
-            draws.at(j, lane, g1, g2);
+            draw(j, g1, g2);
             // ---- score this lane's slot
             const int r = (svc >> 16) & 0xFF, c = svc >> 24;
             const bool mine = lane < f;
@@ -502,12 +529,12 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const int N = __shfl_sync(kFull, incl, 31);
             if (N == 0) {
                 // every candidate tabu: no move, the clock still advances (partial.hpp:121-122)
-                if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)f;
+                if (lane == 0) acc += 2u * (unsigned)w1 * (unsigned)f;
                 if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                     trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
                 ++j;
-                if (!((int64_t)j < budget) ||
-                    ((j & 63) == 0 && poll_stop(j)))
+                if (!((int)j < budget) ||
+                    ((j & 63) == 0 && poll64(j)))
                     break;
                 continue;
             }
@@ -583,21 +610,16 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 pc_sparse += (unsigned long long)(clock64() - t_step);
                 ++pn_sparse;
             }
-            if (!((int64_t)j < budget && bestf > stop_f)) break;
-            if ((j & 63) == 0 && poll_stop(j)) break;
+            if (!((int)j < budget && bestf > stop_f)) break;
+            if ((j & 63) == 0 && poll64(j)) break;
         }
     }
     if (pending) pad_snapshot<W>(g, s, a.improved + (size_t)i * g.nvpad, lane);
-    {
-        // lanes 0..2 hold the byte-counter parts
-        const unsigned long long a1 = __shfl_sync(kFull, acc, 1), a2 = __shfl_sync(kFull, acc, 2);
-        acc += a1 + a2;
-    }
+    flush_bytes();
     if (lane == 0) {
         a.best_f[i] = bestf;
         a.repaired_f[i] = repaired_f;
         a.iters[i] = (int64_t)j;
-        a.bytes[i] = acc;
         // every until written by this individual is < base + j + 1 + tenure_cap
         *slot_clock = base + j + 2 + a.tenure_cap;
     }
@@ -692,6 +714,7 @@ __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs
     s.R = reinterpret_cast<uint64_t*>(wbase + L.w_R);
     s.C = reinterpret_cast<uint64_t*>(wbase + L.w_C);
     s.U = reinterpret_cast<uint32_t*>(wbase + L.w_U);
+    s.seed = reinterpret_cast<uint64_t*>(wbase + L.w_seed);
     // the pad bytes of both copies: 0xFF, written once (only real cells are ever stored afterwards)
     for (int x = lane; x < (a.rp_bytes + a.cp_bytes) / 16; x += 32)
         reinterpret_cast<uint4*>(wbase + L.w_rp)[x] = make_uint4(~0u, ~0u, ~0u, ~0u);

@@ -21,6 +21,7 @@ struct WarpSmem {
     uint32_t* U;
     uint8_t* colT;   // improve: colour of vertex cl[x] (column-major copy)
     uint16_t* list;  // improve: 32-entry seed list of sparse mode
+    uint64_t* seed = nullptr;  // k_improve: the individual's stream seed
 };
 
 template <int W>
