@@ -240,8 +240,19 @@ __device__ __forceinline__ TabuRec apply_move_pad(const Graph<W>& g, const WarpS
     acc += (act ? 4u * dg + 2u : 0u) +
            (lane == 0 ? 2u * (uint32_t)w1 * (uint32_t)f_before + (improved ? 2u * (uint32_t)g.nv : 0u) : 0u);
     if (act && lane > 0) {
-        until[(size_t)uu * w1 + ks] = ut;
+        // the dense until[][] row is only read while the vertex's cache is overflowed (three or more live
+        // colours), so it is only written then: the new entry while overflowed, plus the two cached pairs at
+        // the moment the cache overflows.  Colours outside a non-overflowed cache hold untils <= t there.
+        const uint32_t kk0 = nr.kk, u10 = nr.u1, u20 = nr.u2;
         cache_forbid_nb(nr, ks, ut, t);
+        if (nr.kk >> 16) {
+            uint32_t* row = until + (size_t)uu * w1;
+            row[ks] = ut;
+            if (!(kk0 >> 16)) {
+                row[kk0 & 0xFF] = u10;
+                row[(kk0 >> 8) & 0xFF] = u20;
+            }
+        }
         rec[uu] = nr;
     }
     return nr;

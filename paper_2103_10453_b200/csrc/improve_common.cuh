@@ -382,48 +382,46 @@ __device__ void probe_dump(const ImproveArgs& a, const Graph<W>& g, const WarpSm
     int total = 0, mism = 0;
     for (int v0 = 0; v0 < nv; v0 += 32) {
         const int v = v0 + lane;
-        int nl = 0;
+        // the kernel's effective tabu view: a non-overflowed cache is exact on its own; an overflowed one
+        // defers to the dense table (which k_improve writes only then)
         uint64_t live[W];
 #pragma unroll
         for (int z = 0; z < W; ++z) live[z] = 0;
-        if (v < nv)
-            for (int k = 1; k <= g.n; ++k)
-                if (until[(size_t)v * w1 + k] > t) {
-                    live[k >> 6] |= 1ULL << (k & 63);
-                    ++nl;
-                }
+        uint32_t lu[2] = {0, 0};
+        int lk[2] = {0, 0};
+        bool dense_view = false;
+        if (v < nv) {
+            const TabuRec tr = rec[v];
+            dense_view = (tr.kk >> 16) != 0;
+            if (!dense_view) {
+                lk[0] = tr.kk & 0xFF;
+                lk[1] = (tr.kk >> 8) & 0xFF;
+                lu[0] = tr.u1;
+                lu[1] = tr.u2;
+                for (int z = 0; z < 2; ++z)
+                    if (lu[z] > t) live[lk[z] >> 6] |= 1ULL << (lk[z] & 63);
+                mism += (lu[0] > t && lu[1] > t && lk[0] == lk[1]);  // a colour cached twice
+            } else {
+                for (int k = 1; k <= g.n; ++k)
+                    if (until[(size_t)v * w1 + k] > t) live[k >> 6] |= 1ULL << (k & 63);
+            }
+        }
+        int nl = 0;
+#pragma unroll
+        for (int z = 0; z < W; ++z) nl += __popcll(live[z]);
         const int incl = warp_incl_sum(nl);
         int at = total + incl - nl;
-        if (v < nv) {
+        if (v < nv)
             for (int k = 1; k <= g.n; ++k)
                 if ((live[k >> 6] >> (k & 63)) & 1) {
+                    const uint32_t u = dense_view ? until[(size_t)v * w1 + k] : (k == lk[0] && lu[0] > t ? lu[0] : lu[1]);
                     if (at < a.probe.cap) {
                         tb[3 * at] = v;
                         tb[3 * at + 1] = k;
-                        tb[3 * at + 2] = (int32_t)(until[(size_t)v * w1 + k] - base);
+                        tb[3 * at + 2] = (int32_t)(u - base);
                     }
                     ++at;
                 }
-            const TabuRec tr = rec[v];
-            if (!(tr.kk >> 16)) {  // exact cache: its live pairs must be the dense table's live set
-                uint64_t cm[W];
-#pragma unroll
-                for (int z = 0; z < W; ++z) cm[z] = 0;
-                const int k1 = tr.kk & 0xFF, k2 = (tr.kk >> 8) & 0xFF;
-                bool bad = false;
-                if (tr.u1 > t) {
-                    cm[k1 >> 6] |= 1ULL << (k1 & 63);
-                    bad |= until[(size_t)v * w1 + k1] != tr.u1;
-                }
-                if (tr.u2 > t) {
-                    cm[k2 >> 6] |= 1ULL << (k2 & 63);
-                    bad |= until[(size_t)v * w1 + k2] != tr.u2;
-                }
-#pragma unroll
-                for (int z = 0; z < W; ++z) bad |= cm[z] != live[z];
-                mism += bad;
-            }
-        }
         total += __shfl_sync(kFull, incl, 31);
     }
     mism = (int)__reduce_add_sync(kFull, (unsigned)mism);
