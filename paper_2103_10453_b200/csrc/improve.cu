@@ -651,7 +651,9 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
 template <int W, bool kDebug>
 __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int lane;  // %laneid through volatile asm: kept in a register instead of re-derived from %tid every use
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
     const int n = a.n, nv = a.nv;
     const PadSmemLayout L = pad_smem_layout(n, nv, a.lane_words, W, a.rp_bytes, a.cp_bytes);
     uint16_t* s_cell = reinterpret_cast<uint16_t*>(smem + L.cell);
