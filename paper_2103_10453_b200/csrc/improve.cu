@@ -506,17 +506,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             dom_mask<W>(g, r, c, dom);
 #pragma unroll
             for (int z = 0; z < W; ++z) dom[z] = mine ? dom[z] : 0ULL;  // an empty slot has no candidates
-            // tabu mask from the two cached pairs; a vertex whose cache overflowed (three or more live colours)
-            // reads its dense row instead -- rare, so behind a warp-uniform test
-            {
-                const int k1 = skk & 0xFF, k2 = (skk >> 8) & 0xFF;
-#pragma unroll
-                for (int z = 0; z < W; ++z)
-                    T[z] = ((su1 > ts && (k1 >> 6) == z) ? 1ULL << (k1 & 63) : 0ULL) |
-                           ((su2 > ts && (k2 >> 6) == z) ? 1ULL << (k2 & 63) : 0ULL);
-                if (__any_sync(kFull, skk >> 16) && (skk >> 16))
-                    tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
-            }
+            tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
             // delta -1 / 0 masks first; the +1 class (2% of the steps at C3) only when no lane has a move at or
             // below 0 (warp-uniform branch)
             uint64_t o0 = 0, o1 = 0;
