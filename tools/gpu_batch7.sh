@@ -23,4 +23,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 ncu --set full --clock-control none -k regex:k_sim_tc --launch-skip 2 -c 1 -o gpurun_out/k3_$TAG -f \
   python bench.py --steps 1 --warmup 1 --no-ttb --no-cpu-baseline > gpurun_out/k3_$TAG.log 2>&1
 ncu -i gpurun_out/k3_$TAG.ncu-rep --page raw --csv > gpurun_out/k3_${TAG}_raw.csv 2>&1
+PLSE_BENCH_DIST=gloo PLSE_BENCH_ONE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --pop 4096 --steps 2 --warmup 3 --no-ttb \
+  --no-cpu-baseline > gpurun_out/functional_2rank_$TAG.json 2> gpurun_out/functional_2rank_$TAG.err
 tail -2 gpurun_out/t_$TAG.log
