@@ -64,10 +64,11 @@ def main():
         "inst_per_move": inst / moves if inst and moves else None,
         "issue_active_pct": num(r.get("sm__inst_issued.avg.pct_of_peak_sustained_active")),
         "warps_active_pct": num(r.get("sm__warps_active.avg.pct_of_peak_sustained_active")),
-        "sm_mhz": (num(r.get("sm__cycles_elapsed.avg.per_second")) or 0) / 1e6 or None,
+        "sm_ghz": num(r.get("sm__cycles_elapsed.avg.per_second")),  # ncu reports it in GHz
         "source": os.path.relpath(raw, ROOT), "generation": gen,
-        "note": "ncu --set full --clock-control none of one launch (the generation above) of improve_probe.py; "
-                "dram bytes = dram__bytes_read.sum + dram__bytes_write.sum",
+        "note": "ncu --clock-control none (sections SpeedOfLight/LaunchStats/Occupancy/WarpStateStats/"
+                "SchedulerStats plus instruction and DRAM metrics) of one launch (the generation above) of "
+                "improve_probe.py; dram bytes = dram__bytes_read.sum + dram__bytes_write.sum",
     }
     with open(out, "w") as f:
         json.dump(summary, f, indent=1)
