@@ -443,7 +443,7 @@ def run_ours(a):
                                    "reference's step reads; this kernel derives gamma from occupancy masks)"),
                 "kernel_share_of_step": imp_ms / ms,
                 "binding_limit": "instruction issue (the gamma table is never materialised: measured DRAM "
-                                 "traffic is a few % of the algorithmic bytes)"}
+                                 "traffic is well under 1% of the algorithmic bytes; see roofline.issue)"}
         if prof and prof.get("inst_per_move") and clk.get("sm_mhz"):
             peak_inst = 148 * 4 * clk["sm_mhz"] * 1e6
             ach_inst = prof["inst_per_move"] * improve_rate
