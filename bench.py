@@ -276,7 +276,7 @@ def run_reference(a):
     v = moves / secs
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": 1000 * secs / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": 1000 * secs / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic (generate_instance(60,0.5,12345), random initial population)",
         "config": {"workload": f"PLSE n={a.n} r={a.r} seed={a.seed}: reference improve phase "
                                + (f"(plits_run, parallel_for) on {s} individuals, budgets 100|V| + 2|V|" if mpma else
