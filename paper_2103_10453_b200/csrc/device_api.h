@@ -115,10 +115,10 @@ __host__ __device__ inline PadSmemLayout pad_smem_layout(int n, int nv, int lane
     o += (size_t)n * 8;
     L.cinfo = o;
     o += (size_t)n * 8;
-    L.pr = o;
-    o += (size_t)n * W * 8;
+    L.pr = o;  // n + 1 lines: line n is the all-prefilled dummy line of the empty slot-list lanes
+    o += (size_t)(n + 1) * W * 8;
     L.pc = o;
-    o += (size_t)n * W * 8;
+    o += (size_t)(n + 1) * W * 8;
     o = align_up_(o, 16);
     L.graph_bytes = o;
     L.warp0 = o;
@@ -132,10 +132,10 @@ __host__ __device__ inline PadSmemLayout pad_smem_layout(int n, int nv, int lane
     L.w_seed = w;  // the individual's 64-bit stream seed (read when a 32-step draw window is refilled)
     w += 16;
     w = align_up_(w, 16);
-    L.w_R = w;
-    w += (size_t)n * W * 8;
+    L.w_R = w;  // n + 1 lines (line n: the dummy line, always empty)
+    w += (size_t)(n + 1) * W * 8;
     L.w_C = w;
-    w += (size_t)n * W * 8;
+    w += (size_t)(n + 1) * W * 8;
     L.w_U = w;
     w += (size_t)32 * lane_words * 4;
     L.warp_bytes = align_up_(w, 16);

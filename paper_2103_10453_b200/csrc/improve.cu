@@ -23,7 +23,7 @@
 //     record per vertex caches its two most recent (colour, until) pairs plus
 //     an overflow flag; only a vertex with three or more live tabu colours
 //     reads the dense table.
-//   * Sparse mode (|V0| <= 32, i.e. everything after the first ~1% of the
+//   * Sparse mode (|V0| <= 31, i.e. everything after the first ~1% of the
 //     descent) is a tight, branch-light inner loop: lane l holds the l-th
 //     uncoloured vertex (ascending id, with its row / column packed in) and
 //     its tabu pairs in registers, so scoring costs four shared loads per
@@ -189,7 +189,7 @@ __device__ int pad_prologue(const ImproveArgs& a, const Graph<W>& g, const WarpS
         __syncwarp();
     }
     // ---- occupancy masks R / C and the uncoloured bitmask U
-    for (int x = lane; x < n * W; x += 32) {
+    for (int x = lane; x < (n + 1) * W; x += 32) {
         s.R[x] = 0;
         s.C[x] = 0;
     }
@@ -373,7 +373,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
         const uint32_t t = base + j;
         uint32_t h1, h2;
         draw(j, h1, h2);
-        if (f > 32) {
+        if (f > 31) {  // sparse mode holds at most 31 so lane 31 is always an empty slot
             // ============================================== dense step (start of the descent)
             if (prof) t_step = clock64();
             int c0 = 0, c1 = 0, c2 = 0;
@@ -463,10 +463,12 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             continue;
         }
 
-        // ================================================== sparse phase (|V0| <= 32)
+        // ================================================== sparse phase (|V0| <= 31)
         if (prof) ++pn_enter;
         // lane l takes the l-th uncoloured vertex (ascending v) with its tabu cache
-        uint32_t svc = 0xFFFFu, su1 = 0, su2 = 0, skk = 0;
+        // an empty lane holds the dummy vertex 0xFFFF on the dummy line n: empty domain, no candidates
+        const uint32_t kEmpty = 0xFFFFu | ((uint32_t)n << 16) | ((uint32_t)n << 24);
+        uint32_t svc = kEmpty, su1 = 0, su2 = 0, skk = 0;
         {
             int cnt = 0;
             for (int q = 0; q < g.lane_words; ++q) cnt += __popc(s.U[lane * g.lane_words + q]);
@@ -491,6 +493,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             }
             __syncwarp();
         }
+        uint32_t jnext = min((uint32_t)budget, (j + 64) & ~63u);  // next budget / poll check point
         for (;;) {
             if (prof) t_step = clock64();
             if (kDebug) probe_at(j);
@@ -505,8 +508,8 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             uint64_t dom[W], T[W], m0[W], m1[W], m2[W];
             dom_mask<W>(g, r, c, dom);
 #pragma unroll
-            for (int z = 0; z < W; ++z) dom[z] = mine ? dom[z] : 0ULL;  // an empty slot has no candidates
             tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
+            const uint64_t tmask = asp_s ? 0ULL : ~0ULL;
             // delta -1 / 0 masks first; the +1 class (2% of the steps at C3) only when no lane has a move at or
             // below 0 (warp-uniform branch)
             uint64_t o0 = 0, o1 = 0;
@@ -514,7 +517,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             for (int z = 0; z < W; ++z) {
                 const uint64_t Rr = s.R[r * W + z], Cc = s.C[c * W + z];
                 const uint64_t fr = dom[z] & ~Rr & ~Cc;
-                m0[z] = asp_s ? fr : (fr & ~T[z]);
+                m0[z] = fr & ~(T[z] & tmask);  // aspiration (f = best f) admits the tabu delta -1 moves
                 m1[z] = dom[z] & (Rr ^ Cc) & ~T[z];
                 o0 |= m0[z];
                 o1 |= m1[z];
@@ -544,9 +547,10 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                     trace_step(j, -1, 0, -1, -1, 0, 0, f, f, bestf, -1, 0, 2);
                 ++j;
-                if (!((int)j < budget) ||
-                    ((j & 63) == 0 && poll64(j)))
-                    break;
+                if (j == jnext) {
+                    if (!((int)j < budget) || ((j & 63) == 0 && poll64(j))) break;
+                    jnext = min((uint32_t)budget, (j + 64) & ~63u);
+                }
                 continue;
             }
             const uint32_t rnk = __umulhi(g1, (uint32_t)N);
@@ -580,7 +584,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             if (tracing && lane == 0 && (int64_t)j < a.trace_cap)
                 trace_step(j, vs, ks, ur, uc, rs_, cs_, fb, f, bestf, (int)tenure, N, lvl);
             ++j;
-            if (f_new > 32) {
+            if (f_new > 31) {
                 __syncwarp();
                 rebuild_U<W>(g, s, lane);  // sparse mode leaves U stale; dense mode scans it
                 if (prof) {
@@ -599,7 +603,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 const int pr_ = ur >= 0 ? __popc(br) + ((unsigned)uc < (unsigned)ur) : 64;
                 const int pc_ = uc >= 0 ? __popc(bc) + ((unsigned)ur < (unsigned)uc) : 64;
                 const int y = lane - (pr_ < lane) - (pc_ < lane);
-                const int src = (y >= wl ? y + 1 : y) & 31;
+                const int src = min(y >= wl ? y + 1 : y, 31);  // lanes past the list read the empty lane 31
                 const uint32_t mvc = __shfl_sync(kFull, svc, src);
                 const uint32_t mu1 = __shfl_sync(kFull, su1, src);
                 const uint32_t mu2 = __shfl_sync(kFull, su2, src);
@@ -621,8 +625,13 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 pc_sparse += (unsigned long long)(clock64() - t_step);
                 ++pn_sparse;
             }
-            if (!((int)j < budget && bestf > stop_f)) break;
-            if ((j & 63) == 0 && poll64(j)) break;
+            // the budget, the stop f and the 64-step poll only at the precomputed next check point (or after an
+            // improvement, the only time best f changes)
+            if (j == jnext || improved) {
+                if (!((int)j < budget && bestf > stop_f)) break;
+                if ((j & 63) == 0 && poll64(j)) break;
+                jnext = min((uint32_t)budget, (j + 64) & ~63u);
+            }
         }
     }
     if (pending) pad_snapshot<W>(g, s, a.improved + (size_t)i * g.nvpad, lane);
@@ -681,9 +690,10 @@ __global__ void __launch_bounds__(kPadMaxThreads, 1) k_improve(const ImproveArgs
         s_ri[x] = a.rinfo[x];
         s_ci[x] = a.cinfo[x] + (uint64_t)a.rp_bytes;  // column offsets relative to s.col (the copies are adjacent)
     }
-    for (int x = threadIdx.x; x < n * W; x += blockDim.x) {
-        s_pr[x] = a.pre_row[x];
-        s_pc[x] = a.pre_col[x];
+    for (int x = threadIdx.x; x < (n + 1) * W; x += blockDim.x) {
+        // line n: every symbol prefilled -> the empty domain of the dummy vertex held by empty slot-list lanes
+        s_pr[x] = x < n * W ? a.pre_row[x] : ~0ULL;
+        s_pc[x] = x < n * W ? a.pre_col[x] : ~0ULL;
     }
     __syncthreads();
     for (int x = threadIdx.x; x < nv; x += blockDim.x) {
