@@ -507,7 +507,6 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
             const bool mine = lane < f;
             uint64_t dom[W], T[W], m0[W], m1[W], m2[W];
             dom_mask<W>(g, r, c, dom);
-#pragma unroll
             tabu_of<W>(su1, su2, skk, until + (size_t)(svc & 0xFFFFu) * w1, dom, ts, T);
             const uint64_t tmask = asp_s ? 0ULL : ~0ULL;
             // delta -1 / 0 masks first; the +1 class (2% of the steps at C3) only when no lane has a move at or
