@@ -8,13 +8,11 @@
 // equality-kernel factorisation (the equality matrix on D(v) has rank |D(v)|).
 //
 // k_onehot expands u8 colour rows into 0/1 u8 rows (K padded to 128);
-// k_sim_tc is persistent (one CTA per SM) over 128x256 output tiles: TMA
-// (128B swizzle) -> 4-stage shared-memory ring -> tcgen05.mma.cta_group::1.kind::i8
-// (K = 32 per instruction, s32 accumulators in TMEM) into one of two 256-column
-// accumulators -> tcgen05.ld epilogue (|V| - S as u16) by four epilogue warps
-// while the MMAs of the next tile fill the other accumulator.  One thread issues
-// TMA, one issues MMA.
-#include <algorithm>
+// k_sim_tc computes 128x256 output tiles: TMA (128B swizzle) -> 4-stage
+// shared-memory ring -> tcgen05.mma.cta_group::1.kind::i8 (K = 32 per
+// instruction, s32 accumulators in TMEM, 256 columns) -> tcgen05.ld epilogue
+// that writes |V| - S as u16.  One elected thread issues TMA, one issues MMA;
+// all four warps drain TMEM.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -28,7 +26,7 @@ constexpr int kTcGroupM = 12;  // tile rows per raster group
 constexpr int kTcABytes = kTcBM * kTcBK;  // 16 KB
 constexpr int kTcBBytes = kTcBN * kTcBK;  // 32 KB
 constexpr int kTcStageBytes = kTcABytes + kTcBBytes;
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 + 256;  // ring + alignment slack + barriers / TMEM slot
+constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024 + 256;
 constexpr uint32_t kTcTmemCols = 256;
 
 // ---------------------------------------------------------------- one-hot
@@ -113,55 +111,38 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 }
 
 // ---------------------------------------------------------------- GEMM
-// Persistent: one CTA per SM walks the output tiles (grouped raster, strictly-lower tiles of a symmetric
-// block skipped).  Warp 0: TMA producer (one lane); warp 1: MMA issuer (one lane); warps 2-5: epilogue.
-// Two 256-column TMEM accumulators (512 columns): the epilogue of tile t drains one while the MMAs of tile
-// t+1 fill the other, so the tensor pipe does not idle behind the TMEM -> registers -> global epilogue.
-constexpr int kTcThreads = 192;
-constexpr uint32_t kTcTmemAlloc = 2 * kTcTmemCols;
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ bool tile_of(int lin, int M, int N, int upper, int& tile_m, int& tile_n) {
-    const int nt_n = (N + kTcBN - 1) / kTcBN, nt_m = (M + kTcBM - 1) / kTcBM;
-    const int per_group = kTcGroupM * nt_n;
-    const int first_m = (lin / per_group) * kTcGroupM, gm = min(nt_m - first_m, kTcGroupM);
-    tile_m = first_m + (lin % per_group) % gm;
-    tile_n = (lin % per_group) / gm;
-    // symmetric block (A == B): tiles strictly below the diagonal are skipped, the consumer reads [min][max]
-    return !(upper && (tile_n + 1) * kTcBN <= tile_m * kTcBM);
-}
-
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(128, 1)
     k_sim_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
              int num_kb, int nv, uint16_t* __restrict__ D, int ldd, int upper) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kTcStages + 4);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kTcStages + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tiles = ((N + kTcBN - 1) / kTcBN) * ((M + kTcBM - 1) / kTcBM);
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcStages);
-    const uint32_t accf0 = smem_u32(bars + 2 * kTcStages), acce0 = smem_u32(bars + 2 * kTcStages + 2);
+    // grouped raster: consecutive CTAs walk kTcGroupM tile rows, then the next tile column, so one wave
+    // of resident CTAs shares ~12 A tiles and ~12 B tiles per K slab in L2 (row-major order would stream
+    // every B tile once per tile row from DRAM)
+    const int nt_n = (N + kTcBN - 1) / kTcBN, nt_m = (M + kTcBM - 1) / kTcBM;
+    const int lin = blockIdx.x, per_group = kTcGroupM * nt_n;
+    const int first_m = (lin / per_group) * kTcGroupM, gm = min(nt_m - first_m, kTcGroupM);
+    const int tile_m = first_m + (lin % per_group) % gm, tile_n = (lin % per_group) / gm;
+    // symmetric block (A == B): tiles strictly below the diagonal are skipped, the consumer reads [min][max]
+    if (upper && (tile_n + 1) * kTcBN <= tile_m * kTcBM) return;
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kTcStages), done = smem_u32(bars + 2 * kTcStages);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(accf0 + 8 * b, 1);  // the MMA issuer's commit
-            mbar_init(acce0 + 8 * b, 4);  // one arrive per epilogue warp
-        }
+        mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTcTmemAlloc));
+                     "r"(kTcTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -169,111 +150,76 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_d = *tmem_slot;
 
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---- TMA producer: the smem ring runs continuously across this CTA's tiles
-            int it = 0;
-            for (int lin = blockIdx.x; lin < tiles; lin += gridDim.x) {
-                int tm, tn;
-                if (!tile_of(lin, M, N, upper, tm, tn)) continue;
-                for (int kb = 0; kb < num_kb; ++kb, ++it) {
-                    const int s = it % kTcStages;
-                    const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
-                    mbar_wait(empty0 + 8 * s, ph ^ 1u);
-                    uint8_t* sa = smem + s * kTcStageBytes;
-                    mbar_expect_tx(full0 + 8 * s, kTcStageBytes);
-                    tma_load_2d(smem_u32(sa), &tmA, full0 + 8 * s, kb * kTcBK, tm * kTcBM);
-                    tma_load_2d(smem_u32(sa + kTcABytes), &tmB, full0 + 8 * s, kb * kTcBK, tn * kTcBN);
-                }
-            }
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (uint32_t)(kb / kTcStages) & 1u;
+            if (kb >= kTcStages) mbar_wait(empty0 + 8 * s, ph ^ 1u);
+            uint8_t* sa = smem + s * kTcStageBytes;
+            mbar_expect_tx(full0 + 8 * s, kTcStageBytes);
+            tma_load_2d(smem_u32(sa), &tmA, full0 + 8 * s, kb * kTcBK, tile_m * kTcBM);
+            tma_load_2d(smem_u32(sa + kTcABytes), &tmB, full0 + 8 * s, kb * kTcBK, tile_n * kTcBN);
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ---- MMA issuer (one thread for the CTA), alternating between the two TMEM accumulators
-            int it = 0, lt = 0;
-            for (int lin = blockIdx.x; lin < tiles; lin += gridDim.x) {
-                int tm, tn;
-                if (!tile_of(lin, M, N, upper, tm, tn)) continue;
-                const int acc = lt & 1;
-                const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-                mbar_wait(acce0 + 8 * acc, aph ^ 1u);  // the epilogue drained this accumulator
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t td = tmem_d + (uint32_t)(acc * kTcTmemCols);
-                for (int kb = 0; kb < num_kb; ++kb, ++it) {
-                    const int s = it % kTcStages;
-                    const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
-                    mbar_wait(full0 + 8 * s, ph);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t sa = smem_u32(smem + s * kTcStageBytes);
-                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kTcABytes);
-#pragma unroll
-                    for (int kk = 0; kk < kTcBK / 32; ++kk)
-                        umma_i8(td, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), kTcIdesc, (kb | kk) != 0);
-                    umma_commit(empty0 + 8 * s);  // frees the stage when these MMAs retire
-                }
-                umma_commit(accf0 + 8 * acc);  // the accumulator is complete
-                ++lt;
-            }
-        }
-    } else {
-        // ---- epilogue: warp w drains TMEM lanes [32 (w % 4), +32) = output rows of the tile
-        const int g = warp & 3;
-        int lt = 0;
-        for (int lin = blockIdx.x; lin < tiles; lin += gridDim.x) {
-            int tm, tn;
-            if (!tile_of(lin, M, N, upper, tm, tn)) continue;
-            const int acc = lt & 1;
-            const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-            mbar_wait(accf0 + 8 * acc, aph);
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer (one thread for the CTA)
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (uint32_t)(kb / kTcStages) & 1u;
+            mbar_wait(full0 + 8 * s, ph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int row = tm * kTcBM + g * 32 + lane;
-            uint16_t* drow = D + (size_t)row * ldd + (size_t)tn * kTcBN;
+            const uint32_t sa = smem_u32(smem + s * kTcStageBytes);
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kTcABytes);
+#pragma unroll
+            for (int kk = 0; kk < kTcBK / 32; ++kk)
+                umma_i8(tmem_d, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), kTcIdesc, (kb | kk) != 0);
+            umma_commit(empty0 + 8 * s);  // frees the stage when these MMAs retire
+        }
+        umma_commit(done);
+    }
+    __syncwarp();
+
+    // ---- epilogue: warp w drains TMEM lanes [32w, 32w+32) = output rows of this warp
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = tile_m * kTcBM + warp * 32 + lane;
+    uint16_t* drow = D + (size_t)row * ldd + (size_t)tile_n * kTcBN;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kTcBN; c0 += 32) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem_d + ((uint32_t)(g * 32) << 16) + (uint32_t)(acc * kTcTmemCols + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
-                    "[%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < M) {
-                    const int col0 = tn * kTcBN + c0;
-                    if (col0 + 32 <= N) {
-                        uint32_t pk[16];
+    for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M) {
+            const int col0 = tile_n * kTcBN + c0;
+            if (col0 + 32 <= N) {
+                uint32_t pk[16];
 #pragma unroll
-                        for (int q = 0; q < 16; ++q)
-                            pk[q] = ((uint32_t)(nv - (int)v[2 * q]) & 0xFFFFu) | ((uint32_t)(nv - (int)v[2 * q + 1]) << 16);
-                        uint4* d4 = reinterpret_cast<uint4*>(drow + c0);
-                        if ((reinterpret_cast<uintptr_t>(d4) & 15) == 0) {
+                for (int q = 0; q < 16; ++q)
+                    pk[q] = ((uint32_t)(nv - (int)v[2 * q]) & 0xFFFFu) | ((uint32_t)(nv - (int)v[2 * q + 1]) << 16);
+                uint4* d4 = reinterpret_cast<uint4*>(drow + c0);
+                if ((reinterpret_cast<uintptr_t>(d4) & 15) == 0) {
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                        } else {
+                    for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                } else {
 #pragma unroll
-                            for (int q = 0; q < 32; ++q) drow[c0 + q] = (uint16_t)(nv - (int)v[q]);
-                        }
-                    } else {
-                        for (int q = 0; q < 32 && col0 + q < N; ++q) drow[c0 + q] = (uint16_t)(nv - (int)v[q]);
-                    }
+                    for (int q = 0; q < 32; ++q) drow[c0 + q] = (uint16_t)(nv - (int)v[q]);
                 }
+            } else {
+                for (int q = 0; q < 32 && col0 + q < N; ++q) drow[c0 + q] = (uint16_t)(nv - (int)v[q]);
             }
-            // every lane's TMEM reads are complete (wait::ld); hand the accumulator back to the MMA issuer
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acce0 + 8 * acc);
-            ++lt;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(kTcTmemAlloc));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(kTcTmemCols));
 }
 
 // ---------------------------------------------------------------- host
@@ -317,10 +263,7 @@ cudaError_t launch_similarity_tc(const uint8_t* HA, int M, const uint8_t* HB, in
     CUtensorMap ma, mb;
     if (!make_map(&ma, HA, M, Kpad, kTcBM) || !make_map(&mb, HB, N, Kpad, kTcBN)) return cudaErrorInvalidValue;
     const int tiles = ((N + kTcBN - 1) / kTcBN) * ((M + kTcBM - 1) / kTcBM);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    k_sim_tc<<<std::min(tiles, nsm), kTcThreads, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd, upper);
+    k_sim_tc<<<tiles, 128, kTcSmem, st>>>(ma, mb, M, N, Kpad / kTcBK, nv, D, ldd, upper);
     return cudaGetLastError();
 }
 
