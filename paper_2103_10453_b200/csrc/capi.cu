@@ -14,6 +14,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "device_api.h"
 #include "host_internal.h"
 #include "plse_b200.h"
@@ -23,6 +25,13 @@ using namespace plse_dev;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range per phase (header-only NVTX v3: no library dependency; a no-op without a tool attached), so
+// ncu --nvtx / any NVTX-aware profiler can attribute the generation's kernels to run()'s phases
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // run()'s deadline on the device clock: now + remaining (engine.hpp:148-151)
 __global__ void k_set_deadline(unsigned long long* deadline, unsigned long long remaining_ns) {
@@ -1094,6 +1103,7 @@ int plse_device_colors(plse_ctx* c, int32_t which, void** dev_ptr, int64_t* row_
 }
 
 int plse_init_population(plse_ctx* c) {
+    NvtxRange nvtx_("plse.init_population");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1111,6 +1121,7 @@ int plse_full_distances(plse_ctx* c) {
 }
 
 int plse_improve(plse_ctx* c, uint64_t generation, int64_t* iters_total, int32_t* best_f, int32_t* best_idx) {
+    NvtxRange nvtx_("plse.improve");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1120,6 +1131,7 @@ int plse_improve(plse_ctx* c, uint64_t generation, int64_t* iters_total, int32_t
 }
 
 int plse_distances(plse_ctx* c) {
+    NvtxRange nvtx_("plse.distances");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1132,6 +1144,7 @@ int plse_distances(plse_ctx* c) {
 }
 
 int plse_update(plse_ctx* c, int32_t* pool_best_f, int32_t* n_shortfall, int32_t* shortfall_slots) {
+    NvtxRange nvtx_("plse.update");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1151,6 +1164,7 @@ int plse_reset_exclusion(plse_ctx* c) {
 }
 
 int plse_offspring(plse_ctx* c, uint64_t generation) {
+    NvtxRange nvtx_("plse.offspring");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1239,6 +1253,7 @@ int plse_probe(plse_ctx* c, int32_t idx, uint64_t generation, int32_t n_steps, c
 }
 
 int plse_export_elites(plse_ctx* c, int32_t n_elite, void* dev_out, int32_t* f_out) {
+    NvtxRange nvtx_("plse.export_elites");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1258,6 +1273,7 @@ int plse_export_elites(plse_ctx* c, int32_t n_elite, void* dev_out, int32_t* f_o
 }
 
 int plse_import_migrants(plse_ctx* c, int32_t n_in, const void* dev_in) {
+    NvtxRange nvtx_("plse.import_migrants");
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
@@ -1396,8 +1412,11 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
         for (int64_t gen = 1;; ++gen) {
             int64_t it = 0;
             int32_t bf = 0, bi = -1;
-            improve_impl(c, (uint64_t)gen, -1, 0, nullptr, p, 0);
-            collect_improve(c, &it, &bf, &bi);
+            {
+                NvtxRange r_("plse.solve.improve");
+                improve_impl(c, (uint64_t)gen, -1, 0, nullptr, p, 0);
+                collect_improve(c, &it, &bf, &bi);
+            }
             res->total_iterations += it;
             res->generations = gen;
             if (bi >= 0 && bf < res->best_f) {
@@ -1419,9 +1438,12 @@ int plse_solve(int32_t n, const uint16_t* grid, const plse_solver_config* cfg, p
                                    : PLSE_STOP_TARGET);
                 return;
             }
-            cross_distances(c);
             int32_t nsf = 0;
-            update_impl(c, nullptr, cb ? &nsf : nullptr, nullptr);
+            {
+                NvtxRange r_("plse.solve.population");
+                cross_distances(c);
+                update_impl(c, nullptr, cb ? &nsf : nullptr, nullptr);
+            }
             if (c->prm.exclusion == PLSE_E_GENERATION) CK(cudaMemset(c->d_excl, 0, 4ull * p * c->excl_words));
             offspring_impl(c, (uint64_t)gen);
             emit_stats(gen, nsf);
