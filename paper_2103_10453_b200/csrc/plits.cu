@@ -51,6 +51,8 @@ struct PlitsWarp {
     uint64_t* T;      // [nv][W] GLOBAL (the slot's tabu-record area, L1-resident for a lone warp): colours
                       //         possibly tabu -- a superset of the live until[][] entries, so only those
                       //         colours read until[][]
+    uint16_t* X;      // [2n][n+1] GLOBAL (same area, after T): per row (then per column) and colour, the XOR of
+                      //         the ids of its cells holding that colour -- the one cell when the count is 1
 };
 
 // tabu-blind minimum delta over v's candidates (plits.hpp:135-176 without the tabu test)
@@ -154,23 +156,71 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int lane, int
     __syncwarp();
 }
 
+// x / wc with the phase-1 weight wc = 1 kept off the integer-division path
+__device__ __forceinline__ int div_wc(int x, int wc) { return wc == 1 ? x : x / wc; }
+
+// the xor-of-ids tables of the colouring in s.col: lane l builds lines l, l + 32, ... (rows, then columns)
+template <int W>
+__device__ void plits_build_xor(const Graph<W>& g, const PlitsWarp& s, int lane) {
+    const int n = g.n, w1 = n + 1;
+    for (int line = lane; line < 2 * n; line += 32) {
+        const bool is_row = line < n;
+        const int idx = is_row ? line : line - n;
+        uint16_t* X = s.X + (size_t)line * w1;
+        for (int k = 0; k <= n; ++k) X[k] = 0;
+        const int lo = is_row ? g.rs[idx] : g.cs[idx], hi = is_row ? g.rs[idx + 1] : g.cs[idx + 1];
+        for (int x = lo; x < hi; ++x) {
+            const int u = is_row ? x : g.cl[x];
+            const int k = s.col[u];
+            if (k) X[k] ^= (uint16_t)u;
+        }
+    }
+    __syncwarp();
+}
+
+// plane_move that also returns the line's counts of `from` and `to` after the move (0 for colour 0)
+template <int W, int NP>
+__device__ __forceinline__ void plane_move_count(uint64_t* P, int from, int to, int& cf, int& ct) {
+    cf = 0;
+    ct = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const bool hf = from && (from >> 6) == q, ht = to && (to >> 6) == q;
+        if (!hf && !ht) continue;
+        uint64_t borrow = hf ? 1ULL << (from & 63) : 0ULL;
+        uint64_t carry = ht ? 1ULL << (to & 63) : 0ULL;
+#pragma unroll
+        for (int b = 0; b < NP; ++b) {
+            const uint64_t old = P[b * W + q];
+            const uint64_t mid = old ^ borrow;
+            borrow &= ~old;
+            const uint64_t x = mid ^ carry;
+            carry &= mid;
+            P[b * W + q] = x;
+            if (hf) cf |= (int)((x >> (from & 63)) & 1ULL) << b;
+            if (ht) ct |= (int)((x >> (to & 63)) & 1ULL) << b;
+        }
+    }
+}
+
 // the admissible moves of one vertex at delta level dl (plits.hpp:146-147): adm = colours k != 0,
-// adm0 = the move to 0.  Only colours in the possibly-tabu mask (tv, loaded by the caller ahead of the
-// move classes so the load overlaps them) read until[][] (independent batches of four); expired ones
-// leave the mask Tv.
+// adm0 = the move to 0.  Only colours in the possibly-tabu mask tv (loaded by the caller ahead of the
+// move classes so the load overlaps them) read until[][] (independent pairs of loads); expired ones
+// leave tv (tv_changed tells the caller to store it back).
 template <int W>
 __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
-                                         uint64_t* Tv, const uint64_t (&tv)[W], uint32_t t, uint64_t (&adm)[W],
-                                         bool& adm0) {
+                                         uint64_t (&tv)[W], uint32_t t, uint64_t (&adm)[W], bool& adm0,
+                                         bool& tv_changed) {
     constexpr int NB = PlitsK<W>::NB;
     const int qv = dl - m.dbase;
+    tv_changed = false;
 #pragma unroll
     for (int q = 0; q < W; ++q) adm[q] = m.M[q];
-    if (qv < 0 || qv % wc) {
+    if (qv < 0 || (wc != 1 && qv % wc)) {
 #pragma unroll
         for (int q = 0; q < W; ++q) adm[q] = 0;
     } else {
-        sliced_eq<W, NB>(m.S, qv / wc, adm);
+        sliced_eq<W, NB>(m.S, div_wc(qv, wc), adm);
     }
     adm0 = m.cur && m.d0 == dl;
     if (!asp_all && (adm0 || popc_w<W>(adm))) {
@@ -180,17 +230,17 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
             if (q == 0 && adm0) x |= tv[0] & 1ULL;
             uint64_t expired = 0;
             while (x) {
-                int ks[4];
-                uint32_t us[4];
+                int ks[2];
+                uint32_t us[2];
 #pragma unroll
-                for (int z = 0; z < 4; ++z) {
+                for (int z = 0; z < 2; ++z) {
                     ks[z] = x ? __ffsll((long long)x) - 1 : -1;
                     x &= x - 1;
                 }
 #pragma unroll
-                for (int z = 0; z < 4; ++z) us[z] = ks[z] >= 0 ? urow[q * 64 + ks[z]] : 0u;
+                for (int z = 0; z < 2; ++z) us[z] = ks[z] >= 0 ? urow[q * 64 + ks[z]] : 0u;
 #pragma unroll
-                for (int z = 0; z < 4; ++z) {
+                for (int z = 0; z < 2; ++z) {
                     if (ks[z] < 0) continue;
                     if (us[z] > t) {
                         if (q == 0 && ks[z] == 0)
@@ -202,10 +252,254 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
                     }
                 }
             }
-            if (expired) Tv[q] = tv[q] & ~expired;
+            if (expired) {
+                tv[q] &= ~expired;
+                tv_changed = true;
+            }
         }
     }
     return popc_w<W>(adm) + (adm0 ? 1 : 0);
+}
+
+// ---- register-resident mode: while |active| <= 32 lane L holds the L-th active vertex (ascending id)
+// with its move classes, tabu-blind minimum and possibly-tabu mask in registers, and a move updates the
+// list in place: only the cells of the moved vertex's row and column whose colour is the old or the new
+// one can change membership (their counts are the only ones that moved), so no re-classification scan
+// and no compaction run per step.  The shared-memory active bitmask and minima are not maintained in
+// this mode; they are rebuilt from the list when the set outgrows a warp.
+constexpr int kNoV = 0xFFFF;      // an empty lane: sorts after every vertex id
+constexpr int kSparseEnter = 28;  // enter at <= 28 active vertices, leave above 32 (hysteresis)
+
+template <int W>
+struct LaneVertex {
+    int v, rc;  // vertex (kNoV: empty lane), its cell row << 8 | column
+    VertexMoves<W> m;
+    int vmin;        // tabu-blind minimum delta over v's moves
+    uint64_t tv[W];  // possibly-tabu colours of v (a superset of its live until[][] entries)
+};
+
+template <int W>
+__device__ __forceinline__ int moves_min(const VertexMoves<W>& m, int wc) {
+    constexpr int NB = PlitsK<W>::NB;
+    int vm = m.cur ? m.d0 : INT_MAX;
+    if (popc_w<W>(m.M)) {
+        uint64_t sel[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) sel[q] = m.M[q];
+        vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, sel));
+    }
+    return vm;
+}
+
+// the lane's move classes and minimum from the planes (L.v and L.rc set)
+template <int W>
+__device__ __forceinline__ void lane_load(const Graph<W>& g, const PlitsWarp& s, LaneVertex<W>& L, int wf, int wc) {
+    if (L.v == kNoV) {
+        L.rc = 0xFFFF;  // no row or column n <= 127 matches 0xFF
+        L.m.cur = 0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) L.m.M[q] = 0;
+        L.vmin = INT_MAX;
+        return;
+    }
+    vertex_moves_rc<W>(g, s, L.v, L.rc, wf, wc, L.m);
+    L.vmin = moves_min<W>(L.m, wc);
+}
+
+// enter the register mode from the bitmask s.A (|active| = na <= 32)
+template <int W>
+__device__ __forceinline__ void sparse_enter(const Graph<W>& g, const PlitsWarp& s, LaneVertex<W>& L, int wf, int wc,
+                                             int lane) {
+    const int v_lo = lane * 32 * g.lane_words;
+    int my = 0;
+    for (int q = 0; q < g.lane_words; ++q) my += __popc(s.A[lane * g.lane_words + q]);
+    int pos = warp_incl_sum(my) - my;
+    for (int q = 0; q < g.lane_words; ++q) {
+        uint32_t bits = s.A[lane * g.lane_words + q];
+        while (bits) {
+            s.list[pos++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
+            bits &= bits - 1;
+        }
+    }
+    const int na = __shfl_sync(kFull, pos, 31);
+    __syncwarp();
+    L.v = lane < na ? s.list[lane] : kNoV;
+    if (L.v != kNoV) L.rc = g.cell[L.v];
+#pragma unroll
+    for (int q = 0; q < W; ++q) L.tv[q] = L.v != kNoV ? s.T[(size_t)L.v * W + q] : 0ULL;
+    lane_load<W>(g, s, L, wf, wc);
+    __syncwarp();
+}
+
+// leave it: the bitmask and the cached minima of every member (the list plus up to two vertices that
+// did not fit), from the planes as they are after the move
+template <int W>
+__device__ __forceinline__ void sparse_leave(const Graph<W>& g, const PlitsWarp& s, int lv, int lvmin, int x1, int x2,
+                                             int wf, int wc, int lane) {
+    for (int q = lane; q < 32 * g.lane_words; q += 32) s.A[q] = 0;
+    __syncwarp();
+    if (lv != kNoV) {
+        atomicOr(&s.A[lv >> 5], 1u << (lv & 31));
+        s.vmin[lv] = lvmin;
+    }
+    const int x = lane == 0 ? x1 : lane == 1 ? x2 : -1;
+    if (x >= 0) {
+        atomicOr(&s.A[x >> 5], 1u << (x & 31));
+        s.vmin[x] = vertex_min<W>(g, s, x, wf, wc);
+    }
+    __syncwarp();
+}
+
+// lanes >= pos take the next lane's vertex (pos: the lane of a deleted vertex)
+template <int W>
+__device__ __forceinline__ void list_delete(LaneVertex<W>& L, int pos, int lane, bool& dirty) {
+    const int v = __shfl_down_sync(kFull, L.v, 1);
+    const int rc = __shfl_down_sync(kFull, L.rc, 1);
+    uint64_t tv[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) tv[q] = __shfl_down_sync(kFull, L.tv[q], 1);
+    if (lane >= pos) {
+        L.v = lane == 31 ? kNoV : v;
+        L.rc = rc;
+#pragma unroll
+        for (int q = 0; q < W; ++q) L.tv[q] = tv[q];
+        dirty = true;
+    }
+}
+
+// insert u (cell rcu, possibly-tabu mask tu) at its ascending position (the list holds < 32 vertices, not u)
+template <int W>
+__device__ __forceinline__ void list_insert(LaneVertex<W>& L, int u, int rcu, const uint64_t (&tu)[W], int lane,
+                                            bool& dirty) {
+    const int pos = __popc(__ballot_sync(kFull, L.v < u));
+    const int v = __shfl_up_sync(kFull, L.v, 1);
+    const int rc = __shfl_up_sync(kFull, L.rc, 1);
+    uint64_t tv[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) tv[q] = __shfl_up_sync(kFull, L.tv[q], 1);
+    if (lane > pos) {
+        L.v = v;
+        L.rc = rc;
+#pragma unroll
+        for (int q = 0; q < W; ++q) L.tv[q] = tv[q];
+        dirty = true;
+    } else if (lane == pos) {
+        L.v = u;
+        L.rc = rcu;
+#pragma unroll
+        for (int q = 0; q < W; ++q) L.tv[q] = tu[q];
+        dirty = true;
+    }
+}
+
+// what one line (lane 0: the moved vertex's row, lane 1: its column) reports after the move
+template <int W>
+struct LineChange {
+    int uF;         // the cell left alone with `from` (its count fell to 1), or -1
+    bool keepF;     // ... stays active: its other line repeats `from`
+    int uT, rcT;    // the other cell with `to` (its count rose to 2) and its cell, or -1
+    int ct;         // the line's count of `to` after the move
+    uint64_t tT[W]; // possibly-tabu mask of uT
+};
+
+// lanes 0 (row r of vs) and 1 (column c) apply the move from colour `from` to `to` to their line: count
+// planes and xor-of-ids table, and report the membership changes it can cause (plits.hpp:193-212): only
+// cells of this line with colour `from` or `to` change their counts.  The two lanes touch different
+// lines, and each reads only lines the other does not write.
+template <int W>
+__device__ __forceinline__ void line_move(const Graph<W>& g, const PlitsWarp& s, int vs, int r, int c, int from, int to,
+                                          bool want_tabu, int lane, LineChange<W>& lc) {
+    constexpr int NP = PlitsK<W>::NP;
+    const int n = g.n, w1 = n + 1;
+    lc.uF = -1;
+    lc.keepF = false;
+    lc.uT = -1;
+    lc.rcT = 0;
+    lc.ct = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) lc.tT[q] = 0;
+    if (lane < 2) {
+        if (lane == 0) s.col[vs] = (uint8_t)to;
+        uint64_t* P = lane ? s.cp + (size_t)c * NP * W : s.rp + (size_t)r * NP * W;
+        int cf, ct;
+        plane_move_count<W, NP>(P, from, to, cf, ct);
+        uint16_t* X = s.X + (size_t)(lane ? n + c : r) * w1;
+        int xf = 0, xt = 0;
+        if (from) {
+            xf = X[from] ^ vs;
+            X[from] = (uint16_t)xf;
+        }
+        if (to) {
+            xt = X[to] ^ vs;
+            X[to] = (uint16_t)xt;
+        }
+        lc.ct = ct;
+        if (from && cf == 1) {
+            lc.uF = xf;
+            const uint16_t rc = g.cell[xf];
+            lc.keepF = plane_multi<W, NP>(lane ? s.rp + (size_t)(rc >> 8) * NP * W : s.cp + (size_t)(rc & 0xFF) * NP * W,
+                                          from);
+        }
+        if (to && ct == 2) {
+            lc.uT = xt ^ vs;
+            lc.rcT = g.cell[lc.uT];
+            if (want_tabu) {
+#pragma unroll
+                for (int q = 0; q < W; ++q) lc.tT[q] = s.T[(size_t)lc.uT * W + q];
+            }
+        }
+    }
+}
+
+// the register list after the move of vs (row r, column c) to colour `to`, from the two lines' reports:
+// deletions of the cells left alone with `from` (unless their other line repeats it) and of vs when it no
+// longer conflicts; insertions of the cells that now share `to` with vs.  Then every lane whose vertex
+// changed or lies in row r or column c reloads its move classes.  Returns false when the set outgrew the
+// warp (the bitmask mode is set up instead); na is the new |active|.
+template <int W>
+__device__ __forceinline__ bool sparse_membership(const Graph<W>& g, const PlitsWarp& s, LaneVertex<W>& L, int vs,
+                                                  int r, int c, int to, const LineChange<W>& lc, int wf, int wc,
+                                                  int lane, int& na) {
+    const int uF0 = __shfl_sync(kFull, lc.uF, 0), uF1 = __shfl_sync(kFull, lc.uF, 1);
+    const unsigned keep = __ballot_sync(kFull, lc.keepF);
+    const int uT0 = __shfl_sync(kFull, lc.uT, 0), uT1 = __shfl_sync(kFull, lc.uT, 1);
+    const int rcT0 = __shfl_sync(kFull, lc.rcT, 0), rcT1 = __shfl_sync(kFull, lc.rcT, 1);
+    const int ct0 = __shfl_sync(kFull, lc.ct, 0), ct1 = __shfl_sync(kFull, lc.ct, 1);
+    uint64_t t0[W], t1[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        t0[q] = __shfl_sync(kFull, lc.tT[q], 0);
+        t1[q] = __shfl_sync(kFull, lc.tT[q], 1);
+    }
+    const int d1 = (uF0 >= 0 && !(keep & 1u)) ? uF0 : -1;
+    const int d2 = (uF1 >= 0 && !(keep & 2u)) ? uF1 : -1;
+    const int d3 = (to && ct0 < 2 && ct1 < 2) ? vs : -1;
+    bool dirty = false;
+    int cnt = na;
+#pragma unroll
+    for (int z = 0; z < 3; ++z) {
+        const int d = z == 0 ? d1 : z == 1 ? d2 : d3;
+        if (d < 0) continue;
+        const unsigned b = __ballot_sync(kFull, L.v == d);
+        list_delete<W>(L, __ffs(b) - 1, lane, dirty);
+        --cnt;
+    }
+    const int i1 = (uT0 >= 0 && !__any_sync(kFull, L.v == uT0)) ? uT0 : -1;
+    const int i2 = (uT1 >= 0 && !__any_sync(kFull, L.v == uT1)) ? uT1 : -1;
+    const int nins = (i1 >= 0) + (i2 >= 0);
+    if (cnt + nins > 32) {
+        // refresh the listed vertices in row r / column c, then hand over to the bitmask mode
+        if (dirty || (L.rc >> 8) == r || (L.rc & 0xFF) == c) lane_load<W>(g, s, L, wf, wc);
+        __syncwarp();
+        sparse_leave<W>(g, s, L.v, L.vmin, i1, i2, wf, wc, lane);
+        na = cnt + nins;
+        return false;
+    }
+    if (i1 >= 0) list_insert<W>(L, i1, rcT0, t0, lane, dirty);
+    if (i2 >= 0) list_insert<W>(L, i2, rcT1, t1, lane, dirty);
+    na = cnt + nins;
+    if (dirty || (L.rc >> 8) == r || (L.rc & 0xFF) == c) lane_load<W>(g, s, L, wf, wc);
+    return true;
 }
 
 // plse_probe on PLITS: gamma[v][k] = cnt_row[r][k] + cnt_col[c][k] - 2 [k = col v] for k >= 1 (the
@@ -302,12 +596,17 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     bool pending = true;  // the phase best equals the current colouring
     int best_f = f, best_c = c;
     unsigned long long acc = 0;
+    bool sparse = false;  // the register-resident active list is in use
+    LaneVertex<W> L;
 
     for (int phase = 1; phase <= 2; ++phase) {
         const int wf = 2;
         const int wc = phase == 1 ? 1 : 2 * nv;  // PhaseWeights::from_phi(0.5 / |V|), plits.hpp:27-33
         const int64_t budget = phase == 1 ? a.budget : a.budget2;
         if (phase == 2) plits_build<W>(g, s, lane, wf, wc, f, c, active);  // from phase 1's best
+        plits_build_xor<W>(g, s, lane);
+        sparse = active <= 32;
+        if (sparse) sparse_enter<W>(g, s, L, wf, wc, lane);
         int64_t best_scaled = (int64_t)wf * f + (int64_t)wc * c;
         best_f = f;
         best_c = c;
@@ -342,98 +641,222 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             };
 
             if (prof) pc[7] += (unsigned)active;
-            // ---- compact the active set into ascending ids; lane L takes the L-th contiguous block, so
-            // lanes in order then list order is the ascending (v, k) order of the canonical rule
-            int na = 0;
-            {
-                int my = 0;
-                for (int q = 0; q < g.lane_words; ++q) my += __popc(s.A[lane * g.lane_words + q]);
-                const int incl = warp_incl_sum(my);
-                na = __shfl_sync(kFull, incl, 31);
-                int pos = incl - my;
-                for (int q = 0; q < g.lane_words; ++q) {
-                    uint32_t bits = s.A[lane * g.lane_words + q];
-                    while (bits) {
-                        s.list[pos++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
-                        bits &= bits - 1;
+            int N = 0, dl = INT_MAX, vs = -1, ks = 0, dcs = 0;
+            if (sparse) {
+                tick(1);
+                // ---- the lowest level with an admissible candidate, all from registers (until[][] only
+                // for possibly-tabu colours at the level)
+                bool hp = false;
+                int prev = 0, cnt = 0;
+                uint64_t adm[W];
+                bool adm0 = false;
+                for (;;) {
+                    int lm = L.vmin;
+                    if (hp) {
+                        uint64_t M2[W];
+#pragma unroll
+                        for (int q = 0; q < W; ++q) M2[q] = L.m.M[q];
+                        lm = INT_MAX;
+                        if (L.v != kNoV) {
+                            const int x = prev - L.m.dbase;
+                            sliced_ge<W, NB>(L.m.S, (wc == 1 ? x : floor_div(x, wc)) + 1, M2);
+                            if (L.m.cur && L.m.d0 > prev) lm = L.m.d0;
+                            if (popc_w<W>(M2)) lm = min(lm, L.m.dbase + wc * sliced_min<W, NB>(L.m.S, M2));
+                        }
+                    }
+                    dl = __reduce_min_sync(kFull, lm);
+                    if (dl == INT_MAX) break;  // every candidate tabu
+                    const bool asp_all = dl < thr;
+                    cnt = 0;
+                    adm0 = false;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) adm[q] = 0;
+                    if (L.v != kNoV && (hp || L.vmin <= dl)) {
+                        bool ch;
+                        cnt = level_adm<W>(L.m, dl, wc, asp_all, until + (size_t)L.v * w1, L.tv, t, adm, adm0, ch);
+                    }
+                    N = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+                    if (N > 0) break;
+                    hp = true;
+                    prev = dl;
+                    if (prof) ++pc[6];
+                }
+                tick(2);
+                if (N > 0) {
+                    // ---- the r-th admissible candidate in ascending (v, k): lanes are in ascending v
+                    const uint32_t rnk = __umulhi(h1, (uint32_t)N);
+                    const int incl = warp_incl_sum(cnt);
+                    const bool owner = (uint32_t)(incl - cnt) <= rnk && rnk < (uint32_t)incl;
+                    int sk = 0, sdc = 0;
+                    if (owner) {
+                        const int local = (int)rnk - (incl - cnt);
+                        sk = (adm0 && local == 0) ? 0 : nth_bit_w<W>(adm, local - (adm0 ? 1 : 0));
+                        const int gcur = L.m.cur ? div_wc(wf - L.m.d0, wc) : 0;
+                        sdc = (sk ? div_wc(dl - L.m.dbase, wc) : 0) - gcur;
+                    }
+                    const int wl = __ffs(__ballot_sync(kFull, owner)) - 1;
+                    vs = __shfl_sync(kFull, L.v, wl);
+                    ks = __shfl_sync(kFull, sk, wl);
+                    dcs = __shfl_sync(kFull, sdc, wl);
+                }
+                tick(3);
+            } else {
+                // ---- compact the active set into ascending ids; lane L takes the L-th contiguous block, so
+                // lanes in order then list order is the ascending (v, k) order of the canonical rule
+                int na = 0;
+                {
+                    int my = 0;
+                    for (int q = 0; q < g.lane_words; ++q) my += __popc(s.A[lane * g.lane_words + q]);
+                    const int incl = warp_incl_sum(my);
+                    na = __shfl_sync(kFull, incl, 31);
+                    int pos = incl - my;
+                    for (int q = 0; q < g.lane_words; ++q) {
+                        uint32_t bits = s.A[lane * g.lane_words + q];
+                        while (bits) {
+                            s.list[pos++] = (uint16_t)(v_lo + 32 * q + __ffs(bits) - 1);
+                            bits &= bits - 1;
+                        }
                     }
                 }
-            }
-            __syncwarp();
-            const int per = (na + 31) >> 5;
-            const int i_lo = min(na, lane * per), i_hi = min(na, i_lo + per);
-            tick(1);
-            // ---- the lowest delta level holding an admissible candidate: its tabu-blind minimum from
-            // the cached per-vertex minima, then the until[][] reads of the candidates at that level only
-            bool has_prev = false;
-            int prev = 0, dl = INT_MAX, N = 0, lc = 0;
-            bool asp_all = false;
-            int c_v = -1, c_d0 = 0, c_dbase = 0;  // this lane's first vertex with admissible moves at dl
-            uint64_t c_adm[W];
-            bool c_adm0 = false;
-            for (;;) {
-                int lmin = INT_MAX;
-                for (int idx = i_lo; idx < i_hi; ++idx) {
-                    {
-                        const int v = s.list[idx];
-                        int vm;
-                        if (!has_prev) {
-                            vm = s.vmin[v];
-                        } else {
+                __syncwarp();
+                const int per = (na + 31) >> 5;
+                const int i_lo = min(na, lane * per), i_hi = min(na, i_lo + per);
+                tick(1);
+                // ---- the lowest delta level holding an admissible candidate: its tabu-blind minimum from
+                // the cached per-vertex minima, then the until[][] reads of the candidates at that level only
+                bool has_prev = false;
+                int prev = 0, lc = 0;
+                bool asp_all = false;
+                int c_v = -1, c_d0 = 0, c_dbase = 0;  // this lane's first vertex with admissible moves at dl
+                uint64_t c_adm[W];
+                bool c_adm0 = false;
+                for (;;) {
+                    int lmin = INT_MAX;
+                    for (int idx = i_lo; idx < i_hi; ++idx) {
+                        {
+                            const int v = s.list[idx];
+                            int vm;
+                            if (!has_prev) {
+                                vm = s.vmin[v];
+                            } else {
+                                VertexMoves<W> m;
+                                vertex_moves<W>(g, s, v, wf, wc, m);
+                                sliced_ge<W, NB>(m.S, floor_div(prev - m.dbase, wc) + 1, m.M);
+                                vm = (m.cur && m.d0 > prev) ? m.d0 : INT_MAX;
+                                if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
+                            }
+                            lmin = min(lmin, vm);
+                        }
+                    }
+                    dl = __reduce_min_sync(kFull, lmin);
+                    long long tl0 = prof ? clock64() : 0;
+                    if (prof) pc[has_prev ? 13 : 11] += (unsigned long long)(tl0 - tp1);
+                    if (dl == INT_MAX) break;  // every candidate tabu
+                    asp_all = dl < thr;
+                    lc = 0;
+                    c_v = -1;
+                    for (int idx = i_lo; idx < i_hi; ++idx) {
+                        {
+                            const int v = s.list[idx];
+                            if (!has_prev && s.vmin[v] > dl) continue;
+                            uint64_t tv[W];
+#pragma unroll
+                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)v * W + q];
                             VertexMoves<W> m;
                             vertex_moves<W>(g, s, v, wf, wc, m);
-                            sliced_ge<W, NB>(m.S, floor_div(prev - m.dbase, wc) + 1, m.M);
-                            vm = (m.cur && m.d0 > prev) ? m.d0 : INT_MAX;
-                            if (popc_w<W>(m.M)) vm = min(vm, m.dbase + wc * sliced_min<W, NB>(m.S, m.M));
-                        }
-                        lmin = min(lmin, vm);
-                    }
-                }
-                dl = __reduce_min_sync(kFull, lmin);
-                long long tl0 = prof ? clock64() : 0;
-                if (prof) pc[has_prev ? 13 : 11] += (unsigned long long)(tl0 - tp1);
-                if (dl == INT_MAX) break;  // every candidate tabu
-                asp_all = dl < thr;
-                lc = 0;
-                c_v = -1;
-                for (int idx = i_lo; idx < i_hi; ++idx) {
-                    {
-                        const int v = s.list[idx];
-                        if (!has_prev && s.vmin[v] > dl) continue;
-                        uint64_t tv[W];
+                            uint64_t adm[W];
+                            bool adm0;
+                            bool ch;
+                            const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, tv, t, adm, adm0, ch);
+                            if (ch) {
 #pragma unroll
-                        for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)v * W + q];
-                        VertexMoves<W> m;
-                        vertex_moves<W>(g, s, v, wf, wc, m);
+                                for (int q = 0; q < W; ++q) s.T[(size_t)v * W + q] = tv[q];
+                            }
+                            if (cnt && c_v < 0) {
+                                c_v = v;
+                                c_adm0 = adm0;
+                                c_d0 = m.d0;
+                                c_dbase = m.dbase;
+#pragma unroll
+                                for (int qq = 0; qq < W; ++qq) c_adm[qq] = adm[qq];
+                            }
+                            s.vcnt[v] = (uint8_t)cnt;
+                            lc += cnt;
+                        }
+                    }
+                    N = (int)__reduce_add_sync(kFull, (unsigned)lc);
+                    if (prof) {
+                        const long long x = clock64();
+                        pc[has_prev ? 13 : 12] += (unsigned long long)(x - tl0);
+                        tp1 = x;
+                    }
+                    if (N > 0) break;
+                    has_prev = true;
+                    prev = dl;
+                    if (prof) ++pc[6];
+                }
+                __syncwarp();
+                tick(2);
+                if (N > 0) {
+                    // ---- the r-th admissible candidate in ascending (v, k)
+                    const uint32_t rnk = __umulhi(h1, (uint32_t)N);
+                    const int incl = warp_incl_sum(lc);
+                    const bool owner = (uint32_t)(incl - lc) <= rnk && rnk < (uint32_t)incl;
+                    int sv = -1, sk = 0, sdc = 0;
+                    if (owner) {
+                        int local = (int)rnk - (incl - lc);
+                        for (int idx = i_lo; idx < i_hi && sv < 0; ++idx) {
+                            {
+                                const int v = s.list[idx];
+                                if (!has_prev && s.vmin[v] > dl) continue;
+                                const int cnt = s.vcnt[v];
+                                if (local < cnt) {
+                                    sv = v;
+                                    break;
+                                }
+                                local -= cnt;
+                            }
+                        }
                         uint64_t adm[W];
                         bool adm0;
-                        const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, s.T + (size_t)v * W,
-                                                     tv, t, adm, adm0);
-                        if (cnt && c_v < 0) {
-                            c_v = v;
-                            c_adm0 = adm0;
-                            c_d0 = m.d0;
-                            c_dbase = m.dbase;
+                        int d0, dbase, cur;
+                        if (sv == c_v) {
+                            adm0 = c_adm0;
+                            d0 = c_d0;
+                            dbase = c_dbase;
 #pragma unroll
-                            for (int qq = 0; qq < W; ++qq) c_adm[qq] = adm[qq];
+                            for (int q = 0; q < W; ++q) adm[q] = c_adm[q];
+                        } else {
+                            VertexMoves<W> m;
+                            vertex_moves<W>(g, s, sv, wf, wc, m);
+                            uint64_t tv[W];
+#pragma unroll
+                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)sv * W + q];
+                            bool ch;
+                            level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, tv, t, adm, adm0, ch);
+                            if (ch) {
+#pragma unroll
+                                for (int q = 0; q < W; ++q) s.T[(size_t)sv * W + q] = tv[q];
+                            }
+                            d0 = m.d0;
+                            dbase = m.dbase;
                         }
-                        s.vcnt[v] = (uint8_t)cnt;
-                        lc += cnt;
+                        cur = col[sv];
+                        if (adm0 && local == 0)
+                            sk = 0;
+                        else
+                            sk = nth_bit_w<W>(adm, local - (adm0 ? 1 : 0));
+                        // every candidate at level dl has gamma[v][k] = (dl - dbase) / wc; gamma[v][cur] from d0
+                        const int gcur = cur ? (wf - d0) / wc : 0;
+                        sdc = (sk ? (dl - dbase) / wc : 0) - gcur;
                     }
+                    tick(3);
+                    const int wl = __ffs(__ballot_sync(kFull, owner)) - 1;
+                    vs = __shfl_sync(kFull, sv, wl);
+                    ks = __shfl_sync(kFull, sk, wl);
+                    dcs = __shfl_sync(kFull, sdc, wl);
                 }
-                N = (int)__reduce_add_sync(kFull, (unsigned)lc);
-                if (prof) {
-                    const long long x = clock64();
-                    pc[has_prev ? 13 : 12] += (unsigned long long)(x - tl0);
-                    tp1 = x;
-                }
-                if (N > 0) break;
-                has_prev = true;
-                prev = dl;
-                if (prof) ++pc[6];
             }
-            __syncwarp();
-            tick(2);
             if (N == 0) {
                 // every candidate tabu: the clock still advances (plits.hpp:178-179)
                 if (lane == 0) acc += 2ULL * (unsigned)w1 * (unsigned)active_before;
@@ -446,58 +869,6 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 continue;
             }
 
-            // ---- the r-th admissible candidate in ascending (v, k)
-            const uint32_t rnk = __umulhi(h1, (uint32_t)N);
-            const int incl = warp_incl_sum(lc);
-            const bool owner = (uint32_t)(incl - lc) <= rnk && rnk < (uint32_t)incl;
-            int sv = -1, sk = 0, sdc = 0;
-            if (owner) {
-                int local = (int)rnk - (incl - lc);
-                for (int idx = i_lo; idx < i_hi && sv < 0; ++idx) {
-                    {
-                        const int v = s.list[idx];
-                        if (!has_prev && s.vmin[v] > dl) continue;
-                        const int cnt = s.vcnt[v];
-                        if (local < cnt) {
-                            sv = v;
-                            break;
-                        }
-                        local -= cnt;
-                    }
-                }
-                uint64_t adm[W];
-                bool adm0;
-                int d0, dbase, cur;
-                if (sv == c_v) {
-                    adm0 = c_adm0;
-                    d0 = c_d0;
-                    dbase = c_dbase;
-#pragma unroll
-                    for (int q = 0; q < W; ++q) adm[q] = c_adm[q];
-                } else {
-                    VertexMoves<W> m;
-                    vertex_moves<W>(g, s, sv, wf, wc, m);
-                    uint64_t tv[W];
-#pragma unroll
-                    for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)sv * W + q];
-                    level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, s.T + (size_t)sv * W, tv, t, adm, adm0);
-                    d0 = m.d0;
-                    dbase = m.dbase;
-                }
-                cur = col[sv];
-                if (adm0 && local == 0)
-                    sk = 0;
-                else
-                    sk = nth_bit_w<W>(adm, local - (adm0 ? 1 : 0));
-                // every candidate at level dl has gamma[v][k] = (dl - dbase) / wc; gamma[v][cur] from d0
-                const int gcur = cur ? (wf - d0) / wc : 0;
-                sdc = (sk ? (dl - dbase) / wc : 0) - gcur;
-            }
-            tick(3);
-            const int wl = __ffs(__ballot_sync(kFull, owner)) - 1;
-            const int vs = __shfl_sync(kFull, sv, wl);
-            const int ks = __shfl_sync(kFull, sk, wl);
-            const int dcs = __shfl_sync(kFull, sdc, wl);
             const int from = col[vs];
             const int dfs = (ks == 0) - (from == 0);
             const int64_t now = cur_scaled + dl;
@@ -509,25 +880,24 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             __syncwarp();
             const uint16_t rcs = g.cell[vs];
             const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-            if (lane == 0) {
-                col[vs] = (uint8_t)ks;
-                plane_move<W, NP>(s.rp + (size_t)rs_ * NP * W, from, ks);
-            }
-            if (lane == 1) plane_move<W, NP>(s.cp + (size_t)cs_ * NP * W, from, ks);
+            LineChange<W> lch;
+            line_move<W>(g, s, vs, rs_, cs_, from, ks, sparse, lane, lch);
             __syncwarp();
             long long tm0 = prof ? clock64() : 0;
             if (prof) pc[8] += (unsigned long long)(tm0 - tp1);
-            plits_membership<W>(g, s, rs_, cs_, from, ks, wf, wc, lane);
-            __syncwarp();
+            if (sparse) {
+                sparse = sparse_membership<W>(g, s, L, vs, rs_, cs_, ks, lch, wf, wc, lane, active);
+            } else {
+                plits_membership<W>(g, s, rs_, cs_, from, ks, wf, wc, lane);
+                __syncwarp();
+                int al = 0;
+                for (int q = 0; q < g.lane_words; ++q) al += __popc(s.A[lane * g.lane_words + q]);
+                active = (int)__reduce_add_sync(kFull, (unsigned)al);
+            }
             if (prof) {
                 const long long x = clock64();
                 pc[9] += (unsigned long long)(x - tm0);
                 tm0 = x;
-            }
-            {
-                int al = 0;
-                for (int q = 0; q < g.lane_words; ++q) al += __popc(s.A[lane * g.lane_words + q]);
-                active = (int)__reduce_add_sync(kFull, (unsigned)al);
             }
             f += dfs;
             c += dcs;
@@ -536,6 +906,11 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 until[(size_t)vs * w1 + from] = t + 1 + tenure;
                 s.T[(size_t)vs * W + (from >> 6)] |= 1ULL << (from & 63);
                 acc += 2ULL * (unsigned)w1 * (unsigned)active_before + 4ULL * g.deg[vs] + 2ULL;
+            }
+            if (sparse && L.v == vs) {
+#pragma unroll
+                for (int q = 0; q < W; ++q)
+                    if ((from >> 6) == q) L.tv[q] |= 1ULL << (from & 63);
             }
             if (now < best_scaled) {
                 best_scaled = now;
@@ -552,6 +927,10 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
+            if (!sparse && active <= kSparseEnter) {
+                sparse_enter<W>(g, s, L, wf, wc, lane);
+                sparse = true;
+            }
             if (prof) pc[10] += (unsigned long long)(clock64() - tm0);
             tick(4);
             if (prof) {
@@ -634,7 +1013,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 }
 
 template <int W, bool kDebug>
-__global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits(const ImproveArgs a) {
+// one CTA per SM: the register-resident active list needs more than 128 registers per thread
+__global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits(const ImproveArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int n = a.n, nv = a.nv;
@@ -704,6 +1084,7 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, kPlitsMinBlocks) k_plits(con
     // the possibly-tabu mask lives in the slot's tabu-record area (nv * 16 >= nv * 8 W bytes); any stale
     // content is a harmless superset: every until[][] entry of an earlier individual is below its clock
     s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
+    s.X = reinterpret_cast<uint16_t*>(s.T + (size_t)nv * W);  // capi.cu sizes rec_stride for both
     for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
          i = next_individual(a.first, a.nslots, a.work_counter, lane))
         plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane);

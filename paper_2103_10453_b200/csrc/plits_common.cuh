@@ -132,10 +132,9 @@ struct VertexMoves {
 };
 
 template <int W, class St>
-__device__ __forceinline__ void vertex_moves(const Graph<W>& g, const St& s, int v, int wf, int wc,
-                                             VertexMoves<W>& m) {
+__device__ __forceinline__ void vertex_moves_rc(const Graph<W>& g, const St& s, int v, int rc, int wf, int wc,
+                                                VertexMoves<W>& m) {
     constexpr int NP = PlitsK<W>::NP;
-    const uint16_t rc = g.cell[v];
     const int r = rc >> 8, c = rc & 0xFF;
     plane_sum<W, NP>(s.rp + (size_t)r * NP * W, s.cp + (size_t)c * NP * W, m.S);
     m.cur = s.col[v];
@@ -146,6 +145,12 @@ __device__ __forceinline__ void vertex_moves(const Graph<W>& g, const St& s, int
 #pragma unroll
     for (int q = 0; q < W; ++q)
         if (m.cur && (m.cur >> 6) == q) m.M[q] &= ~(1ULL << (m.cur & 63));
+}
+
+template <int W, class St>
+__device__ __forceinline__ void vertex_moves(const Graph<W>& g, const St& s, int v, int wf, int wc,
+                                             VertexMoves<W>& m) {
+    vertex_moves_rc<W>(g, s, v, g.cell[v], wf, wc, m);
 }
 
 // one lane moves a cell of this line from colour `from` to `to`: the two single-bit ripples (-1 at
