@@ -629,9 +629,9 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     c->threads = 32 * c->wpc;
     c->warps_per_sm = best_ind / per_warp;
     c->slots = c->grid * c->wpc * per_warp;
-    // PLITS (canonical) keeps its possibly-tabu masks and its xor-of-ids tables in the same area (plits.cu)
-    const size_t plits_area = (size_t)nv * 8 * W + (size_t)4 * n * (n + 1);
-    c->rec_stride = up(std::max((size_t)nv * tabu_rec_bytes(W), c->plits && !c->ref_ties ? plits_area : 0), 256);
+    // PLITS (canonical) keeps W words of possibly-tabu colours and an until bound per vertex there (plits.cu)
+    const size_t rec_bytes = std::max(tabu_rec_bytes(W), c->plits && !c->ref_ties ? (size_t)8 * (W + 1) : (size_t)0);
+    c->rec_stride = up((size_t)nv * rec_bytes, 256);
     c->until_stride = up((size_t)nv * (n + 1), 64);
     c->d_rec = dalloc<uint8_t>((size_t)c->slots * c->rec_stride);
     c->d_until = dalloc<uint32_t>((size_t)c->slots * c->until_stride);

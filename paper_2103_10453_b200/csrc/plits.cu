@@ -48,11 +48,14 @@ struct PlitsWarp {
     int32_t* vmin;    // [nv] per active vertex: tabu-blind minimum delta of its moves (refreshed when its
                       //      row or column changes)
     uint8_t* vcnt;    // [nv] per active vertex at the step's level: its admissible moves
-    uint64_t* T;      // [nv][W] GLOBAL (the slot's tabu-record area, L1-resident for a lone warp): colours
-                      //         possibly tabu -- a superset of the live until[][] entries, so only those
-                      //         colours read until[][]
-    uint16_t* X;      // [2n][n+1] GLOBAL (same area, after T): per row (then per column) and colour, the XOR of
-                      //         the ids of its cells holding that colour -- the one cell when the count is 1
+    uint64_t* T;      // [nv][W + 1] GLOBAL (the slot's tabu-record area, L1-resident for a lone warp): W words
+                      //         of colours possibly tabu -- a superset of the live until[][] entries, so only
+                      //         those colours read until[][] -- and the largest until ever written for v
+                      //         (low half of word W)
+    uint8_t* X;       // [2n][n+1] register mode only, over list / vmin / vcnt (which only the bitmask mode
+                      //         uses): per row and colour the XOR of the row offsets (u - rs[r]) of its cells
+                      //         holding that colour, per column the XOR of their row indices -- the one cell
+                      //         when the count is 1
 };
 
 // tabu-blind minimum delta over v's candidates (plits.hpp:135-176 without the tabu test)
@@ -159,20 +162,21 @@ __device__ void plits_build(const Graph<W>& g, const PlitsWarp& s, int lane, int
 // x / wc with the phase-1 weight wc = 1 kept off the integer-division path
 __device__ __forceinline__ int div_wc(int x, int wc) { return wc == 1 ? x : x / wc; }
 
-// the xor-of-ids tables of the colouring in s.col: lane l builds lines l, l + 32, ... (rows, then columns)
+// the xor tables of the colouring in s.col (register mode): lane l builds lines l, l + 32, ... (rows, then
+// columns)
 template <int W>
 __device__ void plits_build_xor(const Graph<W>& g, const PlitsWarp& s, int lane) {
     const int n = g.n, w1 = n + 1;
     for (int line = lane; line < 2 * n; line += 32) {
         const bool is_row = line < n;
         const int idx = is_row ? line : line - n;
-        uint16_t* X = s.X + (size_t)line * w1;
+        uint8_t* X = s.X + (size_t)line * w1;
         for (int k = 0; k <= n; ++k) X[k] = 0;
         const int lo = is_row ? g.rs[idx] : g.cs[idx], hi = is_row ? g.rs[idx + 1] : g.cs[idx + 1];
         for (int x = lo; x < hi; ++x) {
             const int u = is_row ? x : g.cl[x];
             const int k = s.col[u];
-            if (k) X[k] ^= (uint16_t)u;
+            if (k) X[k] ^= (uint8_t)(is_row ? x - lo : g.cell[u] >> 8);
         }
     }
     __syncwarp();
@@ -207,13 +211,11 @@ __device__ __forceinline__ void plane_move_count(uint64_t* P, int from, int to, 
 // adm0 = the move to 0.  Only colours in the possibly-tabu mask tv (loaded by the caller ahead of the
 // move classes so the load overlaps them) read until[][] (independent pairs of loads); expired ones
 // leave tv (tv_changed tells the caller to store it back).
+// v's moves at delta level dl, tabu-blind: adm = colours k != 0, adm0 = the move to 0
 template <int W>
-__device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
-                                         uint64_t (&tv)[W], uint32_t t, uint64_t (&adm)[W], bool& adm0,
-                                         bool& tv_changed) {
+__device__ __forceinline__ void level_class(const VertexMoves<W>& m, int dl, int wc, uint64_t (&adm)[W], bool& adm0) {
     constexpr int NB = PlitsK<W>::NB;
     const int qv = dl - m.dbase;
-    tv_changed = false;
 #pragma unroll
     for (int q = 0; q < W; ++q) adm[q] = m.M[q];
     if (qv < 0 || (wc != 1 && qv % wc)) {
@@ -223,6 +225,14 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
         sliced_eq<W, NB>(m.S, div_wc(qv, wc), adm);
     }
     adm0 = m.cur && m.d0 == dl;
+}
+
+template <int W>
+__device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc, bool asp_all, const uint32_t* urow,
+                                         uint64_t (&tv)[W], uint32_t t, uint64_t (&adm)[W], bool& adm0,
+                                         bool& tv_changed) {
+    tv_changed = false;
+    level_class<W>(m, dl, wc, adm, adm0);
     if (!asp_all && (adm0 || popc_w<W>(adm))) {
 #pragma unroll
         for (int q = 0; q < W; ++q) {
@@ -274,9 +284,81 @@ template <int W>
 struct LaneVertex {
     int v, rc;  // vertex (kNoV: empty lane), its cell row << 8 | column
     VertexMoves<W> m;
-    int vmin;        // tabu-blind minimum delta over v's moves
-    uint64_t tv[W];  // possibly-tabu colours of v (a superset of its live until[][] entries)
+    int vmin;  // tabu-blind minimum delta over v's moves
+    // v's live tabu entries: exactly {k1 if u1 > t, k2 if u2 > t} (tk = k1 | k2 << 8), or, with the
+    // overflow flag (tk bit 16), a superset tv read through until[][]; umax bounds every until of v
+    uint32_t u1, u2, tk, umax;
+    uint64_t tv[W];
 };
+constexpr uint32_t kTabuOvf = 1u << 16;
+
+// level_adm on the lane's cached tabu entries (no memory access)
+template <int W>
+__device__ __forceinline__ int level_adm_cached(const LaneVertex<W>& L, int dl, int wc, bool asp_all, uint32_t t,
+                                                uint64_t (&adm)[W], bool& adm0) {
+    level_class<W>(L.m, dl, wc, adm, adm0);
+    if (!asp_all) {
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+            const int k = z ? (L.tk >> 8) & 0xFF : L.tk & 0xFF;
+            if ((z ? L.u2 : L.u1) > t) {
+                if (k == 0) adm0 = false;
+#pragma unroll
+                for (int q = 0; q < W; ++q)
+                    if (k && (k >> 6) == q) adm[q] &= ~(1ULL << (k & 63));
+            }
+        }
+    }
+    return popc_w<W>(adm) + (adm0 ? 1 : 0);
+}
+
+// the lane's vertex got the tabu entry (k, un) (until[v][k] = un overwrites any earlier entry)
+template <int W>
+__device__ __forceinline__ void lane_tabu_write(LaneVertex<W>& L, int k, uint32_t un, uint32_t t) {
+    L.umax = max(L.umax, un);
+    if (L.tk & kTabuOvf) {
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+            if ((k >> 6) == q) L.tv[q] |= 1ULL << (k & 63);
+        return;
+    }
+    const int k1 = L.tk & 0xFF, k2 = (L.tk >> 8) & 0xFF;
+    if (k1 == k) {
+        L.u1 = un;
+    } else if (k2 == k) {
+        L.u2 = un;
+    } else if (L.u1 <= t) {
+        L.tk = (L.tk & ~0xFFu) | (uint32_t)k;
+        L.u1 = un;
+    } else if (L.u2 <= t) {
+        L.tk = (L.tk & ~0xFF00u) | (uint32_t)k << 8;
+        L.u2 = un;
+    } else {
+        // three live entries: the superset {k1, k2, k} is read through until[][] from now on
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            uint64_t m = 0;
+            if ((k1 >> 6) == q) m |= 1ULL << (k1 & 63);
+            if ((k2 >> 6) == q) m |= 1ULL << (k2 & 63);
+            if ((k >> 6) == q) m |= 1ULL << (k & 63);
+            L.tv[q] = m;
+        }
+        L.tk |= kTabuOvf;
+    }
+}
+
+// a vertex entering the list starts in overflow mode on its stored possibly-tabu mask and until bound
+// (loaded here, first used at the next step: the bound usually shows that nothing is live any more)
+template <int W>
+__device__ __forceinline__ void lane_tabu_load(const PlitsWarp& s, LaneVertex<W>& L, int u) {
+    const uint64_t* rec = s.T + (size_t)u * (W + 1);
+#pragma unroll
+    for (int q = 0; q < W; ++q) L.tv[q] = rec[q];
+    L.umax = (uint32_t)rec[W];
+    L.tk = kTabuOvf;
+    L.u1 = 0;
+    L.u2 = 0;
+}
 
 template <int W>
 __device__ __forceinline__ int moves_min(const VertexMoves<W>& m, int wc) {
@@ -324,9 +406,15 @@ __device__ __forceinline__ void sparse_enter(const Graph<W>& g, const PlitsWarp&
     const int na = __shfl_sync(kFull, pos, 31);
     __syncwarp();
     L.v = lane < na ? s.list[lane] : kNoV;
-    if (L.v != kNoV) L.rc = g.cell[L.v];
-#pragma unroll
-    for (int q = 0; q < W; ++q) L.tv[q] = L.v != kNoV ? s.T[(size_t)L.v * W + q] : 0ULL;
+    __syncwarp();
+    plits_build_xor<W>(g, s, lane);  // over the list
+    if (L.v != kNoV) {
+        L.rc = g.cell[L.v];
+        lane_tabu_load<W>(s, L, L.v);
+    } else {
+        L.tk = 0;
+        L.u1 = L.u2 = L.umax = 0;
+    }
     lane_load<W>(g, s, L, wf, wc);
     __syncwarp();
 }
@@ -355,97 +443,110 @@ template <int W>
 __device__ __forceinline__ void list_delete(LaneVertex<W>& L, int pos, int lane, bool& dirty) {
     const int v = __shfl_down_sync(kFull, L.v, 1);
     const int rc = __shfl_down_sync(kFull, L.rc, 1);
+    const uint32_t u1 = __shfl_down_sync(kFull, L.u1, 1), u2 = __shfl_down_sync(kFull, L.u2, 1);
+    const uint32_t tk = __shfl_down_sync(kFull, L.tk, 1), um = __shfl_down_sync(kFull, L.umax, 1);
     uint64_t tv[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) tv[q] = __shfl_down_sync(kFull, L.tv[q], 1);
     if (lane >= pos) {
         L.v = lane == 31 ? kNoV : v;
         L.rc = rc;
+        L.u1 = u1;
+        L.u2 = u2;
+        L.tk = tk;
+        L.umax = um;
 #pragma unroll
         for (int q = 0; q < W; ++q) L.tv[q] = tv[q];
         dirty = true;
     }
 }
 
-// insert u (cell rcu, possibly-tabu mask tu) at its ascending position (the list holds < 32 vertices, not u)
+// insert u (cell rcu) at its ascending position (the list holds < 32 vertices, not u); its possibly-tabu
+// mask is loaded here and first used in the next step's level search
 template <int W>
-__device__ __forceinline__ void list_insert(LaneVertex<W>& L, int u, int rcu, const uint64_t (&tu)[W], int lane,
+__device__ __forceinline__ void list_insert(const PlitsWarp& s, LaneVertex<W>& L, int u, int rcu, int lane,
                                             bool& dirty) {
     const int pos = __popc(__ballot_sync(kFull, L.v < u));
     const int v = __shfl_up_sync(kFull, L.v, 1);
     const int rc = __shfl_up_sync(kFull, L.rc, 1);
+    const uint32_t u1 = __shfl_up_sync(kFull, L.u1, 1), u2 = __shfl_up_sync(kFull, L.u2, 1);
+    const uint32_t tk = __shfl_up_sync(kFull, L.tk, 1), um = __shfl_up_sync(kFull, L.umax, 1);
     uint64_t tv[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) tv[q] = __shfl_up_sync(kFull, L.tv[q], 1);
     if (lane > pos) {
         L.v = v;
         L.rc = rc;
+        L.u1 = u1;
+        L.u2 = u2;
+        L.tk = tk;
+        L.umax = um;
 #pragma unroll
         for (int q = 0; q < W; ++q) L.tv[q] = tv[q];
         dirty = true;
     } else if (lane == pos) {
         L.v = u;
         L.rc = rcu;
-#pragma unroll
-        for (int q = 0; q < W; ++q) L.tv[q] = tu[q];
+        lane_tabu_load<W>(s, L, u);
         dirty = true;
     }
 }
 
 // what one line (lane 0: the moved vertex's row, lane 1: its column) reports after the move
-template <int W>
 struct LineChange {
-    int uF;         // the cell left alone with `from` (its count fell to 1), or -1
-    bool keepF;     // ... stays active: its other line repeats `from`
-    int uT, rcT;    // the other cell with `to` (its count rose to 2) and its cell, or -1
-    int ct;         // the line's count of `to` after the move
-    uint64_t tT[W]; // possibly-tabu mask of uT
+    int rcF;     // cell of the one left with `from` (its count fell to 1), or -1
+    bool keepF;  // ... stays active: its other line repeats `from`
+    int rcT;     // cell of the other one with `to` (its count rose to 2), or -1
+    int uT;      // its vertex id (the row's lane; -1 for the column's: resolved by the warp)
+    int ct;      // the line's count of `to` after the move
 };
 
 // lanes 0 (row r of vs) and 1 (column c) apply the move from colour `from` to `to` to their line: count
-// planes and xor-of-ids table, and report the membership changes it can cause (plits.hpp:193-212): only
-// cells of this line with colour `from` or `to` change their counts.  The two lanes touch different
-// lines, and each reads only lines the other does not write.
+// planes, and in the register mode the xor table, reporting the membership changes the move can cause
+// (plits.hpp:193-212): only cells of this line with colour `from` or `to` change their counts.  The two
+// lanes touch different lines, and each reads only lines the other does not write.
 template <int W>
 __device__ __forceinline__ void line_move(const Graph<W>& g, const PlitsWarp& s, int vs, int r, int c, int from, int to,
-                                          bool want_tabu, int lane, LineChange<W>& lc) {
+                                          bool xor_tables, int lane, LineChange& lc) {
     constexpr int NP = PlitsK<W>::NP;
     const int n = g.n, w1 = n + 1;
-    lc.uF = -1;
+    lc.rcF = -1;
     lc.keepF = false;
+    lc.rcT = -1;
     lc.uT = -1;
-    lc.rcT = 0;
     lc.ct = 0;
-#pragma unroll
-    for (int q = 0; q < W; ++q) lc.tT[q] = 0;
     if (lane < 2) {
         if (lane == 0) s.col[vs] = (uint8_t)to;
         uint64_t* P = lane ? s.cp + (size_t)c * NP * W : s.rp + (size_t)r * NP * W;
         int cf, ct;
         plane_move_count<W, NP>(P, from, to, cf, ct);
-        uint16_t* X = s.X + (size_t)(lane ? n + c : r) * w1;
-        int xf = 0, xt = 0;
-        if (from) {
-            xf = X[from] ^ vs;
-            X[from] = (uint16_t)xf;
-        }
-        if (to) {
-            xt = X[to] ^ vs;
-            X[to] = (uint16_t)xt;
-        }
         lc.ct = ct;
-        if (from && cf == 1) {
-            lc.uF = xf;
-            const uint16_t rc = g.cell[xf];
-            lc.keepF = plane_multi<W, NP>(lane ? s.rp + (size_t)(rc >> 8) * NP * W : s.cp + (size_t)(rc & 0xFF) * NP * W,
-                                          from);
-        }
-        if (to && ct == 2) {
-            lc.uT = xt ^ vs;
-            lc.rcT = g.cell[lc.uT];
-            if (want_tabu) {
-#pragma unroll
-                for (int q = 0; q < W; ++q) lc.tT[q] = s.T[(size_t)lc.uT * W + q];
+        if (xor_tables) {
+            const int r0 = g.rs[r];
+            uint8_t* X = s.X + (size_t)(lane ? n + c : r) * w1;
+            const int key = lane ? r : vs - r0;  // vs's entry: its row offset / its row index
+            int xf = 0, xt = 0;
+            if (from) {
+                xf = X[from] ^ key;
+                X[from] = (uint8_t)xf;
+            }
+            if (to) {
+                xt = X[to] ^ key;
+                X[to] = (uint8_t)xt;
+            }
+            if (from && cf == 1) {
+                lc.rcF = lane ? (xf << 8 | c) : g.cell[r0 + xf];
+                lc.keepF = plane_multi<W, NP>(lane ? s.rp + (size_t)xf * NP * W
+                                                   : s.cp + (size_t)(lc.rcF & 0xFF) * NP * W, from);
+            }
+            if (to && ct == 2) {
+                const int o = xt ^ key;
+                if (lane) {
+                    lc.rcT = o << 8 | c;
+                } else {
+                    lc.uT = r0 + o;
+                    lc.rcT = g.cell[lc.uT];
+                }
             }
         }
     }
@@ -458,45 +559,48 @@ __device__ __forceinline__ void line_move(const Graph<W>& g, const PlitsWarp& s,
 // warp (the bitmask mode is set up instead); na is the new |active|.
 template <int W>
 __device__ __forceinline__ bool sparse_membership(const Graph<W>& g, const PlitsWarp& s, LaneVertex<W>& L, int vs,
-                                                  int r, int c, int to, const LineChange<W>& lc, int wf, int wc,
+                                                  int r, int c, int to, const LineChange& lc, int wf, int wc,
                                                   int lane, int& na) {
-    const int uF0 = __shfl_sync(kFull, lc.uF, 0), uF1 = __shfl_sync(kFull, lc.uF, 1);
+    const int rcF0 = __shfl_sync(kFull, lc.rcF, 0), rcF1 = __shfl_sync(kFull, lc.rcF, 1);
     const unsigned keep = __ballot_sync(kFull, lc.keepF);
-    const int uT0 = __shfl_sync(kFull, lc.uT, 0), uT1 = __shfl_sync(kFull, lc.uT, 1);
     const int rcT0 = __shfl_sync(kFull, lc.rcT, 0), rcT1 = __shfl_sync(kFull, lc.rcT, 1);
+    const int uT0 = __shfl_sync(kFull, lc.uT, 0);
     const int ct0 = __shfl_sync(kFull, lc.ct, 0), ct1 = __shfl_sync(kFull, lc.ct, 1);
-    uint64_t t0[W], t1[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-        t0[q] = __shfl_sync(kFull, lc.tT[q], 0);
-        t1[q] = __shfl_sync(kFull, lc.tT[q], 1);
-    }
-    const int d1 = (uF0 >= 0 && !(keep & 1u)) ? uF0 : -1;
-    const int d2 = (uF1 >= 0 && !(keep & 2u)) ? uF1 : -1;
-    const int d3 = (to && ct0 < 2 && ct1 < 2) ? vs : -1;
+    const int d1 = (rcF0 >= 0 && !(keep & 1u)) ? rcF0 : -1;
+    const int d2 = (rcF1 >= 0 && !(keep & 2u)) ? rcF1 : -1;
+    const int d3 = (to && ct0 < 2 && ct1 < 2) ? (r << 8 | c) : -1;
     bool dirty = false;
     int cnt = na;
 #pragma unroll
     for (int z = 0; z < 3; ++z) {
         const int d = z == 0 ? d1 : z == 1 ? d2 : d3;
         if (d < 0) continue;
-        const unsigned b = __ballot_sync(kFull, L.v == d);
+        const unsigned b = __ballot_sync(kFull, L.v != kNoV && L.rc == d);
         list_delete<W>(L, __ffs(b) - 1, lane, dirty);
         --cnt;
     }
-    const int i1 = (uT0 >= 0 && !__any_sync(kFull, L.v == uT0)) ? uT0 : -1;
-    const int i2 = (uT1 >= 0 && !__any_sync(kFull, L.v == uT1)) ? uT1 : -1;
-    const int nins = (i1 >= 0) + (i2 >= 0);
+    const bool in1 = rcT0 >= 0 && !__any_sync(kFull, L.v != kNoV && L.rc == rcT0);
+    const bool in2 = rcT1 >= 0 && !__any_sync(kFull, L.v != kNoV && L.rc == rcT1);
+    int uT1 = -1;
+    if (in2) {
+        // the column's cell: its id from its row (cells of a row are consecutive ids, in column order)
+        const int rr = rcT1 >> 8, lo = g.rs[rr], nr = g.rs[rr + 1] - lo;
+        for (int x0 = 0; x0 < nr; x0 += 32) {
+            const unsigned b = __ballot_sync(kFull, x0 + lane < nr && g.cell[lo + x0 + lane] == rcT1);
+            if (b) uT1 = lo + x0 + __ffs(b) - 1;
+        }
+    }
+    const int nins = (int)in1 + (int)in2;
     if (cnt + nins > 32) {
         // refresh the listed vertices in row r / column c, then hand over to the bitmask mode
         if (dirty || (L.rc >> 8) == r || (L.rc & 0xFF) == c) lane_load<W>(g, s, L, wf, wc);
         __syncwarp();
-        sparse_leave<W>(g, s, L.v, L.vmin, i1, i2, wf, wc, lane);
+        sparse_leave<W>(g, s, L.v, L.vmin, in1 ? uT0 : -1, in2 ? uT1 : -1, wf, wc, lane);
         na = cnt + nins;
         return false;
     }
-    if (i1 >= 0) list_insert<W>(L, i1, rcT0, t0, lane, dirty);
-    if (i2 >= 0) list_insert<W>(L, i2, rcT1, t1, lane, dirty);
+    if (in1) list_insert<W>(s, L, uT0, rcT0, lane, dirty);
+    if (in2) list_insert<W>(s, L, uT1, rcT1, lane, dirty);
     na = cnt + nins;
     if (dirty || (L.rc >> 8) == r || (L.rc & 0xFF) == c) lane_load<W>(g, s, L, wf, wc);
     return true;
@@ -549,7 +653,7 @@ __device__ void plits_probe_dump(const ImproveArgs& a, const Graph<W>& g, const 
 
 template <int W, bool kDebug>
 __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWarp& s, uint32_t* until,
-                          uint32_t* slot_clock, int i, int lane) {
+                          uint32_t* slot_clock, int i, int lane, bool sparse_ok) {
     constexpr int NP = PlitsK<W>::NP;
     constexpr int NB = PlitsK<W>::NB;
     const int n = g.n, nv = g.nv, w1 = n + 1;
@@ -604,8 +708,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         const int wc = phase == 1 ? 1 : 2 * nv;  // PhaseWeights::from_phi(0.5 / |V|), plits.hpp:27-33
         const int64_t budget = phase == 1 ? a.budget : a.budget2;
         if (phase == 2) plits_build<W>(g, s, lane, wf, wc, f, c, active);  // from phase 1's best
-        plits_build_xor<W>(g, s, lane);
-        sparse = active <= 32;
+        sparse = sparse_ok && active <= 32;
         if (sparse) sparse_enter<W>(g, s, L, wf, wc, lane);
         int64_t best_scaled = (int64_t)wf * f + (int64_t)wc * c;
         best_f = f;
@@ -650,6 +753,10 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                 int prev = 0, cnt = 0;
                 uint64_t adm[W];
                 bool adm0 = false;
+                if ((L.tk & kTabuOvf) && L.umax <= t) {  // every entry of v has expired
+                    L.tk = 0;
+                    L.u1 = L.u2 = 0;
+                }
                 for (;;) {
                     int lm = L.vmin;
                     if (hp) {
@@ -672,8 +779,13 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
 #pragma unroll
                     for (int q = 0; q < W; ++q) adm[q] = 0;
                     if (L.v != kNoV && (hp || L.vmin <= dl)) {
-                        bool ch;
-                        cnt = level_adm<W>(L.m, dl, wc, asp_all, until + (size_t)L.v * w1, L.tv, t, adm, adm0, ch);
+                        if (L.tk & kTabuOvf) {
+                            bool ch;
+                            cnt = level_adm<W>(L.m, dl, wc, asp_all, until + (size_t)L.v * w1, L.tv, t, adm, adm0,
+                                               ch);
+                        } else {
+                            cnt = level_adm_cached<W>(L, dl, wc, asp_all, t, adm, adm0);
+                        }
                     }
                     N = (int)__reduce_add_sync(kFull, (unsigned)cnt);
                     if (N > 0) break;
@@ -761,7 +873,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                             if (!has_prev && s.vmin[v] > dl) continue;
                             uint64_t tv[W];
 #pragma unroll
-                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)v * W + q];
+                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)v * (W + 1) + q];
                             VertexMoves<W> m;
                             vertex_moves<W>(g, s, v, wf, wc, m);
                             uint64_t adm[W];
@@ -770,7 +882,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                             const int cnt = level_adm<W>(m, dl, wc, asp_all, until + (size_t)v * w1, tv, t, adm, adm0, ch);
                             if (ch) {
 #pragma unroll
-                                for (int q = 0; q < W; ++q) s.T[(size_t)v * W + q] = tv[q];
+                                for (int q = 0; q < W; ++q) s.T[(size_t)v * (W + 1) + q] = tv[q];
                             }
                             if (cnt && c_v < 0) {
                                 c_v = v;
@@ -831,12 +943,12 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                             vertex_moves<W>(g, s, sv, wf, wc, m);
                             uint64_t tv[W];
 #pragma unroll
-                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)sv * W + q];
+                            for (int q = 0; q < W; ++q) tv[q] = s.T[(size_t)sv * (W + 1) + q];
                             bool ch;
                             level_adm<W>(m, dl, wc, asp_all, until + (size_t)sv * w1, tv, t, adm, adm0, ch);
                             if (ch) {
 #pragma unroll
-                                for (int q = 0; q < W; ++q) s.T[(size_t)sv * W + q] = tv[q];
+                                for (int q = 0; q < W; ++q) s.T[(size_t)sv * (W + 1) + q] = tv[q];
                             }
                             d0 = m.d0;
                             dbase = m.dbase;
@@ -880,7 +992,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             __syncwarp();
             const uint16_t rcs = g.cell[vs];
             const int rs_ = rcs >> 8, cs_ = rcs & 0xFF;
-            LineChange<W> lch;
+            LineChange lch;
             line_move<W>(g, s, vs, rs_, cs_, from, ks, sparse, lane, lch);
             __syncwarp();
             long long tm0 = prof ? clock64() : 0;
@@ -904,14 +1016,13 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             const uint32_t tenure = __umulhi(h2, 10u) + (uint32_t)(alpha * (double)active);
             if (lane == 0) {
                 until[(size_t)vs * w1 + from] = t + 1 + tenure;
-                s.T[(size_t)vs * W + (from >> 6)] |= 1ULL << (from & 63);
+                // fire-and-forget reductions: nothing in the step waits for them
+                uint64_t* rec = s.T + (size_t)vs * (W + 1);
+                atomicOr(reinterpret_cast<unsigned long long*>(rec + (from >> 6)), 1ULL << (from & 63));
+                atomicMax(reinterpret_cast<unsigned int*>(rec + W), t + 1 + tenure);
                 acc += 2ULL * (unsigned)w1 * (unsigned)active_before + 4ULL * g.deg[vs] + 2ULL;
             }
-            if (sparse && L.v == vs) {
-#pragma unroll
-                for (int q = 0; q < W; ++q)
-                    if ((from >> 6) == q) L.tv[q] |= 1ULL << (from & 63);
-            }
+            if (sparse && L.v == vs) lane_tabu_write<W>(L, from, t + 1 + tenure, t);
             if (now < best_scaled) {
                 best_scaled = now;
                 best_f = f;
@@ -927,7 +1038,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
-            if (!sparse && active <= kSparseEnter) {
+            if (!sparse && sparse_ok && active <= kSparseEnter) {
                 sparse_enter<W>(g, s, L, wf, wc, lane);
                 sparse = true;
             }
@@ -1078,16 +1189,20 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits(const ImproveArgs
     s.list = reinterpret_cast<uint16_t*>(wbase + L.w_list);
     s.vmin = reinterpret_cast<int32_t*>(wbase + L.w_vmin);
     s.vcnt = wbase + L.w_vcnt;
+    s.X = wbase + L.w_list;
+    // the register mode needs its xor tables to fit over list / vmin / vcnt (|V| >= ~0.3 n^2)
+    const bool sparse_ok = (size_t)2 * n * (n + 1) <= L.warp_bytes - L.w_list;
 
     const int slot = blockIdx.x * nwarps + warp;
     uint32_t* until = a.until + (size_t)slot * a.until_stride;
-    // the possibly-tabu mask lives in the slot's tabu-record area (nv * 16 >= nv * 8 W bytes); any stale
-    // content is a harmless superset: every until[][] entry of an earlier individual is below its clock
+    // the possibly-tabu masks and until bounds live in the slot's tabu-record area (capi.cu sizes it for
+    // nv * 8 (W + 1) bytes); stale content is harmless: a superset mask, and every until[][] entry of an
+    // earlier individual is below its clock
     s.T = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.tabu_rec) + (size_t)slot * a.rec_stride);
-    s.X = reinterpret_cast<uint16_t*>(s.T + (size_t)nv * W);  // capi.cu sizes rec_stride for both
+
     for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
          i = next_individual(a.first, a.nslots, a.work_counter, lane))
-        plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane);
+        plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane, sparse_ok);
 }
 
 const void* plits_kernel_ptr(int W, bool debug) {

@@ -15,3 +15,8 @@ if [ -n "$NCU" ]; then
   ncu -i gpurun_out/plits4_$TAG.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/plits4_${TAG}_src.csv 2>&1
   ncu -i gpurun_out/plits4_$TAG.ncu-rep --page raw --csv > gpurun_out/plits4_${TAG}_raw.csv 2>&1
 fi
+if [ -n "$TAIL" ]; then
+  N=50 R=0.4 POP=8192 GENS=6 timeout 600 python tools/probes/improve_probe.py > gpurun_out/tail_c2_$TAG.log 2>&1
+  POP=2048 GENS=6 timeout 600 python tools/probes/improve_probe.py > gpurun_out/tail_c3_2k_$TAG.log 2>&1
+  N=50 R=0.4 POP=8192 GENS=4 PLSE_PROFILE=1 timeout 600 python tools/probes/improve_probe.py > gpurun_out/tail_c2p_$TAG.log 2>&1
+fi

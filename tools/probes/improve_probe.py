@@ -18,8 +18,9 @@ for gen in range(1, gens + 1):
     it, bf, bi = pop.improve(gen)
     ctr = pop.counters()
     f, c, iters = pop.stats(P.IMPROVED)
+    q = np.percentile(iters, [50, 90, 99, 99.9, 100]).astype(int).tolist()
     print(f"gen {gen} moves {it} improve_ms {ctr.improve_ms:.1f} rate {it / ctr.improve_ms * 1e3:.4g} best_f {bf} "
-          f"iters p50/max {np.percentile(iters, 50):.0f}/{iters.max()}", flush=True)
+          f"iters p50/p90/p99/p99.9/max {q} n_full {(iters >= iters.max()).sum()} mean_f {f.mean():.2f}", flush=True)
     pop.compute_cross_distances()
     pop.update_population()
     pop.build_offspring(gen)
