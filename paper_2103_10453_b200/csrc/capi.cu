@@ -22,6 +22,10 @@
 
 using namespace plse_dev;
 
+namespace plse_dev {
+cudaError_t set_plits_list_cap(int cap, cudaStream_t st);  // plits.cu: the instrumented kernel's list capacity
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -753,9 +757,13 @@ void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, p
     const int grid = c->wpc == 1 ? std::max(1, std::min(c->grid, p_eff - first)) : c->grid;
     if (c->plits && c->ref_ties)
         c->launched(launch_plits_ref(a, c->W, grid, c->threads, c->smem, c->st));
-    else if (c->plits)
+    else if (c->plits) {
+        // the instrumented kernel (traces, probes, PLSE_PROFILE) reads its register-list capacity
+        const bool debug = a.trace != nullptr || a.prof != nullptr || a.probe.n > 0;
+        const char* cap = a.prof ? std::getenv("PLSE_PLITS_CAP") : nullptr;
+        if (debug) CK(set_plits_list_cap(cap ? std::atoi(cap) : 32, c->st));
         c->launched(launch_plits(a, c->W, grid, c->threads, c->smem, c->st));
-    else if (c->ref_ties)
+    } else if (c->ref_ties)
         c->launched(launch_improve_ref(a, c->W, grid, c->threads, c->smem, c->st));
     else
         c->launched(launch_improve(a, c->W, grid, c->threads, c->smem, c->st));
@@ -802,9 +810,11 @@ void collect_improve(plse_ctx* c, int64_t* iters_total, int32_t* best_f, int32_t
         std::fprintf(stderr,
                      "[plse-prof plits] indiv %llu steps %llu | cyc/step: list %.0f level %.0f select %.0f move %.0f "
                      "total %.0f | extra level passes %.3f/step | mean active %.1f | move: select->membership %.0f "
-                     "membership %.0f tail %.0f | level: minimum %.0f admissible %.0f extra passes %.0f\n",
+                     "membership %.0f tail %.0f | level: minimum %.0f admissible %.0f extra passes %.0f | register "
+                     "mode: %llu entries, %llu exits\n",
                      pr[8], pr[0], pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[5] / st, pr[6] / st, pr[7] / st,
-                     pr[9] / st, pr[10] / st, pr[11] / st, pr[12] / st, pr[13] / st, pr[14] / st);
+                     pr[9] / st, pr[10] / st, pr[11] / st, pr[12] / st, pr[13] / st, pr[14] / st, pr[15] & 0xFFFFFFFFull,
+                     pr[15] >> 32);
     } else if (c->d_prof && std::getenv("PLSE_PROFILE")) {
         unsigned long long pr[16];
         CK(cudaMemcpy(pr, c->d_prof, sizeof(pr), cudaMemcpyDeviceToHost));

@@ -278,7 +278,10 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
 // and no compaction run per step.  The shared-memory active bitmask and minima are not maintained in
 // this mode; they are rebuilt from the list when the set outgrows a warp.
 constexpr int kNoV = 0xFFFF;      // an empty lane: sorts after every vertex id
-constexpr int kSparseEnter = 28;  // enter at <= 28 active vertices, leave above 32 (hysteresis)
+constexpr int kSparseEnter = 4;  // enter at <= cap - 4 active vertices, leave above cap (hysteresis)
+// the list capacity: 32 (one vertex per lane); the instrumented kernel takes a smaller one from
+// PLSE_PLITS_CAP so that tests drive the mode transitions often
+__device__ int g_plits_list_cap = 32;
 
 template <int W>
 struct LaneVertex {
@@ -560,7 +563,7 @@ __device__ __forceinline__ void line_move(const Graph<W>& g, const PlitsWarp& s,
 template <int W>
 __device__ __forceinline__ bool sparse_membership(const Graph<W>& g, const PlitsWarp& s, LaneVertex<W>& L, int vs,
                                                   int r, int c, int to, const LineChange& lc, int wf, int wc,
-                                                  int lane, int& na) {
+                                                  int lane, int cap, int& na) {
     const int rcF0 = __shfl_sync(kFull, lc.rcF, 0), rcF1 = __shfl_sync(kFull, lc.rcF, 1);
     const unsigned keep = __ballot_sync(kFull, lc.keepF);
     const int rcT0 = __shfl_sync(kFull, lc.rcT, 0), rcT1 = __shfl_sync(kFull, lc.rcT, 1);
@@ -591,7 +594,7 @@ __device__ __forceinline__ bool sparse_membership(const Graph<W>& g, const Plits
         }
     }
     const int nins = (int)in1 + (int)in2;
-    if (cnt + nins > 32) {
+    if (cnt + nins > cap) {
         // refresh the listed vertices in row r / column c, then hand over to the bitmask mode
         if (dirty || (L.rc >> 8) == r || (L.rc & 0xFF) == c) lane_load<W>(g, s, L, wf, wc);
         __syncwarp();
@@ -666,6 +669,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     unsigned long long* prof = kDebug ? a.prof : nullptr;
     // steps, list, level, select, move, step, level iters, sum na | move: plane, membership, tail
     unsigned long long pc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long modes = 0;  // register-mode entries (low half) and exits (high half)
+    const int cap = kDebug ? min(max(g_plits_list_cap, kSparseEnter + 1), 32) : 32;
     long long tp0 = 0, tp1 = 0;
 
     // ---- tabu clock of this warp slot (two phases, each followed by a skip of tenure_cap + 2)
@@ -708,8 +713,11 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
         const int wc = phase == 1 ? 1 : 2 * nv;  // PhaseWeights::from_phi(0.5 / |V|), plits.hpp:27-33
         const int64_t budget = phase == 1 ? a.budget : a.budget2;
         if (phase == 2) plits_build<W>(g, s, lane, wf, wc, f, c, active);  // from phase 1's best
-        sparse = sparse_ok && active <= 32;
-        if (sparse) sparse_enter<W>(g, s, L, wf, wc, lane);
+        sparse = sparse_ok && active <= cap;
+        if (sparse) {
+            sparse_enter<W>(g, s, L, wf, wc, lane);
+            if (prof) ++modes;
+        }
         int64_t best_scaled = (int64_t)wf * f + (int64_t)wc * c;
         best_f = f;
         best_c = c;
@@ -998,7 +1006,8 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             long long tm0 = prof ? clock64() : 0;
             if (prof) pc[8] += (unsigned long long)(tm0 - tp1);
             if (sparse) {
-                sparse = sparse_membership<W>(g, s, L, vs, rs_, cs_, ks, lch, wf, wc, lane, active);
+                sparse = sparse_membership<W>(g, s, L, vs, rs_, cs_, ks, lch, wf, wc, lane, cap, active);
+                if (prof && !sparse) modes += 1ULL << 32;
             } else {
                 plits_membership<W>(g, s, rs_, cs_, from, ks, wf, wc, lane);
                 __syncwarp();
@@ -1038,9 +1047,10 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
-            if (!sparse && sparse_ok && active <= kSparseEnter) {
+            if (!sparse && sparse_ok && active <= cap - kSparseEnter) {
                 sparse_enter<W>(g, s, L, wf, wc, lane);
                 sparse = true;
+                if (prof) ++modes;
             }
             if (prof) pc[10] += (unsigned long long)(clock64() - tm0);
             tick(4);
@@ -1118,6 +1128,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
             for (int z = 0; z < 8; ++z) atomicAdd(prof + z, pc[z]);
             atomicAdd(prof + 8, 1ULL);
             for (int z = 8; z < 14; ++z) atomicAdd(prof + z + 1, pc[z]);
+            atomicAdd(prof + 15, modes);
         }
     }
     __syncwarp();
@@ -1203,6 +1214,10 @@ __global__ void __launch_bounds__(kPlitsMaxThreads, 1) k_plits(const ImproveArgs
     for (int i = first_individual(a.first, a.nslots, a.p, warp); i < a.p;
          i = next_individual(a.first, a.nslots, a.work_counter, lane))
         plits_one<W, kDebug>(a, g, s, until, a.slot_clock + slot, i, lane, sparse_ok);
+}
+
+cudaError_t set_plits_list_cap(int cap, cudaStream_t st) {
+    return cudaMemcpyToSymbolAsync(g_plits_list_cap, &cap, sizeof(int), 0, cudaMemcpyHostToDevice, st);
 }
 
 const void* plits_kernel_ptr(int W, bool debug) {

@@ -7,6 +7,8 @@ pins the kernel: final colourings, f, iteration counts (both phases), the
 per-step trace (move, delta, N, tenure, active-set size, f, c, best 2F) and the
 algorithmic byte counter; then the MPMA run() end to end.
 """
+import re
+
 import numpy as np
 import pytest
 
@@ -127,3 +129,37 @@ def test_mpma_cli_json_reports_variant(plse, orc, tmp_path):
     o = orc.run(grid, p=16, seed=31337, generation_limit=5, tie=oracle.TIE_CANON, variant=0)
     assert (j["f"], j["total_iterations"], j["generations"]) == (o["best_f"], o["total_iterations"],
                                                                  o["generations"])
+
+
+@pytest.mark.parametrize("cap", [32, 8])
+def test_plits_register_mode_transitions(plse, orc, capfd, monkeypatch, cap):
+    """The register-resident active list (|active| <= 32) is entered and left inside searches and the
+    results stay equal to the oracle's.  PLSE_PROFILE=1 runs the instrumented kernel, which counts the
+    transitions; PLSE_PLITS_CAP shrinks its list capacity so that the searches leave the mode too (with 32
+    lanes the active set rarely outgrows the list once it has shrunk into it)."""
+    monkeypatch.setenv("PLSE_PROFILE", "1")
+    monkeypatch.setenv("PLSE_PLITS_CAP", str(cap))
+    entries = exits = 0
+    for n, r, s in [(30, 0.5, 12345), (60, 0.5, 12345), (70, 0.6, 12345)]:
+        grid = orc.generate_instance(n, r, s)
+        g = plse.preprocess(grid)
+        p, b1, b2 = 16, 3000, 300
+        dp = plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=21, phase1_iters=b1, phase2_iters=b2,
+                                                        variant=plse.MPMA))
+        off = _offspring(orc, grid, g, p, 21)
+        dp.offspring = off
+        dp.improve(3)
+        imp = dp.improved
+        _, _, iters = dp.stats(plse.IMPROVED)
+        stop_f = 1 if g.l == 1 else 0
+        for i in range(p):
+            o = orc.plits(grid, off[i], orc.derive_seed(21, 2, 3 * p + i), b1, b2, 0.6, stop_f, tie=oracle.TIE_CANON)
+            assert iters[i] == o["iterations"] and np.array_equal(imp[i], o["best"]), (n, i)
+        err = capfd.readouterr().err
+        m = re.search(r"register mode: (\d+) entries, (\d+) exits", err)
+        assert m, err[-500:]
+        entries += int(m.group(1))
+        exits += int(m.group(2))
+    assert entries > 0
+    if cap < 32:
+        assert exits > 0
