@@ -41,7 +41,8 @@ def main():
             return None
         unit = u.get(name, "")
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9,
-                "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
+                "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+                "s": 1.0}.get(unit, 1.0)
         return v * mult
 
     moves = None
@@ -66,9 +67,9 @@ def main():
         "warps_active_pct": num(r.get("sm__warps_active.avg.pct_of_peak_sustained_active")),
         "sm_ghz": num(r.get("sm__cycles_elapsed.avg.per_second")),  # ncu reports it in GHz
         "source": os.path.relpath(raw, ROOT), "generation": gen,
-        "note": "ncu --clock-control none (sections SpeedOfLight/LaunchStats/Occupancy/WarpStateStats/"
-                "SchedulerStats plus instruction and DRAM metrics) of one launch (the generation above) of "
-                "improve_probe.py; dram bytes = dram__bytes_read.sum + dram__bytes_write.sum",
+        "note": os.environ.get("NOTE", "ncu --clock-control none (sections SpeedOfLight/LaunchStats/Occupancy/"
+                "WarpStateStats/SchedulerStats plus instruction and DRAM metrics) of one launch (the generation "
+                "above) of improve_probe.py; dram bytes = dram__bytes_read.sum + dram__bytes_write.sum"),
     }
     with open(out, "w") as f:
         json.dump(summary, f, indent=1)
