@@ -400,16 +400,18 @@ def run_ours(a):
     launches = last.kernel_launches - launches0
     timed_phase = dict(phase)
 
-    # e2e through the public API with host buffers: H2D offspring, generation, D2H next offspring + stats
-    host_off = pop.offspring
+    # e2e through the public API with host buffers: H2D offspring, generation, D2H next offspring + stats.
+    # The host rows live in pinned memory allocated once, as a serving loop would keep them.
+    host_off = torch.empty((p_rank, nv), dtype=torch.int16, pin_memory=True).numpy().view("uint16")
+    pop.read_colors(P.OFFSPRING, host_off)
     e2e_moves = 0
     barrier()
     t0 = time.perf_counter()
     for _ in range(a.e2e_steps):
-        pop.offspring = host_off
+        pop.write_colors(P.OFFSPRING, host_off)
         it, _, _, _ = generation()
         e2e_moves += it
-        host_off = pop.offspring
+        pop.read_colors(P.OFFSPRING, host_off)
         f, c, iters = pop.stats(P.IMPROVED)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -482,7 +484,8 @@ def run_ours(a):
                                                          peak),
             "best_f_seen": best,
             "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": a.e2e_steps},
+                    "d2h_bytes_per_step": d2h, "steps": a.e2e_steps,
+                    "host": "pinned u16 rows through write_colors / read_colors"},
             "gen1": gen1,
         }
         if world > 1 and (one_gpu or backend != "nccl"):

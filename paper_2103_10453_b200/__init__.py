@@ -533,9 +533,22 @@ class DevicePopulation:
         _check(_lib.plse_set_colors(self._ctx, which, a, a.size), self._ctx)
 
     def _get(self, which):
-        a = np.zeros(self.p * self.nv, np.uint16)
-        _check(_lib.plse_get_colors(self._ctx, which, a), self._ctx)
-        return a.reshape(self.p, self.nv)
+        return self.read_colors(which)
+
+    def read_colors(self, which, out=None) -> np.ndarray:
+        """Copy one of the device colourings (MEMBERS / OFFSPRING / IMPROVED) into `out` -- a C-contiguous
+        uint16 [p, |V|] array the caller keeps, e.g. over pinned memory, so repeated reads allocate nothing
+        and run at the full copy rate -- or into a new array."""
+        if out is None:
+            out = np.empty((self.p, self.nv), np.uint16)
+        if out.dtype != np.uint16 or out.shape != (self.p, self.nv) or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous uint16 array of shape ({self.p}, {self.nv})")
+        _check(_lib.plse_get_colors(self._ctx, which, out.reshape(-1)), self._ctx)
+        return out
+
+    def write_colors(self, which, colors) -> None:
+        """Upload a colouring (uint16 [p, |V|]; checked against the vertex domains on the device)."""
+        self._set(which, colors)
 
     members = property(lambda s: s._get(MEMBERS), lambda s, v: s._set(MEMBERS, v))
     offspring = property(lambda s: s._get(OFFSPRING), lambda s, v: s._set(OFFSPRING, v))

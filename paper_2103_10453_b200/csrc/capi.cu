@@ -24,6 +24,11 @@ using namespace plse_dev;
 
 namespace plse_dev {
 cudaError_t set_plits_list_cap(int cap, cudaStream_t st);  // plits.cu: the instrumented kernel's list capacity
+// population.cu: u16 host-format rows <-> u8 device rows, with the domain check
+cudaError_t launch_unpack_colors(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, int n, int W,
+                                 const uint16_t* cell, const uint64_t* pr, const uint64_t* pc, int* bad,
+                                 cudaStream_t st);
+cudaError_t launch_pack_colors(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad, cudaStream_t st);
 }
 
 namespace {
@@ -148,6 +153,10 @@ struct plse_ctx {
     // host staging (pinned, so host<->device copies run at full PCIe rate)
     uint8_t* stage = nullptr;
     size_t stage_bytes = 0;
+    // device copies of a host-format colouring (u16 rows) and its u8 form, allocated on first use
+    uint16_t* d_c16 = nullptr;
+    uint8_t* d_c8 = nullptr;
+    int* d_bad = nullptr;
     cudaEvent_t tm0 = nullptr, tm1 = nullptr;
     plse_counters ctr{};
     std::string err;
@@ -160,7 +169,7 @@ struct plse_ctx {
                         d_conf_scratch, d_work, d_prof, d_race, d_deadline, d_dsum, d_colvert, d_hA, d_hB, d_imc,
                         d_rpos, d_cpos, d_rinfo, d_cinfo,
                         d_nf, d_nc, ps.keys0, ps.keys1, ps.order, ps.sel, ps.nsel, ps.slots, ps.info, ps.legal,
-                        ps.admitted, ps.ok, ps.conf, d_migr, d_gf, d_gc, d_migd, d_hM, d_sum};
+                        ps.admitted, ps.ok, ps.conf, d_migr, d_gf, d_gc, d_migd, d_hM, d_sum, d_c16, d_c8, d_bad};
         for (void* b : bufs)
             if (b) cudaFree(b);
         if (stage) cudaFreeHost(stage);
@@ -651,23 +660,30 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     *out = ctx.release();
 }
 
+void ensure_color_buffers(plse_ctx* c) {
+    if (c->d_c16) return;
+    c->d_c16 = dalloc<uint16_t>((size_t)c->prm.p * c->nv);
+    c->d_c8 = dalloc<uint8_t>((size_t)c->prm.p * c->nvpad);
+    c->d_bad = dalloc<int>(1);
+}
+
+// the caller's u16 rows go to the device as they are; a kernel narrows them to the u8 rows and checks
+// every colour against its vertex's domain, and only a valid colouring replaces the target buffer
 void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) {
-    const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad, W = c->W;
+    const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad;
     if (!host) throw std::invalid_argument("null colours");
     if (count != (int64_t)p * nv) throw std::invalid_argument("assignment size mismatch");
-    uint8_t* stage = c->staging((size_t)p * nvpad);
-    for (int i = 0; i < p; ++i) {
-        uint8_t* row = stage + (size_t)i * nvpad;
-        for (int v = 0; v < nv; ++v) {
-            const uint16_t k = host[(size_t)i * nv + v];
-            if (k > c->n || !((c->h_dommask[(size_t)v * W + k / 64] >> (k % 64)) & 1))
-                throw std::invalid_argument("assignment leaves vertex domain");
-            row[v] = (uint8_t)k;
-        }
-        std::memset(row + nv, 0, nvpad - nv);
-    }
+    ensure_color_buffers(c);
+    CK(cudaMemcpyAsync(c->d_c16, host, (size_t)count * sizeof(uint16_t), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->d_bad, 0, sizeof(int), c->st));
+    c->launched(launch_unpack_colors(c->d_c16, c->d_c8, p, nv, nvpad, c->n, c->W, c->d_cell, c->d_pr, c->d_pc,
+                                     c->d_bad, c->st));
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (bad) throw std::invalid_argument("assignment leaves vertex domain");
     uint8_t* dst = c->colors(which);
-    CK(cudaMemcpyAsync(dst, stage, (size_t)p * nvpad, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dst, c->d_c8, (size_t)p * nvpad, cudaMemcpyDeviceToDevice, c->st));
     if (which == PLSE_MEMBERS) eval_into(c, dst, c->d_mf, c->d_mc);
     if (which == PLSE_IMPROVED) eval_into(c, dst, c->d_best_f, c->d_imc);
     c->onehot_valid = false;
@@ -677,11 +693,10 @@ void upload_colors(plse_ctx* c, int which, const uint16_t* host, int64_t count) 
 void download_colors(plse_ctx* c, int which, uint16_t* host) {
     const int p = c->prm.p, nv = c->nv, nvpad = c->nvpad;
     if (!host) throw std::invalid_argument("null output");
-    uint8_t* stage = c->staging((size_t)p * nvpad);
-    CK(cudaMemcpyAsync(stage, c->colors(which), (size_t)p * nvpad, cudaMemcpyDeviceToHost, c->st));
+    ensure_color_buffers(c);
+    c->launched(launch_pack_colors(c->colors(which), c->d_c16, p, nv, nvpad, c->st));
+    CK(cudaMemcpyAsync(host, c->d_c16, (size_t)p * nv * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    for (int i = 0; i < p; ++i)
-        for (int v = 0; v < nv; ++v) host[(size_t)i * nv + v] = stage[(size_t)i * nvpad + v];
 }
 
 void improve_impl(plse_ctx* c, uint64_t gen, int trace_idx, int64_t trace_cap, plse_step* d_trace, int p_eff,

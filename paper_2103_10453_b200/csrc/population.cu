@@ -71,6 +71,58 @@ cudaError_t launch_eval_fc(const PopGraph& g, int p, const uint8_t* colors, int3
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- host-format colourings
+// plse_set_colors / plse_get_colors exchange u16 rows [p][nv] with the caller; the device keeps u8 rows
+// [p][nvpad] (zero padding).  The conversion and the domain check (every colour 0 or not prefilled in its
+// row or column, lsgraph.hpp:152-156) run here, over the copied u16 rows, instead of a host loop.
+__global__ void k_unpack_colors(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, int n, int W,
+                                const uint16_t* cell, const uint64_t* pr, const uint64_t* pc, int* bad) {
+    const int quads = nvpad >> 2;
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (size_t)p * quads) return;
+    const int i = (int)(t / quads), v0 = (int)(t % quads) * 4;
+    const uint16_t* row = in + (size_t)i * nv;
+    uint32_t word = 0;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int v = v0 + j;
+        if (v >= nv) break;
+        const int k = row[v];
+        if (k) {
+            const uint16_t rc = cell[v];
+            const int q = k >> 6;
+            const bool taken = q < W && (((pr[(rc >> 8) * W + q] | pc[(rc & 0xFF) * W + q]) >> (k & 63)) & 1ULL);
+            ok &= k <= n && !taken;
+        }
+        word |= (uint32_t)(k & 0xFF) << (8 * j);
+    }
+    if (!ok) atomicOr(bad, 1);
+    reinterpret_cast<uint32_t*>(out + (size_t)i * nvpad)[v0 >> 2] = word;
+}
+
+__global__ void k_pack_colors(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (size_t)p * nv) return;
+    const int i = (int)(t / nv), v = (int)(t % nv);
+    out[t] = in[(size_t)i * nvpad + v];
+}
+
+cudaError_t launch_unpack_colors(const uint16_t* in, uint8_t* out, int p, int nv, int nvpad, int n, int W,
+                                 const uint16_t* cell, const uint64_t* pr, const uint64_t* pc, int* bad,
+                                 cudaStream_t st) {
+    const size_t threads = (size_t)p * (nvpad >> 2);
+    k_unpack_colors<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(in, out, p, nv, nvpad, n, W, cell, pr, pc,
+                                                                       bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_colors(const uint8_t* in, uint16_t* out, int p, int nv, int nvpad, cudaStream_t st) {
+    const size_t threads = (size_t)p * nv;
+    k_pack_colors<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(in, out, p, nv, nvpad);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- K4b matching
 // crossover.hpp:67-83 + nearest_neighbor population.hpp:209-228.  The partner
 // loop is sequential in the reference but every row reads and writes only its
