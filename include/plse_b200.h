@@ -183,6 +183,10 @@ int plse_verify_certificate(int32_t n, const uint16_t* instance, int32_t m, cons
 /* ---- device context */
 int plse_create(const plse_graph* graph, const plse_params* params, int32_t device, plse_ctx** out);
 void plse_destroy(plse_ctx* ctx);
+/* colourings as u16 rows [p][|V|] (vertex order of plse_preprocess).  set: the rows are copied as they are
+   and checked on the device (every colour 0 or in the vertex's domain, lsgraph.hpp:152-156); an invalid
+   colouring returns PLSE_ERR_INVALID ("assignment leaves vertex domain") and leaves the buffer unchanged.
+   Pinned host rows (cudaHostAlloc / cudaHostRegister) copy at the full link rate; pageable ones work too. */
 int plse_set_colors(plse_ctx* ctx, int32_t which, const uint16_t* host, int64_t count /* p*|V| */);
 int plse_get_colors(plse_ctx* ctx, int32_t which, uint16_t* host);
 int plse_get_dist(plse_ctx* ctx, int32_t which, int32_t* host /* p*p */);
