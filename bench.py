@@ -444,8 +444,11 @@ def run_ours(a):
                               else "SURVEY 8(d) B_t summed over every step of the launch (int16 gamma rows the "
                                    "reference's step reads; this kernel derives gamma from occupancy masks)"),
                 "kernel_share_of_step": imp_ms / ms,
-                "binding_limit": "instruction issue (the gamma table is never materialised: measured DRAM "
-                                 "traffic is well under 1% of the algorithmic bytes; see roofline.issue)"}
+                "binding_limit": ("single-warp step latency: from generation 2 on a generation lasts as long as "
+                                  "the ~55 individuals that run the whole budget, one lone warp each (DESIGN.md "
+                                  "'PLITS kernel'); DRAM traffic is well under 1% of the algorithmic bytes" if mpma
+                                  else "instruction issue (the gamma table is never materialised: measured DRAM "
+                                       "traffic is well under 1% of the algorithmic bytes; see roofline.issue)")}
         if prof and prof.get("inst_per_move") and clk.get("sm_mhz"):
             peak_inst = 148 * 4 * clk["sm_mhz"] * 1e6
             ach_inst = prof["inst_per_move"] * improve_rate
