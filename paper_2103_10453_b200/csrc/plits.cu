@@ -272,13 +272,13 @@ __device__ __forceinline__ int level_adm(const VertexMoves<W>& m, int dl, int wc
 }
 
 // ---- register-resident mode: while |active| <= 32 lane L holds the L-th active vertex (ascending id)
-// with its move classes, tabu-blind minimum and possibly-tabu mask in registers, and a move updates the
-// list in place: only the cells of the moved vertex's row and column whose colour is the old or the new
-// one can change membership (their counts are the only ones that moved), so no re-classification scan
-// and no compaction run per step.  The shared-memory active bitmask and minima are not maintained in
-// this mode; they are rebuilt from the list when the set outgrows a warp.
-constexpr int kNoV = 0xFFFF;      // an empty lane: sorts after every vertex id
-constexpr int kSparseEnter = 4;  // enter at <= cap - 4 active vertices, leave above cap (hysteresis)
+// with its move classes, tabu-blind minimum and tabu entries in registers, and a move updates the list
+// in place: only the cells of the moved vertex's row and column whose colour is the old or the new one
+// can change membership (their counts are the only ones that moved), so no re-classification scan and
+// no compaction run per step.  The shared-memory active bitmask and minima are not maintained in this
+// mode (their space holds the xor tables); they are rebuilt from the list when the set outgrows a warp.
+constexpr int kNoV = 0xFFFF;        // an empty lane: sorts after every vertex id
+constexpr int kListHysteresis = 4;  // enter at <= cap - 4 active vertices, leave above cap
 // the list capacity: 32 (one vertex per lane); the instrumented kernel takes a smaller one from
 // PLSE_PLITS_CAP so that tests drive the mode transitions often
 __device__ int g_plits_list_cap = 32;
@@ -670,7 +670,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
     // steps, list, level, select, move, step, level iters, sum na | move: plane, membership, tail
     unsigned long long pc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long modes = 0;  // register-mode entries (low half) and exits (high half)
-    const int cap = kDebug ? min(max(g_plits_list_cap, kSparseEnter + 1), 32) : 32;
+    const int cap = kDebug ? min(max(g_plits_list_cap, kListHysteresis + 1), 32) : 32;
     long long tp0 = 0, tp1 = 0;
 
     // ---- tabu clock of this warp slot (two phases, each followed by a skip of tenure_cap + 2)
@@ -1047,7 +1047,7 @@ __device__ void plits_one(const ImproveArgs& a, const Graph<W>& g, const PlitsWa
                                 N, dl};
             }
             __syncwarp();
-            if (!sparse && sparse_ok && active <= cap - kSparseEnter) {
+            if (!sparse && sparse_ok && active <= cap - kListHysteresis) {
                 sparse_enter<W>(g, s, L, wf, wc, lane);
                 sparse = true;
                 if (prof) ++modes;
