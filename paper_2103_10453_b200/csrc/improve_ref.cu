@@ -65,6 +65,49 @@ __device__ __forceinline__ int popc_range(const uint64_t (&m)[W], int pos, int e
     return c;
 }
 
+// the fast paths' draws: M consecutive outputs of the individual's xoshiro256++ stream, 32 at a time.
+// Only the state update is a serial chain, so lane 0 runs just that (14 word ops per output) and parks
+// each output's inputs (s0, s3 before the update) in stage[]; the lanes then form the outputs
+// rotl(s0 + s3, 23) + s0 in parallel.  For output d: d < E is an early draw (only its possible rejection
+// matters), d >= E is the draw of final-segment member j = d - E + 2, kept iff next_below(j) == 0.
+// Returns, per lane, the largest kept member (0: none) and raises `bad` on an output below 2^32 (a
+// rejection is possible: the caller takes the exact walk).
+__device__ __forceinline__ int ref_stream_draws(Xoshiro& rng, uint64_t* stage, int E, int M, int lane, bool& bad) {
+    int bestj = 0;
+    bool low = false;
+    for (int d0 = 0; d0 < M; d0 += 32) {
+        const int cnt = min(32, M - d0);
+        if (lane == 0) {
+            uint64_t s0 = rng.s0, s1 = rng.s1, s2 = rng.s2, s3 = rng.s3;
+            for (int d = 0; d < cnt; ++d) {
+                reinterpret_cast<ulonglong2*>(stage)[d] = make_ulonglong2(s0, s3);
+                const uint64_t t = s1 << 17;
+                s2 ^= s0;
+                s3 ^= s1;
+                s1 ^= s2;
+                s0 ^= s3;
+                s2 ^= t;
+                s3 = Xoshiro::rotl(s3, 45);
+            }
+            rng.s0 = s0;
+            rng.s1 = s1;
+            rng.s2 = s2;
+            rng.s3 = s3;
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            const ulonglong2 in = reinterpret_cast<const ulonglong2*>(stage)[lane];
+            const uint64_t y = Xoshiro::rotl(in.x + in.y, 23) + in.x;
+            low |= (y >> 32) == 0;
+            const int d = d0 + lane;
+            if (d >= E && divides((uint64_t)(d - E + 2), y)) bestj = d - E + 2;
+        }
+        __syncwarp();
+    }
+    bad = __any_sync(kFull, low);
+    return bestj;
+}
+
 // draws the reference makes inside one vertex entered at running level cur (3 = nothing found yet),
 // stopping at its first level-`stop` candidate when stop < 3
 template <int W>
@@ -189,31 +232,12 @@ __device__ __forceinline__ bool partial_ref_fast(const Graph<W>& g, const WarpSm
     }
     fstamp(7);
     // ---- final-segment member j (1-based; the first is j = 1) keeps the choice iff next_below(j) == 0,
-    // draw E + j - 2 of the stream: lane 0 generates it 32 outputs at a time into msk, the lanes test the
-    // members round-robin
+    // draw E + j - 2 of the stream (ref_stream_draws)
     const Xoshiro saved = rng;
-    uint32_t bad = 0;  // lane 0: an output below 2^32, a rejection is possible
-    if (lane == 0) {
-#pragma unroll 4
-        for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
-    }
-    int bestj = 0;
-    for (int j0 = 2; j0 <= ND; j0 += 32) {
-        const int cnt = min(32, ND - j0 + 1);
-        if (lane == 0) {
-#pragma unroll 4
-            for (int d = 0; d < cnt; ++d) {
-                const uint64_t y = rng.next();
-                bad |= (uint32_t)((y >> 32) == 0);
-                msk[d] = y;
-            }
-        }
-        __syncwarp();
-        if (lane < cnt && divides((uint64_t)(j0 + lane), msk[lane])) bestj = j0 + lane;
-        __syncwarp();
-    }
+    bool bad = false;
+    const int bestj = ref_stream_draws(rng, msk, E, E + ND - 1, lane, bad);
     fstamp(8);
-    if (__shfl_sync(kFull, bad, 0)) {
+    if (bad) {
         if (lane == 0) rng = saved;  // take the exact path
         return false;
     }
@@ -357,28 +381,10 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 const int ND = __shfl_sync(kFull, sD, 31);
                 sD -= cD;  // exclusive: index (0-based) of this lane's first level-D candidate
                 const Xoshiro saved = rng;
-                uint32_t bad = 0;  // lane 0: an output below 2^32, a rejection is possible
                 if (prof) pc[10] += (unsigned)E;
-                if (lane == 0) {
-#pragma unroll 4
-                    for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
-                }
-                int bestj = 0;
-                for (int j0 = 2; j0 <= ND; j0 += 32) {
-                    const int cnt = min(32, ND - j0 + 1);
-                    if (lane == 0) {
-#pragma unroll 4
-                        for (int d = 0; d < cnt; ++d) {
-                            const uint64_t y = rng.next();
-                            bad |= (uint32_t)((y >> 32) == 0);
-                            msk[d] = y;
-                        }
-                    }
-                    __syncwarp();
-                    if (lane < cnt && divides((uint64_t)(j0 + lane), msk[lane])) bestj = j0 + lane;
-                    __syncwarp();
-                }
-                if (!__shfl_sync(kFull, bad, 0)) {
+                bool bad = false;
+                const int bestj = ref_stream_draws(rng, msk, E, E + ND - 1, lane, bad);
+                if (!bad) {
                     int J = (int)__reduce_max_sync(kFull, (unsigned)bestj);
                     if (J == 0) J = 1;
                     const bool own = sD < J && J <= sD + cD;
