@@ -65,50 +65,6 @@ __device__ __forceinline__ int popc_range(const uint64_t (&m)[W], int pos, int e
     return c;
 }
 
-// the fast paths' draws: M consecutive outputs of the individual's xoshiro256++ stream, 32 at a time.
-// Only the state update is a serial chain, so lane 0 runs just that (14 word ops per output) and parks
-// each output's inputs (s0, s3 before the update) in stage[0, 64); the lanes then form the outputs
-// rotl(s0 + s3, 23) + s0 in parallel.  For output d: d < E is an early draw (only its possible rejection
-// matters), d >= E is the draw of final-segment member j = d - E + 2, kept iff next_below(j) == 0.
-// Returns, per lane, the largest kept member (0: none) and raises `bad` on an output below 2^32 (a
-// rejection is possible: the caller takes the exact walk).
-__device__ __forceinline__ int ref_stream_draws(Xoshiro& rng, uint64_t* stage, int E, int M, int lane, bool& bad) {
-    int bestj = 0;
-    bool low = false;
-    for (int d0 = 0; d0 < M; d0 += 32) {
-        const int cnt = min(32, M - d0);
-        if (lane == 0) {
-            uint64_t s0 = rng.s0, s1 = rng.s1, s2 = rng.s2, s3 = rng.s3;
-            for (int d = 0; d < cnt; ++d) {
-                stage[d] = s0;  // two 64-bit stores from the state's own register pairs (no packing moves)
-                stage[32 + d] = s3;
-                const uint64_t t = s1 << 17;
-                s2 ^= s0;
-                s3 ^= s1;
-                s1 ^= s2;
-                s0 ^= s3;
-                s2 ^= t;
-                s3 = Xoshiro::rotl(s3, 45);
-            }
-            rng.s0 = s0;
-            rng.s1 = s1;
-            rng.s2 = s2;
-            rng.s3 = s3;
-        }
-        __syncwarp();
-        if (lane < cnt) {
-            const uint64_t x0 = stage[lane], x3 = stage[32 + lane];
-            const uint64_t y = Xoshiro::rotl(x0 + x3, 23) + x0;
-            low |= (y >> 32) == 0;
-            const int d = d0 + lane;
-            if (d >= E && divides((uint64_t)(d - E + 2), y)) bestj = d - E + 2;
-        }
-        __syncwarp();
-    }
-    bad = __any_sync(kFull, low);
-    return bestj;
-}
-
 // draws the reference makes inside one vertex entered at running level cur (3 = nothing found yet),
 // stopping at its first level-`stop` candidate when stop < 3
 template <int W>

@@ -335,7 +335,7 @@ __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRef
         }
     };
     const int nch = (nseq + 31) >> 5;
-    uint64_t* out = s.stage;  // 32 outputs of the stream at a time
+    uint64_t* out = s.stage;  // the inputs of 32 stream outputs at a time (ref_stream_draws)
     const int64_t asp64 = best_scaled - cur_scaled;
     const int asp = (int)max((int64_t)INT_MIN / 4, min((int64_t)INT_MAX / 4, asp64));
     auto empty = [](LaneView<W>& x) {
@@ -391,29 +391,11 @@ __device__ __forceinline__ bool plits_ref_fast(const Graph<W>& g, const PlitsRef
     // member j (1-based, in walk order) of the final segment keeps the choice iff next_below(j) == 0
     // (j >= 2): draw E + j - 2 of the stream
     const Xoshiro before = rng;
-    uint32_t bad = 0;  // lane 0: an output below 2^32 -- a rejection is possible, take the exact path
     if (tp) tp[5] += (unsigned)(E + ND - 1);
-    if (lane == 0) {
-#pragma unroll 4
-        for (int d = 0; d < E; ++d) bad |= (uint32_t)((rng.next() >> 32) == 0);
-    }
-    int bestj = 0;
-    for (int j0 = 2; j0 <= ND; j0 += 32) {
-        const int cnt = min(32, ND - j0 + 1);
-        if (lane == 0) {
-#pragma unroll 4
-            for (int d = 0; d < cnt; ++d) {
-                const uint64_t y = rng.next();
-                bad |= (uint32_t)((y >> 32) == 0);
-                out[d] = y;
-            }
-        }
-        __syncwarp();
-        if (lane < cnt && divides((uint64_t)(j0 + lane), out[lane])) bestj = j0 + lane;
-        __syncwarp();
-    }
+    bool bad = false;  // an output below 2^32: a rejection is possible, take the exact path
+    const int bestj = ref_stream_draws(rng, out, E, E + ND - 1, lane, bad);
     stamp(3);
-    if (__shfl_sync(kFull, bad, 0)) {
+    if (bad) {
         if (lane == 0) rng = before;
         return false;
     }
