@@ -71,7 +71,7 @@ def args_():
     ap.add_argument("--budget2", type=int, default=0, help="PLITS phase-2 iterations (0 = 2|V|)")
     ap.add_argument("--tie", default="canon", choices=["canon", "ref"],
                     help="PartialCol tie-break: canonical (throughput) or the reference's draws (bit-exact)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--migrate-every", type=int, default=2)
     ap.add_argument("--elites", type=int, default=32)
     ap.add_argument("--cpu-per-thread", type=int, default=72, help="individuals per host thread in the CPU sample")
