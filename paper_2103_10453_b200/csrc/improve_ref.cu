@@ -65,6 +65,23 @@ __device__ __forceinline__ int popc_range(const uint64_t (&m)[W], int pos, int e
     return c;
 }
 
+// dense_masks with the vertex's tabu record held by the lane (the fast path |V0| <= 32 keeps each IndexSet
+// position's record in its lane across steps: no vertex that stays uncoloured is written by anyone else);
+// a cache rebuild is still written back, so HBM stays authoritative for the vertex's next owner
+template <int W>
+__device__ __forceinline__ void dense_masks_held(const Graph<W>& g, const WarpSmem& s, TabuRec* rec,
+                                                 const uint32_t* until, int v, uint32_t t, bool asp, TabuRec& tr,
+                                                 uint64_t (&m0)[W], uint64_t (&m1)[W], uint64_t (&m2)[W]) {
+    const uint16_t rc = g.cell[v];
+    const int r = rc >> 8, c = rc & 0xFF;
+    uint64_t dom[W], T[W];
+    dom_mask<W>(g, r, c, dom);
+    const uint32_t kk0 = tr.kk;
+    tabu_of<W>(tr.u1, tr.u2, tr.kk, until + (size_t)v * (g.n + 1), dom, t, T);
+    if (tr.kk != kk0) rec[v] = tr;
+    level_masks<W>(s, r, c, dom, T, asp, m0, m1, m2);
+}
+
 // draws the reference makes inside one vertex entered at running level cur (3 = nothing found yet),
 // stopping at its first level-`stop` candidate when stop < 3
 template <int W>
@@ -278,6 +295,10 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
     }
     __syncwarp();
 
+    // the tabu record of IndexSet position `lane` while |V0| <= 32 (held_v: its vertex, -1 = not held)
+    TabuRec held{0, 0, 0, 0};
+    int held_v = -1;
+
     const uint64_t seed = derive_seed(a.master, 2, a.generation * a.p_total + a.offset + (uint64_t)i);
     Xoshiro rng(seed);  // the stream of Rng(derive_stream(master, kImprove, gen*p + i)), engine.hpp:189-191
     const int repaired_f = f;
@@ -317,7 +338,14 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
             uint64_t a0[W], a1[W], a2[W];
 #pragma unroll
             for (int q = 0; q < W; ++q) a0[q] = a1[q] = a2[q] = 0;
-            if (lane < f) dense_masks<W>(g, s, rec, until, el[lane], t, asp, a0, a1, a2);
+            if (lane < f) {
+                const int v = el[lane];
+                if (v != held_v) {
+                    held = rec[v];
+                    held_v = v;
+                }
+                dense_masks_held<W>(g, s, rec, until, v, t, asp, held, a0, a1, a2);
+            }
             const int m = (lane >= f) ? 3 : popc_w<W>(a0) ? 0 : popc_w<W>(a1) ? 1 : popc_w<W>(a2) ? 2 : 3;
             const int D = (int)__reduce_min_sync(kFull, (unsigned)m);
             if (D == 3) {
@@ -364,8 +392,10 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
                 __syncwarp();
             }
         } else {
+            held_v = -1;  // the rounds of 32 read (and may rebuild) the records in HBM
             fast_done = partial_ref_fast<W>(g, s, rec, until, el, msk, f, t, asp, lane, rng, st, prof ? pc : nullptr);
         }
+        if (!fast_done) held_v = -1;  // the serial walk reads the records in HBM
         if (prof) {
             const long long x = clock64();
             pc[2] += (unsigned long long)(x - tq);
@@ -451,7 +481,27 @@ __device__ void improve_ref_one(const ImproveArgs& a, const Graph<W>& g, const W
         const uint32_t ut = t + 1 + tenure;
         const bool improved = f_new < bestf;
         __syncwarp();
-        apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, f_before, improved, ut, t, lane, acc);
+        const TabuRec evr = apply_move_lanes<W>(g, s, rec, until, vs, ur, uc, ks, rs_, cs_, inR, inC, f_before,
+                                                improved, ut, t, lane, acc);
+        {
+            // the held records follow the IndexSet: position ps takes the last position's, the evictees'
+            // (appended at f - 1, f) are the records the move just wrote (lanes 1 / 2)
+            const int lv = __shfl_sync(kFull, held_v, f - 1);
+            const uint32_t l1 = __shfl_sync(kFull, held.u1, f - 1), l2 = __shfl_sync(kFull, held.u2, f - 1);
+            const uint32_t lk = __shfl_sync(kFull, held.kk, f - 1);
+            const int src0 = ev0 == ur ? 1 : 2, src1 = ev1 == ur ? 1 : 2;
+            const int srcl = lane == f - 1 ? src0 : src1;
+            const uint32_t e1 = __shfl_sync(kFull, evr.u1, srcl), e2 = __shfl_sync(kFull, evr.u2, srcl);
+            const uint32_t ek = __shfl_sync(kFull, evr.kk, srcl);
+            if (lane == ps) {
+                held_v = lv;
+                held = TabuRec{l1, l2, lk, 0};
+            }
+            if ((lane == f - 1 && ev0 >= 0) || (lane == f && ev1 >= 0)) {
+                held_v = lane == f - 1 ? ev0 : ev1;
+                held = TabuRec{e1, e2, ek, 0};
+            }
+        }
         f = f_new;
         if (improved) {
             bestf = f;
