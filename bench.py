@@ -405,7 +405,9 @@ def run_ours(a):
     host_off = torch.empty((p_rank, nv), dtype=torch.int16, pin_memory=True).numpy().view("uint16")
     pop.read_colors(P.OFFSPRING, host_off)
     e2e_moves = 0
+    e2e_gen0 = gen + 1
     barrier()
+    pop.timer_start()
     t0 = time.perf_counter()
     for _ in range(a.e2e_steps):
         pop.write_colors(P.OFFSPRING, host_off)
@@ -415,6 +417,11 @@ def run_ours(a):
         f, c, iters = pop.stats(P.IMPROVED)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    # the same steps on the stream's clock: e2e / this rate is the host-side cost alone, while e2e / value
+    # also carries the search's drift between the timed generations and these later ones (more
+    # individuals stop early at f = 0 as the population converges; the generation still lasts as long as
+    # its full-budget walks)
+    e2e_dev_ms = pop.timer_stop()
     h2d = p_rank * nv * 2
     d2h = p_rank * nv * 2 + p_rank * (4 + 4 + 8)
 
@@ -488,6 +495,10 @@ def run_ours(a):
             "best_f_seen": best,
             "e2e": {"value": tot_e2e / e2e_max if e2e_max > 0 else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": a.e2e_steps,
+                    "generations": [e2e_gen0, e2e_gen0 + a.e2e_steps - 1],
+                    "timed_generations": [a.warmup + 1, a.warmup + a.steps],
+                    "device_rate_same_steps": (e2e_moves / (e2e_dev_ms / 1e3) if world == 1 and e2e_dev_ms > 0
+                                               else None),
                     "host": "pinned u16 rows through write_colors / read_colors"},
             "gen1": gen1,
         }
