@@ -212,21 +212,44 @@ __global__ void __launch_bounds__(kPoolBlock) k_pool_resolve(const int32_t* orde
     }
     __syncthreads();
     if (warp != 0) return;
-    uint32_t blocked = 0;
+    // 32 candidates (one word) at a time: lane j holds the within-word part of candidate j's conflict row
+    // (later candidates of the word within |V|/gamma of it), so the greedy in pool order only visits the
+    // candidates still available -- the lowest one is admitted and knocks out its later conflicts -- with
+    // no shared-memory round trip per candidate; the admitted rows then update the words of the later
+    // candidates in one pass (independent loads).
+    uint32_t blocked = 0;  // lane l: word l of "within |V|/gamma of a candidate admitted in this block"
     for (int wi = 0; wi < cwords && ns < p; ++wi) {
-        uint32_t cand = s_ok[wi];
-        while (cand && ns < p) {
-            const int b = __ffs(cand) - 1;
-            cand &= cand - 1;
-            const int t = wi * 32 + b;
-            const uint32_t wbits = __shfl_sync(kFull, blocked, wi);
-            if (!((wbits >> b) & 1u)) {
-                if (lane == 0) {
-                    sel[ns] = order[blk_lo + t];
-                    admitted[blk_lo + t] = 1;
-                }
-                ++ns;
-                if (lane < cwords) blocked |= s_conf[t * cwords + lane];
+        const uint32_t okw = s_ok[wi];
+        const int t = wi * 32 + lane;
+        const uint32_t R = ((okw >> lane) & 1u) ? s_conf[t * cwords + wi] : 0u;
+        uint32_t avail = okw & ~__shfl_sync(kFull, blocked, wi);
+        uint32_t A = 0;
+        while (avail) {
+            const int b = __ffs(avail) - 1;
+            A |= 1u << b;
+            avail &= ~__shfl_sync(kFull, R, b) & (avail - 1);  // drop b and the later ones it conflicts with
+        }
+        // admission stops at p members (population.hpp:146): keep the first p - ns in pool order
+        const int room = p - ns;
+        if (__popc(A) > room) {
+            uint32_t keep = 0, x = A;
+            for (int k = 0; k < room; ++k) {
+                keep |= x & (0u - x);
+                x &= x - 1;
+            }
+            A = keep;
+        }
+        if ((A >> lane) & 1u) {
+            sel[ns + __popc(A & ((1u << lane) - 1u))] = order[blk_lo + t];
+            admitted[blk_lo + t] = 1;
+        }
+        ns += __popc(A);
+        if (lane < cwords) {
+            uint32_t x = A;
+            while (x) {
+                const int b = __ffs(x) - 1;
+                x &= x - 1;
+                blocked |= s_conf[(wi * 32 + b) * cwords + lane];
             }
         }
     }
