@@ -189,6 +189,9 @@ void plse_destroy(plse_ctx* ctx);
    Pinned host rows (cudaHostAlloc / cudaHostRegister) copy at the full link rate; pageable ones work too. */
 int plse_set_colors(plse_ctx* ctx, int32_t which, const uint16_t* host, int64_t count /* p*|V| */);
 int plse_get_colors(plse_ctx* ctx, int32_t which, uint16_t* host);
+/* one row (individual `index`) of a population buffer: |V| u16 colours (the run's best without the whole
+   population crossing the link) */
+int plse_get_row(plse_ctx* ctx, int32_t which, int32_t index, uint16_t* host /* |V| */);
 int plse_get_dist(plse_ctx* ctx, int32_t which, int32_t* host /* p*p */);
 int plse_set_dist(plse_ctx* ctx, int32_t which, const int32_t* host);
 /* f, c (conflicting edges) and the last improve's iterations per individual; any may be NULL */

@@ -151,6 +151,7 @@ def _load() -> C.CDLL:
         "plse_destroy": ([ctx], None),
         "plse_set_colors": ([ctx, C.c_int32, u16p, C.c_int64], C.c_int),
         "plse_get_colors": ([ctx, C.c_int32, u16p], C.c_int),
+        "plse_get_row": ([ctx, C.c_int32, C.c_int32, u16p], C.c_int),
         "plse_get_dist": ([ctx, C.c_int32, i32p], C.c_int),
         "plse_set_dist": ([ctx, C.c_int32, i32p], C.c_int),
         "plse_get_stats": ([ctx, C.c_int32, vp, vp, vp], C.c_int),
@@ -544,6 +545,12 @@ class DevicePopulation:
         if out.dtype != np.uint16 or out.shape != (self.p, self.nv) or not out.flags.c_contiguous:
             raise ValueError(f"out must be a C-contiguous uint16 array of shape ({self.p}, {self.nv})")
         _check(_lib.plse_get_colors(self._ctx, which, out.reshape(-1)), self._ctx)
+        return out
+
+    def read_row(self, which, index: int) -> np.ndarray:
+        """One individual's colouring (uint16 [|V|]) without copying the whole population."""
+        out = np.empty(self.nv, np.uint16)
+        _check(_lib.plse_get_row(self._ctx, which, int(index), out), self._ctx)
         return out
 
     def write_colors(self, which, colors) -> None:

@@ -1020,6 +1020,20 @@ int plse_get_colors(plse_ctx* c, int32_t which, uint16_t* host) {
     });
 }
 
+int plse_get_row(plse_ctx* c, int32_t which, int32_t index, uint16_t* host) {
+    if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!host) throw std::invalid_argument("null output");
+        if (index < 0 || index >= c->prm.p) throw std::invalid_argument("individual index out of range");
+        std::vector<uint8_t> row((size_t)c->nvpad);
+        CK(cudaMemcpyAsync(row.data(), c->colors(which) + (size_t)index * c->nvpad, (size_t)c->nvpad,
+                           cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (int v = 0; v < c->nv; ++v) host[v] = row[v];
+    });
+}
+
 int plse_get_dist(plse_ctx* c, int32_t which, int32_t* host) {
     if (!c) return finish(nullptr, PLSE_ERR_INVALID, "null context");
     return guard(c, [&] {

@@ -206,7 +206,7 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
         lf = int(f[loc]) if loc >= 0 else nv
         gf, owner, _, _ = glob(lf, 0)
         if gf < best_f:
-            take_best(gf, owner, pop.members[loc] if rank == owner else None)
+            take_best(gf, owner, pop.read_row(P.MEMBERS, loc) if rank == owner else None)
         members = lambda: pop.members if keep_members else None
         if not config.disable_optimal_stop and is_opt(best_f):
             return result(best_f, best, "optimal", 0, 0, ttb, members())
@@ -221,7 +221,7 @@ def run_islands(grid: np.ndarray, config, migrate_every: int = 2, n_elite: int =
             gf, owner, git, el = glob(bf if bi >= 0 else nv, it)
             total += git
             if gf < best_f:
-                take_best(gf, owner, pop.improved[bi] if rank == owner else None)
+                take_best(gf, owner, pop.read_row(P.IMPROVED, bi) if rank == owner else None)
             optimal = not config.disable_optimal_stop and is_opt(best_f)
             time_up = config.time_limit > 0 and el >= config.time_limit
             iters_up = config.iteration_limit > 0 and total >= config.iteration_limit

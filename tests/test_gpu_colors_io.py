@@ -39,6 +39,10 @@ def test_round_trip_and_domain_check(plse, orc, n, r, s, p):
     with pytest.raises(ValueError, match="assignment leaves vertex domain"):
         pop.write_colors(plse.MEMBERS, too_big)
     assert np.array_equal(pop.read_colors(plse.MEMBERS), cols)
+    for i in (0, p // 3, p - 1):
+        assert np.array_equal(pop.read_row(plse.MEMBERS, i), cols[i])
+    with pytest.raises(ValueError, match="out of range"):
+        pop.read_row(plse.MEMBERS, p)
     with pytest.raises(ValueError, match="size mismatch"):
         pop.write_colors(plse.MEMBERS, cols[:-1])
     with pytest.raises(ValueError):

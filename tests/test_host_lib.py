@@ -139,6 +139,7 @@ def test_raw_abi_rejects_null_and_bad_arguments(plse):
         "plse_get_counters": (nul, nul),
         "plse_timer_start": (nul,),
         "plse_get_colors": (nul, ctypes.c_int32(0), buf),
+        "plse_get_row": (nul, ctypes.c_int32(0), ctypes.c_int32(0), buf),
         "plse_to_grid": (nul, buf, buf),
         "plse_solve_exact": (nul, ctypes.c_int64(10), ctypes.byref(i32), ctypes.byref(i32), ctypes.byref(i64), buf),
         "plse_verify_certificate": (ctypes.c_int32(2), nul, ctypes.c_int32(2), nul, ctypes.byref(i32),
