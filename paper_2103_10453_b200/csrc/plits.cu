@@ -304,12 +304,13 @@ __device__ __forceinline__ int level_adm_cached(const LaneVertex<W>& L, int dl, 
 #pragma unroll
         for (int z = 0; z < 2; ++z) {
             const int k = z ? (L.tk >> 8) & 0xFF : L.tk & 0xFF;
-            if ((z ? L.u2 : L.u1) > t) {
-                if (k == 0) adm0 = false;
+            const bool live = (z ? L.u2 : L.u1) > t;
+            if (live && k == 0) adm0 = false;
+            // a select per word (a conditional update per word would be folded into adm[k >> 6], which
+            // puts the array in local memory for W = 2)
+            const uint64_t clear = (live && k) ? 1ULL << (k & 63) : 0ULL;
 #pragma unroll
-                for (int q = 0; q < W; ++q)
-                    if (k && (k >> 6) == q) adm[q] &= ~(1ULL << (k & 63));
-            }
+            for (int q = 0; q < W; ++q) adm[q] &= ((k >> 6) == q) ? ~clear : ~0ULL;
         }
     }
     return popc_w<W>(adm) + (adm0 ? 1 : 0);
