@@ -596,7 +596,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
         graph_bytes = L.graph_bytes;
         warp_bytes = L.warp_bytes;
     }
-    // k_improve runs up to 32 warps in one CTA per SM (the graph tables staged once per SM)
+    // k_improve runs up to 28 warps in one CTA per SM (the graph tables staged once per SM)
     const bool big_ctas = !c->plits && !c->ref_ties;
     const int per_warp = 1;
     int best_ind = 0;
@@ -604,7 +604,7 @@ void create_impl(const plse_graph* gr, const plse_params* pp, int device, plse_c
     if (const char* env = std::getenv("PLSE_IMPROVE_WPC")) force_wpc = std::atoi(env);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    for (int wpc : {32, 16, 8, 4, 2, 1}) {
+    for (int wpc : {28, 16, 8, 4, 2, 1}) {
         if (force_wpc && wpc != force_wpc) continue;
         if (wpc > 8 && !big_ctas) continue;
         const size_t smem = graph_bytes + (size_t)wpc * warp_bytes;

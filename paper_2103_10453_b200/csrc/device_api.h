@@ -11,8 +11,8 @@ namespace plse_dev {
 
 constexpr int kImproveMaxThreads = 256;
 constexpr int kImproveMinBlocks = 4;  // 32 resident warps per SM -> <= 64 registers
-// k_improve: up to 32 warps in ONE CTA per SM, so the graph tables are staged once per SM
-constexpr int kPadMaxThreads = 1024;
+// k_improve: up to 28 warps in ONE CTA per SM, so the graph tables are staged once per SM
+constexpr int kPadMaxThreads = 896;  // 28 warps per SM: 72 registers per thread (32 warps cap them at 64)
 
 // state probe of the per-step parity contract (plse_probe): gamma table and live tabu entries of the
 // traced individual at chosen steps

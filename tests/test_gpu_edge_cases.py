@@ -84,14 +84,14 @@ def test_lsc_instance_run(plse, orc):
 def test_results_do_not_depend_on_launch_geometry(plse, orc, monkeypatch, variant, tie):
     """Warp slots keep tabu state across individuals (monotone clocks, possibly-tabu masks) and the
     block shape follows the population size: the same population improved under different block
-    shapes (one-warp CTAs, 8-warp CTAs, the 32-warp CTA of k_improve, the default) -- so different
+    shapes (one-warp CTAs, 8-warp CTAs, the 28-warp CTA of k_improve, the default) -- so different
     individual -> slot assignments, with p = 6000 above the resident slot count so that slots are reused
     inside one launch -- must give identical colourings and iteration counts.  (compute-sanitizer is closed
     on this GPU pool; this, the trace parity and the oracle comparisons are the race evidence.)"""
     grid = orc.generate_instance(20, 0.5, 9)
     g = plse.preprocess(grid)
     outs = []
-    shapes = ("1", "8", "32", "0") if (variant, tie) == ("partial", 0) else ("1", "8", "0")
+    shapes = ("1", "8", "28", "0") if (variant, tie) == ("partial", 0) else ("1", "8", "0")
     for wpc in shapes:
         monkeypatch.setenv("PLSE_IMPROVE_WPC", wpc)
         dp = plse.DevicePopulation(g, plse.SolverConfig(
