@@ -521,7 +521,7 @@ __device__ void improve_one(const ImproveArgs& a, const Graph<W>& g, const WarpS
                 o0 |= m0[z];
                 o1 |= m1[z];
             }
-            int lc = (int)__reduce_min_sync(kFull, o0 ? 0u : o1 ? 1u : 2u);
+            int lc = __any_sync(kFull, o0 != 0) ? 0 : __any_sync(kFull, o1 != 0) ? 1 : 2;
             uint64_t m[W];
             if (lc == 2) {
                 uint64_t o2 = 0;

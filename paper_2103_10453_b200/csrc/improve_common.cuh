@@ -230,6 +230,16 @@ __device__ __forceinline__ int warp_incl_min(int x) {
 // broadcast and lane l tests bit l of the word holding the answer (warp-uniform result)
 template <int W>
 __device__ __forceinline__ int warp_nth_bit(const uint64_t (&m)[W], int rr, int src, int lane) {
+    if (W == 1) {
+        // one 64-bit mask: pick its half by the low half's popcount, then lane l tests bit l of that half
+        const uint32_t lo = __shfl_sync(kFull, (uint32_t)m[0], src), hi = __shfl_sync(kFull, (uint32_t)(m[0] >> 32), src);
+        const int clo = __popc(lo);
+        const bool up = rr >= clo;
+        const uint32_t word = up ? hi : lo;
+        const int r2 = up ? rr - clo : rr;
+        const bool hit = ((word >> lane) & 1u) && __popc(word & ((1u << lane) - 1u)) == r2;
+        return (up ? 32 : 0) + __ffs(__ballot_sync(kFull, hit)) - 1;
+    }
     uint32_t word = 0;
     int wbase = 0, r2 = 0;
 #pragma unroll
