@@ -111,3 +111,25 @@ def test_results_do_not_depend_on_launch_geometry(plse, orc, monkeypatch, varian
     for other in outs[1:]:
         for (a_col, a_f, a_it), (b_col, b_f, b_it) in zip(outs[0], other):
             assert np.array_equal(a_col, b_col) and np.array_equal(a_f, b_f) and np.array_equal(a_it, b_it)
+
+
+def test_two_word_masks_in_the_28_warp_cta(plse, orc, monkeypatch):
+    """n = 70 (two mask words per vertex, the C4 instance) in k_improve's 28-warp CTA -- the shape whose
+    shared memory now fits n = 70 (its 32-warp CTA did not) -- with p = 6000 above the resident slot count:
+    sampled individuals, including ones served by a reused slot, equal the oracle's."""
+    monkeypatch.setenv("PLSE_IMPROVE_WPC", "28")
+    grid = orc.generate_instance(70, 0.6, 12345)
+    g = plse.preprocess(grid)
+    p, budget = 6000, 2000
+    dp = plse.DevicePopulation(g, plse.SolverConfig(p=p, master_seed=6, phase1_iters=budget))
+    assert dp.counters().slots < p
+    dp.initialize_population()
+    off = dp.members
+    dp.offspring = off
+    dp.improve(1)
+    imp = dp.improved
+    _, _, iters = dp.stats(plse.IMPROVED)
+    for i in (0, 1, 147, 148 * 27 + 5, 4200, 5999):
+        o = orc.improve(grid, off[i], orc.derive_seed(6, 2, p + i), budget, 0.6, 0, oracle.TIE_CANON)
+        assert iters[i] == o["iterations"] and np.array_equal(imp[i], o["best"]), i
+    dp.close()
